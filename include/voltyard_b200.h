@@ -1,0 +1,211 @@
+/*
+ * voltyard_b200.h — C ABI of the B200-native vectorised charging-station step.
+ *
+ * This is the drop-in boundary for the reference's batched rollout path.  The
+ * reference binds its stepping core through a Python plugin registry:
+ *
+ *   make_core(tables, states, outs, backend)        backends/__init__.py:43-47
+ *   core.reset_env(b, episode)                      backends/_kernel.pyx:239-261
+ *   core.step_range(b0, b1, actions[int64 B x N+1]) backends/_kernel.pyx:275-279
+ *
+ * Each entry point below replaces one of those (see the per-function notes).
+ * Differences are deliberate and B200-first: every call is batched over the
+ * whole env range (no per-env host calls), all buffers are device pointers
+ * borrowed from the caller (PyTorch allocates them; this library allocates only
+ * its private read-only tables), and calls are asynchronous on a caller-given
+ * CUDA stream.  Errors are returned as status codes with a thread-local
+ * message from vy_last_error(); device-side range violations (an action index
+ * outside [0, 2K]) set a sticky error word read by vy_poll_error().
+ *
+ * Plain C types only: no torch, no CUDA runtime types (streams are void*).
+ */
+#ifndef VOLTYARD_B200_H
+#define VOLTYARD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VY_ABI_VERSION 1
+
+/* status codes */
+#define VY_OK 0
+#define VY_ERR_ARG 1       /* bad argument (maps to ValueError)            */
+#define VY_ERR_CUDA 2      /* CUDA runtime failure (maps to RuntimeError)  */
+#define VY_ERR_UNSUPPORTED 3 /* configuration outside the compiled kernels */
+#define VY_ERR_STATE 4     /* call order violated (maps to EpisodeDone)    */
+
+/* action element types accepted by vy_step */
+#define VY_ACT_U8 0
+#define VY_ACT_I32 1
+#define VY_ACT_I64 2
+
+/* vy_step / vy_rollout flags */
+#define VY_F_AUTO_RESET 1u   /* reset done envs to episode+1 inside the kernel (engine.py:460-462) */
+#define VY_F_INFOS 2u        /* write the info block (engine.py:282-336 'StepOutputs')             */
+#define VY_F_INJECT 4u       /* take arrival draws from vy_draws instead of the reference stream  */
+#define VY_F_OUT_F64 8u      /* obs/reward buffers are float64 (exact drop-in) instead of float32  */
+
+/*
+ * Read-only model tables (host pointers; copied to the device by vy_create).
+ * Field-for-field the content of the reference's KernelTables
+ * (engine.py:30-104, built by build_tables engine.py:107-218).
+ */
+typedef struct vy_tables {
+  /* station (topology.py:169-214) */
+  int32_t n_ports, n_slots, n_nodes, max_passes;
+  const double *volt, *imax_c, *imax_d, *eta_c, *eta_d, *i_denom; /* [n_ports] */
+  const int32_t *kind, *order;                                     /* [n_ports] */
+  const double *node_cap, *node_eta;                               /* [n_nodes] */
+  const int32_t *node_ptr;                                         /* [n_nodes+1] */
+  const int32_t *node_leaf;                                        /* [node_ptr[n_nodes]] */
+  const int32_t *node_order;                                       /* [n_nodes] deepest first */
+  /* station battery (engine.py:112-118, 149, 178) */
+  int32_t battery_enabled;
+  double b_volt, b_cap, b_rmax, b_tau, b_eta_c, b_eta_d, b_init_soc, b_imax, b_idenom;
+  /* config (config.py:33-96) */
+  int32_t k, episode_steps, steps_per_day, dt_min, horizon, obs_len, allow_discharge;
+  double dt_h, p_sell, c_dt, beta;
+  double alphas[8]; /* PENALTY_NAMES order (config.py:19-28) */
+  /* exogenous data (data.py:40-183) */
+  int32_t n_days, lam_len, has_moer, has_dgrid;
+  double wk_scale, we_scale;
+  const double *buy, *sellg;  /* [n_days*24] */
+  const double *lam;          /* [lam_len] */
+  const int8_t *weekday;      /* [n_days] */
+  const double *moer, *dgrid; /* [n_days*24] (or [1] zeros when absent) */
+  const double *sin_t, *cos_t;/* [steps_per_day] */
+  /* car catalogue and user scenario */
+  int32_t n_cat, stay_lo, stay_hi;
+  const double *cat_cum, *cat_cap, *cat_rac, *cat_rdc, *cat_tau; /* [n_cat] */
+  double soc_lo, soc_hi, frac_lo, frac_hi, p_charge;
+} vy_tables;
+
+/*
+ * Device state, struct-of-arrays.  Per-port arrays are port-major [n_ports][ld]
+ * (element (b, i) at i*ld + b) so a warp of 32 consecutive envs touches one
+ * contiguous 256 B run per field and port.  Continuous quantities stay float64:
+ * the kernels reproduce the reference's float64 arithmetic operation for
+ * operation, which is what makes discrete state bit-exact at any batch size.
+ * Replaces StateArrays (engine.py:221-279); cap/rbar/tau/rhat are not stored:
+ * cap/rbar/tau come from the car-profile table via `meta`, rhat is recomputed
+ * from soc exactly as the reference stores it (_kernel.pyx:389, 505).
+ */
+typedef struct vy_state {
+  int64_t ld;            /* leading dimension (>= batch) of per-port arrays */
+  double *port_i;        /* [n_ports][ld] i_drawn (A)                       */
+  double *port_soc;      /* [n_ports][ld]                                   */
+  double *port_de;       /* [n_ports][ld] remaining requested energy (kWh)  */
+  int16_t *port_dtrem;   /* [n_ports][ld] remaining stay (steps)            */
+  uint8_t *port_meta;    /* [n_ports][ld] bit0 occ, bit1 pref, bits2..7 profile */
+  int32_t *step, *day, *episode; /* [B] */
+  uint64_t *env_seed;    /* [B] */
+  uint64_t *akey;        /* [B] arrival-stream prefix key of the current episode */
+  double *b_i, *b_soc;   /* [B] station battery */
+  double *ep_profit, *ep_reward, *ep_missing, *ep_energy; /* [B] */
+  int32_t *ep_overtime, *ep_declined, *ep_departures;     /* [B] */
+} vy_state;
+
+/*
+ * Per-step outputs.  obs is row-major [B][obs_len] (float32, or float64 with
+ * VY_F_OUT_F64), reward [B] same dtype, done uint8 [B].  The info block is
+ * written only with VY_F_INFOS and is feature-major [k][ld] (all NULL otherwise);
+ * ep_stats and term_overtime are written whenever an episode ends.
+ */
+typedef struct vy_outputs {
+  void *obs;
+  void *reward;
+  uint8_t *done;
+  double *ep_stats;      /* [8][ld]  */
+  int32_t *term_overtime;/* [ld]     */
+  /* info block */
+  double *breakdown;     /* [10][ld] */
+  double *flows;         /* [5][ld]  */
+  int32_t *declined, *arrivals_m, *dep_n; /* [ld] */
+  int32_t *dep_port, *dep_overtime, *dep_early, *dep_pref; /* [n_ports][ld] */
+  double *dep_missing, *dep_cap, *dep_soc;                 /* [n_ports][ld] */
+  double *i_att, *i_used;  /* [n_slots][ld] */
+  double *delivered;       /* [n_ports][ld] */
+  double *b_delivered;     /* [ld] */
+} vy_outputs;
+
+/*
+ * Injected arrival draws (VY_F_INJECT).  Env b samples
+ * M_b = off[b+1] - off[b] cars this step; car j of env b is entry off[b]+j.
+ * `profile` indexes the car-profile table (0..n_cat-1 are catalogue entries).
+ * Replaces the draws of Stream(stream_key(seed, ep, 1, t)) consumed by
+ * _kernel.pyx:461-488 (sample_arrival_count/sample_car/sample_user).
+ */
+typedef struct vy_draws {
+  const int32_t *off;    /* [B+1] */
+  const uint8_t *profile;
+  const int32_t *stay;
+  const double *soc0, *frac;
+  const uint8_t *pref;
+} vy_draws;
+
+typedef struct vy_handle vy_handle;
+
+int vy_abi_version(void);
+const char *vy_last_error(void);
+
+/* Build device tables for `batch` envs on `device`.  Replaces build_tables +
+ * make_core (engine.py:370, 379-380; backends/__init__.py:43-47). */
+int vy_create(const vy_tables *t, int64_t batch, int device, vy_handle **out);
+int vy_destroy(vy_handle *h);
+
+/* Register an extra car profile (capacity, AC/DC rate, tau) for state
+ * injection (the reference's tests write cap/rbar/tau directly,
+ * tests/helpers.py:163-189).  Returns the profile id (>= n_cat) or -1. */
+int vy_add_profile(vy_handle *h, double cap, double r_ac, double r_dc, double tau);
+/* Copy profile p's derived values to host: cap, r_ac, r_dc, tau. */
+int vy_get_profile(vy_handle *h, int p, double out4[4]);
+
+/* Borrow caller-owned device buffers (engine.py:375-378 ownership). */
+int vy_bind(vy_handle *h, const vy_state *s, const vy_outputs *o);
+
+/* Reset envs.  mask: device uint8 [B] (NULL = all).  episode_mode 0: episode
+ * := 0 (first reset); 1: episode := episode+1 (engine.py:414-424).  The day
+ * is drawn from Stream(stream_key(seed, episode, 0, 0)) (_kernel.pyx:239-261)
+ * unless inj_day (device int32 [B]) is given.  Writes the reset observation. */
+int vy_reset(vy_handle *h, const uint8_t *mask, int32_t episode_mode,
+             const int32_t *inj_day, uint32_t flags, void *stream);
+
+/* Set the seed of every env: env_seed[b] = split_seed(master, b + index0)
+ * (engine.py:371-372, 407-412).  Does not reset. */
+int vy_seed_envs(vy_handle *h, int64_t master_seed, int64_t index0, void *stream);
+
+/* One step of every env.  actions: device array of `dtype` with element
+ * (b, slot) at b*row_stride + slot*col_stride.  Replaces step_range(0, B, a)
+ * plus the auto-reset loop (engine.py:446-462). */
+int vy_step(vy_handle *h, const void *actions, int32_t dtype, int64_t row_stride,
+            int64_t col_stride, uint32_t flags, const vy_draws *inj, void *stream);
+
+/* RandomPolicy.actions (policies.py:51-73) on device: row b uses the stream
+ * stream_key(seed, b + index0, 2); `call` is the number of earlier calls.
+ * Writes uint8 [B][n_ports+1]. */
+int vy_random_actions(vy_handle *h, uint64_t seed, int64_t index0, int64_t call,
+                      uint8_t *out, void *stream);
+
+/* Fused multi-step rollout: T steps with in-kernel RandomPolicy actions and
+ * auto-reset, state held in registers across steps.  Step t writes obs to
+ * obs + t*obs_step_stride (elements; 0 = overwrite one buffer), reward to
+ * reward + t*rew_step_stride, done to done + t*rew_step_stride.  Equivalent to
+ * T iterations of the throughput_probe loop (engine.py:541-545). */
+int vy_rollout(vy_handle *h, int32_t T, uint64_t policy_seed, int64_t index0, int64_t call0,
+               void *obs, int64_t obs_step_stride, void *reward, uint8_t *done,
+               int64_t rew_step_stride, uint32_t flags, void *stream);
+
+/* Sticky device error word (bit0: action index out of range).  Synchronises
+ * the stream; clears the word when `clear` is non-zero. */
+int vy_poll_error(vy_handle *h, int clear, void *stream, uint32_t *out);
+
+/* Number of kernel launches issued through this handle (for bench accounting). */
+int64_t vy_launch_count(vy_handle *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOLTYARD_B200_H */

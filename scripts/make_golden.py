@@ -1,0 +1,219 @@
+"""Generate golden fixtures from the reference implementation itself.
+
+Runs ONLY in the build container (needs /root/reference).  Imports voltyard
+from a scratch build of /root/reference/pkg (compiled Cython kernel when
+available, else the bit-identical pure-Python kernel), runs the scenarios
+below through the reference's own BatchEnv + RandomPolicy/MaxChargePolicy,
+and writes tests/golden/<name>.npz holding
+
+  * the scenario inputs (config dict, station dict, dataset arrays, seeds),
+  * the reference's build_tables() output (pins our tables.py),
+  * the actions fed, and every per-step output the engine exposes.
+
+The GPU box has no /root/reference: tests rebuild each scenario from the
+fixture alone.  Usage:  python scripts/make_golden.py [--ref /tmp/vyref/src]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+OUT = ROOT / "tests" / "golden"
+
+
+def ensure_ref(path: str | None) -> str:
+    if path:
+        return path
+    scratch = Path("/tmp/vyref")
+    if not (scratch / "src" / "voltyard").exists():
+        shutil.copytree("/root/reference/pkg", scratch)
+        subprocess.run(["chmod", "-R", "u+w", str(scratch)], check=True)
+        subprocess.run([sys.executable, "setup.py", "build_ext", "--inplace"], cwd=scratch, check=True,
+                       stdout=subprocess.DEVNULL)
+    return str(scratch / "src")
+
+
+def scenarios(vy, helpers):
+    EnvConfig, BatterySpec = vy.EnvConfig, vy.BatterySpec
+    mk, single, rnd = helpers.make_dataset, helpers.single_node_station, helpers.random_station
+    batt = BatterySpec(voltage_v=800.0, capacity_kwh=120.0, r_max_kw=60.0, tau=0.75,
+                       eta_charge=0.95, eta_discharge=0.93)
+    all_alpha = {"constraint": 0.1, "sat0": 0.2, "sat1": 0.3, "sustain": 0.4,
+                 "declined": 0.5, "degrad_battery": 0.6, "degrad_cars": 0.7, "grid": 0.8}
+    # the six backend-parity scenarios (tests/test_backend_parity.py:23-34)
+    yield "bp_default", EnvConfig(episode_steps=96), single(n_ports=4, cap_a=600.0), mk(lam=2.0), 3, 17, 23, "random", 192
+    yield "bp_battery_penalties", EnvConfig(episode_steps=96, battery_enabled=True, battery_init_soc=0.4, beta=0.5,
+                                            alpha=all_alpha), \
+        single(n_ports=3, cap_a=300.0, eta_charge=0.92, eta_discharge=0.9, battery=batt), \
+        mk(lam=2.5, moer=0.35, grid_demand=3.0), 3, 17, 23, "random", 192
+    yield "bp_no_discharge", EnvConfig(episode_steps=64, allow_discharge=False), single(n_ports=3, cap_a=200.0), \
+        mk(lam=1.0), 3, 17, 23, "random", 128
+    yield "bp_nested", EnvConfig(episode_steps=64, discretization_k=4, observe_price_horizon=6), \
+        vy.preset_station("nested_splitters", 4, 4), mk(lam=3.0), 3, 17, 23, "random", 128
+    yield "bp_coarse_dt", EnvConfig(episode_steps=96, dt_min=15), single(n_ports=2), mk(lam=1.0, dt_min=15), \
+        3, 17, 23, "random", 192
+    yield "bp_random_tree", EnvConfig(episode_steps=64), rnd(np.random.default_rng(99)), mk(lam=2.0), \
+        3, 17, 23, "random", 128
+    # config C1 literally: default station, 16 envs x 288 steps (+ crossing the auto-reset)
+    rc = vy.default_setup()
+    yield "c1_default", rc.env, rc.station, rc.dataset, 16, 0, 0, "random", 300
+    # saturating policy: exercises the tree rescale every step
+    yield "default_maxcharge", rc.env, rc.station, rc.dataset, 4, 5, 0, "max_charge", 200
+    # config C4 shape: 64 DC ports, 3-level splitter tree, battery, profit + satisfaction reward
+    cfg4 = EnvConfig(battery_enabled=True, alpha={"sat0": 1.0, "sat1": 0.5}, beta=0.2)
+    st4 = vy.preset_station("nested_splitters", ac_count=0, dc_count=64, battery=vy.DEFAULT_BATTERY)
+    ds4 = vy.generate_synthetic_defaults("highway", "high", "eu", seed=0)
+    yield "c4_highway64", cfg4, st4, ds4, 2, 3, 1, "random", 120
+    # aux series (MOER + grid demand), all penalties, fixed cost, world region catalogue
+    cfg_aux = EnvConfig(episode_steps=96, alpha=all_alpha, beta=0.3, fixed_cost_per_step=0.05)
+    rca = vy.default_setup(cfg_aux, scenario="work", traffic="high", region="world", seed=4, days=30, with_aux=True)
+    yield "aux_all_penalties", rca.env, rca.station, rca.dataset, 3, 9, 2, "random", 150
+    # non-identity parking order + AC-only single node
+    leaves = tuple(vy.EvseSpec(id=i, voltage_v=230.0, i_max_charge_a=32.0, i_max_discharge_a=16.0,
+                               eta_charge=0.9, eta_discharge=0.85) for i in range(5))
+    st_po = vy.build_station(vy.ArchNode(capacity_a=70.0, children=leaves), evse_order=[3, 1, 4, 0, 2])
+    yield "parking_order", EnvConfig(episode_steps=48), st_po, mk(lam=1.5, days=4), 3, 21, 4, "random", 96
+
+
+def dataset_dict(ds) -> dict:
+    d = {
+        "start_date": ds.prices.start_date.isoformat(),
+        "buy": ds.prices.buy, "sell_grid": ds.prices.sell_grid,
+        "rates": ds.arrivals.rates_per_step,
+        "scales": np.array([ds.arrivals.weekday_scale, ds.arrivals.weekend_scale]),
+        "cars": np.array([[e.profile.capacity_kwh, e.profile.r_max_ac_kw, e.profile.r_max_dc_kw,
+                           e.profile.tau, e.weight] for e in ds.cars.entries]),
+        "scenario": np.array([*ds.scenario.stay_steps_range, *ds.scenario.requested_fraction_range,
+                              *ds.scenario.soc_arrival_range, ds.scenario.p_charge_sensitive]),
+    }
+    if ds.aux.moer_kg_per_kwh is not None:
+        d["moer"] = ds.aux.moer_kg_per_kwh
+    if ds.aux.grid_demand_kwh is not None:
+        d["dgrid"] = ds.aux.grid_demand_kwh
+    return d
+
+
+def run(vy, name, cfg, station, ds, B, master, pseed, policy, steps):
+    from voltyard.engine import build_tables
+
+    env = vy.BatchEnv(cfg, station, ds, batch_size=B, master_seed=master)
+    pol = vy.make_policy(policy, station.n_ports, cfg.discretization_k, seed=pseed)
+    pol.bind(range(B))
+    obs = env.reset()
+    rec: dict[str, list] = {k: [] for k in (
+        "actions", "obs", "reward", "done", "breakdown", "flows", "declined", "arrivals_m", "dep_n",
+        "dep_port", "dep_missing", "dep_overtime", "dep_early", "dep_pref", "dep_cap", "dep_soc",
+        "term_overtime", "i_att", "i_used", "delivered", "b_delivered", "ep_stats", "step", "day", "episode")}
+    obs0 = obs.copy()
+    o, s = env.outs, env.states
+    for _ in range(steps):
+        a = pol.actions(obs)
+        obs, r, d, _ = env.step(a, collect_infos=False)
+        rec["actions"].append(a.astype(np.int64))
+        rec["obs"].append(obs.copy())
+        rec["reward"].append(r.copy())
+        rec["done"].append(d.astype(np.int8))
+        for k in ("breakdown", "flows", "declined", "arrivals_m", "dep_n", "dep_port", "dep_missing",
+                  "dep_overtime", "dep_early", "dep_pref", "dep_cap", "dep_soc", "term_overtime",
+                  "i_att", "i_used", "delivered", "b_delivered"):
+            rec[k].append(getattr(o, k).copy())
+        rec["ep_stats"].append(np.where(d[:, None], o.ep_stats, 0.0))
+        rec["step"].append(s.step.copy())
+        rec["day"].append(s.day.copy())
+        rec["episode"].append(s.episode.copy())
+    # dep_* rows beyond dep_n are stale by design; mask them so fixtures hold only defined entries
+    dn = np.array(rec["dep_n"])
+    for k in ("dep_port", "dep_missing", "dep_overtime", "dep_early", "dep_pref", "dep_cap", "dep_soc"):
+        arr = np.array(rec[k])
+        mask = np.arange(arr.shape[-1])[None, None, :] < dn[:, :, None]
+        rec[k] = np.where(mask, arr, 0)
+    final = {f"final_{k}": getattr(s, k).copy() for k in (
+        "occ", "i_drawn", "soc", "de", "dtrem", "cap", "rbar", "tau", "pref", "rhat", "b_i", "b_soc", "b_rhat",
+        "step", "day", "episode", "env_seed", "ep_profit", "ep_reward", "ep_missing", "ep_energy",
+        "ep_overtime", "ep_declined", "ep_departures")}
+    env.close()
+    tabs = build_tables(cfg, station, ds)
+    tab = {}
+    for k, v in vars(tabs).items():
+        tab[f"tab_{k}"] = np.asarray(v)
+    meta = {
+        "name": name, "config": cfg.to_dict(), "station": vy.topology.station_to_dict(station),
+        "batch": B, "master_seed": master, "policy": policy, "policy_seed": pseed, "steps": steps,
+        "backend": env.backend,
+    }
+    payload = {"meta": np.array(json.dumps(meta)), "obs0": obs0}
+    payload.update({f"ds_{k}": np.asarray(v) for k, v in dataset_dict(ds).items()})
+    payload.update({k: np.array(v) for k, v in rec.items()})
+    payload.update(final)
+    payload.update(tab)
+    OUT.mkdir(parents=True, exist_ok=True)
+    np.savez_compressed(OUT / f"{name}.npz", **payload)
+    return env.backend
+
+
+def synthetic_vectors(vy):
+    """Synthetic generators' arrays for several (scenario, traffic, region, seed)."""
+    out = {}
+    for sc in ("highway", "residential", "work", "shopping"):
+        for tr in ("low", "medium", "high"):
+            a = vy.data.synthetic_arrivals(sc, tr, dt_min=5)
+            out[f"arr_{sc}_{tr}"] = a.rates_per_step
+            out[f"arrscale_{sc}_{tr}"] = np.array([a.weekday_scale, a.weekend_scale])
+        for dtm in (1, 5, 15):
+            m = vy.data.scenario_model(sc, dt_min=dtm)
+            out[f"scen_{sc}_{dtm}"] = np.array([*m.stay_steps_range, *m.requested_fraction_range,
+                                                *m.soc_arrival_range, m.p_charge_sensitive])
+    for rg in ("eu", "us", "world"):
+        for seed in (0, 7):
+            p = vy.data.synthetic_prices(rg, seed=seed, days=40)
+            out[f"price_{rg}_{seed}"] = p.buy
+            out[f"sell_{rg}_{seed}"] = p.sell_grid
+        c = vy.data.car_catalog(rg)
+        out[f"cum_{rg}"] = c.cumulative_weights()
+    aux = vy.data.synthetic_aux(seed=3, days=20)
+    out["aux_moer_3"], out["aux_dgrid_3"] = aux.moer_kg_per_kwh, aux.grid_demand_kwh
+    # RNG known answers
+    from voltyard import rng
+    keys = [rng.stream_key(11, i) for i in range(64)]
+    out["rng_keys"] = np.array(keys, dtype=np.uint64)
+    st = rng.BatchStreams(np.array(keys, dtype=np.uint64))
+    out["rng_u"] = st.uniform_block(9)
+    out["rng_pois"] = np.array([rng.Stream(k).poisson(3.7) for k in keys])
+    out["rng_pois_big"] = np.array([rng.Stream(k).poisson(70.5) for k in keys])
+    out["split_seed"] = np.array([rng.split_seed(m, i) for m in (-17, 0, 42) for i in range(8)], dtype=np.uint64)
+    pol = vy.RandomPolicy(seed=5, n_ports=16, k=10)
+    pol.bind(range(1000, 1032))
+    out["policy_actions"] = np.stack([pol.actions(np.zeros((32, 105))) for _ in range(3)])
+    np.savez_compressed(OUT / "synthetic_vectors.npz", **out)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ref", default=None)
+    args = ap.parse_args()
+    sys.path.insert(0, ensure_ref(args.ref))
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    import voltyard as vy  # noqa: E402
+    import voltyard.data  # noqa: F401,E402
+    import voltyard.topology  # noqa: F401,E402
+    import helpers  # noqa: E402
+
+    print("reference backends:", vy.available_backends())
+    for sc in scenarios(vy, helpers):
+        be = run(vy, *sc)
+        print("wrote", sc[0], "backend", be)
+    synthetic_vectors(vy)
+    print("wrote synthetic_vectors")
+
+
+if __name__ == "__main__":
+    main()
