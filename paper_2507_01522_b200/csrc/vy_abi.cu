@@ -1,0 +1,296 @@
+// vy_abi.cu — C ABI (include/voltyard_b200.h) over the sm_100a kernels.
+//
+// Host responsibilities: validate and flatten the reference tables into the
+// launch parameters (per-port constants by value, long series in device
+// memory), precompute the values whose host computation must match the
+// reference bit for bit (Poisson thresholds exp(-lambda) with the same libm
+// the reference calls, _kernel.pyx:56; the (a-k)/k action grid,
+// _kernel.pyx:305), pick the port-capacity instantiation, and launch.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "vy_launch.cuh"
+
+using namespace vy;
+
+namespace vy {
+thread_local std::string g_err;
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+}  // namespace vy
+
+namespace {
+template <typename T>
+int upload(T** dst, const T* src, size_t n) {
+  if (n == 0) n = 1;
+  VY_CUDA(cudaMalloc(dst, n * sizeof(T)));
+  if (src) VY_CUDA(cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  return VY_OK;
+}
+}  // namespace
+
+namespace vy {
+
+__global__ void k_random_actions(uint64_t seed, int64_t index0, int64_t call, int64_t B, int ns, int hi,
+                                 uint8_t* out) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const uint64_t key = fold(fold(fold(kKey0, seed), (uint64_t)(index0 + b)), 2);
+  const uint64_t j0 = (uint64_t)call * (uint64_t)ns;
+  for (int s = 0; s < ns; ++s) out[b * ns + s] = (uint8_t)policy_action(key, j0 + s + 1, hi);
+}
+
+__global__ void k_seed_envs(uint64_t master, int64_t index0, int64_t B, uint64_t* env_seed) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) env_seed[b] = fold(fold(kKey0, master), (uint64_t)(index0 + b));
+}
+
+}  // namespace vy
+
+namespace {
+
+#define VY_DISPATCH(h, FN, ...)                                   \
+  switch ((h)->np) {                                              \
+    case 8: return FN<8>(h, __VA_ARGS__);                         \
+    case 16: return FN<16>(h, __VA_ARGS__);                       \
+    case 32: return FN<32>(h, __VA_ARGS__);                       \
+    case 64: return FN<64>(h, __VA_ARGS__);                       \
+    default: return fail(VY_ERR_UNSUPPORTED, "no kernel for this port count"); \
+  }
+
+int upload_profiles(vy_handle* h) {
+  std::vector<Profile> all(kMaxProfiles, Profile{1.0, 0.0, 0.0, 0.5, 0.5});
+  for (size_t i = 0; i < h->profiles.size(); ++i) all[i] = h->profiles[i];
+  VY_CUDA(cudaMemcpy(h->d_prof, all.data(), sizeof(Profile) * kMaxProfiles, cudaMemcpyHostToDevice));
+  return VY_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vy_abi_version(void) { return VY_ABI_VERSION; }
+const char* vy_last_error(void) { return g_err.c_str(); }
+
+int vy_create(const vy_tables* t, int64_t batch, int device, vy_handle** out) {
+  if (!t || !out) return fail(VY_ERR_ARG, "null argument");
+  if (batch < 1) return fail(VY_ERR_ARG, "batch_size must be >= 1");
+  const int n = t->n_ports;
+  if (n < 1 || n > 64) return fail(VY_ERR_UNSUPPORTED, "n_ports must be in [1, 64]");
+  if (t->n_cat < 1 || t->n_cat > kMaxProfiles) return fail(VY_ERR_UNSUPPORTED, "catalogue must hold 1..64 cars");
+  if ((int64_t)t->episode_steps + t->stay_hi > 32000 || t->stay_hi > 32000)
+    return fail(VY_ERR_UNSUPPORTED, "stay / episode lengths exceed the int16 dwell-time state");
+  if (t->n_days < 1 || t->lam_len < 1 || t->steps_per_day < 1) return fail(VY_ERR_ARG, "empty series");
+  vy_handle* h = new vy_handle();
+  h->device = device;
+  h->B = batch;
+  h->t = *t;
+  h->np = n <= 8 ? 8 : n <= 16 ? 16 : n <= 32 ? 32 : 64;
+  if (t->n_nodes > 2 * h->np + 2) {
+    delete h;
+    return fail(VY_ERR_UNSUPPORTED, "too many tree nodes for the compiled capacity");
+  }
+  h->volt.assign(t->volt, t->volt + n);
+  h->imax_c.assign(t->imax_c, t->imax_c + n);
+  h->imax_d.assign(t->imax_d, t->imax_d + n);
+  h->eta_c.assign(t->eta_c, t->eta_c + n);
+  h->eta_d.assign(t->eta_d, t->eta_d + n);
+  h->i_denom.assign(t->i_denom, t->i_denom + n);
+  h->kind.assign(t->kind, t->kind + n);
+  h->order.assign(t->order, t->order + n);
+  for (int i = 0; i < n; ++i) h->order_identity &= h->order[i] == i;
+  // tree: contiguous leaf ranges (topology.py:178-196)
+  for (int m = 0; m < t->n_nodes; ++m) {
+    const int a0 = t->node_ptr[m], a1 = t->node_ptr[m + 1];
+    int lo = 0, hi = 0;
+    if (a1 > a0) {
+      lo = t->node_leaf[a0];
+      hi = lo + (a1 - a0);
+      for (int a = a0; a < a1; ++a)
+        if (t->node_leaf[a] != lo + (a - a0)) {
+          delete h;
+          return fail(VY_ERR_UNSUPPORTED, "tree node leaves are not one ascending run");
+        }
+    }
+    if (hi > t->n_slots) {
+      delete h;
+      return fail(VY_ERR_ARG, "tree leaf index out of range");
+    }
+    h->node_lo.push_back(lo);
+    h->node_hi.push_back(hi);
+    h->node_cap.push_back(t->node_cap[m]);
+    h->node_eta.push_back(t->node_eta[m]);
+    h->node_order.push_back(t->node_order[m]);
+  }
+  for (int c = 0; c < t->n_cat; ++c)
+    h->profiles.push_back(Profile{t->cat_cap[c], t->cat_rac[c], t->cat_rdc[c], t->cat_tau[c], 1.0 - t->cat_tau[c]});
+  // Poisson: per (weekday flag, step-of-profile) the number of full 32-chunks and the
+  // threshold of the last chunk, reproducing rng.py:94-115 / _kernel.pyx:55-73 on the host.
+  const int L = t->lam_len;
+  std::vector<double> pthr(2 * L, 0.0);
+  std::vector<int> pfull(2 * L, -1);
+  for (int w = 0; w < 2; ++w)
+    for (int j = 0; j < L; ++j) {
+      double lam = t->lam[j] * (w == 0 ? t->wk_scale : t->we_scale);
+      if (lam <= 0.0) continue;
+      int full = 0;
+      while (lam > 32.0) {
+        lam -= 32.0;
+        ++full;
+      }
+      pfull[w * L + j] = full;
+      pthr[w * L + j] = std::exp(-lam);
+    }
+  h->thr32 = std::exp(-32.0);
+  const int nd = 2 * t->k + 1;
+  std::vector<double> dtab(nd);
+  for (int a = 0; a < nd; ++a) dtab[a] = (double)(a - t->k) / (double)t->k;
+  int rc = cudaSetDevice(device) == cudaSuccess ? VY_OK : fail(VY_ERR_CUDA, "cudaSetDevice failed");
+  const size_t nh = (size_t)t->n_days * 24;
+  if (!rc) rc = upload(&h->d_buy, t->buy, nh);
+  if (!rc) rc = upload(&h->d_sellg, t->sellg, nh);
+  if (!rc) rc = upload(&h->d_moer, t->moer, t->has_moer ? nh : 1);
+  if (!rc) rc = upload(&h->d_dgrid, t->dgrid, t->has_dgrid ? nh : 1);
+  if (!rc) rc = upload(&h->d_sin, t->sin_t, (size_t)t->steps_per_day);
+  if (!rc) rc = upload(&h->d_cos, t->cos_t, (size_t)t->steps_per_day);
+  if (!rc) rc = upload(&h->d_catcum, t->cat_cum, (size_t)t->n_cat);
+  if (!rc) rc = upload(&h->d_wk, t->weekday, (size_t)t->n_days);
+  if (!rc) rc = upload(&h->d_pthr, pthr.data(), pthr.size());
+  if (!rc) rc = upload(&h->d_pfull, pfull.data(), pfull.size());
+  if (!rc) rc = upload(&h->d_dtab, dtab.data(), dtab.size());
+  if (!rc) rc = upload<Profile>(&h->d_prof, nullptr, kMaxProfiles);
+  if (!rc) rc = upload<uint32_t>(&h->d_err, nullptr, 1);
+  if (!rc && cudaMemset(h->d_err, 0, 4) != cudaSuccess) rc = fail(VY_ERR_CUDA, "memset");
+  if (!rc) rc = upload_profiles(h);
+  if (rc) {
+    vy_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return VY_OK;
+}
+
+int vy_destroy(vy_handle* h) {
+  if (!h) return VY_OK;
+  void* ptrs[] = {h->d_buy, h->d_sellg, h->d_moer, h->d_dgrid, h->d_sin, h->d_cos, h->d_catcum,
+                  h->d_pthr, h->d_dtab, h->d_wk, h->d_pfull, h->d_prof, h->d_err};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete h;
+  return VY_OK;
+}
+
+int vy_add_profile(vy_handle* h, double cap, double r_ac, double r_dc, double tau) {
+  if (!h || (int)h->profiles.size() >= kMaxProfiles) {
+    fail(VY_ERR_ARG, "profile table full");
+    return -1;
+  }
+  if (!(cap > 0.0) || !(tau > 0.0 && tau < 1.0)) {
+    fail(VY_ERR_ARG, "profile needs cap > 0 and 0 < tau < 1");
+    return -1;
+  }
+  for (size_t i = 0; i < h->profiles.size(); ++i) {
+    const Profile& p = h->profiles[i];
+    if (p.cap == cap && p.r_ac == r_ac && p.r_dc == r_dc && p.tau == tau) return (int)i;
+  }
+  h->profiles.push_back(Profile{cap, r_ac, r_dc, tau, 1.0 - tau});
+  if (upload_profiles(h)) return -1;
+  return (int)h->profiles.size() - 1;
+}
+
+int vy_get_profile(vy_handle* h, int p, double out4[4]) {
+  if (!h || p < 0 || p >= (int)h->profiles.size()) return fail(VY_ERR_ARG, "bad profile id");
+  out4[0] = h->profiles[p].cap;
+  out4[1] = h->profiles[p].r_ac;
+  out4[2] = h->profiles[p].r_dc;
+  out4[3] = h->profiles[p].tau;
+  return VY_OK;
+}
+
+int vy_bind(vy_handle* h, const vy_state* s, const vy_outputs* o) {
+  if (!h || !s || !o) return fail(VY_ERR_ARG, "null argument");
+  if (s->ld < h->B) return fail(VY_ERR_ARG, "state leading dimension smaller than batch");
+  if (!s->port_i || !s->port_soc || !s->port_de || !s->port_dtrem || !s->port_meta || !s->step || !s->day ||
+      !s->episode || !s->env_seed || !s->akey || !s->b_i || !s->b_soc || !s->ep_profit || !s->ep_reward ||
+      !s->ep_missing || !s->ep_energy || !s->ep_overtime || !s->ep_declined || !s->ep_departures)
+    return fail(VY_ERR_ARG, "state buffer missing");
+  if (!o->obs || !o->reward || !o->done || !o->ep_stats || !o->term_overtime)
+    return fail(VY_ERR_ARG, "output buffer missing");
+  h->st = *s;
+  h->out = *o;
+  h->bound = true;
+  return VY_OK;
+}
+
+static bool infos_bound(const vy_outputs& o) {
+  return o.breakdown && o.flows && o.declined && o.arrivals_m && o.dep_n && o.dep_port && o.dep_overtime &&
+         o.dep_early && o.dep_pref && o.dep_missing && o.dep_cap && o.dep_soc && o.i_att && o.i_used &&
+         o.delivered && o.b_delivered;
+}
+
+int vy_reset(vy_handle* h, const uint8_t* mask, int32_t episode_mode, const int32_t* inj_day, uint32_t flags,
+             void* stream) {
+  if (!h || !h->bound) return fail(VY_ERR_STATE, "handle not bound");
+  VY_DISPATCH(h, launch_reset, mask, episode_mode, inj_day, flags, (cudaStream_t)stream);
+}
+
+int vy_seed_envs(vy_handle* h, int64_t master_seed, int64_t index0, void* stream) {
+  if (!h || !h->bound) return fail(VY_ERR_STATE, "handle not bound");
+  const unsigned grid = (unsigned)((h->B + 255) / 256);
+  k_seed_envs<<<grid, 256, 0, (cudaStream_t)stream>>>((uint64_t)master_seed, index0, h->B, h->st.env_seed);
+  VY_CUDA(cudaGetLastError());
+  ++h->launches;
+  return VY_OK;
+}
+
+int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride, int64_t col_stride,
+            uint32_t flags, const vy_draws* inj, void* stream) {
+  if (!h || !h->bound) return fail(VY_ERR_STATE, "handle not bound");
+  if (!actions) return fail(VY_ERR_ARG, "null actions");
+  if (dtype != VY_ACT_U8 && dtype != VY_ACT_I32 && dtype != VY_ACT_I64) return fail(VY_ERR_ARG, "bad action dtype");
+  if ((flags & VY_F_INFOS) && !infos_bound(h->out)) return fail(VY_ERR_ARG, "info buffers not bound");
+  if ((flags & VY_F_INJECT) && (!inj || !inj->off || !inj->profile || !inj->stay || !inj->soc0 || !inj->frac ||
+                                !inj->pref))
+    return fail(VY_ERR_ARG, "injected draws missing");
+  VY_DISPATCH(h, launch_step, actions, dtype, row_stride, col_stride, flags, inj, (cudaStream_t)stream);
+}
+
+int vy_random_actions(vy_handle* h, uint64_t seed, int64_t index0, int64_t call, uint8_t* out, void* stream) {
+  if (!h || !out) return fail(VY_ERR_ARG, "null argument");
+  const int ns = h->t.n_ports + 1, hi = 2 * h->t.k + 1;
+  if (hi > 256) return fail(VY_ERR_UNSUPPORTED, "uint8 actions need 2k+1 <= 256");
+  const unsigned grid = (unsigned)((h->B + 255) / 256);
+  k_random_actions<<<grid, 256, 0, (cudaStream_t)stream>>>(seed, index0, call, h->B, ns, hi, out);
+  VY_CUDA(cudaGetLastError());
+  ++h->launches;
+  return VY_OK;
+}
+
+int vy_rollout(vy_handle* h, int32_t T, uint64_t policy_seed, int64_t index0, int64_t call0, void* obs,
+               int64_t obs_step_stride, void* reward, uint8_t* done, int64_t rew_step_stride, uint32_t flags,
+               void* stream) {
+  if (!h || !h->bound) return fail(VY_ERR_STATE, "handle not bound");
+  if (T < 1 || !obs || !reward || !done) return fail(VY_ERR_ARG, "bad rollout arguments");
+  if (flags & (VY_F_INFOS | VY_F_INJECT)) return fail(VY_ERR_UNSUPPORTED, "rollout supports lean outputs only");
+  VY_DISPATCH(h, launch_rollout, T, policy_seed, index0, call0, obs, obs_step_stride, reward, done,
+              rew_step_stride, flags, (cudaStream_t)stream);
+}
+
+int vy_poll_error(vy_handle* h, int clear, void* stream, uint32_t* out) {
+  if (!h || !out) return fail(VY_ERR_ARG, "null argument");
+  VY_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  VY_CUDA(cudaMemcpy(out, h->d_err, 4, cudaMemcpyDeviceToHost));
+  if (clear) VY_CUDA(cudaMemset(h->d_err, 0, 4));
+  return VY_OK;
+}
+
+int64_t vy_launch_count(vy_handle* h) { return h ? h->launches : -1; }
+
+}  // extern "C"

@@ -50,3 +50,32 @@ class Fixture:
 
     def __getitem__(self, k):
         return self.z[k]
+
+
+# --- small builders (same parameters as the reference's tests/helpers.py:22-101) ---
+
+def make_dataset(lam: float = 0.0, buy: float = 0.10, sell_grid=None, days: int = 3, dt_min: int = 5,
+                 stay_range=(6, 24), frac_range=(0.3, 0.9), soc_range=(0.2, 0.7), p_charge: float = 0.3,
+                 cars=None, moer=None, grid_demand=None) -> Dataset:
+    n = days * 24
+    cars = cars or CarCatalog((CatalogEntry(CarProfile(60.0, 11.0, 120.0, 0.8, name="a"), 1.0),
+                               CatalogEntry(CarProfile(40.0, 7.4, 60.0, 0.8, name="b"), 1.0)))
+    return Dataset(
+        prices=PriceSeries(dt.date(2022, 1, 3), np.full(n, buy), np.full(n, buy if sell_grid is None else sell_grid)),
+        arrivals=ArrivalProfile(np.full(1440 // dt_min, lam)),
+        cars=cars,
+        scenario=UserScenarioModel(stay_range, frac_range, soc_range, p_charge),
+        aux=AuxSeries(None if moer is None else np.full(n, moer),
+                      None if grid_demand is None else np.full(n, grid_demand)),
+    )
+
+
+def single_node_station(n_ports: int = 2, cap_a: float = 1e9, voltage_v: float = 400.0, i_max: float = 400.0,
+                        i_max_discharge=None, eta_charge: float = 1.0, eta_discharge: float = 1.0,
+                        kind: str = "dc", node_eta: float = 1.0, battery=None):
+    from paper_2507_01522_b200.station import ArchNode, EvseSpec, build_station
+
+    leaves = tuple(EvseSpec(id=i, voltage_v=voltage_v, i_max_charge_a=i_max,
+                            i_max_discharge_a=i_max if i_max_discharge is None else i_max_discharge,
+                            eta_charge=eta_charge, eta_discharge=eta_discharge, kind=kind) for i in range(n_ports))
+    return build_station(ArchNode(capacity_a=cap_a, eta=node_eta, children=leaves), battery=battery)
