@@ -60,7 +60,11 @@ class DeviceState:
     """Struct-of-arrays env state in HBM (vy_state).  Per-port tensors are [N, B]."""
 
     def __init__(self, B: int, n: int, device: torch.device):
+        # leading dimension padded to whole 32-env warp tiles (vy_bind requires it)
+        self.ld = ld = -(-B // 32) * 32
+        self.B = B
         z = lambda *s, dt: torch.zeros(*s, dtype=dt, device=device)  # noqa: E731
+        B = ld
         self.port_i = z(n, B, dt=torch.float64)
         self.port_soc = z(n, B, dt=torch.float64)
         self.port_de = z(n, B, dt=torch.float64)
@@ -83,13 +87,18 @@ class DeviceState:
 
     def ctypes(self, B: int) -> nat.VyState:
         s = nat.VyState()
-        s.ld = B
+        s.ld = self.ld
         for name, _ in nat.VyState._fields_[1:]:
             setattr(s, name, getattr(self, name).data_ptr())
         return s
 
     def bytes(self) -> int:
         return sum(v.numel() * v.element_size() for v in vars(self).values() if isinstance(v, torch.Tensor))
+
+    def view(self, name: str) -> torch.Tensor:
+        """Field without the warp-tile padding: [N, B] per port, [B] per env."""
+        t = getattr(self, name)
+        return t[..., : self.B]
 
 
 class DeviceOutputs:
@@ -98,17 +107,18 @@ class DeviceOutputs:
     def __init__(self, B: int, n: int, ns: int, obs_len: int, obs_dtype: torch.dtype, device: torch.device):
         self.device = device
         self.B, self.n, self.ns = B, n, ns
+        self.ld = -(-B // 32) * 32
         self.obs = torch.zeros(B, obs_len, dtype=obs_dtype, device=device)
         self.reward = torch.zeros(B, dtype=obs_dtype, device=device)
         self.done = torch.zeros(B, dtype=torch.uint8, device=device)
-        self.ep_stats = torch.zeros(8, B, dtype=torch.float64, device=device)
-        self.term_overtime = torch.zeros(B, dtype=torch.int32, device=device)
+        self.ep_stats = torch.zeros(8, self.ld, dtype=torch.float64, device=device)
+        self.term_overtime = torch.zeros(self.ld, dtype=torch.int32, device=device)
         self.info = None
 
     def ensure_info(self) -> None:
         if self.info is not None:
             return
-        B, n, ns, d = self.B, self.n, self.ns, self.device
+        B, n, ns, d = self.ld, self.n, self.ns, self.device
         f = lambda *s: torch.zeros(*s, dtype=torch.float64, device=d)  # noqa: E731
         i = lambda *s: torch.zeros(*s, dtype=torch.int32, device=d)  # noqa: E731
         self.info = dict(
@@ -171,7 +181,7 @@ class BatchEnv:
             self._seed_from_master(master_seed)
         else:
             seeds = np.array([int(s) & ((1 << 64) - 1) for s in env_seeds], dtype=np.uint64)
-            self.states.env_seed.copy_(torch.from_numpy(seeds.view(np.int64)).to(self.device))
+            self.states.env_seed[:B].copy_(torch.from_numpy(seeds.view(np.int64)).to(self.device))
         self._needs_reset = True
         self._t = None  # common step counter while all envs move in lockstep
         self.profile_base = t.n_cat
@@ -330,7 +340,7 @@ class BatchEnv:
     def _episode_over(self) -> bool:
         if self._t is not None:
             return self._t >= self.tables.episode_steps
-        return bool((self.states.step >= self.tables.episode_steps).any().item())
+        return bool((self.states.view("step") >= self.tables.episode_steps).any().item())
 
     def rollout(self, T: int, policy_seed: int, call0: int, obs_out: torch.Tensor, reward_out: torch.Tensor,
                 done_out: torch.Tensor) -> None:
@@ -388,7 +398,8 @@ class BatchEnv:
     def reference_state(self) -> dict:
         """State in the reference StateArrays layout (engine.py:221-279), numpy."""
         torch.cuda.synchronize(self.device)
-        s, t = self.states, self.tables
+        t = self.tables
+        s = _Views(self.states)
         meta = s.port_meta.cpu().numpy().T.astype(np.int64)
         occ = (meta & 1).astype(np.int8)
         pref = ((meta >> 1) & 1).astype(np.int8)
@@ -427,13 +438,14 @@ class BatchEnv:
     def reference_outputs(self) -> dict:
         """Info block in the reference StepOutputs layout ([B, k], engine.py:282-336)."""
         torch.cuda.synchronize(self.device)
-        o = {k: v.cpu().numpy().T.copy() if v.dim() == 2 else v.cpu().numpy().copy()
+        B = self.batch_size
+        o = {k: v[..., :B].cpu().numpy().T.copy() if v.dim() == 2 else v[:B].cpu().numpy().copy()
              for k, v in (self.outs.info or {}).items()}
         for k in ("declined", "arrivals_m", "dep_n", "dep_port", "dep_overtime", "dep_early", "dep_pref"):
             if k in o:
                 o[k] = o[k].astype(np.int64)
-        o["ep_stats"] = self.outs.ep_stats.cpu().numpy().T.copy()
-        o["term_overtime"] = self.outs.term_overtime.cpu().numpy().astype(np.int64)
+        o["ep_stats"] = self.outs.ep_stats[:, :B].cpu().numpy().T.copy()
+        o["term_overtime"] = self.outs.term_overtime[:B].cpu().numpy().astype(np.int64)
         return o
 
     def _build_infos(self) -> list:
@@ -454,6 +466,16 @@ class BatchEnv:
         s.port_soc[port, b] = float(soc)
         s.port_de[port, b] = float(de)
         s.port_dtrem[port, b] = int(dtrem)
+
+
+class _Views:
+    """Attribute access to DeviceState fields without tile padding."""
+
+    def __init__(self, st: DeviceState):
+        self._st = st
+
+    def __getattr__(self, name):
+        return self._st.view(name)
 
 
 class DeviceRandomPolicy:

@@ -5,7 +5,7 @@
 // memory), precompute the values whose host computation must match the
 // reference bit for bit (Poisson thresholds exp(-lambda) with the same libm
 // the reference calls, _kernel.pyx:56; the (a-k)/k action grid,
-// _kernel.pyx:305), pick the port-capacity instantiation, and launch.
+// _kernel.pyx:305), size the per-warp shared-memory tiles, and launch.
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -14,19 +14,24 @@
 #include <string>
 #include <vector>
 
-#include "vy_launch.cuh"
+#include "vy_kernels.cuh"
 
 using namespace vy;
 
-namespace vy {
+namespace {
 thread_local std::string g_err;
+
 int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
-}  // namespace vy
 
-namespace {
+#define VY_CUDA(call)                                                                                       \
+  do {                                                                                                      \
+    cudaError_t e_ = (call);                                                                                \
+    if (e_ != cudaSuccess) return fail(VY_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_));       \
+  } while (0)
+
 template <typename T>
 int upload(T** dst, const T* src, size_t n) {
   if (n == 0) n = 1;
@@ -54,16 +59,169 @@ __global__ void k_seed_envs(uint64_t master, int64_t index0, int64_t B, uint64_t
 
 }  // namespace vy
 
+struct vy_handle {
+  int device = 0;
+  int64_t B = 0;
+  vy_tables t{};  // scalars only (pointers are not retained)
+  std::vector<double> volt, imax_c, imax_d, eta_c, eta_d, i_denom, node_cap, node_eta;
+  std::vector<int> kind, order, node_lo, node_hi, node_order;
+  bool order_identity = true;
+  std::vector<Profile> profiles;
+  double *d_buy = nullptr, *d_sellg = nullptr, *d_moer = nullptr, *d_dgrid = nullptr, *d_sin = nullptr,
+         *d_cos = nullptr, *d_catcum = nullptr, *d_pthr = nullptr, *d_dtab = nullptr;
+  int8_t* d_wk = nullptr;
+  int* d_pfull = nullptr;
+  Profile* d_prof = nullptr;
+  uint32_t* d_err = nullptr;
+  double thr32 = 0.0;
+  vy_state st{};
+  vy_outputs out{};
+  bool bound = false;
+  int64_t launches = 0;
+  int smem_per_sm = 0, num_sms = 0;
+};
+
 namespace {
 
-#define VY_DISPATCH(h, FN, ...)                                   \
-  switch ((h)->np) {                                              \
-    case 8: return FN<8>(h, __VA_ARGS__);                         \
-    case 16: return FN<16>(h, __VA_ARGS__);                       \
-    case 32: return FN<32>(h, __VA_ARGS__);                       \
-    case 64: return FN<64>(h, __VA_ARGS__);                       \
-    default: return fail(VY_ERR_UNSUPPORTED, "no kernel for this port count"); \
+// per-warp tile layout; `extra` reserves rollout-only obs staging for port columns
+TileLayout tile_layout(const vy_tables& t, bool rollout) {
+  TileLayout L{};
+  const int n = t.n_ports;
+  int off = 0;
+  L.idr = off;
+  off += n * 256;
+  L.soc = off;
+  off += n * 256;
+  L.de = off;
+  off += n * 256;
+  L.dtrem = off;
+  off += n * 64;
+  L.meta = off;
+  off += ((n * 32) + 127) & ~127;
+  L.gobs = off;
+  off += (9 + t.horizon) * 128;
+  L.extra = 0;
+  if (rollout) {
+    L.extra = off;
+    off += 6 * n * 128;
   }
+  L.bytes = (off + 127) & ~127;
+  return L;
+}
+
+void fill(vy_handle* h, Params& P, bool rollout) {
+  const vy_tables& t = h->t;
+  std::memset(&P, 0, sizeof(P));
+  P.n_ports = t.n_ports;
+  P.n_slots = t.n_slots;
+  P.n_nodes = t.n_nodes;
+  P.max_passes = t.max_passes;
+  P.k = t.k;
+  P.episode_steps = t.episode_steps;
+  P.steps_per_day = t.steps_per_day;
+  P.dt_min = t.dt_min;
+  P.horizon = t.horizon;
+  P.obs_len = t.obs_len;
+  P.n_days = t.n_days;
+  P.lam_len = t.lam_len;
+  P.n_cat = t.n_cat;
+  P.stay_lo = t.stay_lo;
+  P.stay_span = t.stay_hi - t.stay_lo + 1;
+  P.allow_discharge = t.allow_discharge;
+  P.battery = t.battery_enabled;
+  P.has_moer = t.has_moer;
+  P.has_dgrid = t.has_dgrid;
+  P.order_identity = h->order_identity;
+  P.B = h->B;
+  P.ld = h->st.ld;
+  P.dt_h = t.dt_h;
+  P.p_sell = t.p_sell;
+  P.c_dt = t.c_dt;
+  P.beta = t.beta;
+  P.soc_lo = t.soc_lo;
+  P.soc_span = t.soc_hi - t.soc_lo;  // same runtime expression as _kernel.pyx:486
+  P.frac_lo = t.frac_lo;
+  P.frac_span = t.frac_hi - t.frac_lo;
+  P.p_charge = t.p_charge;
+  P.thr32 = h->thr32;
+  for (int i = 0; i < 8; ++i) P.alphas[i] = t.alphas[i];
+  P.b_volt = t.b_volt;
+  P.b_cap = t.b_cap;
+  P.b_rmax = t.b_rmax;
+  P.b_tau = t.b_tau;
+  P.b_omt = 1.0 - t.b_tau;
+  P.b_eta_c = t.b_eta_c;
+  P.b_eta_d = t.b_eta_d;
+  P.b_init_soc = t.b_init_soc;
+  P.b_imax = t.b_imax;
+  P.b_idenom = t.b_idenom;
+  P.b_dtv = t.dt_h * t.b_volt;
+  for (int i = 0; i < t.n_ports; ++i) {
+    P.volt[i] = h->volt[i];
+    P.imax_c[i] = h->imax_c[i];
+    P.imax_d[i] = h->imax_d[i];
+    P.eta_c[i] = h->eta_c[i];
+    P.eta_d[i] = h->eta_d[i];
+    P.i_denom[i] = h->i_denom[i];
+    P.dtv[i] = t.dt_h * h->volt[i];  // (dt_h * V) * I / 1000 evaluates left to right (_kernel.pyx:366)
+    P.kind[i] = h->kind[i];
+    P.order[i] = h->order[i];
+  }
+  for (int m = 0; m < t.n_nodes; ++m) {
+    P.node_cap[m] = h->node_cap[m];
+    P.node_eta[m] = h->node_eta[m];
+    P.node_lo[m] = h->node_lo[m];
+    P.node_hi[m] = h->node_hi[m];
+    P.node_order[m] = h->node_order[m];
+  }
+  P.buy = h->d_buy;
+  P.sellg = h->d_sellg;
+  P.moer = h->d_moer;
+  P.dgrid = h->d_dgrid;
+  P.sin_t = h->d_sin;
+  P.cos_t = h->d_cos;
+  P.cat_cum = h->d_catcum;
+  P.weekday = h->d_wk;
+  P.pois_thr = h->d_pthr;
+  P.pois_full = h->d_pfull;
+  P.profiles = h->d_prof;
+  P.delta_tab = h->d_dtab;
+  P.st = h->st;
+  P.out = h->out;
+  P.err = h->d_err;
+  P.L = tile_layout(t, rollout);
+}
+
+// Warps per CTA: fill the SM's shared memory with as many tiles as possible
+// (<= 8 warps per CTA), one CTA per SM if a single tile set is that large.
+struct Geometry {
+  int warps, smem;
+  unsigned grid;
+};
+
+template <typename K>
+int geometry(vy_handle* h, K kernel, const TileLayout& L, Geometry& g) {
+  const int per_sm = h->smem_per_sm;
+  int best_w = 1, best_total = 0;
+  for (int w = 1; w <= 8; ++w) {
+    const int bytes = kTablesBytes + w * L.bytes;
+    if (bytes > per_sm - 1024) break;
+    const int blocks = per_sm / (bytes + 1024);
+    const int total = blocks * w;
+    if (blocks >= 1 && total > best_total) {
+      best_total = total;
+      best_w = w;
+    }
+  }
+  g.warps = best_w;
+  g.smem = kTablesBytes + best_w * L.bytes;
+  if (g.smem > per_sm - 1024) return fail(VY_ERR_UNSUPPORTED, "station too large for one shared-memory tile");
+  if (g.smem > 48 * 1024)
+    VY_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem));
+  const int64_t tiles = (h->B + 31) / 32;
+  g.grid = (unsigned)((tiles + best_w - 1) / best_w);
+  return VY_OK;
+}
 
 int upload_profiles(vy_handle* h) {
   std::vector<Profile> all(kMaxProfiles, Profile{1.0, 0.0, 0.0, 0.5, 0.5});
@@ -92,8 +250,7 @@ int vy_create(const vy_tables* t, int64_t batch, int device, vy_handle** out) {
   h->device = device;
   h->B = batch;
   h->t = *t;
-  h->np = n <= 8 ? 8 : n <= 16 ? 16 : n <= 32 ? 32 : 64;
-  if (t->n_nodes > 2 * h->np + 2) {
+  if (t->n_nodes > kMaxNodes) {
     delete h;
     return fail(VY_ERR_UNSUPPORTED, "too many tree nodes for the compiled capacity");
   }
@@ -153,6 +310,10 @@ int vy_create(const vy_tables* t, int64_t batch, int device, vy_handle** out) {
   std::vector<double> dtab(nd);
   for (int a = 0; a < nd; ++a) dtab[a] = (double)(a - t->k) / (double)t->k;
   int rc = cudaSetDevice(device) == cudaSuccess ? VY_OK : fail(VY_ERR_CUDA, "cudaSetDevice failed");
+  if (!rc && cudaDeviceGetAttribute(&h->smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device) != cudaSuccess)
+    rc = fail(VY_ERR_CUDA, "device query failed");
+  if (!rc && cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+    rc = fail(VY_ERR_CUDA, "device query failed");
   const size_t nh = (size_t)t->n_days * 24;
   if (!rc) rc = upload(&h->d_buy, t->buy, nh);
   if (!rc) rc = upload(&h->d_sellg, t->sellg, nh);
@@ -216,7 +377,8 @@ int vy_get_profile(vy_handle* h, int p, double out4[4]) {
 
 int vy_bind(vy_handle* h, const vy_state* s, const vy_outputs* o) {
   if (!h || !s || !o) return fail(VY_ERR_ARG, "null argument");
-  if (s->ld < h->B) return fail(VY_ERR_ARG, "state leading dimension smaller than batch");
+  if (s->ld < ((h->B + 31) / 32) * 32 || s->ld % 32)
+    return fail(VY_ERR_ARG, "state leading dimension must be a multiple of 32 covering the batch");
   if (!s->port_i || !s->port_soc || !s->port_de || !s->port_dtrem || !s->port_meta || !s->step || !s->day ||
       !s->episode || !s->env_seed || !s->akey || !s->b_i || !s->b_soc || !s->ep_profit || !s->ep_reward ||
       !s->ep_missing || !s->ep_energy || !s->ep_overtime || !s->ep_declined || !s->ep_departures)
@@ -238,7 +400,15 @@ static bool infos_bound(const vy_outputs& o) {
 int vy_reset(vy_handle* h, const uint8_t* mask, int32_t episode_mode, const int32_t* inj_day, uint32_t flags,
              void* stream) {
   if (!h || !h->bound) return fail(VY_ERR_STATE, "handle not bound");
-  VY_DISPATCH(h, launch_reset, mask, episode_mode, inj_day, flags, (cudaStream_t)stream);
+  Params P;
+  fill(h, P, false);
+  P.flags = flags;
+  Geometry g;
+  if (int rc = geometry(h, k_reset, P.L, g)) return rc;
+  k_reset<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P, mask, episode_mode, inj_day);
+  VY_CUDA(cudaGetLastError());
+  ++h->launches;
+  return VY_OK;
 }
 
 int vy_seed_envs(vy_handle* h, int64_t master_seed, int64_t index0, void* stream) {
@@ -259,7 +429,20 @@ int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride
   if ((flags & VY_F_INJECT) && (!inj || !inj->off || !inj->profile || !inj->stay || !inj->soc0 || !inj->frac ||
                                 !inj->pref))
     return fail(VY_ERR_ARG, "injected draws missing");
-  VY_DISPATCH(h, launch_step, actions, dtype, row_stride, col_stride, flags, inj, (cudaStream_t)stream);
+  Params P;
+  fill(h, P, false);
+  P.flags = flags;
+  P.actions = actions;
+  P.act_dtype = dtype;
+  P.act_row = row_stride;
+  P.act_col = col_stride;
+  if (inj) P.inj = *inj;
+  Geometry g;
+  if (int rc = geometry(h, k_step, P.L, g)) return rc;
+  k_step<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P);
+  VY_CUDA(cudaGetLastError());
+  ++h->launches;
+  return VY_OK;
 }
 
 int vy_random_actions(vy_handle* h, uint64_t seed, int64_t index0, int64_t call, uint8_t* out, void* stream) {
@@ -279,8 +462,20 @@ int vy_rollout(vy_handle* h, int32_t T, uint64_t policy_seed, int64_t index0, in
   if (!h || !h->bound) return fail(VY_ERR_STATE, "handle not bound");
   if (T < 1 || !obs || !reward || !done) return fail(VY_ERR_ARG, "bad rollout arguments");
   if (flags & (VY_F_INFOS | VY_F_INJECT)) return fail(VY_ERR_UNSUPPORTED, "rollout supports lean outputs only");
-  VY_DISPATCH(h, launch_rollout, T, policy_seed, index0, call0, obs, obs_step_stride, reward, done,
-              rew_step_stride, flags, (cudaStream_t)stream);
+  if (2 * h->t.k + 1 > 256) return fail(VY_ERR_UNSUPPORTED, "rollout needs 2k+1 <= 256");
+  Params P;
+  fill(h, P, true);
+  P.flags = flags;
+  P.out.obs = obs;
+  P.out.reward = reward;
+  P.out.done = done;
+  Geometry g;
+  if (int rc = geometry(h, k_rollout, P.L, g)) return rc;
+  k_rollout<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P, T, policy_seed, index0, call0, obs_step_stride,
+                                                                   rew_step_stride);
+  VY_CUDA(cudaGetLastError());
+  ++h->launches;
+  return VY_OK;
 }
 
 int vy_poll_error(vy_handle* h, int clear, void* stream, uint32_t* out) {

@@ -1,11 +1,12 @@
-// vy_device.cuh — launch parameters and the splitmix64 stream on the device.
+// vy_device.cuh — launch parameters, per-warp tile layout, and the
+// splitmix64 stream on the device.
 //
 // The RNG is the reference's own counter-based stream (rng.py:20-115,
 // _kernel.pyx:19-73): draw j of key k is mix64(k + j*GOLDEN).  Being
 // counter-based, every env regenerates exactly the reference's draws with no
 // sequential host state, so arrivals and the reset day are bit-identical to
-// the CPU reference at any batch size ("reference stream" mode).  An injected
-// draw buffer (vy_draws) can replace the arrival draws (VY_F_INJECT).
+// the CPU reference at any batch size.  An injected draw buffer (vy_draws)
+// can replace the arrival draws (VY_F_INJECT).
 #pragma once
 
 #include <cstdint>
@@ -16,7 +17,11 @@ namespace vy {
 
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
 constexpr uint64_t kKey0 = 0x8C2F9D1B6E4A5533ULL;
+constexpr int kMaxPorts = 64;
+constexpr int kMaxNodes = 2 * kMaxPorts + 2;
 constexpr int kMaxProfiles = 64;  // 6 bits of port_meta
+constexpr int kFastNodes = 4;     // trees up to this many nodes keep node loads in registers
+constexpr uint32_t kFlagStageObs = 0x100u;
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -30,7 +35,7 @@ __device__ __forceinline__ double unit(uint64_t& st) {
   return __dmul_rn((double)(mix64(st) >> 11), 1.0 / 9007199254740992.0);
 }
 __device__ __forceinline__ int below(uint64_t& st, int n) {  // Stream.randint
-  int k = (int)__double2ll_rz(__dmul_rn(unit(st), (double)n));
+  const int k = (int)__double2ll_rz(__dmul_rn(unit(st), (double)n));
   return k >= n ? n - 1 : k;
 }
 // Knuth product of uniforms against a host-computed exp(-lambda) threshold
@@ -43,18 +48,30 @@ __device__ __forceinline__ int knuth(uint64_t& st, double thr) {
     ++k;
   }
 }
+// RandomPolicy draw: row key k, overall draw number j (1-based), hi = 2K+1
+__device__ __forceinline__ int policy_action(uint64_t key, uint64_t j, int hi) {
+  const double u = __dmul_rn((double)(mix64(key + j * kGolden) >> 11), 1.0 / 9007199254740992.0);
+  const int a = (int)__double2ll_rz(__dmul_rn(u, (double)hi));
+  return a >= hi ? hi - 1 : a;
+}
 
 struct Profile {  // car profile: catalogue entry (or injected car)
   double cap, r_ac, r_dc, tau, omt;  // omt = 1.0 - tau, same rounding as the reference's runtime expression
 };
 
-// Everything a launch reads besides state: scalars by value (constant bank),
-// per-port / per-node arrays sized by the template port capacity NP, and
-// device pointers to the long series.
-template <int NP>
+// Byte offsets inside one warp's shared-memory tile (32 envs, lane = env).
+// Per-port fields are [port][lane]; per-env fields [lane].  The float64 port
+// slots (idr/soc/de, 256 B per port each) are reused as the obs staging area
+// once a port has been written back.
+struct TileLayout {
+  int idr, soc, de, dtrem, meta;  // per-port
+  int step, day, akey, b_i, b_soc, ep_f, ep_i;  // per-env (ep_f: 4 x f64, ep_i: 3 x i32)
+  int gobs;   // globals obs staging [9 + horizon][32] f32
+  int extra;  // rollout-only obs staging for port columns [6N][32] f32 (0 if absent)
+  int bytes;
+};
+
 struct Params {
-  static constexpr int NS = NP + 1;
-  static constexpr int NN = 2 * NP + 2;  // node capacity
   // shape
   int n_ports, n_slots, n_nodes, max_passes;
   int k, episode_steps, steps_per_day, dt_min, horizon, obs_len, n_days, lam_len, n_cat;
@@ -65,12 +82,13 @@ struct Params {
   double alphas[8];
   // battery
   double b_volt, b_cap, b_rmax, b_tau, b_omt, b_eta_c, b_eta_d, b_init_soc, b_imax, b_idenom, b_dtv;
-  // ports (index = compile-time port number)
-  double volt[NP], imax_c[NP], imax_d[NP], eta_c[NP], eta_d[NP], i_denom[NP], dtv[NP];
-  int kind[NP], order[NP];
-  // capacity tree: node m sums slots [lo, hi) in order
-  double node_cap[NN], node_eta[NN];
-  int node_lo[NN], node_hi[NN], node_order[NN];
+  // ports
+  double volt[kMaxPorts], imax_c[kMaxPorts], imax_d[kMaxPorts], eta_c[kMaxPorts], eta_d[kMaxPorts];
+  double i_denom[kMaxPorts], dtv[kMaxPorts];
+  int kind[kMaxPorts], order[kMaxPorts];
+  // capacity tree: node m sums slots [lo, hi) in order (battery slot = n_ports, last)
+  double node_cap[kMaxNodes], node_eta[kMaxNodes];
+  int node_lo[kMaxNodes], node_hi[kMaxNodes], node_order[kMaxNodes];
   // series (device)
   const double *buy, *sellg, *moer, *dgrid, *sin_t, *cos_t, *cat_cum;
   const int8_t* weekday;
@@ -86,6 +104,7 @@ struct Params {
   int64_t act_row, act_col;
   vy_draws inj;
   uint32_t* err;
+  TileLayout L;
 };
 
 }  // namespace vy

@@ -1,0 +1,644 @@
+// vy_tile.cuh — the fused environment transition on a shared-memory tile.
+//
+// Semantics: voltyard/backends/_kernel.pyx:239-649 (== pykernel.py:30-429).
+//
+// Mapping.  One thread per environment; a warp owns a tile of 32 consecutive
+// envs.  The tile's per-port state (float64 i_drawn/soc/de, int16 dwell time,
+// uint8 meta) is staged from HBM into the warp's shared-memory tile with
+// 16-byte cp.async copies (port-major [port][lane] columns, so every access
+// below is bank-conflict free), the per-port phases run as *rolled* loops over
+// the runtime port count (one kernel for every station size; the hot code is
+// a few KB instead of a fully unrolled port loop that overflowed the
+// instruction cache), and per-env scalars live in registers.
+//
+// Exactness.  All continuous arithmetic is float64 in the reference's
+// operation order, built with --fmad=false; sums the reference accumulates
+// sequentially (tree node loads, energy flows, satisfaction penalties) are
+// accumulated sequentially here too, in port order.  Each env's trajectory is
+// therefore bit-identical to the reference's compiled kernel.
+#pragma once
+
+#include "vy_device.cuh"
+
+namespace vy {
+
+struct EnvRegs {
+  int step, day;
+  uint64_t akey;
+  double b_i, b_soc;
+  double ep_profit, ep_reward, ep_missing, ep_energy;
+  int ep_overtime, ep_declined, ep_departures;
+};
+
+// one lane's view of its warp's tile
+struct Lane {
+  unsigned char* t;
+  int lane;
+  const TileLayout* L;
+  __device__ __forceinline__ double& idr(int i) const { return *reinterpret_cast<double*>(t + L->idr + i * 256 + lane * 8); }
+  __device__ __forceinline__ double& soc(int i) const { return *reinterpret_cast<double*>(t + L->soc + i * 256 + lane * 8); }
+  __device__ __forceinline__ double& de(int i) const { return *reinterpret_cast<double*>(t + L->de + i * 256 + lane * 8); }
+  __device__ __forceinline__ int16_t& dtrem(int i) const {
+    return *reinterpret_cast<int16_t*>(t + L->dtrem + i * 64 + lane * 2);
+  }
+  __device__ __forceinline__ uint8_t& meta(int i) const { return *(t + L->meta + i * 32 + lane); }
+};
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Warp-cooperative stage-in of a tile's per-port state (HBM -> smem).  Each
+// (field, port) column of 32 envs is one contiguous run in the port-major
+// global layout; lanes copy 16 B each.
+__device__ __forceinline__ void tile_load(const Params& P, unsigned char* t, int64_t b0, int lane) {
+  const int n = P.n_ports;
+  const int64_t ld = P.ld;
+  const TileLayout& L = P.L;
+  const char* f64src[3] = {reinterpret_cast<const char*>(P.st.port_i), reinterpret_cast<const char*>(P.st.port_soc),
+                           reinterpret_cast<const char*>(P.st.port_de)};
+  const int f64dst[3] = {L.idr, L.soc, L.de};
+  const int q16 = (lane & 15) * 16;
+  for (int c = lane >> 4; c < 3 * n; c += 2) {
+    const int f = c / n, i = c - f * n;
+    cp_async16(t + f64dst[f] + i * 256 + q16, f64src[f] + ((int64_t)i * ld + b0) * 8 + q16);
+  }
+  const char* dsrc = reinterpret_cast<const char*>(P.st.port_dtrem);
+  for (int c = lane >> 2; c < n; c += 8)
+    cp_async16(t + L.dtrem + c * 64 + (lane & 3) * 16, dsrc + ((int64_t)c * ld + b0) * 2 + (lane & 3) * 16);
+  const char* msrc = reinterpret_cast<const char*>(P.st.port_meta);
+  for (int c = lane >> 1; c < n; c += 16)
+    cp_async16(t + L.meta + c * 32 + (lane & 1) * 16, msrc + ((int64_t)c * ld + b0) + (lane & 1) * 16);
+  cp_async_wait_all();
+  __syncwarp();
+}
+
+__device__ __forceinline__ void load_env(const Params& P, int64_t b, EnvRegs& E) {
+  const vy_state& s = P.st;
+  E.step = s.step[b];
+  E.day = s.day[b];
+  E.akey = s.akey[b];
+  E.b_i = P.battery ? s.b_i[b] : 0.0;
+  E.b_soc = P.battery ? s.b_soc[b] : 0.0;
+  E.ep_profit = s.ep_profit[b];
+  E.ep_reward = s.ep_reward[b];
+  E.ep_missing = s.ep_missing[b];
+  E.ep_energy = s.ep_energy[b];
+  E.ep_overtime = s.ep_overtime[b];
+  E.ep_declined = s.ep_declined[b];
+  E.ep_departures = s.ep_departures[b];
+}
+
+__device__ __forceinline__ void store_env(const Params& P, int64_t b, const EnvRegs& E, bool reset_too) {
+  const vy_state& s = P.st;
+  s.step[b] = E.step;
+  if (P.battery) {
+    s.b_i[b] = E.b_i;
+    s.b_soc[b] = E.b_soc;
+  }
+  s.ep_profit[b] = E.ep_profit;
+  s.ep_reward[b] = E.ep_reward;
+  s.ep_missing[b] = E.ep_missing;
+  s.ep_energy[b] = E.ep_energy;
+  s.ep_overtime[b] = E.ep_overtime;
+  s.ep_declined[b] = E.ep_declined;
+  s.ep_departures[b] = E.ep_departures;
+  if (reset_too) {
+    s.day[b] = E.day;
+    s.akey[b] = E.akey;
+  }
+}
+
+// charge envelope (vehicles.py:22-35); omt = 1 - tau precomputed with identical rounding
+__device__ __forceinline__ double envelope(double soc, double tau, double omt, double rbar) {
+  return soc <= tau ? rbar : (1.0 - soc) * rbar / omt;
+}
+
+// Clip a requested current (_kernel.pyx:309-325 ports, :329-345 battery).  Charging
+// is bounded by rhat = envelope(soc) (the value the reference stores,
+// _kernel.pyx:389/505), discharging by envelope(1 - soc); one select-based path.
+__device__ __forceinline__ double clip_current(double tgt, double soc, double tau, double omt, double rbar,
+                                               double volt, double imax_c, double imax_d) {
+  const bool chg = tgt >= 0.0;
+  const double s = chg ? soc : 1.0 - soc;
+  const double r = envelope(s, tau, omt, rbar);
+  const double lim = 1000.0 * r / volt;
+  double v = chg ? tgt : -tgt;
+  if (lim < v) v = lim;
+  const double pm = chg ? imax_c : imax_d;
+  if (pm < v) v = pm;
+  return chg ? v : -v;
+}
+
+__device__ __forceinline__ double node_load(double s, double eta) {
+  // x / 1.0 == x and x * 1.0 == x exactly, so unit efficiencies skip the divide
+  if (s > 0.0) return eta == 1.0 ? s : s / eta;
+  return s * eta;
+}
+
+// node m's load sum over its slot range, sequentially in leaf order
+__device__ __forceinline__ double node_sum(const Params& P, const Lane& T, double cb, int m) {
+  const int lo = P.node_lo[m], hi = P.node_hi[m];
+  const int hp = hi < P.n_ports ? hi : P.n_ports;
+  double s = 0.0;
+  for (int j = lo; j < hp; ++j) s += T.idr(j);
+  if (P.battery && lo <= P.n_ports && P.n_ports < hi) s += cb;
+  return s;
+}
+
+// _kernel.pyx:626-649: deepest-first proportional scaling to a fixed point.
+// Currents live in the i_drawn slots (they become i_drawn after the rescale).
+__device__ __noinline__ void fit_tree(const Params& P, const Lane& T, double& cb) {
+  for (int pass = 0; pass < P.max_passes; ++pass) {
+    bool moved = false;
+    for (int q = 0; q < P.n_nodes; ++q) {
+      const int m = P.node_order[q];
+      const double mag = fabs(node_load(node_sum(P, T, cb, m), P.node_eta[m]));
+      if (mag > P.node_cap[m]) {
+        const double f = P.node_cap[m] / mag;
+        const int lo = P.node_lo[m], hi = P.node_hi[m];
+        const int hp = hi < P.n_ports ? hi : P.n_ports;
+        for (int j = lo; j < hp; ++j) {
+          const double v = T.idr(j) * f;
+          if (v != T.idr(j)) {
+            T.idr(j) = v;
+            moved = true;
+          }
+        }
+        if (P.battery && lo <= P.n_ports && P.n_ports < hi) {
+          const double v = cb * f;
+          if (v != cb) {
+            cb = v;
+            moved = true;
+          }
+        }
+      }
+    }
+    if (!moved) return;
+  }
+}
+
+// reset_env (_kernel.pyx:239-261): clear the env's ports and scalars, draw the day.
+__device__ __forceinline__ void reset_env(const Params& P, const Lane& T, EnvRegs& E, uint64_t seed, int episode,
+                                          int inj_day, bool use_inj) {
+  uint64_t st = fold(fold(fold(fold(kKey0, seed), (uint64_t)(int64_t)episode), 0), 0);
+  E.day = use_inj ? inj_day : below(st, P.n_days);
+  E.step = 0;
+  E.akey = fold(fold(fold(kKey0, seed), (uint64_t)(int64_t)episode), 1);
+  for (int i = 0; i < P.n_ports; ++i) {
+    T.idr(i) = T.soc(i) = T.de(i) = 0.0;
+    T.dtrem(i) = 0;
+    T.meta(i) = 0;
+  }
+  E.b_soc = P.battery ? P.b_init_soc : 0.0;
+  E.b_i = 0.0;
+  E.ep_profit = E.ep_reward = E.ep_missing = E.ep_energy = 0.0;
+  E.ep_overtime = E.ep_declined = E.ep_departures = 0;
+}
+
+struct StepResult {
+  double reward;
+  bool done;
+};
+
+// One transition of one env (_kernel.pyx:283-571).  `act(slot)` returns the
+// action index of a slot; `b` is the global env index (infos / injected draws).
+template <class Act>
+__device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* __restrict__ prof,
+                                                const double* __restrict__ dtab, const Lane& T, EnvRegs& E,
+                                                int64_t b, Act act) {
+  const int n = P.n_ports;
+  const int64_t ld = P.ld;
+  const bool info = P.flags & VY_F_INFOS;
+  const vy_outputs& O = P.out;
+  const int t = E.step;
+
+  // frame (_kernel.pyx:289-295)
+  const int64_t minutes = (int64_t)t * P.dt_min;
+  const int eff_day = (int)(((int64_t)E.day + minutes / 1440) % P.n_days);
+  const int hidx = eff_day * 24 + (int)((minutes / 60) % 24);
+  const double p_buy = __ldg(P.buy + hidx), p_sg = __ldg(P.sellg + hidx);
+  const int lam_idx = (__ldg(P.weekday + eff_day) ? 0 : P.lam_len) + t % P.lam_len;
+
+  // phase 1: apply actions (_kernel.pyx:297-356); the clipped current replaces
+  // i_drawn in its smem slot, node loads accumulate in leaf order on the fly
+  const int hi_a = 2 * P.k;
+  auto delta_of = [&](int a) -> double {
+    if (a < 0 || a > hi_a) {
+      atomicOr(P.err, 1u);
+      a = a < 0 ? 0 : hi_a;
+    }
+    return dtab ? dtab[a] : (double)(a - P.k) / (double)P.k;
+  };
+  const bool fast = P.n_nodes <= kFastNodes;
+  double nsum[kFastNodes];
+#pragma unroll
+  for (int m = 0; m < kFastNodes; ++m) nsum[m] = 0.0;
+#pragma unroll 1
+  for (int i = 0; i < n; ++i) {
+    const double d = delta_of(act(i));
+    const uint32_t mt = T.meta(i);
+    double c = 0.0;
+    if (mt & 1u) {
+      double tgt = T.idr(i) + d * P.imax_c[i];
+      if (!P.allow_discharge && tgt < 0.0) tgt = 0.0;
+      const Profile& pr = prof[mt >> 2];
+      c = clip_current(tgt, T.soc(i), pr.tau, pr.omt, P.kind[i] ? pr.r_dc : pr.r_ac, P.volt[i], P.imax_c[i],
+                       P.imax_d[i]);
+    }
+    T.idr(i) = c;
+    if (info) O.i_att[i * ld + b] = c;
+    if (fast) {
+#pragma unroll
+      for (int m = 0; m < kFastNodes; ++m)
+        if (m < P.n_nodes && i >= P.node_lo[m] && i < P.node_hi[m]) nsum[m] += c;
+    }
+  }
+  double cb = 0.0;
+  {
+    // the battery slot is validated even when the battery is disabled (engine.py:440-442)
+    const double d = delta_of(act(n));
+    if (P.battery) {
+      const double tgt = E.b_i + d * P.b_imax;
+      cb = clip_current(tgt, E.b_soc, P.b_tau, P.b_omt, P.b_rmax, P.b_volt, P.b_imax, P.b_imax);
+      if (info) O.i_att[n * ld + b] = cb;
+      if (fast) {
+#pragma unroll
+        for (int m = 0; m < kFastNodes; ++m)
+          if (m < P.n_nodes && P.node_lo[m] <= n && n < P.node_hi[m]) nsum[m] += cb;
+      }
+    }
+  }
+  // tree: excess on the requested currents (_kernel.pyx:611-624), then rescale
+  double excess = 0.0;
+  if (fast) {
+#pragma unroll
+    for (int m = 0; m < kFastNodes; ++m) {
+      if (m < P.n_nodes) {
+        const double over = fabs(node_load(nsum[m], P.node_eta[m])) - P.node_cap[m];
+        if (over > excess) excess = over;
+      }
+    }
+  } else {
+    for (int m = 0; m < P.n_nodes; ++m) {
+      const double over = fabs(node_load(node_sum(P, T, cb, m), P.node_eta[m])) - P.node_cap[m];
+      if (over > excess) excess = over;
+    }
+  }
+  // no node over capacity => the reference's first rescale pass changes nothing and returns
+  if (excess > 0.0) fit_tree(P, T, cb);
+  if (info) {
+    for (int i = 0; i < n; ++i) O.i_used[i * ld + b] = T.idr(i);
+    if (P.battery) O.i_used[n * ld + b] = cb;
+  }
+  if (P.battery) E.b_i = cb;
+
+  // phases 2+3: charge (_kernel.pyx:358-424), dwell countdown (:420-422) and
+  // departures (:426-458) fused into one pass in port order
+  double e_net = 0.0, e_in = 0.0, e_out = 0.0;
+  double sat0 = 0.0, sat1 = 0.0;
+  int nd = 0;
+  uint64_t occm = 0;
+#pragma unroll 1
+  for (int i = 0; i < n; ++i) {
+    const uint32_t mt = T.meta(i);
+    double got = 0.0;
+    if (mt & 1u) {
+      const double cap = prof[mt >> 2].cap;
+      const double cur = T.idr(i), soc0 = T.soc(i), de0 = T.de(i);
+      const double raw = P.dtv[i] * cur / 1000.0;
+      got = raw;
+      if (raw >= 0.0) {
+        if (de0 < got) got = de0;
+        const double room = cap * (1.0 - soc0);
+        if (room < got) got = room;
+      } else {
+        const double fl = -cap * soc0;
+        if (got < fl) got = fl;
+      }
+      double soc = soc0 + got / cap;
+      soc = soc < 0.0 ? 0.0 : (soc > 1.0 ? 1.0 : soc);
+      double de = de0 - got;
+      de = de < 0.0 ? 0.0 : de;
+      e_net += got;
+      if (got > 0.0)
+        e_in += P.eta_c[i] == 1.0 ? got : got / P.eta_c[i];
+      else if (got < 0.0)
+        e_out += got * P.eta_d[i];
+      const int dt = T.dtrem(i) - 1;
+      const int p = (mt >> 1) & 1u;
+      if ((p == 0 && dt <= 0) || (p == 1 && de == 0.0)) {
+        const int over = dt < 0 ? -dt : 0, early = dt > 0 ? dt : 0;
+        if (info) {
+          const int64_t at = (int64_t)nd * ld + b;
+          O.dep_port[at] = i;
+          O.dep_missing[at] = de;
+          O.dep_overtime[at] = over;
+          O.dep_early[at] = early;
+          O.dep_pref[at] = p;
+          O.dep_cap[at] = cap;
+          O.dep_soc[at] = soc;
+        }
+        if (p == 0)
+          sat0 += de;
+        else
+          sat1 += (double)over - P.beta * (double)early;
+        E.ep_missing += de;
+        E.ep_overtime += over;
+        E.ep_departures += 1;
+        T.meta(i) = 0;
+        T.idr(i) = T.soc(i) = T.de(i) = 0.0;
+        T.dtrem(i) = 0;
+        ++nd;
+      } else {
+        T.soc(i) = soc;
+        T.de(i) = de;
+        T.dtrem(i) = (int16_t)dt;
+        occm |= 1ull << i;
+      }
+    }
+    if (info) O.delivered[i * ld + b] = got;
+  }
+  double e_b = 0.0, bgot = 0.0;
+  if (P.battery) {
+    bgot = P.b_dtv * E.b_i / 1000.0;
+    if (bgot >= 0.0) {
+      const double room = P.b_cap * (1.0 - E.b_soc);
+      if (room < bgot) bgot = room;
+    } else {
+      const double fl = -P.b_cap * E.b_soc;
+      if (bgot < fl) bgot = fl;
+    }
+    const double soc = E.b_soc + bgot / P.b_cap;
+    E.b_soc = soc < 0.0 ? 0.0 : (soc > 1.0 ? 1.0 : soc);
+    e_b = bgot > 0.0 ? bgot / P.b_eta_c : bgot * P.b_eta_d;
+  }
+  if (info) {
+    O.b_delivered[b] = bgot;
+    O.dep_n[b] = nd;
+  }
+  const double e_grid_net = e_in + e_out + e_b;
+
+  // phase 4: arrivals (_kernel.pyx:460-509); draws of Stream(key4(seed, ep, 1, t))
+  uint64_t st = fold(E.akey, (uint64_t)(int64_t)t);
+  const bool inj = P.flags & VY_F_INJECT;
+  int m = 0;
+  int64_t inj0 = 0;
+  if (inj) {
+    inj0 = P.inj.off[b];
+    m = P.inj.off[b + 1] - (int)inj0;
+  } else {
+    const int full = __ldg(P.pois_full + lam_idx);
+    if (full >= 0) {
+      for (int c = 0; c < full; ++c) m += knuth(st, P.thr32);
+      m += knuth(st, __ldg(P.pois_thr + lam_idx));
+    }
+  }
+  const int nfree = n - __popcll(occm);
+  const int admitted = m < nfree ? m : nfree;
+  const int declined = m - admitted;
+  for (int j = 0; j < m; ++j) {
+    int car, stay;
+    double soc0, frac;
+    uint32_t pref;
+    if (inj) {
+      car = P.inj.profile[inj0 + j];
+      stay = P.inj.stay[inj0 + j];
+      soc0 = P.inj.soc0[inj0 + j];
+      frac = P.inj.frac[inj0 + j];
+      pref = P.inj.pref[inj0 + j] ? 1u : 0u;
+    } else {
+      const double u = unit(st);
+      car = P.n_cat - 1;
+      for (int e = 0; e < P.n_cat - 1; ++e)
+        if (u < __ldg(P.cat_cum + e)) {
+          car = e;
+          break;
+        }
+      stay = P.stay_lo + below(st, P.stay_span);
+      soc0 = P.soc_lo + unit(st) * P.soc_span;
+      frac = P.frac_lo + unit(st) * P.frac_span;
+      pref = unit(st) < P.p_charge ? 1u : 0u;
+    }
+    if (j >= admitted) continue;
+    const uint64_t freem = ~occm & (n == 64 ? ~0ull : ((1ull << n) - 1));
+    int port = 0;
+    if (P.order_identity) {
+      port = __ffsll((long long)freem) - 1;
+    } else {
+      for (int q = 0; q < n; ++q)
+        if ((freem >> P.order[q]) & 1ull) {
+          port = P.order[q];
+          break;
+        }
+    }
+    occm |= 1ull << port;
+    T.meta(port) = (uint8_t)(1u | (pref << 1) | ((uint32_t)car << 2));
+    T.idr(port) = 0.0;
+    T.soc(port) = soc0;
+    T.de(port) = frac * prof[car].cap * (1.0 - soc0);
+    T.dtrem(port) = (int16_t)stay;
+  }
+  E.ep_declined += declined;
+  if (info) {
+    O.arrivals_m[b] = m;
+    O.declined[b] = declined;
+  }
+
+  // reward (_kernel.pyx:511-551)
+  const double price = e_grid_net > 0.0 ? p_buy : p_sg;
+  const double profit = P.p_sell * e_net - price * e_grid_net - P.c_dt;
+  double c[8];
+  c[0] = excess;
+  c[1] = sat0;
+  c[2] = sat1;
+  c[3] = P.has_moer ? __ldg(P.moer + hidx) * e_grid_net : 0.0;
+  c[4] = (double)declined;
+  c[5] = e_b < 0.0 ? -e_b : 0.0;
+  c[6] = e_out < 0.0 ? -e_out : 0.0;
+  if (P.has_dgrid) {
+    const double d = e_net - __ldg(P.dgrid + hidx);
+    c[7] = d >= 0.0 ? d : -d;
+  } else {
+    c[7] = 0.0;
+  }
+  double reward = profit;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) reward -= P.alphas[q] * c[q];
+  if (info) {
+    O.breakdown[b] = profit;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) O.breakdown[(q + 1) * ld + b] = c[q];
+    O.breakdown[9 * ld + b] = reward;
+    O.flows[b] = e_net;
+    O.flows[ld + b] = e_in;
+    O.flows[2 * ld + b] = e_out;
+    O.flows[3 * ld + b] = e_b;
+    O.flows[4 * ld + b] = e_grid_net;
+  }
+  E.ep_profit += profit;
+  E.ep_reward += reward;
+  E.ep_energy += e_net;
+
+  // advance (_kernel.pyx:553-570)
+  E.step = t + 1;
+  const bool done = t + 1 == P.episode_steps;
+  if (done || info) {
+    int tover = 0;
+    if (done) {
+      for (int i = 0; i < n; ++i)
+        if ((T.meta(i) & 3u) == 3u && T.dtrem(i) < 0) tover += -T.dtrem(i);
+      double* es = O.ep_stats;
+      es[b] = E.ep_profit;
+      es[ld + b] = E.ep_reward;
+      es[2 * ld + b] = E.ep_missing;
+      es[3 * ld + b] = (double)E.ep_overtime;
+      es[4 * ld + b] = (double)E.ep_declined;
+      es[5 * ld + b] = E.ep_energy;
+      es[6 * ld + b] = (double)E.ep_departures;
+      es[7 * ld + b] = (double)tover;
+    }
+    O.term_overtime[b] = tover;
+  }
+  return {reward, done};
+}
+
+// ---- observation (_kernel.pyx:575-607; layout config.py:99-130) ----------------
+
+// calendar position of the env's current step
+struct Cal {
+  int eff_day, hidx, sod;
+};
+__device__ __forceinline__ Cal calendar(const Params& P, int step, int day) {
+  const int64_t minutes = (int64_t)step * P.dt_min;
+  Cal c;
+  c.eff_day = (int)(((int64_t)day + minutes / 1440) % P.n_days);
+  c.hidx = c.eff_day * 24 + (int)((minutes / 60) % 24);
+  c.sod = step % P.steps_per_day;
+  return c;
+}
+
+// the six per-port features, exact float64 values
+__device__ __forceinline__ void port_features(const Params& P, const Profile* prof, int i, uint32_t mt, double idr,
+                                              double soc, double de, int dtrem, double v[6]) {
+  const bool occ = mt & 1u;
+  v[0] = occ ? 1.0 : 0.0;
+  v[1] = idr == 0.0 ? idr : idr / P.i_denom[i];
+  v[2] = soc;
+  v[3] = occ ? (de == 0.0 ? de : de / prof[mt >> 2].cap) : 0.0;
+  v[4] = dtrem == 0 ? 0.0 : (double)dtrem / (double)P.episode_steps;
+  v[5] = (double)((mt >> 1) & 1u);
+}
+
+// globals: battery [soc, I/Imax], [buy, sellg, p_sell, sin, cos, weekday, day/365], horizon
+__device__ __forceinline__ double global_feature(const Params& P, const EnvRegs& E, const Cal& C, int k) {
+  switch (k) {
+    case 0: return E.b_soc;
+    case 1: return E.b_i == 0.0 ? E.b_i : E.b_i / P.b_idenom;
+    case 2: return __ldg(P.buy + C.hidx);
+    case 3: return __ldg(P.sellg + C.hidx);
+    case 4: return P.p_sell;
+    case 5: return __ldg(P.sin_t + C.sod);
+    case 6: return __ldg(P.cos_t + C.sod);
+    case 7: return (double)__ldg(P.weekday + C.eff_day);
+    case 8: return (double)C.eff_day / 365.0;
+    default: {
+      const int h = k - 9;
+      const int64_t fmin = (int64_t)(E.step + 1 + h) * P.dt_min;
+      const int64_t fday = ((int64_t)E.day + fmin / 1440) % P.n_days;
+      return __ldg(P.buy + fday * 24 + (fmin / 60) % 24);
+    }
+  }
+}
+
+// Staged obs cell (row = lane, col c) of the warp tile.  Port columns live in
+// the port's float64 slots (in place, after write-back) or in the extra
+// region; the row index is rotated by the column so that both the per-lane
+// writes (fixed c) and the row-major read-out (consecutive c) are conflict free.
+__device__ __forceinline__ float* obs_cell(unsigned char* t, const TileLayout& L, bool in_place, int r, int c,
+                                           int n) {
+  const int rot = ((r + c) & 31) * 4;
+  if (c < 6 * n) {
+    const int i = c / 6, f = c - 6 * i;
+    int base;
+    if (in_place)
+      base = (f < 2 ? L.idr : f < 4 ? L.soc : L.de) + i * 256 + (f & 1) * 128;
+    else
+      base = L.extra + c * 128;
+    return reinterpret_cast<float*>(t + base + rot);
+  }
+  return reinterpret_cast<float*>(t + L.gobs + (c - 6 * n) * 128 + rot);
+}
+
+// Write this tile's obs rows (and, with store_state, the port state back to
+// HBM).  float32 obs are staged and leave with row-major coalesced stores;
+// float64 obs (exact drop-in mode) are written per lane.
+__device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, const Lane& T, const EnvRegs& E,
+                                         int64_t b0, bool active, void* obs_base, bool store_state, bool in_place) {
+  const int n = P.n_ports;
+  const int lane = T.lane;
+  const int64_t b = b0 + lane;
+  const int64_t ld = P.ld;
+  const int OL = P.obs_len;
+  const bool f64 = P.flags & VY_F_OUT_F64;
+  const Cal C = calendar(P, E.step, E.day);
+  double* row64 = f64 ? reinterpret_cast<double*>(obs_base) + b * OL : nullptr;
+#pragma unroll 1
+  for (int i = 0; i < n; ++i) {
+    const uint32_t mt = T.meta(i);
+    const double idr = T.idr(i), soc = T.soc(i), de = T.de(i);
+    const int dt = T.dtrem(i);
+    if (store_state && active) {
+      const vy_state& s = P.st;
+      s.port_i[i * ld + b] = idr;
+      s.port_soc[i * ld + b] = soc;
+      s.port_de[i * ld + b] = de;
+      s.port_dtrem[i * ld + b] = (int16_t)dt;
+      s.port_meta[i * ld + b] = (uint8_t)mt;
+    }
+    double v[6];
+    port_features(P, prof, i, mt, idr, soc, de, dt, v);
+    if (f64) {
+      if (active)
+#pragma unroll
+        for (int f = 0; f < 6; ++f) row64[6 * i + f] = v[f];
+    } else {
+      if (in_place) __syncwarp();  // every lane has read port i before its slots are reused
+#pragma unroll
+      for (int f = 0; f < 6; ++f) *obs_cell(T.t, *T.L, in_place, lane, 6 * i + f, n) = (float)v[f];
+    }
+  }
+  const int ng = OL - 6 * n;
+  for (int k = 0; k < ng; ++k) {
+    const double g = global_feature(P, E, C, k);
+    if (f64) {
+      if (active) row64[6 * n + k] = g;
+    } else {
+      *obs_cell(T.t, *T.L, in_place, lane, 6 * n + k, n) = (float)g;
+    }
+  }
+  if (f64) return;
+  __syncwarp();
+  // row-major read-out: element e of the warp's [32][OL] block
+  float* gobs = reinterpret_cast<float*>(obs_base) + b0 * OL;
+  const int64_t left = P.B - b0;
+  const int rows = left >= 32 ? 32 : (int)left;
+  const int total = rows * OL;
+  int r = lane / OL, c = lane - (lane / OL) * OL;
+  for (int e = lane; e < total; e += 32) {
+    gobs[e] = *obs_cell(T.t, *T.L, in_place, r, c, n);
+    c += 32;
+    while (c >= OL) {
+      c -= OL;
+      ++r;
+    }
+  }
+  __syncwarp();
+}
+
+}  // namespace vy
