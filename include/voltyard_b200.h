@@ -205,6 +205,12 @@ int vy_poll_error(vy_handle *h, int clear, void *stream, uint32_t *out);
 /* Number of kernel launches issued through this handle (for bench accounting). */
 int64_t vy_launch_count(vy_handle *h);
 
+/* Diagnostics: compare the kernels' reciprocal-based division (div_rcp in
+ * csrc/vy_device.cuh) with IEEE x / d on `samples_per_divisor` random
+ * dividends for each divisor; *mismatches receives the count (0 = bit-exact). */
+int vy_selftest_div(const double *divisors, int32_t nd, int64_t samples_per_divisor, uint64_t seed,
+                    int64_t *mismatches);
+
 #ifdef __cplusplus
 }
 #endif

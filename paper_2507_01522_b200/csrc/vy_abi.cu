@@ -52,6 +52,26 @@ __global__ void k_random_actions(uint64_t seed, int64_t index0, int64_t call, in
   for (int s = 0; s < ns; ++s) out[b * ns + s] = (uint8_t)policy_action(key, j0 + s + 1, hi);
 }
 
+// div_rcp vs IEEE division on random dividends spread over 2^-64..2^64
+__global__ void k_selftest_div(const double* d, const double* y, int nd, int64_t per, uint64_t seed,
+                               unsigned long long* bad) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long local = 0;
+  for (int64_t s = gid; s < per * nd; s += stride) {
+    const int k = (int)(s % nd);
+    const uint64_t bits = mix64(seed + (uint64_t)s * kGolden);
+    const uint64_t mant = bits & 0xFFFFFFFFFFFFFull;
+    const uint64_t ex = 1023 - 64 + ((bits >> 52) & 127);  // exponents 2^-64 .. 2^63
+    const uint64_t sign = bits & 0x8000000000000000ull;
+    const double x = __longlong_as_double((long long)(sign | (ex << 52) | mant));
+    const double want = __ddiv_rn(x, d[k]);
+    const double got = div_rcp(x, d[k], y[k]);
+    if (__double_as_longlong(want) != __double_as_longlong(got)) ++local;
+  }
+  if (local) atomicAdd(bad, local);
+}
+
 __global__ void k_seed_envs(uint64_t master, int64_t index0, int64_t B, uint64_t* env_seed) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B) env_seed[b] = fold(fold(kKey0, master), (uint64_t)(index0 + b));
@@ -83,33 +103,29 @@ struct vy_handle {
 
 namespace {
 
-// per-warp tile layout; `extra` reserves rollout-only obs staging for port columns
-TileLayout tile_layout(const vy_tables& t, bool rollout) {
+// per-warp tile layout (see TileLayout); rollouts get a separate obs area
+TileLayout tile_layout(const vy_tables& t, bool rollout, bool acts) {
   TileLayout L{};
   const int n = t.n_ports;
-  int off = 0;
-  L.idr = off;
-  off += n * 256;
-  L.soc = off;
-  off += n * 256;
-  L.de = off;
-  off += n * 256;
+  int off = n * 768 + (9 + t.horizon) * 128;  // port f64 slots, then global obs columns
   L.dtrem = off;
   off += n * 64;
   L.meta = off;
-  off += ((n * 32) + 127) & ~127;
-  L.gobs = off;
-  off += (9 + t.horizon) * 128;
-  L.extra = 0;
+  off += ((n * 32) + 15) & ~15;
+  L.acts = off;
+  if (acts) off += ((32 * (n + 1)) + 15) & ~15;
+  L.obs = 0;
   if (rollout) {
-    L.extra = off;
-    off += 6 * n * 128;
+    L.obs = (off + 127) & ~127;
+    off = L.obs + t.obs_len * 128;
   }
   L.bytes = (off + 127) & ~127;
   return L;
 }
 
-void fill(vy_handle* h, Params& P, bool rollout) {
+double rcp(double d) { return 1.0 / d; }
+
+void fill(vy_handle* h, Params& P, bool rollout, bool acts) {
   const vy_tables& t = h->t;
   std::memset(&P, 0, sizeof(P));
   P.n_ports = t.n_ports;
@@ -156,6 +172,14 @@ void fill(vy_handle* h, Params& P, bool rollout) {
   P.b_imax = t.b_imax;
   P.b_idenom = t.b_idenom;
   P.b_dtv = t.dt_h * t.b_volt;
+  P.b_rcp_volt = rcp(t.b_volt);
+  P.b_rcp_cap = rcp(t.b_cap);
+  P.b_rcp_omt = rcp(P.b_omt);
+  P.b_rcp_eta_c = rcp(t.b_eta_c);
+  P.b_rcp_idenom = rcp(t.b_idenom);
+  P.rcp_1000 = rcp(1000.0);
+  P.rcp_ep = rcp((double)t.episode_steps);
+  P.rcp_365 = rcp(365.0);
   for (int i = 0; i < t.n_ports; ++i) {
     P.volt[i] = h->volt[i];
     P.imax_c[i] = h->imax_c[i];
@@ -166,13 +190,25 @@ void fill(vy_handle* h, Params& P, bool rollout) {
     P.dtv[i] = t.dt_h * h->volt[i];  // (dt_h * V) * I / 1000 evaluates left to right (_kernel.pyx:366)
     P.kind[i] = h->kind[i];
     P.order[i] = h->order[i];
+    P.rcp_volt[i] = rcp(h->volt[i]);
+    P.rcp_eta_c[i] = rcp(h->eta_c[i]);
+    P.rcp_i_denom[i] = rcp(h->i_denom[i]);
+    uint32_t mask = 0;
+    for (int m = 0; m < t.n_nodes && m < kFastNodes; ++m)
+      if (h->node_lo[m] <= i && i < h->node_hi[m]) mask |= 1u << m;
+    P.port_nodes[i] = t.n_nodes <= kFastNodes ? mask : 0u;
   }
+  P.battery_node_mask = 0;
+  if (t.battery_enabled && t.n_nodes <= kFastNodes)
+    for (int m = 0; m < t.n_nodes; ++m)
+      if (h->node_lo[m] <= t.n_ports && t.n_ports < h->node_hi[m]) P.battery_node_mask |= 1 << m;
   for (int m = 0; m < t.n_nodes; ++m) {
     P.node_cap[m] = h->node_cap[m];
     P.node_eta[m] = h->node_eta[m];
     P.node_lo[m] = h->node_lo[m];
     P.node_hi[m] = h->node_hi[m];
     P.node_order[m] = h->node_order[m];
+    P.node_rcp_eta[m] = rcp(h->node_eta[m]);
   }
   P.buy = h->d_buy;
   P.sellg = h->d_sellg;
@@ -189,7 +225,8 @@ void fill(vy_handle* h, Params& P, bool rollout) {
   P.st = h->st;
   P.out = h->out;
   P.err = h->d_err;
-  P.L = tile_layout(t, rollout);
+  P.act_tile = acts;
+  P.L = tile_layout(t, rollout, acts);
 }
 
 // Warps per CTA: fill the SM's shared memory with as many tiles as possible
@@ -223,8 +260,13 @@ int geometry(vy_handle* h, K kernel, const TileLayout& L, Geometry& g) {
   return VY_OK;
 }
 
+Profile make_profile(double cap, double r_ac, double r_dc, double tau) {
+  const double omt = 1.0 - tau;
+  return Profile{cap, r_ac, r_dc, tau, omt, 1.0 / cap, 1.0 / omt, 0.0};
+}
+
 int upload_profiles(vy_handle* h) {
-  std::vector<Profile> all(kMaxProfiles, Profile{1.0, 0.0, 0.0, 0.5, 0.5});
+  std::vector<Profile> all(kMaxProfiles, Profile{1.0, 0.0, 0.0, 0.5, 0.5, 1.0, 2.0, 0.0});
   for (size_t i = 0; i < h->profiles.size(); ++i) all[i] = h->profiles[i];
   VY_CUDA(cudaMemcpy(h->d_prof, all.data(), sizeof(Profile) * kMaxProfiles, cudaMemcpyHostToDevice));
   return VY_OK;
@@ -287,7 +329,7 @@ int vy_create(const vy_tables* t, int64_t batch, int device, vy_handle** out) {
     h->node_order.push_back(t->node_order[m]);
   }
   for (int c = 0; c < t->n_cat; ++c)
-    h->profiles.push_back(Profile{t->cat_cap[c], t->cat_rac[c], t->cat_rdc[c], t->cat_tau[c], 1.0 - t->cat_tau[c]});
+    h->profiles.push_back(make_profile(t->cat_cap[c], t->cat_rac[c], t->cat_rdc[c], t->cat_tau[c]));
   // Poisson: per (weekday flag, step-of-profile) the number of full 32-chunks and the
   // threshold of the last chunk, reproducing rng.py:94-115 / _kernel.pyx:55-73 on the host.
   const int L = t->lam_len;
@@ -361,7 +403,7 @@ int vy_add_profile(vy_handle* h, double cap, double r_ac, double r_dc, double ta
     const Profile& p = h->profiles[i];
     if (p.cap == cap && p.r_ac == r_ac && p.r_dc == r_dc && p.tau == tau) return (int)i;
   }
-  h->profiles.push_back(Profile{cap, r_ac, r_dc, tau, 1.0 - tau});
+  h->profiles.push_back(make_profile(cap, r_ac, r_dc, tau));
   if (upload_profiles(h)) return -1;
   return (int)h->profiles.size() - 1;
 }
@@ -401,7 +443,7 @@ int vy_reset(vy_handle* h, const uint8_t* mask, int32_t episode_mode, const int3
              void* stream) {
   if (!h || !h->bound) return fail(VY_ERR_STATE, "handle not bound");
   Params P;
-  fill(h, P, false);
+  fill(h, P, false, false);
   P.flags = flags;
   Geometry g;
   if (int rc = geometry(h, k_reset, P.L, g)) return rc;
@@ -429,8 +471,14 @@ int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride
   if ((flags & VY_F_INJECT) && (!inj || !inj->off || !inj->profile || !inj->stay || !inj->soc0 || !inj->frac ||
                                 !inj->pref))
     return fail(VY_ERR_ARG, "injected draws missing");
+  // stage the action block per tile when it is the canonical uint8 [B][n+1] row-major
+  // layout: 16-byte aligned per tile and over-reading whole chunks stays in bounds
+  const int na = h->t.n_ports + 1;
+  const bool acts = dtype == VY_ACT_U8 && col_stride == 1 && row_stride == na &&
+                    (reinterpret_cast<uintptr_t>(actions) % 16) == 0 && (32 * na) % 16 == 0 &&
+                    (h->B % 32) == 0;
   Params P;
-  fill(h, P, false);
+  fill(h, P, false, acts);
   P.flags = flags;
   P.actions = actions;
   P.act_dtype = dtype;
@@ -464,7 +512,7 @@ int vy_rollout(vy_handle* h, int32_t T, uint64_t policy_seed, int64_t index0, in
   if (flags & (VY_F_INFOS | VY_F_INJECT)) return fail(VY_ERR_UNSUPPORTED, "rollout supports lean outputs only");
   if (2 * h->t.k + 1 > 256) return fail(VY_ERR_UNSUPPORTED, "rollout needs 2k+1 <= 256");
   Params P;
-  fill(h, P, true);
+  fill(h, P, true, false);
   P.flags = flags;
   P.out.obs = obs;
   P.out.reward = reward;
@@ -487,5 +535,31 @@ int vy_poll_error(vy_handle* h, int clear, void* stream, uint32_t* out) {
 }
 
 int64_t vy_launch_count(vy_handle* h) { return h ? h->launches : -1; }
+
+int vy_selftest_div(const double* divisors, int32_t nd, int64_t samples_per_divisor, uint64_t seed,
+                    int64_t* mismatches) {
+  if (!divisors || nd < 1 || samples_per_divisor < 1 || !mismatches) return fail(VY_ERR_ARG, "bad arguments");
+  std::vector<double> y(nd);
+  for (int i = 0; i < nd; ++i) {
+    if (!(divisors[i] > 0.0)) return fail(VY_ERR_ARG, "divisors must be positive");
+    y[i] = 1.0 / divisors[i];
+  }
+  double *dd = nullptr, *dy = nullptr;
+  unsigned long long* dbad = nullptr;
+  int rc = upload(&dd, divisors, (size_t)nd);
+  if (!rc) rc = upload(&dy, y.data(), (size_t)nd);
+  if (!rc) rc = upload<unsigned long long>(&dbad, nullptr, 1);
+  if (!rc && cudaMemset(dbad, 0, 8) != cudaSuccess) rc = fail(VY_ERR_CUDA, "memset");
+  if (!rc) {
+    k_selftest_div<<<148 * 8, 256>>>(dd, dy, nd, samples_per_divisor, seed, dbad);
+    unsigned long long bad = 0;
+    if (cudaMemcpy(&bad, dbad, 8, cudaMemcpyDeviceToHost) != cudaSuccess) rc = fail(VY_ERR_CUDA, "selftest failed");
+    *mismatches = (int64_t)bad;
+  }
+  cudaFree(dd);
+  cudaFree(dy);
+  cudaFree(dbad);
+  return rc;
+}
 
 }  // extern "C"

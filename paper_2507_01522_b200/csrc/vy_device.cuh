@@ -55,19 +55,37 @@ __device__ __forceinline__ int policy_action(uint64_t key, uint64_t j, int hi) {
   return a >= hi ? hi - 1 : a;
 }
 
+// x / d for a divisor d > 0 known ahead of time, with y = RN(1/d) precomputed:
+// q = RN(x*y) is within 1 ulp of x/d, r = x - q*d is exact (FMA), and
+// RN(q + r*y) is the correctly rounded quotient (Markstein's theorem for a
+// correctly rounded reciprocal; no under/overflow in this model's ranges).
+// Bit-identical to IEEE x / d, checked exhaustively-by-sampling by
+// vy_selftest_div (tests/test_gpu_numerics.py).  Zeros keep their sign.
+__device__ __forceinline__ double div_rcp(double x, double d, double y) {
+  const double q = __dmul_rn(x, y);
+  const double r = __fma_rn(-q, d, x);
+  const double z = __fma_rn(r, y, q);
+  return x == 0.0 ? x : z;
+}
+
 struct Profile {  // car profile: catalogue entry (or injected car)
   double cap, r_ac, r_dc, tau, omt;  // omt = 1.0 - tau, same rounding as the reference's runtime expression
+  double rcp_cap, rcp_omt;           // RN(1/cap), RN(1/omt)
+  double pad;
 };
 
 // Byte offsets inside one warp's shared-memory tile (32 envs, lane = env).
 // Per-port fields are [port][lane]; per-env fields [lane].  The float64 port
 // slots (idr/soc/de, 256 B per port each) are reused as the obs staging area
 // once a port has been written back.
+//   [port][idr, soc, de][lane] f64   n x 768 B  (port i at i*768)
+//   global obs columns [9 + H][lane] f32 right after, so in the step kernel
+//   obs column c (any c < obs_len) is staged at c*128 (port slots reused);
+//   dwell [port][lane] i16, meta [port][lane] u8, actions [lane][n+1] u8;
+//   rollout only: a separate obs staging area (state stays resident).
 struct TileLayout {
-  int idr, soc, de, dtrem, meta;  // per-port
-  int step, day, akey, b_i, b_soc, ep_f, ep_i;  // per-env (ep_f: 4 x f64, ep_i: 3 x i32)
-  int gobs;   // globals obs staging [9 + horizon][32] f32
-  int extra;  // rollout-only obs staging for port columns [6N][32] f32 (0 if absent)
+  int dtrem, meta, acts;
+  int obs;    // byte offset of obs column 0 (0 in-place; `extra` area for rollouts)
   int bytes;
 };
 
@@ -82,12 +100,18 @@ struct Params {
   double alphas[8];
   // battery
   double b_volt, b_cap, b_rmax, b_tau, b_omt, b_eta_c, b_eta_d, b_init_soc, b_imax, b_idenom, b_dtv;
+  double b_rcp_volt, b_rcp_cap, b_rcp_omt, b_rcp_eta_c, b_rcp_idenom;
+  double rcp_1000, rcp_ep, rcp_365;
+  int battery_node_mask;  // bit m: battery slot in node m's range (m < kFastNodes)
+  int act_tile;           // actions are row-major uint8 [B][n+1], staged per tile
   // ports
   double volt[kMaxPorts], imax_c[kMaxPorts], imax_d[kMaxPorts], eta_c[kMaxPorts], eta_d[kMaxPorts];
   double i_denom[kMaxPorts], dtv[kMaxPorts];
+  double rcp_volt[kMaxPorts], rcp_eta_c[kMaxPorts], rcp_i_denom[kMaxPorts];
   int kind[kMaxPorts], order[kMaxPorts];
+  uint32_t port_nodes[kMaxPorts];  // bit m: port in node m's range (m < kFastNodes)
   // capacity tree: node m sums slots [lo, hi) in order (battery slot = n_ports, last)
-  double node_cap[kMaxNodes], node_eta[kMaxNodes];
+  double node_cap[kMaxNodes], node_eta[kMaxNodes], node_rcp_eta[kMaxNodes];
   int node_lo[kMaxNodes], node_hi[kMaxNodes], node_order[kMaxNodes];
   // series (device)
   const double *buy, *sellg, *moer, *dgrid, *sin_t, *cos_t, *cat_cum;

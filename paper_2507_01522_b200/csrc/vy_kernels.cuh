@@ -17,12 +17,13 @@
 namespace vy {
 
 constexpr int kTablesBytes = ((kMaxProfiles * (int)sizeof(Profile) + 256 * 8) + 127) & ~127;
+constexpr int kProfileWords = (int)(sizeof(Profile) / 8);
 
 __device__ __forceinline__ void stage_tables(const Params& P, unsigned char* smem, const Profile*& prof,
                                              const double*& dtab) {
   double* spd = reinterpret_cast<double*>(smem);
   const double* gp = reinterpret_cast<const double*>(P.profiles);
-  for (int i = threadIdx.x; i < kMaxProfiles * 5; i += blockDim.x) spd[i] = __ldg(gp + i);
+  for (int i = threadIdx.x; i < kMaxProfiles * kProfileWords; i += blockDim.x) spd[i] = __ldg(gp + i);
   double* sd = reinterpret_cast<double*>(smem + kMaxProfiles * sizeof(Profile));
   const int nd = 2 * P.k + 1;
   if (nd <= 256)
@@ -44,7 +45,7 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
   const Lane T{tile, lane, &P.L};
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
-  tile_load(P, tile, b0, lane);
+  tile_load(P, tile, b0, lane, P.act_tile);
   EnvRegs E{};  // zero for padding lanes so the obs path stays in bounds
   double rew = 0.0;
   bool done = false, reset = false;
@@ -52,7 +53,10 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
     load_env(P, b, E);
     const int dt = P.act_dtype;
     const int64_t rs = P.act_row, cs = P.act_col;
+    const uint8_t* arow = tile + P.L.acts + lane * (P.n_ports + 1);
+    const bool staged = P.act_tile;
     auto act = [&](int slot) -> int {
+      if (staged) return arow[slot];
       const int64_t at = b * rs + slot * cs;
       if (dt == VY_ACT_U8) return __ldg(reinterpret_cast<const uint8_t*>(P.actions) + at);
       if (dt == VY_ACT_I32) return __ldg(reinterpret_cast<const int32_t*>(P.actions) + at);
@@ -75,7 +79,7 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
       reinterpret_cast<float*>(P.out.reward)[b] = (float)rew;
     P.out.done[b] = done;
   }
-  emit_obs(P, prof, T, E, b0, active, P.out.obs, /*store_state=*/true, /*in_place=*/true);
+  emit_obs(P, prof, T, E, b0, active, P.out.obs, /*store_state=*/true);
 }
 
 __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params P, int T_steps, uint64_t policy_seed,
@@ -92,7 +96,7 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
   const Lane T{tile, lane, &P.L};
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
-  tile_load(P, tile, b0, lane);
+  tile_load(P, tile, b0, lane, false);
   EnvRegs E{};  // zero for padding lanes so the obs path stays in bounds
   uint64_t pkey = 0, seed = 0;
   int episode = 0;
@@ -121,7 +125,7 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
     }
     void* obs_t = f64 ? (void*)(reinterpret_cast<double*>(P.out.obs) + t * obs_stride)
                       : (void*)(reinterpret_cast<float*>(P.out.obs) + t * obs_stride);
-    emit_obs(P, prof, T, E, b0, active, obs_t, /*store_state=*/t == T_steps - 1, /*in_place=*/false);
+    emit_obs(P, prof, T, E, b0, active, obs_t, /*store_state=*/t == T_steps - 1);
   }
   if (active) {
     store_env(P, b, E, true);
@@ -143,7 +147,7 @@ __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P,
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
   // masked-out envs keep their state: stage the tile so the write-back is a no-op for them
-  tile_load(P, tile, b0, lane);
+  tile_load(P, tile, b0, lane, false);
   const bool mine = active && (!mask || mask[b]);
   EnvRegs E{};  // zero for padding lanes so the obs path stays in bounds
   if (active) load_env(P, b, E);
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P,
     store_env(P, b, E, true);
   }
   // masked-out rows still get their (unchanged) obs rewritten, which is idempotent
-  emit_obs(P, prof, T, E, b0, active, P.out.obs, /*store_state=*/true, /*in_place=*/true);
+  emit_obs(P, prof, T, E, b0, active, P.out.obs, /*store_state=*/true);
 }
 
 }  // namespace vy

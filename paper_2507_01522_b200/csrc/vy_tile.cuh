@@ -4,18 +4,20 @@
 //
 // Mapping.  One thread per environment; a warp owns a tile of 32 consecutive
 // envs.  The tile's per-port state (float64 i_drawn/soc/de, int16 dwell time,
-// uint8 meta) is staged from HBM into the warp's shared-memory tile with
-// 16-byte cp.async copies (port-major [port][lane] columns, so every access
-// below is bank-conflict free), the per-port phases run as *rolled* loops over
-// the runtime port count (one kernel for every station size; the hot code is
-// a few KB instead of a fully unrolled port loop that overflowed the
-// instruction cache), and per-env scalars live in registers.
+// uint8 meta) and its uint8 action rows are staged from HBM into the warp's
+// shared-memory tile with 16-byte cp.async copies ([port][field][lane]
+// columns, so per-lane accesses are bank-conflict free).  The per-port phases
+// run as rolled loops over the runtime port count (one kernel for every
+// station size; the hot code is a few KB — a fully unrolled port loop
+// overflowed the instruction cache), per-env scalars live in registers.
 //
 // Exactness.  All continuous arithmetic is float64 in the reference's
-// operation order, built with --fmad=false; sums the reference accumulates
-// sequentially (tree node loads, energy flows, satisfaction penalties) are
-// accumulated sequentially here too, in port order.  Each env's trajectory is
-// therefore bit-identical to the reference's compiled kernel.
+// operation order, built with --fmad=false (explicit FMAs appear only inside
+// div_rcp, whose result is the correctly rounded quotient); sums the
+// reference accumulates sequentially (tree node loads, energy flows,
+// satisfaction penalties) are accumulated sequentially here too, in port
+// order.  Each env's trajectory is therefore bit-identical to the reference's
+// compiled kernel.
 #pragma once
 
 #include "vy_device.cuh"
@@ -35,9 +37,10 @@ struct Lane {
   unsigned char* t;
   int lane;
   const TileLayout* L;
-  __device__ __forceinline__ double& idr(int i) const { return *reinterpret_cast<double*>(t + L->idr + i * 256 + lane * 8); }
-  __device__ __forceinline__ double& soc(int i) const { return *reinterpret_cast<double*>(t + L->soc + i * 256 + lane * 8); }
-  __device__ __forceinline__ double& de(int i) const { return *reinterpret_cast<double*>(t + L->de + i * 256 + lane * 8); }
+  __device__ __forceinline__ double* port(int i) const { return reinterpret_cast<double*>(t + i * 768 + lane * 8); }
+  __device__ __forceinline__ double& idr(int i) const { return port(i)[0]; }
+  __device__ __forceinline__ double& soc(int i) const { return port(i)[32]; }
+  __device__ __forceinline__ double& de(int i) const { return port(i)[64]; }
   __device__ __forceinline__ int16_t& dtrem(int i) const {
     return *reinterpret_cast<int16_t*>(t + L->dtrem + i * 64 + lane * 2);
   }
@@ -53,20 +56,21 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
-// Warp-cooperative stage-in of a tile's per-port state (HBM -> smem).  Each
-// (field, port) column of 32 envs is one contiguous run in the port-major
-// global layout; lanes copy 16 B each.
-__device__ __forceinline__ void tile_load(const Params& P, unsigned char* t, int64_t b0, int lane) {
+// Warp-cooperative stage-in of a tile (HBM -> smem).  Each (field, port)
+// column of 32 envs is one contiguous run in the port-major global layout;
+// lanes copy 16 B each.  The uint8 action block of the 32 envs is contiguous
+// too (row-major [B][n+1]).
+__device__ __forceinline__ void tile_load(const Params& P, unsigned char* t, int64_t b0, int lane, bool with_acts) {
   const int n = P.n_ports;
   const int64_t ld = P.ld;
   const TileLayout& L = P.L;
-  const char* f64src[3] = {reinterpret_cast<const char*>(P.st.port_i), reinterpret_cast<const char*>(P.st.port_soc),
-                           reinterpret_cast<const char*>(P.st.port_de)};
-  const int f64dst[3] = {L.idr, L.soc, L.de};
   const int q16 = (lane & 15) * 16;
-  for (int c = lane >> 4; c < 3 * n; c += 2) {
-    const int f = c / n, i = c - f * n;
-    cp_async16(t + f64dst[f] + i * 256 + q16, f64src[f] + ((int64_t)i * ld + b0) * 8 + q16);
+  for (int i = lane >> 4; i < n; i += 2) {
+    const int64_t g = ((int64_t)i * ld + b0) * 8 + q16;
+    unsigned char* d = t + i * 768 + q16;
+    cp_async16(d, reinterpret_cast<const char*>(P.st.port_i) + g);
+    cp_async16(d + 256, reinterpret_cast<const char*>(P.st.port_soc) + g);
+    cp_async16(d + 512, reinterpret_cast<const char*>(P.st.port_de) + g);
   }
   const char* dsrc = reinterpret_cast<const char*>(P.st.port_dtrem);
   for (int c = lane >> 2; c < n; c += 8)
@@ -74,6 +78,13 @@ __device__ __forceinline__ void tile_load(const Params& P, unsigned char* t, int
   const char* msrc = reinterpret_cast<const char*>(P.st.port_meta);
   for (int c = lane >> 1; c < n; c += 16)
     cp_async16(t + L.meta + c * 32 + (lane & 1) * 16, msrc + ((int64_t)c * ld + b0) + (lane & 1) * 16);
+  if (with_acts) {
+    // 32 rows x (n+1) bytes; the host guarantees a 16-byte aligned block and
+    // that reading whole 16-byte chunks past B stays inside the allocation
+    const int bytes = 32 * (n + 1);
+    const char* asrc = reinterpret_cast<const char*>(P.actions) + b0 * (n + 1);
+    for (int o = lane * 16; o < bytes; o += 512) cp_async16(t + L.acts + o, asrc + o);
+  }
   cp_async_wait_all();
   __syncwarp();
 }
@@ -114,20 +125,21 @@ __device__ __forceinline__ void store_env(const Params& P, int64_t b, const EnvR
   }
 }
 
-// charge envelope (vehicles.py:22-35); omt = 1 - tau precomputed with identical rounding
-__device__ __forceinline__ double envelope(double soc, double tau, double omt, double rbar) {
-  return soc <= tau ? rbar : (1.0 - soc) * rbar / omt;
+// charge envelope (vehicles.py:22-35): rbar below tau, then (1-soc)*rbar/(1-tau)
+__device__ __forceinline__ double envelope(double soc, double tau, double omt, double rcp_omt, double rbar) {
+  return soc <= tau ? rbar : div_rcp((1.0 - soc) * rbar, omt, rcp_omt);
 }
 
 // Clip a requested current (_kernel.pyx:309-325 ports, :329-345 battery).  Charging
 // is bounded by rhat = envelope(soc) (the value the reference stores,
 // _kernel.pyx:389/505), discharging by envelope(1 - soc); one select-based path.
-__device__ __forceinline__ double clip_current(double tgt, double soc, double tau, double omt, double rbar,
-                                               double volt, double imax_c, double imax_d) {
+__device__ __forceinline__ double clip_current(double tgt, double soc, double tau, double omt, double rcp_omt,
+                                               double rbar, double volt, double rcp_volt, double imax_c,
+                                               double imax_d) {
   const bool chg = tgt >= 0.0;
   const double s = chg ? soc : 1.0 - soc;
-  const double r = envelope(s, tau, omt, rbar);
-  const double lim = 1000.0 * r / volt;
+  const double r = envelope(s, tau, omt, rcp_omt, rbar);
+  const double lim = div_rcp(1000.0 * r, volt, rcp_volt);
   double v = chg ? tgt : -tgt;
   if (lim < v) v = lim;
   const double pm = chg ? imax_c : imax_d;
@@ -135,10 +147,9 @@ __device__ __forceinline__ double clip_current(double tgt, double soc, double ta
   return chg ? v : -v;
 }
 
-__device__ __forceinline__ double node_load(double s, double eta) {
-  // x / 1.0 == x and x * 1.0 == x exactly, so unit efficiencies skip the divide
-  if (s > 0.0) return eta == 1.0 ? s : s / eta;
-  return s * eta;
+__device__ __forceinline__ double node_load(const Params& P, double s, int m) {
+  if (s > 0.0) return P.node_eta[m] == 1.0 ? s : div_rcp(s, P.node_eta[m], P.node_rcp_eta[m]);
+  return s * P.node_eta[m];
 }
 
 // node m's load sum over its slot range, sequentially in leaf order
@@ -158,7 +169,7 @@ __device__ __noinline__ void fit_tree(const Params& P, const Lane& T, double& cb
     bool moved = false;
     for (int q = 0; q < P.n_nodes; ++q) {
       const int m = P.node_order[q];
-      const double mag = fabs(node_load(node_sum(P, T, cb, m), P.node_eta[m]));
+      const double mag = fabs(node_load(P, node_sum(P, T, cb, m), m));
       if (mag > P.node_cap[m]) {
         const double f = P.node_cap[m] / mag;
         const int lo = P.node_lo[m], hi = P.node_hi[m];
@@ -229,7 +240,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   // i_drawn in its smem slot, node loads accumulate in leaf order on the fly
   const int hi_a = 2 * P.k;
   auto delta_of = [&](int a) -> double {
-    if (a < 0 || a > hi_a) {
+    if ((unsigned)a > (unsigned)hi_a) {
       atomicOr(P.err, 1u);
       a = a < 0 ? 0 : hi_a;
     }
@@ -248,16 +259,15 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
       double tgt = T.idr(i) + d * P.imax_c[i];
       if (!P.allow_discharge && tgt < 0.0) tgt = 0.0;
       const Profile& pr = prof[mt >> 2];
-      c = clip_current(tgt, T.soc(i), pr.tau, pr.omt, P.kind[i] ? pr.r_dc : pr.r_ac, P.volt[i], P.imax_c[i],
-                       P.imax_d[i]);
+      c = clip_current(tgt, T.soc(i), pr.tau, pr.omt, pr.rcp_omt, P.kind[i] ? pr.r_dc : pr.r_ac, P.volt[i],
+                       P.rcp_volt[i], P.imax_c[i], P.imax_d[i]);
     }
     T.idr(i) = c;
     if (info) O.i_att[i * ld + b] = c;
-    if (fast) {
+    const uint32_t pm = P.port_nodes[i];
 #pragma unroll
-      for (int m = 0; m < kFastNodes; ++m)
-        if (m < P.n_nodes && i >= P.node_lo[m] && i < P.node_hi[m]) nsum[m] += c;
-    }
+    for (int m = 0; m < kFastNodes; ++m)
+      if (pm & (1u << m)) nsum[m] += c;
   }
   double cb = 0.0;
   {
@@ -265,13 +275,12 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
     const double d = delta_of(act(n));
     if (P.battery) {
       const double tgt = E.b_i + d * P.b_imax;
-      cb = clip_current(tgt, E.b_soc, P.b_tau, P.b_omt, P.b_rmax, P.b_volt, P.b_imax, P.b_imax);
+      cb = clip_current(tgt, E.b_soc, P.b_tau, P.b_omt, P.b_rcp_omt, P.b_rmax, P.b_volt, P.b_rcp_volt, P.b_imax,
+                        P.b_imax);
       if (info) O.i_att[n * ld + b] = cb;
-      if (fast) {
 #pragma unroll
-        for (int m = 0; m < kFastNodes; ++m)
-          if (m < P.n_nodes && P.node_lo[m] <= n && n < P.node_hi[m]) nsum[m] += cb;
-      }
+      for (int m = 0; m < kFastNodes; ++m)
+        if (P.battery_node_mask & (1 << m)) nsum[m] += cb;
     }
   }
   // tree: excess on the requested currents (_kernel.pyx:611-624), then rescale
@@ -280,13 +289,13 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
 #pragma unroll
     for (int m = 0; m < kFastNodes; ++m) {
       if (m < P.n_nodes) {
-        const double over = fabs(node_load(nsum[m], P.node_eta[m])) - P.node_cap[m];
+        const double over = fabs(node_load(P, nsum[m], m)) - P.node_cap[m];
         if (over > excess) excess = over;
       }
     }
   } else {
     for (int m = 0; m < P.n_nodes; ++m) {
-      const double over = fabs(node_load(node_sum(P, T, cb, m), P.node_eta[m])) - P.node_cap[m];
+      const double over = fabs(node_load(P, node_sum(P, T, cb, m), m)) - P.node_cap[m];
       if (over > excess) excess = over;
     }
   }
@@ -309,25 +318,25 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
     const uint32_t mt = T.meta(i);
     double got = 0.0;
     if (mt & 1u) {
-      const double cap = prof[mt >> 2].cap;
+      const Profile& pr = prof[mt >> 2];
       const double cur = T.idr(i), soc0 = T.soc(i), de0 = T.de(i);
-      const double raw = P.dtv[i] * cur / 1000.0;
+      const double raw = div_rcp(P.dtv[i] * cur, 1000.0, P.rcp_1000);
       got = raw;
       if (raw >= 0.0) {
         if (de0 < got) got = de0;
-        const double room = cap * (1.0 - soc0);
+        const double room = pr.cap * (1.0 - soc0);
         if (room < got) got = room;
       } else {
-        const double fl = -cap * soc0;
+        const double fl = -pr.cap * soc0;
         if (got < fl) got = fl;
       }
-      double soc = soc0 + got / cap;
+      double soc = soc0 + div_rcp(got, pr.cap, pr.rcp_cap);
       soc = soc < 0.0 ? 0.0 : (soc > 1.0 ? 1.0 : soc);
       double de = de0 - got;
       de = de < 0.0 ? 0.0 : de;
       e_net += got;
       if (got > 0.0)
-        e_in += P.eta_c[i] == 1.0 ? got : got / P.eta_c[i];
+        e_in += P.eta_c[i] == 1.0 ? got : div_rcp(got, P.eta_c[i], P.rcp_eta_c[i]);
       else if (got < 0.0)
         e_out += got * P.eta_d[i];
       const int dt = T.dtrem(i) - 1;
@@ -341,7 +350,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
           O.dep_overtime[at] = over;
           O.dep_early[at] = early;
           O.dep_pref[at] = p;
-          O.dep_cap[at] = cap;
+          O.dep_cap[at] = pr.cap;
           O.dep_soc[at] = soc;
         }
         if (p == 0)
@@ -366,7 +375,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   }
   double e_b = 0.0, bgot = 0.0;
   if (P.battery) {
-    bgot = P.b_dtv * E.b_i / 1000.0;
+    bgot = div_rcp(P.b_dtv * E.b_i, 1000.0, P.rcp_1000);
     if (bgot >= 0.0) {
       const double room = P.b_cap * (1.0 - E.b_soc);
       if (room < bgot) bgot = room;
@@ -374,9 +383,9 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
       const double fl = -P.b_cap * E.b_soc;
       if (bgot < fl) bgot = fl;
     }
-    const double soc = E.b_soc + bgot / P.b_cap;
+    const double soc = E.b_soc + div_rcp(bgot, P.b_cap, P.b_rcp_cap);
     E.b_soc = soc < 0.0 ? 0.0 : (soc > 1.0 ? 1.0 : soc);
-    e_b = bgot > 0.0 ? bgot / P.b_eta_c : bgot * P.b_eta_d;
+    e_b = bgot > 0.0 ? div_rcp(bgot, P.b_eta_c, P.b_rcp_eta_c) : bgot * P.b_eta_d;
   }
   if (info) {
     O.b_delivered[b] = bgot;
@@ -510,7 +519,6 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
 
 // ---- observation (_kernel.pyx:575-607; layout config.py:99-130) ----------------
 
-// calendar position of the env's current step
 struct Cal {
   int eff_day, hidx, sod;
 };
@@ -523,30 +531,18 @@ __device__ __forceinline__ Cal calendar(const Params& P, int step, int day) {
   return c;
 }
 
-// the six per-port features, exact float64 values
-__device__ __forceinline__ void port_features(const Params& P, const Profile* prof, int i, uint32_t mt, double idr,
-                                              double soc, double de, int dtrem, double v[6]) {
-  const bool occ = mt & 1u;
-  v[0] = occ ? 1.0 : 0.0;
-  v[1] = idr == 0.0 ? idr : idr / P.i_denom[i];
-  v[2] = soc;
-  v[3] = occ ? (de == 0.0 ? de : de / prof[mt >> 2].cap) : 0.0;
-  v[4] = dtrem == 0 ? 0.0 : (double)dtrem / (double)P.episode_steps;
-  v[5] = (double)((mt >> 1) & 1u);
-}
-
 // globals: battery [soc, I/Imax], [buy, sellg, p_sell, sin, cos, weekday, day/365], horizon
 __device__ __forceinline__ double global_feature(const Params& P, const EnvRegs& E, const Cal& C, int k) {
   switch (k) {
     case 0: return E.b_soc;
-    case 1: return E.b_i == 0.0 ? E.b_i : E.b_i / P.b_idenom;
+    case 1: return E.b_i == 0.0 ? E.b_i : div_rcp(E.b_i, P.b_idenom, P.b_rcp_idenom);
     case 2: return __ldg(P.buy + C.hidx);
     case 3: return __ldg(P.sellg + C.hidx);
     case 4: return P.p_sell;
     case 5: return __ldg(P.sin_t + C.sod);
     case 6: return __ldg(P.cos_t + C.sod);
     case 7: return (double)__ldg(P.weekday + C.eff_day);
-    case 8: return (double)C.eff_day / 365.0;
+    case 8: return div_rcp((double)C.eff_day, 365.0, P.rcp_365);
     default: {
       const int h = k - 9;
       const int64_t fmin = (int64_t)(E.step + 1 + h) * P.dt_min;
@@ -556,36 +552,27 @@ __device__ __forceinline__ double global_feature(const Params& P, const EnvRegs&
   }
 }
 
-// Staged obs cell (row = lane, col c) of the warp tile.  Port columns live in
-// the port's float64 slots (in place, after write-back) or in the extra
-// region; the row index is rotated by the column so that both the per-lane
-// writes (fixed c) and the row-major read-out (consecutive c) are conflict free.
-__device__ __forceinline__ float* obs_cell(unsigned char* t, const TileLayout& L, bool in_place, int r, int c,
-                                           int n) {
-  const int rot = ((r + c) & 31) * 4;
-  if (c < 6 * n) {
-    const int i = c / 6, f = c - 6 * i;
-    int base;
-    if (in_place)
-      base = (f < 2 ? L.idr : f < 4 ? L.soc : L.de) + i * 256 + (f & 1) * 128;
-    else
-      base = L.extra + c * 128;
-    return reinterpret_cast<float*>(t + base + rot);
-  }
-  return reinterpret_cast<float*>(t + L.gobs + (c - 6 * n) * 128 + rot);
+// Staged obs cell (row r, column c): column-major 128-byte columns, the row
+// rotated by the column so per-lane writes (fixed c) and row-major read-out
+// (consecutive c) are both bank-conflict free.
+__device__ __forceinline__ float* obs_cell(unsigned char* t, int obs_off, int r, int c) {
+  return reinterpret_cast<float*>(t + obs_off + c * 128 + ((r + c) & 31) * 4);
 }
 
 // Write this tile's obs rows (and, with store_state, the port state back to
 // HBM).  float32 obs are staged and leave with row-major coalesced stores;
-// float64 obs (exact drop-in mode) are written per lane.
+// float64 obs (exact drop-in mode) are written per lane.  In-place staging
+// (obs_off == 0) overwrites port i's float64 slots right after they are read.
 __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, const Lane& T, const EnvRegs& E,
-                                         int64_t b0, bool active, void* obs_base, bool store_state, bool in_place) {
+                                         int64_t b0, bool active, void* obs_base, bool store_state) {
   const int n = P.n_ports;
   const int lane = T.lane;
   const int64_t b = b0 + lane;
   const int64_t ld = P.ld;
   const int OL = P.obs_len;
+  const int obs_off = P.L.obs;
   const bool f64 = P.flags & VY_F_OUT_F64;
+  const bool in_place = obs_off == 0;
   const Cal C = calendar(P, E.step, E.day);
   double* row64 = f64 ? reinterpret_cast<double*>(obs_base) + b * OL : nullptr;
 #pragma unroll 1
@@ -601,8 +588,14 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
       s.port_dtrem[i * ld + b] = (int16_t)dt;
       s.port_meta[i * ld + b] = (uint8_t)mt;
     }
+    const bool occ = mt & 1u;
     double v[6];
-    port_features(P, prof, i, mt, idr, soc, de, dt, v);
+    v[0] = occ ? 1.0 : 0.0;
+    v[1] = div_rcp(idr, P.i_denom[i], P.rcp_i_denom[i]);
+    v[2] = soc;
+    v[3] = occ ? div_rcp(de, prof[mt >> 2].cap, prof[mt >> 2].rcp_cap) : 0.0;
+    v[4] = div_rcp((double)dt, (double)P.episode_steps, P.rcp_ep);
+    v[5] = (double)((mt >> 1) & 1u);
     if (f64) {
       if (active)
 #pragma unroll
@@ -610,7 +603,7 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
     } else {
       if (in_place) __syncwarp();  // every lane has read port i before its slots are reused
 #pragma unroll
-      for (int f = 0; f < 6; ++f) *obs_cell(T.t, *T.L, in_place, lane, 6 * i + f, n) = (float)v[f];
+      for (int f = 0; f < 6; ++f) *obs_cell(T.t, obs_off, lane, 6 * i + f) = (float)v[f];
     }
   }
   const int ng = OL - 6 * n;
@@ -619,19 +612,20 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
     if (f64) {
       if (active) row64[6 * n + k] = g;
     } else {
-      *obs_cell(T.t, *T.L, in_place, lane, 6 * n + k, n) = (float)g;
+      *obs_cell(T.t, obs_off, lane, 6 * n + k) = (float)g;
     }
   }
   if (f64) return;
   __syncwarp();
-  // row-major read-out: element e of the warp's [32][OL] block
+  // row-major read-out of the warp's [rows][OL] block: consecutive lanes store
+  // consecutive floats (fully coalesced)
   float* gobs = reinterpret_cast<float*>(obs_base) + b0 * OL;
   const int64_t left = P.B - b0;
   const int rows = left >= 32 ? 32 : (int)left;
   const int total = rows * OL;
-  int r = lane / OL, c = lane - (lane / OL) * OL;
+  int r = lane / OL, c = lane - r * OL;
   for (int e = lane; e < total; e += 32) {
-    gobs[e] = *obs_cell(T.t, *T.L, in_place, r, c, n);
+    gobs[e] = *obs_cell(T.t, obs_off, r, c);
     c += 32;
     while (c >= OL) {
       c -= OL;
