@@ -43,13 +43,26 @@ int upload(T** dst, const T* src, size_t n) {
 
 namespace vy {
 
+// RandomPolicy rows: thread per env computes its n+1 actions into a per-warp
+// smem row block, then the warp writes the contiguous [32][n+1] byte block
+// with coalesced stores (per-thread 17-byte rows would be strided byte stores).
 __global__ void k_random_actions(uint64_t seed, int64_t index0, int64_t call, int64_t B, int ns, int hi,
                                  uint8_t* out) {
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  const uint64_t key = fold(fold(fold(kKey0, seed), (uint64_t)(index0 + b)), 2);
-  const uint64_t j0 = (uint64_t)call * (uint64_t)ns;
-  for (int s = 0; s < ns; ++s) out[b * ns + s] = (uint8_t)policy_action(key, j0 + s + 1, hi);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
+  if (b0 >= B) return;
+  unsigned char* rows = vy_smem + warp * 32 * ns;
+  const int64_t b = b0 + lane;
+  if (b < B) {
+    const uint64_t key = fold(fold(fold(kKey0, seed), (uint64_t)(index0 + b)), 2);
+    const uint64_t j0 = (uint64_t)call * (uint64_t)ns;
+    for (int s = 0; s < ns; ++s) rows[lane * ns + s] = (uint8_t)policy_action(key, j0 + s + 1, hi);
+  }
+  __syncwarp();
+  const int64_t left = B - b0;
+  const int bytes = (left >= 32 ? 32 : (int)left) * ns;
+  uint8_t* g = out + b0 * ns;
+  for (int o = lane; o < bytes; o += 32) g[o] = rows[o];
 }
 
 // div_rcp vs IEEE division on random dividends spread over 2^-64..2^64
@@ -498,7 +511,7 @@ int vy_random_actions(vy_handle* h, uint64_t seed, int64_t index0, int64_t call,
   const int ns = h->t.n_ports + 1, hi = 2 * h->t.k + 1;
   if (hi > 256) return fail(VY_ERR_UNSUPPORTED, "uint8 actions need 2k+1 <= 256");
   const unsigned grid = (unsigned)((h->B + 255) / 256);
-  k_random_actions<<<grid, 256, 0, (cudaStream_t)stream>>>(seed, index0, call, h->B, ns, hi, out);
+  k_random_actions<<<grid, 256, 8 * 32 * ns, (cudaStream_t)stream>>>(seed, index0, call, h->B, ns, hi, out);
   VY_CUDA(cudaGetLastError());
   ++h->launches;
   return VY_OK;

@@ -19,8 +19,8 @@ namespace vy {
 constexpr int kTablesBytes = ((kMaxProfiles * (int)sizeof(Profile) + 256 * 8) + 127) & ~127;
 constexpr int kProfileWords = (int)(sizeof(Profile) / 8);
 
-__device__ __forceinline__ void stage_tables(const Params& P, unsigned char* smem, const Profile*& prof,
-                                             const double*& dtab) {
+__device__ __forceinline__ void stage_tables(const Params& P, const Profile*& prof, const double*& dtab) {
+  unsigned char* smem = vy_smem;
   double* spd = reinterpret_cast<double*>(smem);
   const double* gp = reinterpret_cast<const double*>(P.profiles);
   for (int i = threadIdx.x; i < kMaxProfiles * kProfileWords; i += blockDim.x) spd[i] = __ldg(gp + i);
@@ -34,14 +34,13 @@ __device__ __forceinline__ void stage_tables(const Params& P, unsigned char* sme
 }
 
 __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) {
-  extern __shared__ __align__(128) unsigned char smem[];
   const Profile* prof;
   const double* dtab;
-  stage_tables(P, smem, prof, dtab);
+  stage_tables(P, prof, dtab);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
   if (b0 >= P.B) return;  // whole warp leaves together
-  unsigned char* tile = smem + kTablesBytes + warp * P.L.bytes;
+  const uint32_t tile = kTablesBytes + warp * P.L.bytes;
   const Lane T{tile, lane, &P.L};
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
@@ -53,7 +52,7 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
     load_env(P, b, E);
     const int dt = P.act_dtype;
     const int64_t rs = P.act_row, cs = P.act_col;
-    const uint8_t* arow = tile + P.L.acts + lane * (P.n_ports + 1);
+    const uint8_t* arow = vy_smem + tile + P.L.acts + lane * (P.n_ports + 1);
     const bool staged = P.act_tile;
     auto act = [&](int slot) -> int {
       if (staged) return arow[slot];
@@ -85,14 +84,13 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
 __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params P, int T_steps, uint64_t policy_seed,
                                                  int64_t index0, int64_t call0, int64_t obs_stride,
                                                  int64_t rew_stride) {
-  extern __shared__ __align__(128) unsigned char smem[];
   const Profile* prof;
   const double* dtab;
-  stage_tables(P, smem, prof, dtab);
+  stage_tables(P, prof, dtab);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
   if (b0 >= P.B) return;
-  unsigned char* tile = smem + kTablesBytes + warp * P.L.bytes;
+  const uint32_t tile = kTablesBytes + warp * P.L.bytes;
   const Lane T{tile, lane, &P.L};
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
@@ -135,14 +133,13 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
 
 __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P, const uint8_t* mask,
                                                int episode_mode, const int32_t* inj_day) {
-  extern __shared__ __align__(128) unsigned char smem[];
   const Profile* prof;
   const double* dtab;
-  stage_tables(P, smem, prof, dtab);
+  stage_tables(P, prof, dtab);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
   if (b0 >= P.B) return;
-  unsigned char* tile = smem + kTablesBytes + warp * P.L.bytes;
+  const uint32_t tile = kTablesBytes + warp * P.L.bytes;
   const Lane T{tile, lane, &P.L};
   const int64_t b = b0 + lane;
   const bool active = b < P.B;

@@ -24,6 +24,12 @@
 
 namespace vy {
 
+// Dynamic shared memory of every kernel in this library.  Tiles are addressed
+// by 32-bit offsets into it so the compiler emits LDS/STS with 32-bit address
+// arithmetic (a generic pointer kept in a struct would degrade to 64-bit
+// generic loads).
+extern __shared__ __align__(128) unsigned char vy_smem[];
+
 struct EnvRegs {
   int step, day;
   uint64_t akey;
@@ -34,17 +40,19 @@ struct EnvRegs {
 
 // one lane's view of its warp's tile
 struct Lane {
-  unsigned char* t;
+  uint32_t t;  // byte offset of the warp's tile in vy_smem
   int lane;
   const TileLayout* L;
-  __device__ __forceinline__ double* port(int i) const { return reinterpret_cast<double*>(t + i * 768 + lane * 8); }
+  __device__ __forceinline__ double* port(int i) const {
+    return reinterpret_cast<double*>(vy_smem + t + i * 768 + lane * 8);
+  }
   __device__ __forceinline__ double& idr(int i) const { return port(i)[0]; }
   __device__ __forceinline__ double& soc(int i) const { return port(i)[32]; }
   __device__ __forceinline__ double& de(int i) const { return port(i)[64]; }
   __device__ __forceinline__ int16_t& dtrem(int i) const {
-    return *reinterpret_cast<int16_t*>(t + L->dtrem + i * 64 + lane * 2);
+    return *reinterpret_cast<int16_t*>(vy_smem + t + L->dtrem + i * 64 + lane * 2);
   }
-  __device__ __forceinline__ uint8_t& meta(int i) const { return *(t + L->meta + i * 32 + lane); }
+  __device__ __forceinline__ uint8_t& meta(int i) const { return *(vy_smem + t + L->meta + i * 32 + lane); }
 };
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
@@ -60,7 +68,8 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // column of 32 envs is one contiguous run in the port-major global layout;
 // lanes copy 16 B each.  The uint8 action block of the 32 envs is contiguous
 // too (row-major [B][n+1]).
-__device__ __forceinline__ void tile_load(const Params& P, unsigned char* t, int64_t b0, int lane, bool with_acts) {
+__device__ __forceinline__ void tile_load(const Params& P, uint32_t toff, int64_t b0, int lane, bool with_acts) {
+  unsigned char* t = vy_smem + toff;
   const int n = P.n_ports;
   const int64_t ld = P.ld;
   const TileLayout& L = P.L;
@@ -555,8 +564,8 @@ __device__ __forceinline__ double global_feature(const Params& P, const EnvRegs&
 // Staged obs cell (row r, column c): column-major 128-byte columns, the row
 // rotated by the column so per-lane writes (fixed c) and row-major read-out
 // (consecutive c) are both bank-conflict free.
-__device__ __forceinline__ float* obs_cell(unsigned char* t, int obs_off, int r, int c) {
-  return reinterpret_cast<float*>(t + obs_off + c * 128 + ((r + c) & 31) * 4);
+__device__ __forceinline__ float* obs_cell(uint32_t t, int obs_off, int r, int c) {
+  return reinterpret_cast<float*>(vy_smem + t + obs_off + c * 128 + ((r + c) & 31) * 4);
 }
 
 // Write this tile's obs rows (and, with store_state, the port state back to
@@ -617,20 +626,18 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
   }
   if (f64) return;
   __syncwarp();
-  // row-major read-out of the warp's [rows][OL] block: consecutive lanes store
-  // consecutive floats (fully coalesced)
+  // row-major read-out of the warp's [rows][OL] block: per row, consecutive
+  // lanes store consecutive floats (fully coalesced); with the (r + c)
+  // rotation the 32 lanes of a row read 32 distinct banks
   float* gobs = reinterpret_cast<float*>(obs_base) + b0 * OL;
   const int64_t left = P.B - b0;
   const int rows = left >= 32 ? 32 : (int)left;
-  const int total = rows * OL;
-  int r = lane / OL, c = lane - r * OL;
-  for (int e = lane; e < total; e += 32) {
-    gobs[e] = *obs_cell(T.t, obs_off, r, c);
-    c += 32;
-    while (c >= OL) {
-      c -= OL;
-      ++r;
-    }
+  const uint32_t base = T.t + obs_off;
+  for (int r = 0; r < rows; ++r) {
+    float* g = gobs + r * OL;
+#pragma unroll 4
+    for (int c = lane; c < OL; c += 32)
+      g[c] = *reinterpret_cast<const float*>(vy_smem + base + c * 128 + ((r + c) & 31) * 4);
   }
   __syncwarp();
 }
