@@ -239,6 +239,7 @@ void fill(vy_handle* h, Params& P, bool rollout, bool acts) {
   P.out = h->out;
   P.err = h->d_err;
   P.act_tile = acts;
+  P.n_profiles = (int)h->profiles.size();
   P.L = tile_layout(t, rollout, acts);
 }
 

@@ -104,6 +104,7 @@ struct Params {
   double rcp_1000, rcp_ep, rcp_365;
   int battery_node_mask;  // bit m: battery slot in node m's range (m < kFastNodes)
   int act_tile;           // actions are row-major uint8 [B][n+1], staged per tile
+  int n_profiles;         // live entries of the car-profile table
   // ports
   double volt[kMaxPorts], imax_c[kMaxPorts], imax_d[kMaxPorts], eta_c[kMaxPorts], eta_d[kMaxPorts];
   double i_denom[kMaxPorts], dtv[kMaxPorts];

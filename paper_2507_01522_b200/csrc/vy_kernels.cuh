@@ -23,7 +23,7 @@ __device__ __forceinline__ void stage_tables(const Params& P, const Profile*& pr
   unsigned char* smem = vy_smem;
   double* spd = reinterpret_cast<double*>(smem);
   const double* gp = reinterpret_cast<const double*>(P.profiles);
-  for (int i = threadIdx.x; i < kMaxProfiles * kProfileWords; i += blockDim.x) spd[i] = __ldg(gp + i);
+  for (int i = threadIdx.x; i < P.n_profiles * kProfileWords; i += blockDim.x) spd[i] = __ldg(gp + i);
   double* sd = reinterpret_cast<double*>(smem + kMaxProfiles * sizeof(Profile));
   const int nd = 2 * P.k + 1;
   if (nd <= 256)

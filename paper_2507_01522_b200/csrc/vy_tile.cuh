@@ -568,35 +568,65 @@ __device__ __forceinline__ float* obs_cell(uint32_t t, int obs_off, int r, int c
   return reinterpret_cast<float*>(vy_smem + t + obs_off + c * 128 + ((r + c) & 31) * 4);
 }
 
-// Write this tile's obs rows (and, with store_state, the port state back to
-// HBM).  float32 obs are staged and leave with row-major coalesced stores;
-// float64 obs (exact drop-in mode) are written per lane.  In-place staging
-// (obs_off == 0) overwrites port i's float64 slots right after they are read.
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_s2g(void* gdst, uint32_t soff, uint32_t bytes) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(vy_smem + soff);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(s), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+
+// Write the tile's per-port state back to HBM with bulk async copies (the TMA
+// engine streams each 256/64/32-byte column; no per-lane stores or 64-bit
+// address math).  Padding lanes write their (unchanged) padding columns.
+// Returns after the copies have finished READING shared memory, so the
+// caller may overwrite the port slots.
+__device__ __forceinline__ void tile_store(const Params& P, uint32_t toff, int64_t b0, int lane) {
+  const int n = P.n_ports;
+  const int64_t ld = P.ld;
+  fence_async_smem();  // make this warp's STS visible to the async proxy
+  __syncwarp();
+  for (int c = lane; c < 5 * n; c += 32) {
+    const int i = c / 5, f = c - 5 * i;
+    const int64_t e = (int64_t)i * ld + b0;
+    if (f < 3) {
+      double* g = f == 0 ? P.st.port_i : f == 1 ? P.st.port_soc : P.st.port_de;
+      bulk_s2g(g + e, toff + i * 768 + f * 256, 256);
+    } else if (f == 3) {
+      bulk_s2g(P.st.port_dtrem + e, toff + P.L.dtrem + i * 64, 64);
+    } else {
+      bulk_s2g(P.st.port_meta + e, toff + P.L.meta + i * 32, 32);
+    }
+  }
+  bulk_commit();
+  bulk_wait_read();
+  __syncwarp();
+}
+
+// Write this tile's obs rows (and, with store_state, the state back to HBM).
+// float32 obs are staged column-major in shared memory (rows rotated by column
+// so per-lane writes and row-major reads are both bank-conflict free) and
+// leave with coalesced row-major stores; float64 obs (exact drop-in mode) are
+// written per lane.  In the step kernel the staging area is the tile's own
+// float64 port slots (obs_off == 0), free once the state has been written back.
 __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, const Lane& T, const EnvRegs& E,
                                          int64_t b0, bool active, void* obs_base, bool store_state) {
   const int n = P.n_ports;
   const int lane = T.lane;
   const int64_t b = b0 + lane;
-  const int64_t ld = P.ld;
   const int OL = P.obs_len;
   const int obs_off = P.L.obs;
   const bool f64 = P.flags & VY_F_OUT_F64;
-  const bool in_place = obs_off == 0;
   const Cal C = calendar(P, E.step, E.day);
+  if (store_state) tile_store(P, T.t, b0, lane);
   double* row64 = f64 ? reinterpret_cast<double*>(obs_base) + b * OL : nullptr;
+  const uint32_t cells = T.t + obs_off;
 #pragma unroll 1
   for (int i = 0; i < n; ++i) {
     const uint32_t mt = T.meta(i);
     const double idr = T.idr(i), soc = T.soc(i), de = T.de(i);
     const int dt = T.dtrem(i);
-    if (store_state && active) {
-      const vy_state& s = P.st;
-      s.port_i[i * ld + b] = idr;
-      s.port_soc[i * ld + b] = soc;
-      s.port_de[i * ld + b] = de;
-      s.port_dtrem[i * ld + b] = (int16_t)dt;
-      s.port_meta[i * ld + b] = (uint8_t)mt;
-    }
     const bool occ = mt & 1u;
     double v[6];
     v[0] = occ ? 1.0 : 0.0;
@@ -610,34 +640,39 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
 #pragma unroll
         for (int f = 0; f < 6; ++f) row64[6 * i + f] = v[f];
     } else {
-      if (in_place) __syncwarp();  // every lane has read port i before its slots are reused
+      __syncwarp();  // in place: every lane has read port i before its slots are reused
+      const uint32_t col = cells + 6 * i * 128;
+      const int rot = lane + 6 * i;
 #pragma unroll
-      for (int f = 0; f < 6; ++f) *obs_cell(T.t, obs_off, lane, 6 * i + f) = (float)v[f];
+      for (int f = 0; f < 6; ++f)
+        *reinterpret_cast<float*>(vy_smem + col + f * 128 + (((rot + f) & 31) << 2)) = (float)v[f];
     }
   }
   const int ng = OL - 6 * n;
   for (int k = 0; k < ng; ++k) {
     const double g = global_feature(P, E, C, k);
+    const int c = 6 * n + k;
     if (f64) {
-      if (active) row64[6 * n + k] = g;
+      if (active) row64[c] = g;
     } else {
-      *obs_cell(T.t, obs_off, lane, 6 * n + k) = (float)g;
+      *reinterpret_cast<float*>(vy_smem + cells + c * 128 + (((lane + c) & 31) << 2)) = (float)g;
     }
   }
   if (f64) return;
   __syncwarp();
-  // row-major read-out of the warp's [rows][OL] block: per row, consecutive
-  // lanes store consecutive floats (fully coalesced); with the (r + c)
-  // rotation the 32 lanes of a row read 32 distinct banks
-  float* gobs = reinterpret_cast<float*>(obs_base) + b0 * OL;
+  // Row-major read-out: row r, column c = lane + 32 j lives at
+  // cells + c*128 + ((r + c) & 31)*4 = cells + lane*128 + ((r + lane) & 31)*4 + j*4096.
+  float* gobs = reinterpret_cast<float*>(obs_base) + b0 * OL + lane;
   const int64_t left = P.B - b0;
   const int rows = left >= 32 ? 32 : (int)left;
-  const uint32_t base = T.t + obs_off;
+  const int J = (OL + 31) >> 5;
+  const uint32_t lbase = cells + lane * 128;
   for (int r = 0; r < rows; ++r) {
+    const uint32_t a0 = lbase + (((r + lane) & 31) << 2);
     float* g = gobs + r * OL;
 #pragma unroll 4
-    for (int c = lane; c < OL; c += 32)
-      g[c] = *reinterpret_cast<const float*>(vy_smem + base + c * 128 + ((r + c) & 31) * 4);
+    for (int j = 0; j < J; ++j)
+      if (lane + 32 * j < OL) g[32 * j] = *reinterpret_cast<const float*>(vy_smem + a0 + j * 4096);
   }
   __syncwarp();
 }

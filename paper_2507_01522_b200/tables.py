@@ -224,3 +224,10 @@ def build_tables(config: EnvConfig, station: StationTree, dataset: Dataset) -> S
         frac_lo=float(scen.requested_fraction_range[0]), frac_hi=float(scen.requested_fraction_range[1]),
         p_charge=float(scen.p_charge_sensitive),
     )
+
+
+def build_tables_from_kernel_tables(kt) -> StepTables:
+    """StepTables from any object with the reference KernelTables fields
+    (engine.py:30-104), e.g. the reference engine's own ``env.tables``."""
+    names = [f.name for f in fields(StepTables) if not f.name.startswith("_")]
+    return StepTables(**{n: getattr(kt, n) for n in names})
