@@ -661,18 +661,36 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
   if (f64) return;
   __syncwarp();
   // Row-major read-out: row r, column c = lane + 32 j lives at
-  // cells + c*128 + ((r + c) & 31)*4 = cells + lane*128 + ((r + lane) & 31)*4 + j*4096.
-  float* gobs = reinterpret_cast<float*>(obs_base) + b0 * OL + lane;
+  // cells + c*128 + ((r + c) & 31)*4 = cells + lane*128 + ((r + lane) & 31)*4 + j*4096,
+  // so per row each lane needs one rotated base and immediate offsets.
+  float* g = reinterpret_cast<float*>(obs_base) + b0 * OL + lane;
   const int64_t left = P.B - b0;
   const int rows = left >= 32 ? 32 : (int)left;
-  const int J = (OL + 31) >> 5;
   const uint32_t lbase = cells + lane * 128;
-  for (int r = 0; r < rows; ++r) {
-    const uint32_t a0 = lbase + (((r + lane) & 31) << 2);
-    float* g = gobs + r * OL;
-#pragma unroll 4
-    for (int j = 0; j < J; ++j)
-      if (lane + 32 * j < OL) g[32 * j] = *reinterpret_cast<const float*>(vy_smem + a0 + j * 4096);
+  if (OL <= 128) {
+    const bool p0 = lane < OL, p1 = lane + 32 < OL, p2 = lane + 64 < OL, p3 = lane + 96 < OL;
+#pragma unroll 2
+    for (int r = 0; r < rows; ++r) {
+      const unsigned char* a = vy_smem + lbase + (((r + lane) & 31) << 2);
+      // predicated loads: columns past OL may lie past the end of the smem allocation
+      const float v0 = p0 ? *reinterpret_cast<const float*>(a) : 0.f;
+      const float v1 = p1 ? *reinterpret_cast<const float*>(a + 4096) : 0.f;
+      const float v2 = p2 ? *reinterpret_cast<const float*>(a + 8192) : 0.f;
+      const float v3 = p3 ? *reinterpret_cast<const float*>(a + 12288) : 0.f;
+      if (p0) g[0] = v0;
+      if (p1) g[32] = v1;
+      if (p2) g[64] = v2;
+      if (p3) g[96] = v3;
+      g += OL;
+    }
+  } else {
+    const int J = (OL + 31) >> 5;
+    for (int r = 0; r < rows; ++r) {
+      const unsigned char* a = vy_smem + lbase + (((r + lane) & 31) << 2);
+      for (int j = 0; j < J; ++j)
+        if (lane + 32 * j < OL) g[32 * j] = *reinterpret_cast<const float*>(a + j * 4096);
+      g += OL;
+    }
   }
   __syncwarp();
 }
