@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
   const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
   if (b0 >= P.B) return;  // whole warp leaves together
   const uint32_t tile = kTablesBytes + warp * P.L.bytes;
-  const Lane T{tile, lane, &P.L};
+  const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
   tile_load(P, tile, b0, lane, P.act_tile);
@@ -52,10 +52,10 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
     load_env(P, b, E);
     const int dt = P.act_dtype;
     const int64_t rs = P.act_row, cs = P.act_col;
-    const uint8_t* arow = vy_smem + tile + P.L.acts + lane * (P.n_ports + 1);
+    const uint32_t arow = smem_base() + tile + P.L.acts + lane * (P.n_ports + 1);
     const bool staged = P.act_tile;
     auto act = [&](int slot) -> int {
-      if (staged) return arow[slot];
+      if (staged) return (int)lds_u8(arow + slot);
       const int64_t at = b * rs + slot * cs;
       if (dt == VY_ACT_U8) return __ldg(reinterpret_cast<const uint8_t*>(P.actions) + at);
       if (dt == VY_ACT_I32) return __ldg(reinterpret_cast<const int32_t*>(P.actions) + at);
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
   const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
   if (b0 >= P.B) return;
   const uint32_t tile = kTablesBytes + warp * P.L.bytes;
-  const Lane T{tile, lane, &P.L};
+  const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
   tile_load(P, tile, b0, lane, false);
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P,
   const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
   if (b0 >= P.B) return;
   const uint32_t tile = kTablesBytes + warp * P.L.bytes;
-  const Lane T{tile, lane, &P.L};
+  const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
   // masked-out envs keep their state: stage the tile so the write-back is a no-op for them

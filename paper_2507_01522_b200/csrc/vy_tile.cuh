@@ -24,11 +24,40 @@
 
 namespace vy {
 
-// Dynamic shared memory of every kernel in this library.  Tiles are addressed
-// by 32-bit offsets into it so the compiler emits LDS/STS with 32-bit address
-// arithmetic (a generic pointer kept in a struct would degrade to 64-bit
-// generic loads).
+// Dynamic shared memory of every kernel in this library.  Tile data is
+// accessed with explicit 32-bit shared-window addresses (ld/st.shared via
+// inline PTX): pointer arithmetic on the extern array made the compiler
+// re-materialise the window base (S2R CgaCtaId + LEA) at every predicated
+// access.  The asm is volatile so tile accesses keep program order.
 extern __shared__ __align__(128) unsigned char vy_smem[];
+
+__device__ __forceinline__ uint32_t smem_base() { return (uint32_t)__cvta_generic_to_shared(vy_smem); }
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v)); }
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v)); }
+__device__ __forceinline__ int lds_s16(uint32_t a) {
+  int16_t v;
+  asm volatile("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_s16(uint32_t a, int v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((uint16_t)v));
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v)); }
 
 struct EnvRegs {
   int step, day;
@@ -38,22 +67,42 @@ struct EnvRegs {
   int ep_overtime, ep_declined, ep_departures;
 };
 
+// proxies so tile fields read and assign like lvalues
+struct SF64 {
+  uint32_t a;
+  __device__ __forceinline__ operator double() const { return lds_f64(a); }
+  __device__ __forceinline__ void operator=(double v) const { sts_f64(a, v); }
+};
+struct SS16 {
+  uint32_t a;
+  __device__ __forceinline__ operator int() const { return lds_s16(a); }
+  __device__ __forceinline__ void operator=(int v) const { sts_s16(a, v); }
+};
+struct SU8 {
+  uint32_t a;
+  __device__ __forceinline__ operator uint32_t() const { return lds_u8(a); }
+  __device__ __forceinline__ void operator=(uint32_t v) const { sts_u8(a, v); }
+};
+
 // one lane's view of its warp's tile
 struct Lane {
-  uint32_t t;  // byte offset of the warp's tile in vy_smem
+  uint32_t t;   // byte offset of the warp's tile in vy_smem
+  uint32_t s;   // shared-window address of this lane's column 0 of the tile (port slots)
+  uint32_t sd;  // shared-window address of this lane's dwell entry of port 0
+  uint32_t sm;  // shared-window address of this lane's meta entry of port 0
   int lane;
   const TileLayout* L;
-  __device__ __forceinline__ double* port(int i) const {
-    return reinterpret_cast<double*>(vy_smem + t + i * 768 + lane * 8);
-  }
-  __device__ __forceinline__ double& idr(int i) const { return port(i)[0]; }
-  __device__ __forceinline__ double& soc(int i) const { return port(i)[32]; }
-  __device__ __forceinline__ double& de(int i) const { return port(i)[64]; }
-  __device__ __forceinline__ int16_t& dtrem(int i) const {
-    return *reinterpret_cast<int16_t*>(vy_smem + t + L->dtrem + i * 64 + lane * 2);
-  }
-  __device__ __forceinline__ uint8_t& meta(int i) const { return *(vy_smem + t + L->meta + i * 32 + lane); }
+  __device__ __forceinline__ SF64 idr(int i) const { return {s + i * 768}; }
+  __device__ __forceinline__ SF64 soc(int i) const { return {s + i * 768 + 256}; }
+  __device__ __forceinline__ SF64 de(int i) const { return {s + i * 768 + 512}; }
+  __device__ __forceinline__ SS16 dtrem(int i) const { return {sd + i * 64}; }
+  __device__ __forceinline__ SU8 meta(int i) const { return {sm + i * 32}; }
 };
+
+__device__ __forceinline__ Lane make_lane(const Params& P, uint32_t tile, int lane) {
+  const uint32_t b = smem_base() + tile;
+  return Lane{tile, b + lane * 8, b + P.L.dtrem + lane * 2, b + P.L.meta + lane, lane, &P.L};
+}
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(sdst);
@@ -184,8 +233,9 @@ __device__ __noinline__ void fit_tree(const Params& P, const Lane& T, double& cb
         const int lo = P.node_lo[m], hi = P.node_hi[m];
         const int hp = hi < P.n_ports ? hi : P.n_ports;
         for (int j = lo; j < hp; ++j) {
-          const double v = T.idr(j) * f;
-          if (v != T.idr(j)) {
+          const double old = T.idr(j);
+          const double v = old * f;
+          if (v != old) {
             T.idr(j) = v;
             moved = true;
           }
@@ -211,9 +261,11 @@ __device__ __forceinline__ void reset_env(const Params& P, const Lane& T, EnvReg
   E.step = 0;
   E.akey = fold(fold(fold(kKey0, seed), (uint64_t)(int64_t)episode), 1);
   for (int i = 0; i < P.n_ports; ++i) {
-    T.idr(i) = T.soc(i) = T.de(i) = 0.0;
+    T.idr(i) = 0.0;
+    T.soc(i) = 0.0;
+    T.de(i) = 0.0;
     T.dtrem(i) = 0;
-    T.meta(i) = 0;
+    T.meta(i) = 0u;
   }
   E.b_soc = P.battery ? P.b_init_soc : 0.0;
   E.b_i = 0.0;
@@ -259,7 +311,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   double nsum[kFastNodes];
 #pragma unroll
   for (int m = 0; m < kFastNodes; ++m) nsum[m] = 0.0;
-#pragma unroll 1
+#pragma unroll 2
   for (int i = 0; i < n; ++i) {
     const double d = delta_of(act(i));
     const uint32_t mt = T.meta(i);
@@ -322,7 +374,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   double sat0 = 0.0, sat1 = 0.0;
   int nd = 0;
   uint64_t occm = 0;
-#pragma unroll 1
+#pragma unroll 2
   for (int i = 0; i < n; ++i) {
     const uint32_t mt = T.meta(i);
     double got = 0.0;
@@ -369,14 +421,16 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
         E.ep_missing += de;
         E.ep_overtime += over;
         E.ep_departures += 1;
-        T.meta(i) = 0;
-        T.idr(i) = T.soc(i) = T.de(i) = 0.0;
+        T.meta(i) = 0u;
+        T.idr(i) = 0.0;
+        T.soc(i) = 0.0;
+        T.de(i) = 0.0;
         T.dtrem(i) = 0;
         ++nd;
       } else {
         T.soc(i) = soc;
         T.de(i) = de;
-        T.dtrem(i) = (int16_t)dt;
+        T.dtrem(i) = dt;
         occm |= 1ull << i;
       }
     }
@@ -456,11 +510,11 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
         }
     }
     occm |= 1ull << port;
-    T.meta(port) = (uint8_t)(1u | (pref << 1) | ((uint32_t)car << 2));
+    T.meta(port) = 1u | (pref << 1) | ((uint32_t)car << 2);
     T.idr(port) = 0.0;
     T.soc(port) = soc0;
     T.de(port) = frac * prof[car].cap * (1.0 - soc0);
-    T.dtrem(port) = (int16_t)stay;
+    T.dtrem(port) = stay;
   }
   E.ep_declined += declined;
   if (info) {
@@ -510,7 +564,10 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
     int tover = 0;
     if (done) {
       for (int i = 0; i < n; ++i)
-        if ((T.meta(i) & 3u) == 3u && T.dtrem(i) < 0) tover += -T.dtrem(i);
+        if ((T.meta(i) & 3u) == 3u) {
+          const int dt = T.dtrem(i);
+          if (dt < 0) tover += -dt;
+        }
       double* es = O.ep_stats;
       es[b] = E.ep_profit;
       es[ld + b] = E.ep_reward;
@@ -559,13 +616,6 @@ __device__ __forceinline__ double global_feature(const Params& P, const EnvRegs&
       return __ldg(P.buy + fday * 24 + (fmin / 60) % 24);
     }
   }
-}
-
-// Staged obs cell (row r, column c): column-major 128-byte columns, the row
-// rotated by the column so per-lane writes (fixed c) and row-major read-out
-// (consecutive c) are both bank-conflict free.
-__device__ __forceinline__ float* obs_cell(uint32_t t, int obs_off, int r, int c) {
-  return reinterpret_cast<float*>(vy_smem + t + obs_off + c * 128 + ((r + c) & 31) * 4);
 }
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
@@ -621,8 +671,8 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
   const Cal C = calendar(P, E.step, E.day);
   if (store_state) tile_store(P, T.t, b0, lane);
   double* row64 = f64 ? reinterpret_cast<double*>(obs_base) + b * OL : nullptr;
-  const uint32_t cells = T.t + obs_off;
-#pragma unroll 1
+  const uint32_t cells = smem_base() + T.t + obs_off;
+#pragma unroll 2
   for (int i = 0; i < n; ++i) {
     const uint32_t mt = T.meta(i);
     const double idr = T.idr(i), soc = T.soc(i), de = T.de(i);
@@ -644,8 +694,7 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
       const uint32_t col = cells + 6 * i * 128;
       const int rot = lane + 6 * i;
 #pragma unroll
-      for (int f = 0; f < 6; ++f)
-        *reinterpret_cast<float*>(vy_smem + col + f * 128 + (((rot + f) & 31) << 2)) = (float)v[f];
+      for (int f = 0; f < 6; ++f) sts_f32(col + f * 128 + (((rot + f) & 31) << 2), (float)v[f]);
     }
   }
   const int ng = OL - 6 * n;
@@ -655,7 +704,7 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
     if (f64) {
       if (active) row64[c] = g;
     } else {
-      *reinterpret_cast<float*>(vy_smem + cells + c * 128 + (((lane + c) & 31) << 2)) = (float)g;
+      sts_f32(cells + c * 128 + (((lane + c) & 31) << 2), (float)g);
     }
   }
   if (f64) return;
@@ -671,12 +720,12 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
     const bool p0 = lane < OL, p1 = lane + 32 < OL, p2 = lane + 64 < OL, p3 = lane + 96 < OL;
 #pragma unroll 2
     for (int r = 0; r < rows; ++r) {
-      const unsigned char* a = vy_smem + lbase + (((r + lane) & 31) << 2);
+      const uint32_t a = lbase + (((r + lane) & 31) << 2);
       // predicated loads: columns past OL may lie past the end of the smem allocation
-      const float v0 = p0 ? *reinterpret_cast<const float*>(a) : 0.f;
-      const float v1 = p1 ? *reinterpret_cast<const float*>(a + 4096) : 0.f;
-      const float v2 = p2 ? *reinterpret_cast<const float*>(a + 8192) : 0.f;
-      const float v3 = p3 ? *reinterpret_cast<const float*>(a + 12288) : 0.f;
+      const float v0 = p0 ? lds_f32(a) : 0.f;
+      const float v1 = p1 ? lds_f32(a + 4096) : 0.f;
+      const float v2 = p2 ? lds_f32(a + 8192) : 0.f;
+      const float v3 = p3 ? lds_f32(a + 12288) : 0.f;
       if (p0) g[0] = v0;
       if (p1) g[32] = v1;
       if (p2) g[64] = v2;
@@ -686,9 +735,9 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
   } else {
     const int J = (OL + 31) >> 5;
     for (int r = 0; r < rows; ++r) {
-      const unsigned char* a = vy_smem + lbase + (((r + lane) & 31) << 2);
+      const uint32_t a = lbase + (((r + lane) & 31) << 2);
       for (int j = 0; j < J; ++j)
-        if (lane + 32 * j < OL) g[32 * j] = *reinterpret_cast<const float*>(a + j * 4096);
+        if (lane + 32 * j < OL) g[32 * j] = lds_f32(a + j * 4096);
       g += OL;
     }
   }
