@@ -120,17 +120,21 @@ namespace {
 TileLayout tile_layout(const vy_tables& t, bool rollout, bool acts) {
   TileLayout L{};
   const int n = t.n_ports;
-  int off = n * 768 + (9 + t.horizon) * 128;  // port f64 slots, then global obs columns
+  L.ports = (24 * n + 15) & ~15;
+  int off = L.ports + n * 768;
   L.dtrem = off;
   off += n * 64;
   L.meta = off;
   off += ((n * 32) + 15) & ~15;
   L.acts = off;
   if (acts) off += ((32 * (n + 1)) + 15) & ~15;
+  const int staging = 132 * t.obs_len;
   L.obs = 0;
   if (rollout) {
-    L.obs = (off + 127) & ~127;
-    off = L.obs + t.obs_len * 128;
+    L.obs = (off + 15) & ~15;
+    off = L.obs + staging;
+  } else if (off < staging) {
+    off = staging;  // in-place staging may run past the state into the dwell/meta/action area
   }
   L.bytes = (off + 127) & ~127;
   return L;

@@ -78,12 +78,15 @@ struct Profile {  // car profile: catalogue entry (or injected car)
 // Per-port fields are [port][lane]; per-env fields [lane].  The float64 port
 // slots (idr/soc/de, 256 B per port each) are reused as the obs staging area
 // once a port has been written back.
-//   [port][idr, soc, de][lane] f64   n x 768 B  (port i at i*768)
-//   global obs columns [9 + H][lane] f32 right after, so in the step kernel
-//   obs column c (any c < obs_len) is staged at c*128 (port slots reused);
-//   dwell [port][lane] i16, meta [port][lane] u8, actions [lane][n+1] u8;
-//   rollout only: a separate obs staging area (state stays resident).
+//   [pad 24n][port][idr, soc, de][lane] f64 (n x 768 B at `ports`),
+//   dwell [port][lane] i16, meta [port][lane] u8, actions [lane][n+1] u8.
+//   Obs staging: column c, row r at obs + c*132 + r*4 (33-word columns: per
+//   lane writes and per row reads are both bank-conflict free).  In the step
+//   kernel obs = 0: column block 6i..6i+5 (792 B) fits in front of port i+1's
+//   slots thanks to the 24n-byte pad, so the staging reuses the consumed port
+//   slots; rollouts keep their state and stage in a separate area.
 struct TileLayout {
+  int ports;  // byte offset of port 0's float64 slots (port i at ports + i*768)
   int dtrem, meta, acts;
   int obs;    // byte offset of obs column 0 (0 in-place; `extra` area for rollouts)
   int bytes;

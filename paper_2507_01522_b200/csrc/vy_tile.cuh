@@ -31,7 +31,13 @@ namespace vy {
 // access.  The asm is volatile so tile accesses keep program order.
 extern __shared__ __align__(128) unsigned char vy_smem[];
 
-__device__ __forceinline__ uint32_t smem_base() { return (uint32_t)__cvta_generic_to_shared(vy_smem); }
+// shared-window address of vy_smem, produced by opaque asm so it lives in a
+// register instead of being re-materialised at every use
+__device__ __forceinline__ uint32_t smem_base() {
+  uint32_t a;
+  asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(a) : "l"(vy_smem));
+  return a;
+}
 __device__ __forceinline__ double lds_f64(uint32_t a) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
@@ -101,7 +107,7 @@ struct Lane {
 
 __device__ __forceinline__ Lane make_lane(const Params& P, uint32_t tile, int lane) {
   const uint32_t b = smem_base() + tile;
-  return Lane{tile, b + lane * 8, b + P.L.dtrem + lane * 2, b + P.L.meta + lane, lane, &P.L};
+  return Lane{tile, b + P.L.ports + lane * 8, b + P.L.dtrem + lane * 2, b + P.L.meta + lane, lane, &P.L};
 }
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
@@ -125,7 +131,7 @@ __device__ __forceinline__ void tile_load(const Params& P, uint32_t toff, int64_
   const int q16 = (lane & 15) * 16;
   for (int i = lane >> 4; i < n; i += 2) {
     const int64_t g = ((int64_t)i * ld + b0) * 8 + q16;
-    unsigned char* d = t + i * 768 + q16;
+    unsigned char* d = t + L.ports + i * 768 + q16;
     cp_async16(d, reinterpret_cast<const char*>(P.st.port_i) + g);
     cp_async16(d + 256, reinterpret_cast<const char*>(P.st.port_soc) + g);
     cp_async16(d + 512, reinterpret_cast<const char*>(P.st.port_de) + g);
@@ -642,7 +648,7 @@ __device__ __forceinline__ void tile_store(const Params& P, uint32_t toff, int64
     const int64_t e = (int64_t)i * ld + b0;
     if (f < 3) {
       double* g = f == 0 ? P.st.port_i : f == 1 ? P.st.port_soc : P.st.port_de;
-      bulk_s2g(g + e, toff + i * 768 + f * 256, 256);
+      bulk_s2g(g + e, toff + P.L.ports + i * 768 + f * 256, 256);
     } else if (f == 3) {
       bulk_s2g(P.st.port_dtrem + e, toff + P.L.dtrem + i * 64, 64);
     } else {
@@ -691,10 +697,9 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
         for (int f = 0; f < 6; ++f) row64[6 * i + f] = v[f];
     } else {
       __syncwarp();  // in place: every lane has read port i before its slots are reused
-      const uint32_t col = cells + 6 * i * 128;
-      const int rot = lane + 6 * i;
+      const uint32_t col = cells + 6 * i * 132 + lane * 4;
 #pragma unroll
-      for (int f = 0; f < 6; ++f) sts_f32(col + f * 128 + (((rot + f) & 31) << 2), (float)v[f]);
+      for (int f = 0; f < 6; ++f) sts_f32(col + f * 132, (float)v[f]);
     }
   }
   const int ng = OL - 6 * n;
@@ -704,28 +709,27 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
     if (f64) {
       if (active) row64[c] = g;
     } else {
-      sts_f32(cells + c * 128 + (((lane + c) & 31) << 2), (float)g);
+      sts_f32(cells + c * 132 + lane * 4, (float)g);
     }
   }
   if (f64) return;
   __syncwarp();
   // Row-major read-out: row r, column c = lane + 32 j lives at
-  // cells + c*128 + ((r + c) & 31)*4 = cells + lane*128 + ((r + lane) & 31)*4 + j*4096,
-  // so per row each lane needs one rotated base and immediate offsets.
+  // cells + c*132 + r*4 = cells + lane*132 + r*4 + j*4224; bank (lane + r) % 32.
   float* g = reinterpret_cast<float*>(obs_base) + b0 * OL + lane;
   const int64_t left = P.B - b0;
   const int rows = left >= 32 ? 32 : (int)left;
-  const uint32_t lbase = cells + lane * 128;
+  const uint32_t lbase = cells + lane * 132;
   if (OL <= 128) {
     const bool p0 = lane < OL, p1 = lane + 32 < OL, p2 = lane + 64 < OL, p3 = lane + 96 < OL;
 #pragma unroll 2
     for (int r = 0; r < rows; ++r) {
-      const uint32_t a = lbase + (((r + lane) & 31) << 2);
+      const uint32_t a = lbase + r * 4;
       // predicated loads: columns past OL may lie past the end of the smem allocation
       const float v0 = p0 ? lds_f32(a) : 0.f;
-      const float v1 = p1 ? lds_f32(a + 4096) : 0.f;
-      const float v2 = p2 ? lds_f32(a + 8192) : 0.f;
-      const float v3 = p3 ? lds_f32(a + 12288) : 0.f;
+      const float v1 = p1 ? lds_f32(a + 4224) : 0.f;
+      const float v2 = p2 ? lds_f32(a + 8448) : 0.f;
+      const float v3 = p3 ? lds_f32(a + 12672) : 0.f;
       if (p0) g[0] = v0;
       if (p1) g[32] = v1;
       if (p2) g[64] = v2;
@@ -735,9 +739,9 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
   } else {
     const int J = (OL + 31) >> 5;
     for (int r = 0; r < rows; ++r) {
-      const uint32_t a = lbase + (((r + lane) & 31) << 2);
+      const uint32_t a = lbase + r * 4;
       for (int j = 0; j < J; ++j)
-        if (lane + 32 * j < OL) g[32 * j] = lds_f32(a + j * 4096);
+        if (lane + 32 * j < OL) g[32 * j] = lds_f32(a + j * 4224);
       g += OL;
     }
   }
