@@ -44,12 +44,17 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
   const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
-  tile_load(P, tile, b0, lane, P.act_tile);
+  tile_issue(P, tile, b0, lane, P.act_tile);
   EnvRegs E{};  // zero for padding lanes so the obs path stays in bounds
+  if (active) load_env(P, b, E);
+  // exogenous inputs for this step and the obs globals of the next one, in
+  // flight together with the tile copies
+  const Frame F = load_frame(P, E.step, E.day);
+  const ObsGlobals G = load_obs_globals(P, E.step + 1, E.day);
+  tile_wait();
   double rew = 0.0;
   bool done = false, reset = false;
   if (active) {
-    load_env(P, b, E);
     const int dt = P.act_dtype;
     const int64_t rs = P.act_row, cs = P.act_col;
     const uint32_t arow = smem_base() + tile + P.L.acts + lane * (P.n_ports + 1);
@@ -62,7 +67,7 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
       const long long v = __ldg(reinterpret_cast<const long long*>(P.actions) + at);
       return v < INT_MIN ? INT_MIN : (v > INT_MAX ? INT_MAX : (int)v);
     };
-    const StepResult r = tile_step(P, prof, dtab, T, E, b, act);
+    const StepResult r = tile_step(P, prof, dtab, T, E, b, F, act);
     rew = r.reward;
     done = r.done;
     if (done && (P.flags & VY_F_AUTO_RESET)) {
@@ -78,7 +83,7 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
       reinterpret_cast<float*>(P.out.reward)[b] = (float)rew;
     P.out.done[b] = done;
   }
-  emit_obs(P, prof, T, E, b0, active, P.out.obs, /*store_state=*/true);
+  emit_obs(P, prof, T, E, G, b0, active, P.out.obs, /*store_state=*/true);
 }
 
 __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params P, int T_steps, uint64_t policy_seed,
@@ -94,7 +99,8 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
   const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
-  tile_load(P, tile, b0, lane, false);
+  tile_issue(P, tile, b0, lane, false);
+  tile_wait();
   EnvRegs E{};  // zero for padding lanes so the obs path stays in bounds
   uint64_t pkey = 0, seed = 0;
   int episode = 0;
@@ -110,7 +116,8 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
     if (active) {
       const uint64_t j0 = (uint64_t)(call0 + t) * (uint64_t)ns;
       auto act = [&](int slot) -> int { return policy_action(pkey, j0 + slot + 1, hi); };
-      const StepResult r = tile_step(P, prof, dtab, T, E, b, act);
+      const Frame F = load_frame(P, E.step, E.day);
+      const StepResult r = tile_step(P, prof, dtab, T, E, b, F, act);
       if (r.done) {
         ++episode;
         reset_env(P, T, E, seed, episode, 0, false);
@@ -123,7 +130,7 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
     }
     void* obs_t = f64 ? (void*)(reinterpret_cast<double*>(P.out.obs) + t * obs_stride)
                       : (void*)(reinterpret_cast<float*>(P.out.obs) + t * obs_stride);
-    emit_obs(P, prof, T, E, b0, active, obs_t, /*store_state=*/t == T_steps - 1);
+    emit_obs(P, prof, T, E, load_obs_globals(P, E.step, E.day), b0, active, obs_t, /*store_state=*/t == T_steps - 1);
   }
   if (active) {
     store_env(P, b, E, true);
@@ -144,7 +151,8 @@ __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P,
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
   // masked-out envs keep their state: stage the tile so the write-back is a no-op for them
-  tile_load(P, tile, b0, lane, false);
+  tile_issue(P, tile, b0, lane, false);
+  tile_wait();
   const bool mine = active && (!mask || mask[b]);
   EnvRegs E{};  // zero for padding lanes so the obs path stays in bounds
   if (active) load_env(P, b, E);
@@ -155,7 +163,7 @@ __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P,
     store_env(P, b, E, true);
   }
   // masked-out rows still get their (unchanged) obs rewritten, which is idempotent
-  emit_obs(P, prof, T, E, b0, active, P.out.obs, /*store_state=*/true);
+  emit_obs(P, prof, T, E, load_obs_globals(P, E.step, E.day), b0, active, P.out.obs, /*store_state=*/true);
 }
 
 }  // namespace vy

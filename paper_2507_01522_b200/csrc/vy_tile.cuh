@@ -123,7 +123,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // column of 32 envs is one contiguous run in the port-major global layout;
 // lanes copy 16 B each.  The uint8 action block of the 32 envs is contiguous
 // too (row-major [B][n+1]).
-__device__ __forceinline__ void tile_load(const Params& P, uint32_t toff, int64_t b0, int lane, bool with_acts) {
+__device__ __forceinline__ void tile_issue(const Params& P, uint32_t toff, int64_t b0, int lane, bool with_acts) {
   unsigned char* t = vy_smem + toff;
   const int n = P.n_ports;
   const int64_t ld = P.ld;
@@ -149,6 +149,9 @@ __device__ __forceinline__ void tile_load(const Params& P, uint32_t toff, int64_
     const char* asrc = reinterpret_cast<const char*>(P.actions) + b0 * (n + 1);
     for (int o = lane * 16; o < bytes; o += 512) cp_async16(t + L.acts + o, asrc + o);
   }
+}
+
+__device__ __forceinline__ void tile_wait() {
   cp_async_wait_all();
   __syncwarp();
 }
@@ -284,24 +287,65 @@ struct StepResult {
   bool done;
 };
 
+// Exogenous inputs of the step at (step, day) (_kernel.pyx:289-295), loaded
+// before the tile's cp.async copies are awaited so their latency overlaps.
+struct Frame {
+  double p_buy, p_sg, moer, dgrid, pthr;
+  int hidx, lam_idx, pfull;
+};
+__device__ __forceinline__ Frame load_frame(const Params& P, int t, int day) {
+  Frame F;
+  const int64_t minutes = (int64_t)t * P.dt_min;
+  const int eff_day = (int)(((int64_t)day + minutes / 1440) % P.n_days);
+  F.hidx = eff_day * 24 + (int)((minutes / 60) % 24);
+  F.p_buy = __ldg(P.buy + F.hidx);
+  F.p_sg = __ldg(P.sellg + F.hidx);
+  F.moer = P.has_moer ? __ldg(P.moer + F.hidx) : 0.0;
+  F.dgrid = P.has_dgrid ? __ldg(P.dgrid + F.hidx) : 0.0;
+  F.lam_idx = (__ldg(P.weekday + eff_day) ? 0 : P.lam_len) + t % P.lam_len;
+  F.pfull = __ldg(P.pois_full + F.lam_idx);
+  F.pthr = __ldg(P.pois_thr + F.lam_idx);
+  return F;
+}
+
+// Observation globals at (step, day) (_kernel.pyx:577-603): buy, sellg, sin, cos,
+// weekday, day/365 — prefetched for step t+1 at the start of the step.
+struct ObsGlobals {
+  double buy, sellg, sinv, cosv, wk, dayf;
+  int step, day;
+};
+__device__ __forceinline__ ObsGlobals load_obs_globals(const Params& P, int step, int day) {
+  ObsGlobals G;
+  const int64_t minutes = (int64_t)step * P.dt_min;
+  const int eff_day = (int)(((int64_t)day + minutes / 1440) % P.n_days);
+  const int hidx = eff_day * 24 + (int)((minutes / 60) % 24);
+  const int sod = step % P.steps_per_day;
+  G.buy = __ldg(P.buy + hidx);
+  G.sellg = __ldg(P.sellg + hidx);
+  G.sinv = __ldg(P.sin_t + sod);
+  G.cosv = __ldg(P.cos_t + sod);
+  G.wk = (double)__ldg(P.weekday + eff_day);
+  G.dayf = div_rcp((double)eff_day, 365.0, P.rcp_365);
+  G.step = step;
+  G.day = day;
+  return G;
+}
+
 // One transition of one env (_kernel.pyx:283-571).  `act(slot)` returns the
 // action index of a slot; `b` is the global env index (infos / injected draws).
 template <class Act>
 __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* __restrict__ prof,
                                                 const double* __restrict__ dtab, const Lane& T, EnvRegs& E,
-                                                int64_t b, Act act) {
+                                                int64_t b, const Frame& F, Act act) {
   const int n = P.n_ports;
   const int64_t ld = P.ld;
   const bool info = P.flags & VY_F_INFOS;
   const vy_outputs& O = P.out;
   const int t = E.step;
 
-  // frame (_kernel.pyx:289-295)
-  const int64_t minutes = (int64_t)t * P.dt_min;
-  const int eff_day = (int)(((int64_t)E.day + minutes / 1440) % P.n_days);
-  const int hidx = eff_day * 24 + (int)((minutes / 60) % 24);
-  const double p_buy = __ldg(P.buy + hidx), p_sg = __ldg(P.sellg + hidx);
-  const int lam_idx = (__ldg(P.weekday + eff_day) ? 0 : P.lam_len) + t % P.lam_len;
+  const double p_buy = F.p_buy, p_sg = F.p_sg;
+  const int hidx = F.hidx;
+  (void)hidx;
 
   // phase 1: apply actions (_kernel.pyx:297-356); the clipped current replaces
   // i_drawn in its smem slot, node loads accumulate in leaf order on the fly
@@ -471,10 +515,10 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
     inj0 = P.inj.off[b];
     m = P.inj.off[b + 1] - (int)inj0;
   } else {
-    const int full = __ldg(P.pois_full + lam_idx);
+    const int full = F.pfull;
     if (full >= 0) {
       for (int c = 0; c < full; ++c) m += knuth(st, P.thr32);
-      m += knuth(st, __ldg(P.pois_thr + lam_idx));
+      m += knuth(st, F.pthr);
     }
   }
   const int nfree = n - __popcll(occm);
@@ -535,12 +579,12 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   c[0] = excess;
   c[1] = sat0;
   c[2] = sat1;
-  c[3] = P.has_moer ? __ldg(P.moer + hidx) * e_grid_net : 0.0;
+  c[3] = P.has_moer ? F.moer * e_grid_net : 0.0;
   c[4] = (double)declined;
   c[5] = e_b < 0.0 ? -e_b : 0.0;
   c[6] = e_out < 0.0 ? -e_out : 0.0;
   if (P.has_dgrid) {
-    const double d = e_net - __ldg(P.dgrid + hidx);
+    const double d = e_net - F.dgrid;
     c[7] = d >= 0.0 ? d : -d;
   } else {
     c[7] = 0.0;
@@ -591,39 +635,6 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
 
 // ---- observation (_kernel.pyx:575-607; layout config.py:99-130) ----------------
 
-struct Cal {
-  int eff_day, hidx, sod;
-};
-__device__ __forceinline__ Cal calendar(const Params& P, int step, int day) {
-  const int64_t minutes = (int64_t)step * P.dt_min;
-  Cal c;
-  c.eff_day = (int)(((int64_t)day + minutes / 1440) % P.n_days);
-  c.hidx = c.eff_day * 24 + (int)((minutes / 60) % 24);
-  c.sod = step % P.steps_per_day;
-  return c;
-}
-
-// globals: battery [soc, I/Imax], [buy, sellg, p_sell, sin, cos, weekday, day/365], horizon
-__device__ __forceinline__ double global_feature(const Params& P, const EnvRegs& E, const Cal& C, int k) {
-  switch (k) {
-    case 0: return E.b_soc;
-    case 1: return E.b_i == 0.0 ? E.b_i : div_rcp(E.b_i, P.b_idenom, P.b_rcp_idenom);
-    case 2: return __ldg(P.buy + C.hidx);
-    case 3: return __ldg(P.sellg + C.hidx);
-    case 4: return P.p_sell;
-    case 5: return __ldg(P.sin_t + C.sod);
-    case 6: return __ldg(P.cos_t + C.sod);
-    case 7: return (double)__ldg(P.weekday + C.eff_day);
-    case 8: return div_rcp((double)C.eff_day, 365.0, P.rcp_365);
-    default: {
-      const int h = k - 9;
-      const int64_t fmin = (int64_t)(E.step + 1 + h) * P.dt_min;
-      const int64_t fday = ((int64_t)E.day + fmin / 1440) % P.n_days;
-      return __ldg(P.buy + fday * 24 + (fmin / 60) % 24);
-    }
-  }
-}
-
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_s2g(void* gdst, uint32_t soff, uint32_t bytes) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(vy_smem + soff);
@@ -667,14 +678,14 @@ __device__ __forceinline__ void tile_store(const Params& P, uint32_t toff, int64
 // written per lane.  In the step kernel the staging area is the tile's own
 // float64 port slots (obs_off == 0), free once the state has been written back.
 __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, const Lane& T, const EnvRegs& E,
-                                         int64_t b0, bool active, void* obs_base, bool store_state) {
+                                         ObsGlobals G, int64_t b0, bool active, void* obs_base, bool store_state) {
   const int n = P.n_ports;
   const int lane = T.lane;
   const int64_t b = b0 + lane;
   const int OL = P.obs_len;
   const int obs_off = P.L.obs;
   const bool f64 = P.flags & VY_F_OUT_F64;
-  const Cal C = calendar(P, E.step, E.day);
+  if (G.step != E.step || G.day != E.day) G = load_obs_globals(P, E.step, E.day);  // auto-reset happened
   if (store_state) tile_store(P, T.t, b0, lane);
   double* row64 = f64 ? reinterpret_cast<double*>(obs_base) + b * OL : nullptr;
   const uint32_t cells = smem_base() + T.t + obs_off;
@@ -702,14 +713,34 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
       for (int f = 0; f < 6; ++f) sts_f32(col + f * 132, (float)v[f]);
     }
   }
-  const int ng = OL - 6 * n;
-  for (int k = 0; k < ng; ++k) {
-    const double g = global_feature(P, E, C, k);
-    const int c = 6 * n + k;
+  // globals: battery [soc, I/Imax], [buy, sellg, p_sell, sin, cos, weekday, day/365], horizon
+  double gv[9];
+  gv[0] = E.b_soc;
+  gv[1] = div_rcp(E.b_i, P.b_idenom, P.b_rcp_idenom);
+  gv[2] = G.buy;
+  gv[3] = G.sellg;
+  gv[4] = P.p_sell;
+  gv[5] = G.sinv;
+  gv[6] = G.cosv;
+  gv[7] = G.wk;
+  gv[8] = G.dayf;
+  const int c0 = 6 * n;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
     if (f64) {
-      if (active) row64[c] = g;
+      if (active) row64[c0 + k] = gv[k];
     } else {
-      sts_f32(cells + c * 132 + lane * 4, (float)g);
+      sts_f32(cells + (c0 + k) * 132 + lane * 4, (float)gv[k]);
+    }
+  }
+  for (int h = 0; h < P.horizon; ++h) {
+    const int64_t fmin = (int64_t)(E.step + 1 + h) * P.dt_min;
+    const int64_t fday = ((int64_t)E.day + fmin / 1440) % P.n_days;
+    const double v = __ldg(P.buy + fday * 24 + (fmin / 60) % 24);
+    if (f64) {
+      if (active) row64[c0 + 9 + h] = v;
+    } else {
+      sts_f32(cells + (c0 + 9 + h) * 132 + lane * 4, (float)v);
     }
   }
   if (f64) return;
