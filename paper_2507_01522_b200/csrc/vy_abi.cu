@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -254,23 +255,30 @@ struct Geometry {
   unsigned grid;
 };
 
+// Warps per CTA: fill the SM's shared memory with as many warp tiles as
+// possible (several CTAs per SM when they fit, else one large CTA).
 template <typename K>
-int geometry(vy_handle* h, K kernel, const TileLayout& L, Geometry& g) {
+int geometry(vy_handle* h, K kernel, const TileLayout& L, int n_profiles, Geometry& g) {
   const int per_sm = h->smem_per_sm;
+  const int tb = tables_bytes(n_profiles, h->t.k);
   int best_w = 1, best_total = 0;
-  for (int w = 1; w <= 8; ++w) {
-    const int bytes = kTablesBytes + w * L.bytes;
-    if (bytes > per_sm - 1024) break;
+  for (int w = 1; w <= 8; ++w) {  // __launch_bounds__(256)
+    const int bytes = tb + w * L.bytes;
+    if (bytes + 1024 > per_sm) break;
     const int blocks = per_sm / (bytes + 1024);
     const int total = blocks * w;
-    if (blocks >= 1 && total > best_total) {
+    if (blocks >= 1 && total >= best_total) {  // ties: prefer larger CTAs (fewer table copies)
       best_total = total;
       best_w = w;
     }
   }
+  if (const char* ov = std::getenv("VY_WARPS_PER_CTA")) {  // tuning override
+    const int w = std::atoi(ov);
+    if (w >= 1 && w <= 8 && tb + w * L.bytes + 1024 <= per_sm) best_w = w;
+  }
   g.warps = best_w;
-  g.smem = kTablesBytes + best_w * L.bytes;
-  if (g.smem > per_sm - 1024) return fail(VY_ERR_UNSUPPORTED, "station too large for one shared-memory tile");
+  g.smem = tb + best_w * L.bytes;
+  if (g.smem + 1024 > per_sm) return fail(VY_ERR_UNSUPPORTED, "station too large for one shared-memory tile");
   if (g.smem > 48 * 1024)
     VY_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem));
   const int64_t tiles = (h->B + 31) / 32;
@@ -464,7 +472,7 @@ int vy_reset(vy_handle* h, const uint8_t* mask, int32_t episode_mode, const int3
   fill(h, P, false, false);
   P.flags = flags;
   Geometry g;
-  if (int rc = geometry(h, k_reset, P.L, g)) return rc;
+  if (int rc = geometry(h, k_reset, P.L, P.n_profiles, g)) return rc;
   k_reset<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P, mask, episode_mode, inj_day);
   VY_CUDA(cudaGetLastError());
   ++h->launches;
@@ -504,7 +512,7 @@ int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride
   P.act_col = col_stride;
   if (inj) P.inj = *inj;
   Geometry g;
-  if (int rc = geometry(h, k_step, P.L, g)) return rc;
+  if (int rc = geometry(h, k_step, P.L, P.n_profiles, g)) return rc;
   k_step<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P);
   VY_CUDA(cudaGetLastError());
   ++h->launches;
@@ -536,7 +544,7 @@ int vy_rollout(vy_handle* h, int32_t T, uint64_t policy_seed, int64_t index0, in
   P.out.reward = reward;
   P.out.done = done;
   Geometry g;
-  if (int rc = geometry(h, k_rollout, P.L, g)) return rc;
+  if (int rc = geometry(h, k_rollout, P.L, P.n_profiles, g)) return rc;
   k_rollout<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P, T, policy_seed, index0, call0, obs_step_stride,
                                                                    rew_step_stride);
   VY_CUDA(cudaGetLastError());

@@ -16,15 +16,19 @@
 
 namespace vy {
 
-constexpr int kTablesBytes = ((kMaxProfiles * (int)sizeof(Profile) + 256 * 8) + 127) & ~127;
 constexpr int kProfileWords = (int)(sizeof(Profile) / 8);
+// per-CTA table area: live car profiles, then the (a-k)/k action grid
+__host__ __device__ inline int tables_bytes(int n_profiles, int k) {
+  const int nd = (2 * k + 1) <= 256 ? (2 * k + 1) : 0;
+  return (n_profiles * (int)sizeof(Profile) + nd * 8 + 127) & ~127;
+}
 
 __device__ __forceinline__ void stage_tables(const Params& P, const Profile*& prof, const double*& dtab) {
   unsigned char* smem = vy_smem;
   double* spd = reinterpret_cast<double*>(smem);
   const double* gp = reinterpret_cast<const double*>(P.profiles);
   for (int i = threadIdx.x; i < P.n_profiles * kProfileWords; i += blockDim.x) spd[i] = __ldg(gp + i);
-  double* sd = reinterpret_cast<double*>(smem + kMaxProfiles * sizeof(Profile));
+  double* sd = reinterpret_cast<double*>(smem + P.n_profiles * sizeof(Profile));
   const int nd = 2 * P.k + 1;
   if (nd <= 256)
     for (int i = threadIdx.x; i < nd; i += blockDim.x) sd[i] = __ldg(P.delta_tab + i);
@@ -33,20 +37,15 @@ __device__ __forceinline__ void stage_tables(const Params& P, const Profile*& pr
   dtab = nd <= 256 ? sd : nullptr;
 }
 
-__global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) {
-  const Profile* prof;
-  const double* dtab;
-  stage_tables(P, prof, dtab);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
-  if (b0 >= P.B) return;  // whole warp leaves together
-  const uint32_t tile = kTablesBytes + warp * P.L.bytes;
+// One step of the 32 envs of the tile starting at env b0.
+__device__ __forceinline__ void step_tile(const Params& P, const Profile* prof, const double* dtab, uint32_t tile,
+                                          int64_t b0, int lane) {
   const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
-  tile_issue(P, tile, b0, lane, P.act_tile);
   EnvRegs E{};  // zero for padding lanes so the obs path stays in bounds
   if (active) load_env(P, b, E);
+  tile_issue(P, tile, b0, lane, P.act_tile);
   // exogenous inputs for this step and the obs globals of the next one, in
   // flight together with the tile copies
   const Frame F = load_frame(P, E.step, E.day);
@@ -67,7 +66,8 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
       const long long v = __ldg(reinterpret_cast<const long long*>(P.actions) + at);
       return v < INT_MIN ? INT_MIN : (v > INT_MAX ? INT_MAX : (int)v);
     };
-    const StepResult r = tile_step(P, prof, dtab, T, E, b, F, act);
+    StepResult r{0.0, false};
+    if (!(P.flags & 0x200u)) r = tile_step(P, prof, dtab, T, E, b, F, act);  // 0x200: memory-only probe
     rew = r.reward;
     done = r.done;
     if (done && (P.flags & VY_F_AUTO_RESET)) {
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
       P.st.episode[b] = ep;
       reset = true;
     }
-    store_env(P, b, E, reset);
+    if (!(P.flags & 0x800u)) store_env(P, b, E, reset);
     if (P.flags & VY_F_OUT_F64)
       reinterpret_cast<double*>(P.out.reward)[b] = rew;
     else
@@ -84,6 +84,19 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
     P.out.done[b] = done;
   }
   emit_obs(P, prof, T, E, G, b0, active, P.out.obs, /*store_state=*/true);
+}
+
+// One warp per tile.  (A persistent variant with L2 bulk prefetch of the next
+// tile measured slower: the kernel is bound by per-warp latency, not by DRAM
+// requests in flight.)
+__global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) {
+  const Profile* prof;
+  const double* dtab;
+  stage_tables(P, prof, dtab);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
+  if (b0 >= P.B) return;  // whole warp leaves together
+  step_tile(P, prof, dtab, tables_bytes(P.n_profiles, P.k) + warp * P.L.bytes, b0, lane);
 }
 
 __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params P, int T_steps, uint64_t policy_seed,
@@ -95,7 +108,7 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
   if (b0 >= P.B) return;
-  const uint32_t tile = kTablesBytes + warp * P.L.bytes;
+  const uint32_t tile = tables_bytes(P.n_profiles, P.k) + warp * P.L.bytes;
   const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
@@ -146,7 +159,7 @@ __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
   if (b0 >= P.B) return;
-  const uint32_t tile = kTablesBytes + warp * P.L.bytes;
+  const uint32_t tile = tables_bytes(P.n_profiles, P.k) + warp * P.L.bytes;
   const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
   const bool active = b < P.B;

@@ -65,6 +65,41 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
 }
 __device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v)); }
 
+// Global loads issued exactly where written (volatile asm): the compiler
+// otherwise sinks early loads next to their first use at the end of the step,
+// exposing the full DRAM latency there instead of overlapping it with the
+// tile copies.
+__device__ __forceinline__ double ldg_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ldg_nc_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ldg_s32(const int32_t* p) {
+  int v;
+  asm volatile("ld.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ldg_nc_s32(const int* p) {
+  int v;
+  asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint64_t ldg_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ldg_nc_s8(const int8_t* p) {
+  int v;
+  asm volatile("ld.global.nc.s8 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
 struct EnvRegs {
   int step, day;
   uint64_t akey;
@@ -158,18 +193,18 @@ __device__ __forceinline__ void tile_wait() {
 
 __device__ __forceinline__ void load_env(const Params& P, int64_t b, EnvRegs& E) {
   const vy_state& s = P.st;
-  E.step = s.step[b];
-  E.day = s.day[b];
-  E.akey = s.akey[b];
-  E.b_i = P.battery ? s.b_i[b] : 0.0;
-  E.b_soc = P.battery ? s.b_soc[b] : 0.0;
-  E.ep_profit = s.ep_profit[b];
-  E.ep_reward = s.ep_reward[b];
-  E.ep_missing = s.ep_missing[b];
-  E.ep_energy = s.ep_energy[b];
-  E.ep_overtime = s.ep_overtime[b];
-  E.ep_declined = s.ep_declined[b];
-  E.ep_departures = s.ep_departures[b];
+  E.step = ldg_s32(s.step + b);
+  E.day = ldg_s32(s.day + b);
+  E.akey = ldg_u64(s.akey + b);
+  E.b_i = P.battery ? ldg_f64(s.b_i + b) : 0.0;
+  E.b_soc = P.battery ? ldg_f64(s.b_soc + b) : 0.0;
+  E.ep_profit = ldg_f64(s.ep_profit + b);
+  E.ep_reward = ldg_f64(s.ep_reward + b);
+  E.ep_missing = ldg_f64(s.ep_missing + b);
+  E.ep_energy = ldg_f64(s.ep_energy + b);
+  E.ep_overtime = ldg_s32(s.ep_overtime + b);
+  E.ep_declined = ldg_s32(s.ep_declined + b);
+  E.ep_departures = ldg_s32(s.ep_departures + b);
 }
 
 __device__ __forceinline__ void store_env(const Params& P, int64_t b, const EnvRegs& E, bool reset_too) {
@@ -298,13 +333,13 @@ __device__ __forceinline__ Frame load_frame(const Params& P, int t, int day) {
   const int64_t minutes = (int64_t)t * P.dt_min;
   const int eff_day = (int)(((int64_t)day + minutes / 1440) % P.n_days);
   F.hidx = eff_day * 24 + (int)((minutes / 60) % 24);
-  F.p_buy = __ldg(P.buy + F.hidx);
-  F.p_sg = __ldg(P.sellg + F.hidx);
-  F.moer = P.has_moer ? __ldg(P.moer + F.hidx) : 0.0;
-  F.dgrid = P.has_dgrid ? __ldg(P.dgrid + F.hidx) : 0.0;
-  F.lam_idx = (__ldg(P.weekday + eff_day) ? 0 : P.lam_len) + t % P.lam_len;
-  F.pfull = __ldg(P.pois_full + F.lam_idx);
-  F.pthr = __ldg(P.pois_thr + F.lam_idx);
+  F.p_buy = ldg_nc_f64(P.buy + F.hidx);
+  F.p_sg = ldg_nc_f64(P.sellg + F.hidx);
+  F.moer = P.has_moer ? ldg_nc_f64(P.moer + F.hidx) : 0.0;
+  F.dgrid = P.has_dgrid ? ldg_nc_f64(P.dgrid + F.hidx) : 0.0;
+  F.lam_idx = (ldg_nc_s8(P.weekday + eff_day) ? 0 : P.lam_len) + t % P.lam_len;
+  F.pfull = ldg_nc_s32(P.pois_full + F.lam_idx);
+  F.pthr = ldg_nc_f64(P.pois_thr + F.lam_idx);
   return F;
 }
 
@@ -320,11 +355,11 @@ __device__ __forceinline__ ObsGlobals load_obs_globals(const Params& P, int step
   const int eff_day = (int)(((int64_t)day + minutes / 1440) % P.n_days);
   const int hidx = eff_day * 24 + (int)((minutes / 60) % 24);
   const int sod = step % P.steps_per_day;
-  G.buy = __ldg(P.buy + hidx);
-  G.sellg = __ldg(P.sellg + hidx);
-  G.sinv = __ldg(P.sin_t + sod);
-  G.cosv = __ldg(P.cos_t + sod);
-  G.wk = (double)__ldg(P.weekday + eff_day);
+  G.buy = ldg_nc_f64(P.buy + hidx);
+  G.sellg = ldg_nc_f64(P.sellg + hidx);
+  G.sinv = ldg_nc_f64(P.sin_t + sod);
+  G.cosv = ldg_nc_f64(P.cos_t + sod);
+  G.wk = (double)ldg_nc_s8(P.weekday + eff_day);
   G.dayf = div_rcp((double)eff_day, 365.0, P.rcp_365);
   G.step = step;
   G.day = day;
@@ -686,7 +721,7 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
   const int obs_off = P.L.obs;
   const bool f64 = P.flags & VY_F_OUT_F64;
   if (G.step != E.step || G.day != E.day) G = load_obs_globals(P, E.step, E.day);  // auto-reset happened
-  if (store_state) tile_store(P, T.t, b0, lane);
+  if (store_state && !(P.flags & 0x800u)) tile_store(P, T.t, b0, lane);
   double* row64 = f64 ? reinterpret_cast<double*>(obs_base) + b * OL : nullptr;
   const uint32_t cells = smem_base() + T.t + obs_off;
 #pragma unroll 2
@@ -751,6 +786,7 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
   const int64_t left = P.B - b0;
   const int rows = left >= 32 ? 32 : (int)left;
   const uint32_t lbase = cells + lane * 132;
+  if (P.flags & 0x400u) return;
   if (OL <= 128) {
     const bool p0 = lane < OL, p1 = lane + 32 < OL, p2 = lane + 64 < OL, p3 = lane + 96 < OL;
 #pragma unroll 2
