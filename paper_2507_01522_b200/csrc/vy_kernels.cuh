@@ -56,10 +56,10 @@ __device__ __forceinline__ void step_tile(const Params& P, const Profile* prof, 
   if (active) {
     const int dt = P.act_dtype;
     const int64_t rs = P.act_row, cs = P.act_col;
-    const uint32_t arow = smem_base() + tile + P.L.acts + lane * (P.n_ports + 1);
+    const uint8_t* arow = vy_smem + tile + P.L.acts + lane * (P.n_ports + 1);
     const bool staged = P.act_tile;
     auto act = [&](int slot) -> int {
-      if (staged) return (int)lds_u8(arow + slot);
+      if (staged) return arow[slot];
       const int64_t at = b * rs + slot * cs;
       if (dt == VY_ACT_U8) return __ldg(reinterpret_cast<const uint8_t*>(P.actions) + at);
       if (dt == VY_ACT_I32) return __ldg(reinterpret_cast<const int32_t*>(P.actions) + at);

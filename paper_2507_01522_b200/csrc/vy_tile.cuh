@@ -125,24 +125,27 @@ struct SU8 {
   __device__ __forceinline__ void operator=(uint32_t v) const { sts_u8(a, v); }
 };
 
-// one lane's view of its warp's tile
+// One lane's view of its warp's tile.  Plain C++ references into vy_smem
+// (the compiler infers the shared address space and emits LDS/STS) so loads
+// of one port may be scheduled ahead of stores to another in unrolled loops.
 struct Lane {
-  uint32_t t;   // byte offset of the warp's tile in vy_smem
-  uint32_t s;   // shared-window address of this lane's column 0 of the tile (port slots)
-  uint32_t sd;  // shared-window address of this lane's dwell entry of port 0
-  uint32_t sm;  // shared-window address of this lane's meta entry of port 0
+  uint32_t t;  // byte offset of the warp's tile in vy_smem
+  double* p;   // this lane's i_drawn slot of port 0 (soc at +32, de at +64 doubles; ports 96 apart)
+  int16_t* d;  // this lane's dwell entry of port 0 (ports 32 apart)
+  uint8_t* m;  // this lane's meta entry of port 0 (ports 32 apart)
   int lane;
   const TileLayout* L;
-  __device__ __forceinline__ SF64 idr(int i) const { return {s + i * 768}; }
-  __device__ __forceinline__ SF64 soc(int i) const { return {s + i * 768 + 256}; }
-  __device__ __forceinline__ SF64 de(int i) const { return {s + i * 768 + 512}; }
-  __device__ __forceinline__ SS16 dtrem(int i) const { return {sd + i * 64}; }
-  __device__ __forceinline__ SU8 meta(int i) const { return {sm + i * 32}; }
+  __device__ __forceinline__ double& idr(int i) const { return p[i * 96]; }
+  __device__ __forceinline__ double& soc(int i) const { return p[i * 96 + 32]; }
+  __device__ __forceinline__ double& de(int i) const { return p[i * 96 + 64]; }
+  __device__ __forceinline__ int16_t& dtrem(int i) const { return d[i * 32]; }
+  __device__ __forceinline__ uint8_t& meta(int i) const { return m[i * 32]; }
 };
 
 __device__ __forceinline__ Lane make_lane(const Params& P, uint32_t tile, int lane) {
-  const uint32_t b = smem_base() + tile;
-  return Lane{tile, b + P.L.ports + lane * 8, b + P.L.dtrem + lane * 2, b + P.L.meta + lane, lane, &P.L};
+  unsigned char* b = vy_smem + tile;
+  return Lane{tile, reinterpret_cast<double*>(b + P.L.ports + lane * 8),
+              reinterpret_cast<int16_t*>(b + P.L.dtrem + lane * 2), b + P.L.meta + lane, lane, &P.L};
 }
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
@@ -309,7 +312,7 @@ __device__ __forceinline__ void reset_env(const Params& P, const Lane& T, EnvReg
     T.soc(i) = 0.0;
     T.de(i) = 0.0;
     T.dtrem(i) = 0;
-    T.meta(i) = 0u;
+    T.meta(i) = 0;
   }
   E.b_soc = P.battery ? P.b_init_soc : 0.0;
   E.b_i = 0.0;
@@ -506,7 +509,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
         E.ep_missing += de;
         E.ep_overtime += over;
         E.ep_departures += 1;
-        T.meta(i) = 0u;
+        T.meta(i) = 0;
         T.idr(i) = 0.0;
         T.soc(i) = 0.0;
         T.de(i) = 0.0;
@@ -515,7 +518,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
       } else {
         T.soc(i) = soc;
         T.de(i) = de;
-        T.dtrem(i) = dt;
+        T.dtrem(i) = (int16_t)dt;
         occm |= 1ull << i;
       }
     }
@@ -595,11 +598,11 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
         }
     }
     occm |= 1ull << port;
-    T.meta(port) = 1u | (pref << 1) | ((uint32_t)car << 2);
+    T.meta(port) = (uint8_t)(1u | (pref << 1) | ((uint32_t)car << 2));
     T.idr(port) = 0.0;
     T.soc(port) = soc0;
     T.de(port) = frac * prof[car].cap * (1.0 - soc0);
-    T.dtrem(port) = stay;
+    T.dtrem(port) = (int16_t)stay;
   }
   E.ep_declined += declined;
   if (info) {
