@@ -231,7 +231,9 @@ def main() -> None:
     achieved = ab["per_env_step"] * B / (step_kernel_ms / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "step_kernel_dram_bytes.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and B == B_PER_GPU:
+        # dram__bytes_read.sum + dram__bytes_write.sum of one k_step launch at this workload
+        # (ncu --set full capture, summarised by scripts/summarize_ncu.py)
         with open(tpath) as fh:
             traffic = json.load(fh).get("bytes_per_launch")
 
@@ -248,7 +250,7 @@ def main() -> None:
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                      "frac": achieved / peaks.get("hbm_gbs"), "traffic": traffic,
-                     "kernel": "k_step<16>", "kernel_ms": step_kernel_ms,
+                     "kernel": "vy::k_step", "kernel_ms": step_kernel_ms,
                      "bytes_per_env_step": ab["per_env_step"],
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not peaks.get("_fallback") else "fallback"},
         "clocks": clocks.summary(),
