@@ -205,6 +205,13 @@ int vy_poll_error(vy_handle *h, int clear, void *stream, uint32_t *out);
 /* Number of kernel launches issued through this handle (for bench accounting). */
 int64_t vy_launch_count(vy_handle *h);
 
+/* PPO support (config C3): generalised advantage estimation as a reverse
+ * scan over a [T][B] rollout (float32 values/rewards, uint8 dones, last_value
+ * [B]); writes advantages and returns [T][B].  Not part of the reference
+ * (its trainer-free scope); the paper's PPO. */
+int vy_gae(const float *values, const float *rewards, const uint8_t *dones, const float *last_value, int32_t T,
+           int64_t B, float gamma, float lam, float *adv, float *ret, void *stream);
+
 /* Diagnostics: compare the kernels' reciprocal-based division (div_rcp in
  * csrc/vy_device.cuh) with IEEE x / d on `samples_per_divisor` random
  * dividends for each divisor; *mismatches receives the count (0 = bit-exact). */

@@ -201,6 +201,25 @@ class BatchEnv:
         nat.check(self._lib.vy_seed_envs(self._h, int(master_seed), self.global_offset, self._stream),
                   "vy_seed_envs")
 
+    def set_outputs(self, obs: torch.Tensor | None = None, reward: torch.Tensor | None = None,
+                    done: torch.Tensor | None = None) -> None:
+        """Redirect the per-step obs / reward / done outputs into caller buffers
+        (e.g. slices of a rollout buffer) so the kernel writes them in place."""
+        B, L = self.batch_size, self.obs_length
+        o = self.outs.ctypes()
+        for name, t, shape, dt in (("obs", obs, (B, L), self.obs_dtype), ("reward", reward, (B,), self.obs_dtype),
+                                   ("done", done, (B,), torch.uint8)):
+            if t is None:
+                continue
+            if tuple(t.shape) != shape or t.dtype != dt or not t.is_contiguous() or t.device != self.device:
+                raise ValueError(f"{name} buffer must be a contiguous {dt} tensor of shape {shape} on {self.device}")
+            setattr(o, name, t.data_ptr())
+        self._out_c = o
+        nat.check(self._lib.vy_bind(self._h, C.byref(self._st_c), C.byref(self._out_c)), "vy_bind")
+
+    def restore_outputs(self) -> None:
+        self._bind()
+
     def _flags(self, infos: bool) -> int:
         f = nat.F_AUTO_RESET if self.auto_reset else 0
         if infos:

@@ -1,0 +1,264 @@
+"""PPO on the device-resident env (BASELINE config C3).
+
+The reference ships no trainer; the paper trains a PureJaxRL PPO
+agent (hyperparameters PAPER.md:465-490).  This module is that
+loop B200-first:
+
+* rollout: policy forward (bf16 autocast on the tensor cores via cuBLAS),
+  categorical sampling over the 17 x 21 multi-discrete head, and the fused
+  env step kernel, for T steps, captured once as a CUDA graph and replayed
+  every iteration (the rollout is ~5 kernels per step; replay removes the
+  per-launch host overhead);
+* advantages: the vy_gae reverse-scan kernel (csrc/vy_ppo.cu);
+* update: clipped PPO objective with value clipping, entropy bonus, Adam,
+  global-norm gradient clipping; under torch.distributed the flattened
+  gradient is all-reduced (NCCL over NVLink) once per minibatch — the only
+  data-path collective of the whole system.
+
+Network: PureJaxRL's default actor-critic (two 64-unit tanh layers each for
+actor and critic, orthogonal init); the paper does not pin the width, so it
+is a constructor argument (recorded in the bench line).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+import torch.nn as nn
+
+from . import _native as nat
+from .batch import BatchEnv
+
+
+@dataclass
+class PPOConfig:
+    """PAPER.md:465-490 (Table 4)."""
+
+    lr: float = 2.5e-4
+    anneal_lr: bool = True
+    gamma: float = 0.99
+    gae_lambda: float = 0.95
+    max_grad_norm: float = 100.0
+    clip_eps: float = 0.2
+    vf_clip: float = 10.0
+    ent_coef: float = 0.01
+    vf_coef: float = 0.25
+    rollout_steps: int = 300
+    n_minibatches: int = 4
+    update_epochs: int = 4
+    total_timesteps: int = 10_000_000
+    hidden: int = 64
+    seed: int = 0
+    use_graph: bool = True
+
+
+def _ortho(layer: nn.Linear, gain: float) -> nn.Linear:
+    nn.init.orthogonal_(layer.weight, gain)
+    nn.init.zeros_(layer.bias)
+    return layer
+
+
+class ActorCritic(nn.Module):
+    def __init__(self, obs_dim: int, n_slots: int, n_actions: int, hidden: int = 64):
+        super().__init__()
+        self.n_slots, self.n_actions = n_slots, n_actions
+        g = math.sqrt(2.0)
+        self.actor = nn.Sequential(_ortho(nn.Linear(obs_dim, hidden), g), nn.Tanh(),
+                                   _ortho(nn.Linear(hidden, hidden), g), nn.Tanh(),
+                                   _ortho(nn.Linear(hidden, n_slots * n_actions), 0.01))
+        self.critic = nn.Sequential(_ortho(nn.Linear(obs_dim, hidden), g), nn.Tanh(),
+                                    _ortho(nn.Linear(hidden, hidden), g), nn.Tanh(),
+                                    _ortho(nn.Linear(hidden, 1), 1.0))
+
+    def forward(self, obs: torch.Tensor):
+        logits = self.actor(obs).view(-1, self.n_slots, self.n_actions).float()
+        return logits, self.critic(obs).squeeze(-1).float()
+
+
+def gae(values, rewards, dones, last_value, gamma, lam):
+    """Advantages and returns via the vy_gae kernel; [T, B] float32 / uint8 inputs."""
+    T, B = values.shape
+    adv = torch.empty_like(values)
+    ret = torch.empty_like(values)
+    rc = nat.lib().vy_gae(values.data_ptr(), rewards.data_ptr(), dones.data_ptr(), last_value.data_ptr(), T, B,
+                          C.c_float(gamma), C.c_float(lam), adv.data_ptr(), ret.data_ptr(),
+                          torch.cuda.current_stream().cuda_stream)
+    nat.check(rc, "vy_gae")
+    return adv, ret
+
+
+def gae_reference(values, rewards, dones, last_value, gamma, lam):
+    """Plain torch restatement (tests only)."""
+    T = values.shape[0]
+    adv = torch.zeros_like(values)
+    last = torch.zeros_like(last_value)
+    nxt = last_value
+    for t in range(T - 1, -1, -1):
+        nonterm = 1.0 - dones[t].float()
+        delta = rewards[t] + gamma * nxt * nonterm - values[t]
+        last = delta + gamma * lam * nonterm * last
+        adv[t] = last
+        nxt = values[t]
+    return adv, adv + values
+
+
+class PPOTrainer:
+    """Single- or multi-GPU PPO over a BatchEnv (one process per GPU)."""
+
+    def __init__(self, env: BatchEnv, cfg: PPOConfig):
+        self.env, self.cfg = env, cfg
+        dev = env.device
+        torch.manual_seed(cfg.seed + env.global_offset)
+        self.world = dist.get_world_size() if dist.is_initialized() else 1
+        self.net = ActorCritic(env.obs_length, env.action_size, env.actions_per_slot, cfg.hidden).to(dev)
+        if self.world > 1:  # identical initial weights on every rank
+            for p in self.net.parameters():
+                dist.broadcast(p.data, 0)
+        self.opt = torch.optim.Adam(self.net.parameters(), lr=cfg.lr, eps=1e-5)
+        T, B, L, A = cfg.rollout_steps, env.batch_size, env.obs_length, env.action_size
+        self.obs = torch.zeros(T + 1, B, L, device=dev)
+        self.actions = torch.zeros(T, B, A, dtype=torch.uint8, device=dev)
+        self.logp = torch.zeros(T, B, device=dev)
+        self.values = torch.zeros(T + 1, B, device=dev)
+        self.rewards = torch.zeros(T, B, device=dev)
+        self.dones = torch.zeros(T, B, dtype=torch.uint8, device=dev)
+        self.iterations = 0
+        self.n_iters = max(1, cfg.total_timesteps // (T * B * self.world))
+        self._graph = None
+        env.reset(as_numpy=False)
+        self.obs[0].copy_(env.outs.obs)
+
+    # -- rollout -----------------------------------------------------------------
+
+    def _policy_step(self, t: int) -> None:
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            logits, v = self.net(self.obs[t])
+        g = -torch.log(-torch.log(torch.rand_like(logits).clamp_(1e-20, 1.0)))  # Gumbel-max sampling
+        a = torch.argmax(logits + g, dim=-1)
+        lp = torch.log_softmax(logits, dim=-1).gather(-1, a.unsqueeze(-1)).squeeze(-1).sum(-1)
+        self.actions[t].copy_(a)
+        self.logp[t].copy_(lp)
+        self.values[t].copy_(v)
+        # the env writes the next obs / reward / done straight into the rollout buffers
+        self.env.set_outputs(obs=self.obs[t + 1], reward=self.rewards[t], done=self.dones[t])
+        self.env.step(self.actions[t], collect_infos=False)
+
+    def _rollout_body(self) -> None:
+        for t in range(self.cfg.rollout_steps):
+            self._policy_step(t)
+        with torch.no_grad(), torch.autocast("cuda", dtype=torch.bfloat16):
+            _, self.values[-1] = self.net(self.obs[-1])
+
+    @torch.no_grad()
+    def rollout(self) -> None:
+        T = self.cfg.rollout_steps
+        t0 = self.env._t
+        if not self.cfg.use_graph:
+            self._rollout_body()
+        else:
+            if self._graph is None:
+                s = torch.cuda.Stream()
+                s.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(s):  # warm-up outside capture (allocator, autocast caches)
+                    self._rollout_body()
+                torch.cuda.current_stream().wait_stream(s)
+                self.obs[0].copy_(self.obs[-1])
+                self._graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(self._graph):
+                    self._rollout_body()
+            self._graph.replay()
+        if t0 is not None:  # the host mirror of the lockstep clock is not advanced by a graph replay
+            self.env._t = (t0 + T) % self.env.tables.episode_steps
+        self.env.restore_outputs()
+
+    # -- update -------------------------------------------------------------------
+
+    def _allreduce_grads(self) -> None:
+        if self.world == 1:
+            return
+        grads = [p.grad for p in self.net.parameters() if p.grad is not None]
+        flat = torch.cat([g.reshape(-1) for g in grads])
+        dist.all_reduce(flat, op=dist.ReduceOp.AVG)
+        off = 0
+        for g in grads:
+            n = g.numel()
+            g.copy_(flat[off:off + n].view_as(g))
+            off += n
+
+    def update(self) -> dict:
+        cfg = self.cfg
+        T, B = cfg.rollout_steps, self.env.batch_size
+        adv, ret = gae(self.values[:T], self.rewards, self.dones, self.values[T], cfg.gamma, cfg.gae_lambda)
+        if cfg.anneal_lr:
+            frac = 1.0 - self.iterations / self.n_iters
+            for g in self.opt.param_groups:
+                g["lr"] = cfg.lr * max(frac, 0.0)
+        obs = self.obs[:T].reshape(T * B, -1)
+        act = self.actions.reshape(T * B, -1).long()
+        old_lp, old_v = self.logp.reshape(-1), self.values[:T].reshape(-1)
+        adv, ret = adv.reshape(-1), ret.reshape(-1)
+        n = T * B
+        mb = n // cfg.n_minibatches
+        stats = {}
+        for _ in range(cfg.update_epochs):
+            perm = torch.randperm(n, device=obs.device)
+            for k in range(cfg.n_minibatches):
+                idx = perm[k * mb:(k + 1) * mb]
+                with torch.autocast("cuda", dtype=torch.bfloat16):
+                    logits, v = self.net(obs[idx])
+                lsm = torch.log_softmax(logits, dim=-1)
+                lp = lsm.gather(-1, act[idx].unsqueeze(-1)).squeeze(-1).sum(-1)
+                ent = -(lsm.exp() * lsm).sum(-1).sum(-1).mean()
+                a = adv[idx]
+                a = (a - a.mean()) / (a.std() + 1e-8)
+                ratio = torch.exp(lp - old_lp[idx])
+                pg = -torch.min(ratio * a, torch.clamp(ratio, 1 - cfg.clip_eps, 1 + cfg.clip_eps) * a).mean()
+                v_clip = old_v[idx] + (v - old_v[idx]).clamp(-cfg.vf_clip, cfg.vf_clip)
+                vl = 0.5 * torch.max((v - ret[idx]) ** 2, (v_clip - ret[idx]) ** 2).mean()
+                loss = pg + cfg.vf_coef * vl - cfg.ent_coef * ent
+                self.opt.zero_grad(set_to_none=False)
+                loss.backward()
+                self._allreduce_grads()
+                nn.utils.clip_grad_norm_(self.net.parameters(), cfg.max_grad_norm)
+                self.opt.step()
+                stats = {"loss": loss.detach(), "pg": pg.detach(), "vf": vl.detach(), "ent": ent.detach()}
+        self.obs[0].copy_(self.obs[T])
+        self.iterations += 1
+        return stats
+
+    def iterate(self) -> dict:
+        self.rollout()
+        return self.update()
+
+
+def seconds_per_100k(trainer: PPOTrainer, iters: int, warmup: int = 1) -> dict:
+    """Wall-clock (device-synchronised) seconds per 100k env steps of rollout + update."""
+    for _ in range(warmup):
+        trainer.iterate()
+    torch.cuda.synchronize()
+    if dist.is_initialized():
+        dist.barrier()
+    t0 = time.perf_counter()
+    rewards = []
+    for _ in range(iters):
+        trainer.iterate()
+        rewards.append(trainer.rewards.mean())
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if dist.is_initialized():
+        t = torch.tensor([dt], device=trainer.env.device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    steps = iters * trainer.cfg.rollout_steps * trainer.env.batch_size * trainer.world
+    return {"s_per_100k_steps": dt / steps * 1e5, "env_steps_per_s": steps / dt, "iters": iters,
+            "mean_step_reward": float(torch.stack(rewards).mean()) if rewards else float("nan"),
+            "seconds": dt, "steps": steps}
+
+
+__all__ = ["PPOConfig", "ActorCritic", "PPOTrainer", "gae", "gae_reference", "seconds_per_100k", "np"]
