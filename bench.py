@@ -162,7 +162,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--envs", type=int, default=B_PER_GPU)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-extras", action="store_true", help="skip e2e / rollout legs (profiling runs)")
+    ap.add_argument("--no-extras", action="store_true", help="skip e2e / rollout / PPO legs (profiling runs)")
+    ap.add_argument("--ppo-iters", type=int, default=3, help="timed PPO iterations for the C3 leg (0 = skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
@@ -302,6 +303,24 @@ def main() -> None:
                          "h2d_bytes_per_step": h_act.numel(),
                          "d2h_bytes_per_step": h_obs.numel() * 4 + h_rew.numel() * 4 + h_done.numel(),
                          "path": "BatchEnv.step with pinned host actions -> obs/reward/done to pinned host"}
+
+    if not args.no_extras and args.ppo_iters > 0:
+        # config C3: PPO with 4096 envs per GPU, Table 4 hyperparameters,
+        # gradients all-reduced over NCCL when world > 1
+        from paper_2507_01522_b200.ppo import PPOConfig, PPOTrainer, seconds_per_100k
+
+        penv = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=4096, master_seed=1, global_offset=rank * 4096)
+        cfg = PPOConfig(rollout_steps=300)
+        tr = PPOTrainer(penv, cfg)
+        res = seconds_per_100k(tr, args.ppo_iters, warmup=1)
+        result["ppo"] = {"metric": "s per 100k PPO steps", "value": res["s_per_100k_steps"],
+                         "env_steps_per_s": res["env_steps_per_s"], "envs_per_gpu": 4096,
+                         "rollout_steps": cfg.rollout_steps, "epochs": cfg.update_epochs,
+                         "minibatches": cfg.n_minibatches, "hidden": cfg.hidden, "timed_iterations": args.ppo_iters,
+                         "rollout": "CUDA graph (policy fwd bf16 + Gumbel-max sampling + k_step) x 300",
+                         "grad_allreduce": "NCCL all_reduce(AVG) per minibatch" if world > 1 else "none (1 GPU)",
+                         "paper_reference": "Chargax PPO(16) 0.65 s / 100k on RTX 4000 Ada (PAPER.md:239)"}
+        penv.close()
 
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
