@@ -37,13 +37,15 @@ __device__ __forceinline__ void stage_tables(const Params& P, const Profile*& pr
   dtab = nd <= 256 ? sd : nullptr;
 }
 
-// One step of the 32 envs of the tile starting at env b0.
+// One step of the 32 envs of the tile starting at env b0.  Every lane runs
+// the transition (padding lanes on their harmless padding columns, side
+// effects masked) because the fused port loop synchronises the warp.
 __device__ __forceinline__ void step_tile(const Params& P, const Profile* prof, const double* dtab, uint32_t tile,
                                           int64_t b0, int lane) {
   const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
-  EnvRegs E{};  // zero for padding lanes so the obs path stays in bounds
+  EnvRegs E{};  // zero for padding lanes so table lookups stay in bounds
   if (active) load_env(P, b, E);
   tile_issue(P, tile, b0, lane, P.act_tile);
   // exogenous inputs for this step and the obs globals of the next one, in
@@ -51,39 +53,44 @@ __device__ __forceinline__ void step_tile(const Params& P, const Profile* prof, 
   const Frame F = load_frame(P, E.step, E.day);
   const ObsGlobals G = load_obs_globals(P, E.step + 1, E.day);
   tile_wait();
-  double rew = 0.0;
-  bool done = false, reset = false;
-  if (active) {
-    const int dt = P.act_dtype;
-    const int64_t rs = P.act_row, cs = P.act_col;
-    const uint8_t* arow = vy_smem + tile + P.L.acts + lane * (P.n_ports + 1);
-    const bool staged = P.act_tile;
-    auto act = [&](int slot) -> int {
-      if (staged) return arow[slot];
-      const int64_t at = b * rs + slot * cs;
-      if (dt == VY_ACT_U8) return __ldg(reinterpret_cast<const uint8_t*>(P.actions) + at);
-      if (dt == VY_ACT_I32) return __ldg(reinterpret_cast<const int32_t*>(P.actions) + at);
-      const long long v = __ldg(reinterpret_cast<const long long*>(P.actions) + at);
-      return v < INT_MIN ? INT_MIN : (v > INT_MAX ? INT_MAX : (int)v);
-    };
-    StepResult r{0.0, false};
-    if (!(P.flags & 0x200u)) r = tile_step(P, prof, dtab, T, E, b, F, act);  // 0x200: memory-only probe
-    rew = r.reward;
-    done = r.done;
-    if (done && (P.flags & VY_F_AUTO_RESET)) {
-      const int ep = P.st.episode[b] + 1;
-      reset_env(P, T, E, P.st.env_seed[b], ep, 0, false);
-      P.st.episode[b] = ep;
-      reset = true;
+  const ObsSink S = make_sink(P, T, b, P.out.obs, /*in_place=*/true);
+  const int dt = P.act_dtype;
+  const int64_t rs = P.act_row, cs = P.act_col;
+  const uint8_t* arow = vy_smem + tile + P.L.acts + lane * (P.n_ports + 1);
+  const bool staged = P.act_tile;
+  auto act = [&](int slot) -> int {
+    if (staged) return arow[slot];
+    if (!active) return P.k;
+    const int64_t at = b * rs + slot * cs;
+    if (dt == VY_ACT_U8) return __ldg(reinterpret_cast<const uint8_t*>(P.actions) + at);
+    if (dt == VY_ACT_I32) return __ldg(reinterpret_cast<const int32_t*>(P.actions) + at);
+    const long long v = __ldg(reinterpret_cast<const long long*>(P.actions) + at);
+    return v < INT_MIN ? INT_MIN : (v > INT_MAX ? INT_MAX : (int)v);
+  };
+  StepResult r{0.0, false};
+  if (!(P.flags & 0x200u)) r = tile_step(P, prof, dtab, T, E, b, F, S, active, act);  // 0x200: memory-only probe
+  bool reset = false;
+  if (r.done && (P.flags & VY_F_AUTO_RESET)) {
+    // in-kernel auto-reset (engine.py:460-462): the terminal reward/done/infos
+    // stand, the obs row becomes the reset obs of episode + 1
+    const int ep = active ? P.st.episode[b] + 1 : 0;
+    reset_scalars(P, E, active ? P.st.env_seed[b] : 0ull, ep, 0, false);
+    for (int i = 0; i < P.n_ports; ++i) {
+      if (active) store_port(P, b, i, 0u, 0.0, 0.0, 0.0, 0);
+      stage_port_obs(P, prof, S, lane, active, i, 0u, 0.0, 0.0, 0.0, 0);
     }
+    if (active) P.st.episode[b] = ep;
+    reset = true;
+  }
+  if (active) {
     if (!(P.flags & 0x800u)) store_env(P, b, E, reset);
     if (P.flags & VY_F_OUT_F64)
-      reinterpret_cast<double*>(P.out.reward)[b] = rew;
+      reinterpret_cast<double*>(P.out.reward)[b] = r.reward;
     else
-      reinterpret_cast<float*>(P.out.reward)[b] = (float)rew;
-    P.out.done[b] = done;
+      reinterpret_cast<float*>(P.out.reward)[b] = (float)r.reward;
+    P.out.done[b] = r.done;
   }
-  emit_obs(P, prof, T, E, G, b0, active, P.out.obs, /*store_state=*/true);
+  emit_tail(P, T, E, G, S, b0, active, P.out.obs);
 }
 
 // One warp per tile.  (A persistent variant with L2 bulk prefetch of the next
@@ -126,25 +133,29 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
   const int ns = P.n_ports + 1, hi = 2 * P.k + 1;
   const bool f64 = P.flags & VY_F_OUT_F64;
   for (int t = 0; t < T_steps; ++t) {
+    void* obs_t = f64 ? (void*)(reinterpret_cast<double*>(P.out.obs) + t * obs_stride)
+                      : (void*)(reinterpret_cast<float*>(P.out.obs) + t * obs_stride);
+    const ObsSink S = make_sink(P, T, b, obs_t, /*in_place=*/false);
+    const uint64_t j0 = (uint64_t)(call0 + t) * (uint64_t)ns;
+    auto act = [&](int slot) -> int { return policy_action(pkey, j0 + slot + 1, hi); };
+    const Frame F = load_frame(P, E.step, E.day);
+    const StepResult r = tile_step(P, prof, dtab, T, E, b, F, S, active, act);
+    if (r.done) {
+      ++episode;
+      reset_scalars(P, E, seed, episode, 0, false);
+      clear_tile_ports(P, T);
+      for (int i = 0; i < P.n_ports; ++i) stage_port_obs(P, prof, S, lane, active, i, 0u, 0.0, 0.0, 0.0, 0);
+    }
     if (active) {
-      const uint64_t j0 = (uint64_t)(call0 + t) * (uint64_t)ns;
-      auto act = [&](int slot) -> int { return policy_action(pkey, j0 + slot + 1, hi); };
-      const Frame F = load_frame(P, E.step, E.day);
-      const StepResult r = tile_step(P, prof, dtab, T, E, b, F, act);
-      if (r.done) {
-        ++episode;
-        reset_env(P, T, E, seed, episode, 0, false);
-      }
       if (f64)
         reinterpret_cast<double*>(P.out.reward)[t * rew_stride + b] = r.reward;
       else
         reinterpret_cast<float*>(P.out.reward)[t * rew_stride + b] = (float)r.reward;
       P.out.done[t * rew_stride + b] = r.done;
     }
-    void* obs_t = f64 ? (void*)(reinterpret_cast<double*>(P.out.obs) + t * obs_stride)
-                      : (void*)(reinterpret_cast<float*>(P.out.obs) + t * obs_stride);
-    emit_obs(P, prof, T, E, load_obs_globals(P, E.step, E.day), b0, active, obs_t, /*store_state=*/t == T_steps - 1);
+    emit_tail(P, T, E, load_obs_globals(P, E.step, E.day), S, b0, active, obs_t);
   }
+  if (!(P.flags & 0x800u)) tile_store(P, T.t, b0, lane);
   if (active) {
     store_env(P, b, E, true);
     P.st.episode[b] = episode;
@@ -171,7 +182,8 @@ __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P,
   if (active) load_env(P, b, E);
   if (mine) {
     const int ep = episode_mode ? P.st.episode[b] + 1 : 0;
-    reset_env(P, T, E, P.st.env_seed[b], ep, inj_day ? inj_day[b] : 0, inj_day != nullptr);
+    reset_scalars(P, E, P.st.env_seed[b], ep, inj_day ? inj_day[b] : 0, inj_day != nullptr);
+    clear_tile_ports(P, T);
     P.st.episode[b] = ep;
     store_env(P, b, E, true);
   }

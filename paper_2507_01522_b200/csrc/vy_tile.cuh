@@ -300,13 +300,22 @@ __device__ __noinline__ void fit_tree(const Params& P, const Lane& T, double& cb
   }
 }
 
-// reset_env (_kernel.pyx:239-261): clear the env's ports and scalars, draw the day.
-__device__ __forceinline__ void reset_env(const Params& P, const Lane& T, EnvRegs& E, uint64_t seed, int episode,
-                                          int inj_day, bool use_inj) {
+// reset_env (_kernel.pyx:239-261), scalar part: draw the day, zero the clock
+// and the episode accumulators, re-initialise the battery.  The caller clears
+// the ports (tile slots, or HBM + obs staging when the slots hold obs).
+__device__ __forceinline__ void reset_scalars(const Params& P, EnvRegs& E, uint64_t seed, int episode, int inj_day,
+                                              bool use_inj) {
   uint64_t st = fold(fold(fold(fold(kKey0, seed), (uint64_t)(int64_t)episode), 0), 0);
   E.day = use_inj ? inj_day : below(st, P.n_days);
   E.step = 0;
   E.akey = fold(fold(fold(kKey0, seed), (uint64_t)(int64_t)episode), 1);
+  E.b_soc = P.battery ? P.b_init_soc : 0.0;
+  E.b_i = 0.0;
+  E.ep_profit = E.ep_reward = E.ep_missing = E.ep_energy = 0.0;
+  E.ep_overtime = E.ep_declined = E.ep_departures = 0;
+}
+
+__device__ __forceinline__ void clear_tile_ports(const Params& P, const Lane& T) {
   for (int i = 0; i < P.n_ports; ++i) {
     T.idr(i) = 0.0;
     T.soc(i) = 0.0;
@@ -314,10 +323,6 @@ __device__ __forceinline__ void reset_env(const Params& P, const Lane& T, EnvReg
     T.dtrem(i) = 0;
     T.meta(i) = 0;
   }
-  E.b_soc = P.battery ? P.b_init_soc : 0.0;
-  E.b_i = 0.0;
-  E.ep_profit = E.ep_reward = E.ep_missing = E.ep_energy = 0.0;
-  E.ep_overtime = E.ep_declined = E.ep_departures = 0;
 }
 
 struct StepResult {
@@ -369,12 +374,58 @@ __device__ __forceinline__ ObsGlobals load_obs_globals(const Params& P, int step
   return G;
 }
 
+// Where a step's outputs go.  f32 obs are staged column-major in shared
+// memory at `cells` (column c, row r at cells + c*132 + r*4: per-lane writes and
+// per-row reads are both bank-conflict free) and leave with coalesced row-major
+// stores; f64 obs (exact drop-in mode) go straight to this lane's row.  With
+// `in_place` the staging area is the tile's own float64 port slots: port i's
+// state is written to HBM, then its slots take its obs columns (the 24n-byte
+// pad in front of the slots makes column block 6i..6i+5 end before port i+1).
+struct ObsSink {
+  uint32_t cells;
+  double* row64;
+  bool in_place;
+};
+
+__device__ __forceinline__ void stage_port_obs(const Params& P, const Profile* prof, const ObsSink& S, int lane,
+                                               bool active, int i, uint32_t mt, double idr, double soc, double de,
+                                               int dt) {
+  const bool occ = mt & 1u;
+  double v[6];
+  v[0] = occ ? 1.0 : 0.0;
+  v[1] = div_rcp(idr, P.i_denom[i], P.rcp_i_denom[i]);
+  v[2] = soc;
+  v[3] = occ ? div_rcp(de, prof[mt >> 2].cap, prof[mt >> 2].rcp_cap) : 0.0;
+  v[4] = div_rcp((double)dt, (double)P.episode_steps, P.rcp_ep);
+  v[5] = (double)((mt >> 1) & 1u);
+  if (S.row64) {
+    if (active)
+#pragma unroll
+      for (int f = 0; f < 6; ++f) S.row64[6 * i + f] = v[f];
+  } else {
+    const uint32_t col = S.cells + 6 * i * 132 + lane * 4;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) sts_f32(col + f * 132, (float)v[f]);
+  }
+}
+
+__device__ __forceinline__ void store_port(const Params& P, int64_t b, int i, uint32_t mt, double idr, double soc,
+                                           double de, int dt) {
+  const vy_state& s = P.st;
+  const int64_t e = (int64_t)i * P.ld + b;
+  s.port_i[e] = idr;
+  s.port_soc[e] = soc;
+  s.port_de[e] = de;
+  s.port_dtrem[e] = (int16_t)dt;
+  s.port_meta[e] = (uint8_t)mt;
+}
+
 // One transition of one env (_kernel.pyx:283-571).  `act(slot)` returns the
 // action index of a slot; `b` is the global env index (infos / injected draws).
 template <class Act>
 __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* __restrict__ prof,
                                                 const double* __restrict__ dtab, const Lane& T, EnvRegs& E,
-                                                int64_t b, const Frame& F, Act act) {
+                                                int64_t b, const Frame& F, const ObsSink& S, bool active, Act act) {
   const int n = P.n_ports;
   const int64_t ld = P.ld;
   const bool info = P.flags & VY_F_INFOS;
@@ -457,38 +508,42 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   if (P.battery) E.b_i = cb;
 
   // phases 2+3: charge (_kernel.pyx:358-424), dwell countdown (:420-422) and
-  // departures (:426-458) fused into one pass in port order
+  // departures (:426-458) fused into one pass in port order; the same pass
+  // emits each port's final state (HBM, or the resident tile) and its obs
+  // columns.  Arrivals below patch the few ports that receive a car.
   double e_net = 0.0, e_in = 0.0, e_out = 0.0;
   double sat0 = 0.0, sat1 = 0.0;
-  int nd = 0;
+  int nd = 0, tover = 0;
   uint64_t occm = 0;
+  const bool last = t + 1 == P.episode_steps;
 #pragma unroll 2
   for (int i = 0; i < n; ++i) {
-    const uint32_t mt = T.meta(i);
+    uint32_t mt = T.meta(i);
+    double cur = T.idr(i), soc = T.soc(i), de = T.de(i);
+    int dt = T.dtrem(i);
     double got = 0.0;
     if (mt & 1u) {
       const Profile& pr = prof[mt >> 2];
-      const double cur = T.idr(i), soc0 = T.soc(i), de0 = T.de(i);
       const double raw = div_rcp(P.dtv[i] * cur, 1000.0, P.rcp_1000);
       got = raw;
       if (raw >= 0.0) {
-        if (de0 < got) got = de0;
-        const double room = pr.cap * (1.0 - soc0);
+        if (de < got) got = de;
+        const double room = pr.cap * (1.0 - soc);
         if (room < got) got = room;
       } else {
-        const double fl = -pr.cap * soc0;
+        const double fl = -pr.cap * soc;
         if (got < fl) got = fl;
       }
-      double soc = soc0 + div_rcp(got, pr.cap, pr.rcp_cap);
+      soc = soc + div_rcp(got, pr.cap, pr.rcp_cap);
       soc = soc < 0.0 ? 0.0 : (soc > 1.0 ? 1.0 : soc);
-      double de = de0 - got;
+      de = de - got;
       de = de < 0.0 ? 0.0 : de;
       e_net += got;
       if (got > 0.0)
         e_in += P.eta_c[i] == 1.0 ? got : div_rcp(got, P.eta_c[i], P.rcp_eta_c[i]);
       else if (got < 0.0)
         e_out += got * P.eta_d[i];
-      const int dt = T.dtrem(i) - 1;
+      dt -= 1;
       const int p = (mt >> 1) & 1u;
       if ((p == 0 && dt <= 0) || (p == 1 && de == 0.0)) {
         const int over = dt < 0 ? -dt : 0, early = dt > 0 ? dt : 0;
@@ -509,20 +564,27 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
         E.ep_missing += de;
         E.ep_overtime += over;
         E.ep_departures += 1;
-        T.meta(i) = 0;
-        T.idr(i) = 0.0;
-        T.soc(i) = 0.0;
-        T.de(i) = 0.0;
-        T.dtrem(i) = 0;
+        mt = 0;
+        cur = soc = de = 0.0;
+        dt = 0;
         ++nd;
       } else {
-        T.soc(i) = soc;
-        T.de(i) = de;
-        T.dtrem(i) = (int16_t)dt;
         occm |= 1ull << i;
+        if (last && p == 1 && dt < 0) tover += -dt;  // _kernel.pyx:559-561 (arrivals add dt > 0 only)
       }
     }
     if (info) O.delivered[i * ld + b] = got;
+    if (S.in_place) {
+      if (active) store_port(P, b, i, mt, cur, soc, de, dt);
+      __syncwarp();  // every lane has read port i before its slots take obs columns
+    } else {
+      T.meta(i) = (uint8_t)mt;
+      T.idr(i) = cur;
+      T.soc(i) = soc;
+      T.de(i) = de;
+      T.dtrem(i) = (int16_t)dt;
+    }
+    stage_port_obs(P, prof, S, T.lane, active, i, mt, cur, soc, de, dt);
   }
   double e_b = 0.0, bgot = 0.0;
   if (P.battery) {
@@ -598,11 +660,18 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
         }
     }
     occm |= 1ull << port;
-    T.meta(port) = (uint8_t)(1u | (pref << 1) | ((uint32_t)car << 2));
-    T.idr(port) = 0.0;
-    T.soc(port) = soc0;
-    T.de(port) = frac * prof[car].cap * (1.0 - soc0);
-    T.dtrem(port) = (int16_t)stay;
+    const uint32_t mt = 1u | (pref << 1) | ((uint32_t)car << 2);
+    const double de0 = frac * prof[car].cap * (1.0 - soc0);
+    if (S.in_place) {
+      store_port(P, b, port, mt, 0.0, soc0, de0, stay);
+    } else {
+      T.meta(port) = (uint8_t)mt;
+      T.idr(port) = 0.0;
+      T.soc(port) = soc0;
+      T.de(port) = de0;
+      T.dtrem(port) = (int16_t)stay;
+    }
+    stage_port_obs(P, prof, S, T.lane, active, port, mt, 0.0, soc0, de0, stay);
   }
   E.ep_declined += declined;
   if (info) {
@@ -649,13 +718,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   E.step = t + 1;
   const bool done = t + 1 == P.episode_steps;
   if (done || info) {
-    int tover = 0;
     if (done) {
-      for (int i = 0; i < n; ++i)
-        if ((T.meta(i) & 3u) == 3u) {
-          const int dt = T.dtrem(i);
-          if (dt < 0) tover += -dt;
-        }
       double* es = O.ep_stats;
       es[b] = E.ep_profit;
       es[ld + b] = E.ep_reward;
@@ -709,49 +772,23 @@ __device__ __forceinline__ void tile_store(const Params& P, uint32_t toff, int64
   __syncwarp();
 }
 
-// Write this tile's obs rows (and, with store_state, the state back to HBM).
-// float32 obs are staged column-major in shared memory (rows rotated by column
-// so per-lane writes and row-major reads are both bank-conflict free) and
-// leave with coalesced row-major stores; float64 obs (exact drop-in mode) are
-// written per lane.  In the step kernel the staging area is the tile's own
-// float64 port slots (obs_off == 0), free once the state has been written back.
-__device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, const Lane& T, const EnvRegs& E,
-                                         ObsGlobals G, int64_t b0, bool active, void* obs_base, bool store_state) {
+__device__ __forceinline__ ObsSink make_sink(const Params& P, const Lane& T, int64_t b, void* obs_base,
+                                             bool in_place) {
+  ObsSink S;
+  S.cells = smem_base() + T.t + P.L.obs;
+  S.row64 = (P.flags & VY_F_OUT_F64) ? reinterpret_cast<double*>(obs_base) + b * P.obs_len : nullptr;
+  S.in_place = in_place;
+  return S;
+}
+
+// Global obs columns and the coalesced read-out of the staged [rows][OL] block.
+__device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const EnvRegs& E, ObsGlobals G,
+                                          const ObsSink& S, int64_t b0, bool active, void* obs_base) {
   const int n = P.n_ports;
   const int lane = T.lane;
-  const int64_t b = b0 + lane;
   const int OL = P.obs_len;
-  const int obs_off = P.L.obs;
-  const bool f64 = P.flags & VY_F_OUT_F64;
   if (G.step != E.step || G.day != E.day) G = load_obs_globals(P, E.step, E.day);  // auto-reset happened
-  if (store_state && !(P.flags & 0x800u)) tile_store(P, T.t, b0, lane);
-  double* row64 = f64 ? reinterpret_cast<double*>(obs_base) + b * OL : nullptr;
-  const uint32_t cells = smem_base() + T.t + obs_off;
-#pragma unroll 2
-  for (int i = 0; i < n; ++i) {
-    const uint32_t mt = T.meta(i);
-    const double idr = T.idr(i), soc = T.soc(i), de = T.de(i);
-    const int dt = T.dtrem(i);
-    const bool occ = mt & 1u;
-    double v[6];
-    v[0] = occ ? 1.0 : 0.0;
-    v[1] = div_rcp(idr, P.i_denom[i], P.rcp_i_denom[i]);
-    v[2] = soc;
-    v[3] = occ ? div_rcp(de, prof[mt >> 2].cap, prof[mt >> 2].rcp_cap) : 0.0;
-    v[4] = div_rcp((double)dt, (double)P.episode_steps, P.rcp_ep);
-    v[5] = (double)((mt >> 1) & 1u);
-    if (f64) {
-      if (active)
-#pragma unroll
-        for (int f = 0; f < 6; ++f) row64[6 * i + f] = v[f];
-    } else {
-      __syncwarp();  // in place: every lane has read port i before its slots are reused
-      const uint32_t col = cells + 6 * i * 132 + lane * 4;
-#pragma unroll
-      for (int f = 0; f < 6; ++f) sts_f32(col + f * 132, (float)v[f]);
-    }
-  }
-  // globals: battery [soc, I/Imax], [buy, sellg, p_sell, sin, cos, weekday, day/365], horizon
+  // battery [soc, I/Imax], [buy, sellg, p_sell, sin, cos, weekday, day/365], price horizon
   double gv[9];
   gv[0] = E.b_soc;
   gv[1] = div_rcp(E.b_i, P.b_idenom, P.b_rcp_idenom);
@@ -765,31 +802,31 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
   const int c0 = 6 * n;
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
-    if (f64) {
-      if (active) row64[c0 + k] = gv[k];
+    if (S.row64) {
+      if (active) S.row64[c0 + k] = gv[k];
     } else {
-      sts_f32(cells + (c0 + k) * 132 + lane * 4, (float)gv[k]);
+      sts_f32(S.cells + (c0 + k) * 132 + lane * 4, (float)gv[k]);
     }
   }
   for (int h = 0; h < P.horizon; ++h) {
     const int64_t fmin = (int64_t)(E.step + 1 + h) * P.dt_min;
     const int64_t fday = ((int64_t)E.day + fmin / 1440) % P.n_days;
     const double v = __ldg(P.buy + fday * 24 + (fmin / 60) % 24);
-    if (f64) {
-      if (active) row64[c0 + 9 + h] = v;
+    if (S.row64) {
+      if (active) S.row64[c0 + 9 + h] = v;
     } else {
-      sts_f32(cells + (c0 + 9 + h) * 132 + lane * 4, (float)v);
+      sts_f32(S.cells + (c0 + 9 + h) * 132 + lane * 4, (float)v);
     }
   }
-  if (f64) return;
+  if (S.row64) return;
   __syncwarp();
+  if (P.flags & 0x400u) return;  // probe: no obs stores
   // Row-major read-out: row r, column c = lane + 32 j lives at
   // cells + c*132 + r*4 = cells + lane*132 + r*4 + j*4224; bank (lane + r) % 32.
   float* g = reinterpret_cast<float*>(obs_base) + b0 * OL + lane;
   const int64_t left = P.B - b0;
   const int rows = left >= 32 ? 32 : (int)left;
-  const uint32_t lbase = cells + lane * 132;
-  if (P.flags & 0x400u) return;
+  const uint32_t lbase = S.cells + lane * 132;
   if (OL <= 128) {
     const bool p0 = lane < OL, p1 = lane + 32 < OL, p2 = lane + 64 < OL, p3 = lane + 96 < OL;
 #pragma unroll 2
@@ -816,6 +853,24 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
     }
   }
   __syncwarp();
+}
+
+// Obs of the tile's current state (reset kernel): write the state back to HBM
+// (bulk copies) if asked, then stage every port and finish.
+__device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, const Lane& T, const EnvRegs& E,
+                                         ObsGlobals G, int64_t b0, bool active, void* obs_base, bool store_state) {
+  const int64_t b = b0 + T.lane;
+  const ObsSink S = make_sink(P, T, b, obs_base, P.L.obs == 0);
+  if (store_state && !(P.flags & 0x800u)) tile_store(P, T.t, b0, T.lane);
+#pragma unroll 2
+  for (int i = 0; i < P.n_ports; ++i) {
+    const uint32_t mt = T.meta(i);
+    const double idr = T.idr(i), soc = T.soc(i), de = T.de(i);
+    const int dt = T.dtrem(i);
+    if (S.in_place) __syncwarp();  // every lane has read port i before its slots are reused
+    stage_port_obs(P, prof, S, T.lane, active, i, mt, idr, soc, de, dt);
+  }
+  emit_tail(P, T, E, G, S, b0, active, obs_base);
 }
 
 }  // namespace vy
