@@ -612,8 +612,10 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   int m = 0;
   int64_t inj0 = 0;
   if (inj) {
-    inj0 = P.inj.off[b];
-    m = P.inj.off[b + 1] - (int)inj0;
+    if (active) {  // padding lanes have no draw rows
+      inj0 = P.inj.off[b];
+      m = P.inj.off[b + 1] - (int)inj0;
+    }
   } else {
     const int full = F.pfull;
     if (full >= 0) {
