@@ -439,11 +439,17 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   // phase 1: apply actions (_kernel.pyx:297-356); the clipped current replaces
   // i_drawn in its smem slot, node loads accumulate in leaf order on the fly
   const int hi_a = 2 * P.k;
+  // (a-k)/k: with 2k+1 <= 32 the grid lives one entry per lane and a warp
+  // shuffle fetches it (a random-index shared-memory lookup bank-conflicts);
+  // otherwise the staged table, else the IEEE division.
+  const bool shfl_grid = hi_a < 32;
+  const double grid_lane = shfl_grid && dtab ? dtab[T.lane <= hi_a ? T.lane : 0] : 0.0;
   auto delta_of = [&](int a) -> double {
     if ((unsigned)a > (unsigned)hi_a) {
       atomicOr(P.err, 1u);
       a = a < 0 ? 0 : hi_a;
     }
+    if (shfl_grid && dtab) return __shfl_sync(0xffffffffu, grid_lane, a);
     return dtab ? dtab[a] : (double)(a - P.k) / (double)P.k;
   };
   const bool fast = P.n_nodes <= kFastNodes;
