@@ -322,6 +322,31 @@ def main() -> None:
                          "paper_reference": "Chargax PPO(16) 0.65 s / 100k on RTX 4000 Ada (PAPER.md:239)"}
         penv.close()
 
+    if not args.no_extras:
+        # config C5: 36 heterogeneous (region, scenario, traffic, station layout) groups sharing the GPU,
+        # 2^20 envs per GPU (2^23 over 8 GPUs), device RandomPolicy per group
+        from paper_2507_01522_b200.hetero import HeteroBatch, sweep_groups
+
+        hb = HeteroBatch(sweep_groups(B), master_seed=0, global_offset=rank * B, policy_seed=0)
+        hb.reset()
+        for _ in range(3):
+            hb.random_step()
+        barrier()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        hsteps = max(3, min(args.steps, 20))
+        l0 = hb.launch_count()
+        h0.record(stream)
+        for _ in range(hsteps):
+            hb.random_step()
+        h1.record(stream)
+        barrier()
+        hms = max_over_ranks(h0.elapsed_time(h1))
+        result["hetero"] = {"metric": METRIC, "value": hsteps * hb.total * world / (hms / 1e3), "unit": UNIT,
+                            "groups": len(hb.groups), "envs_per_gpu": hb.total, "global_envs": hb.total * world,
+                            "launches_per_step": (hb.launch_count() - l0) // hsteps,
+                            "workload": "C5: regions x scenarios x traffic, single/multi/nested stations"}
+        hb.close()
+
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
         result["cpu_baseline"] = {k: v for k, v in cpu_reference_rate(rc, 1 << 16, 8, threads).items()

@@ -1,0 +1,94 @@
+"""Heterogeneous station configurations on one GPU (BASELINE config C5).
+
+The reference requires one (config, station, dataset) per batch
+(engine.py:370).  ``HeteroBatch`` batches many: each group is a
+regular BatchEnv (own tables, own handle; the generic kernel serves every
+station size), all groups step back-to-back on one CUDA stream so a whole
+heterogeneous step is a short burst of kernel launches.  Env seeds and
+RandomPolicy rows use one global index space across groups (group g's envs
+are global indices offset_g .. offset_g + B_g - 1), so a group's trajectory is
+bit-identical to a standalone BatchEnv with that global_offset — which is
+what the tests check.
+
+``sweep_groups`` builds the C5 sweep: regions {eu, us, world} x scenarios
+{highway, residential, work, shopping} x traffic {low, medium, high}, station
+presets rotating over single / multi / nested layouts.
+"""
+
+from __future__ import annotations
+
+import itertools
+from dataclasses import dataclass
+
+import torch
+
+from .batch import BatchEnv, DeviceRandomPolicy
+from .envconfig import EnvConfig
+from .exogenous import REGIONS, SCENARIOS, TRAFFIC_FACTORS, Dataset, generate_synthetic_defaults
+from .station import StationTree, preset_station
+
+
+@dataclass
+class Group:
+    name: str
+    config: EnvConfig
+    station: StationTree
+    dataset: Dataset
+    batch_size: int
+
+
+_LAYOUTS = (("single_type", 0, 8), ("multi_type", 6, 10), ("nested_splitters", 4, 12))
+
+
+def sweep_groups(total_envs: int, days: int = 365, seed: int = 0) -> list[Group]:
+    """36 (region, scenario, traffic) combinations splitting ``total_envs``."""
+    combos = list(itertools.product(REGIONS, SCENARIOS, TRAFFIC_FACTORS))
+    per = total_envs // len(combos)
+    groups = []
+    for gi, (region, scen, traffic) in enumerate(combos):
+        layout, ac, dc = _LAYOUTS[gi % len(_LAYOUTS)]
+        ds = generate_synthetic_defaults(scen, traffic, region, seed=seed, days=days)
+        groups.append(Group(f"{region}/{scen}/{traffic}/{layout}", EnvConfig(), preset_station(layout, ac, dc), ds,
+                            per if gi < len(combos) - 1 else total_envs - per * (len(combos) - 1)))
+    return groups
+
+
+class HeteroBatch:
+    def __init__(self, groups: list[Group], master_seed: int = 0, global_offset: int = 0, device=None,
+                 policy_seed: int | None = None):
+        self.groups = groups
+        self.envs: list[BatchEnv] = []
+        self.policies: list[DeviceRandomPolicy] = []
+        off = global_offset
+        for g in groups:
+            env = BatchEnv(g.config, g.station, g.dataset, batch_size=g.batch_size, master_seed=master_seed,
+                           global_offset=off, device=device)
+            self.envs.append(env)
+            if policy_seed is not None:
+                pol = DeviceRandomPolicy(policy_seed, env.n_ports, g.config.discretization_k)
+                pol.bind(range(off, off + g.batch_size))
+                self.policies.append(pol)
+            off += g.batch_size
+        self.total = off - global_offset
+
+    def reset(self) -> list[torch.Tensor]:
+        return [e.reset(as_numpy=False) for e in self.envs]
+
+    def step(self, actions: list[torch.Tensor]):
+        """One step of every group; returns per-group (obs, reward, done)."""
+        out = []
+        for env, a in zip(self.envs, actions):
+            o, r, d, _ = env.step(a, collect_infos=False)
+            out.append((o, r, d))
+        return out
+
+    def random_step(self):
+        """One step of every group with its device RandomPolicy actions."""
+        return self.step([p.actions(e) for p, e in zip(self.policies, self.envs)])
+
+    def launch_count(self) -> int:
+        return sum(e.launch_count() for e in self.envs)
+
+    def close(self) -> None:
+        for e in self.envs:
+            e.close()

@@ -74,3 +74,12 @@ def test_two_rank_shards_equal_single_batch():
         np.testing.assert_array_equal(obs, obs_full[off:off + len(obs)])
         np.testing.assert_array_equal(rew, rew_full[:, off:off + rew.shape[1]])
         np.testing.assert_allclose(stats, [rew_full.sum(), eps_full.sum(), GLOBAL], rtol=1e-12)
+
+
+def test_sweep_groups_cover_c5_grid():
+    from paper_2507_01522_b200.hetero import sweep_groups
+
+    gs = sweep_groups(total_envs=1 << 16, days=3)
+    assert len(gs) == 36 and sum(g.batch_size for g in gs) == 1 << 16
+    assert len({g.name.split("/")[0] for g in gs}) == 3 and len({g.name.split("/")[1] for g in gs}) == 4
+    assert {g.station.n_ports for g in gs} == {8, 16}
