@@ -3,8 +3,9 @@
 The reference requires one (config, station, dataset) per batch
 (engine.py:370).  ``HeteroBatch`` batches many: each group is a
 regular BatchEnv (own tables, own handle; the generic kernel serves every
-station size), all groups step back-to-back on one CUDA stream so a whole
-heterogeneous step is a short burst of kernel launches.  Env seeds and
+station size), groups are spread round-robin over a few CUDA streams so the small
+per-group grids run concurrently and fill the GPU (each group's launches stay
+ordered on its stream; a step joins all streams back into the caller's).  Env seeds and
 RandomPolicy rows use one global index space across groups (group g's envs
 are global indices offset_g .. offset_g + B_g - 1), so a group's trajectory is
 bit-identical to a standalone BatchEnv with that global_offset — which is
@@ -55,8 +56,9 @@ def sweep_groups(total_envs: int, days: int = 365, seed: int = 0) -> list[Group]
 
 class HeteroBatch:
     def __init__(self, groups: list[Group], master_seed: int = 0, global_offset: int = 0, device=None,
-                 policy_seed: int | None = None):
+                 policy_seed: int | None = None, n_streams: int = 4):
         self.groups = groups
+        self.streams = [torch.cuda.Stream(device=device) for _ in range(max(1, n_streams))]
         self.envs: list[BatchEnv] = []
         self.policies: list[DeviceRandomPolicy] = []
         off = global_offset
@@ -74,17 +76,34 @@ class HeteroBatch:
     def reset(self) -> list[torch.Tensor]:
         return [e.reset(as_numpy=False) for e in self.envs]
 
+    def _fan_out(self, fn):
+        """Run fn(i) for every group on its stream; join into the current stream."""
+        cur = torch.cuda.current_stream()
+        for s in self.streams:
+            s.wait_stream(cur)
+        out = []
+        for i in range(len(self.envs)):
+            with torch.cuda.stream(self.streams[i % len(self.streams)]):
+                out.append(fn(i))
+        for s in self.streams:
+            cur.wait_stream(s)
+        return out
+
     def step(self, actions: list[torch.Tensor]):
         """One step of every group; returns per-group (obs, reward, done)."""
-        out = []
-        for env, a in zip(self.envs, actions):
-            o, r, d, _ = env.step(a, collect_infos=False)
-            out.append((o, r, d))
-        return out
+        def one(i):
+            o, r, d, _ = self.envs[i].step(actions[i], collect_infos=False)
+            return o, r, d
+
+        return self._fan_out(one)
 
     def random_step(self):
         """One step of every group with its device RandomPolicy actions."""
-        return self.step([p.actions(e) for p, e in zip(self.policies, self.envs)])
+        def one(i):
+            o, r, d, _ = self.envs[i].step(self.policies[i].actions(self.envs[i]), collect_infos=False)
+            return o, r, d
+
+        return self._fan_out(one)
 
     def launch_count(self) -> int:
         return sum(e.launch_count() for e in self.envs)
