@@ -189,6 +189,12 @@ int vy_step(vy_handle *h, const void *actions, int32_t dtype, int64_t row_stride
 int vy_random_actions(vy_handle *h, uint64_t seed, int64_t index0, int64_t call,
                       uint8_t *out, void *stream);
 
+/* As vy_random_actions, with the call index read from (and then incremented
+ * in) a device counter, so the pair of launches can be replayed from a CUDA
+ * graph and still draw the next call's actions every replay. */
+int vy_random_actions_dev(vy_handle *h, uint64_t seed, int64_t index0, int64_t *call_counter, uint8_t *out,
+                          void *stream);
+
 /* Fused multi-step rollout: T steps with in-kernel RandomPolicy actions and
  * auto-reset, state held in registers across steps.  Step t writes obs to
  * obs + t*obs_step_stride (elements; 0 = overwrite one buffer), reward to

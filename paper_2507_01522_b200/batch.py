@@ -519,12 +519,21 @@ class DeviceRandomPolicy:
         self.rows = len(idx)
         self.calls = 0
 
-    def actions(self, env: BatchEnv) -> torch.Tensor:
+    def actions(self, env: BatchEnv, device_counter: bool = False) -> torch.Tensor:
+        """Next call's actions.  With device_counter the call index lives in
+        device memory (graph-replayable); `calls` is then advanced by the caller."""
         B = env.batch_size
         if self.rows is not None and self.rows != B:
             raise ValueError("policy bound to a different batch size")
         if self._out is None or self._out.shape[0] != B:
             self._out = torch.empty(B, self.n_ports + 1, dtype=torch.uint8, device=env.device)
+        if device_counter:
+            if getattr(self, "_counter", None) is None:
+                self._counter = torch.tensor([self.calls], dtype=torch.int64, device=env.device)
+            rc = env._lib.vy_random_actions_dev(env._h, self.seed & ((1 << 64) - 1), self.index0,
+                                                self._counter.data_ptr(), self._out.data_ptr(), env._stream)
+            nat.check(rc, "vy_random_actions_dev")
+            return self._out
         rc = env._lib.vy_random_actions(env._h, self.seed & ((1 << 64) - 1), self.index0, self.calls,
                                         self._out.data_ptr(), env._stream)
         nat.check(rc, "vy_random_actions")

@@ -48,7 +48,8 @@ namespace vy {
 // smem row block, then the warp writes the contiguous [32][n+1] byte block
 // with coalesced stores (per-thread 17-byte rows would be strided byte stores).
 __global__ void k_random_actions(uint64_t seed, int64_t index0, int64_t call, int64_t B, int ns, int hi,
-                                 uint8_t* out) {
+                                 uint8_t* out, const int64_t* call_dev) {
+  if (call_dev) call += *call_dev;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
   if (b0 >= B) return;
@@ -85,6 +86,8 @@ __global__ void k_selftest_div(const double* d, const double* y, int nd, int64_t
   }
   if (local) atomicAdd(bad, local);
 }
+
+__global__ void k_bump(int64_t* c) { *c += 1; }
 
 __global__ void k_seed_envs(uint64_t master, int64_t index0, int64_t B, uint64_t* env_seed) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -524,9 +527,24 @@ int vy_random_actions(vy_handle* h, uint64_t seed, int64_t index0, int64_t call,
   const int ns = h->t.n_ports + 1, hi = 2 * h->t.k + 1;
   if (hi > 256) return fail(VY_ERR_UNSUPPORTED, "uint8 actions need 2k+1 <= 256");
   const unsigned grid = (unsigned)((h->B + 255) / 256);
-  k_random_actions<<<grid, 256, 8 * 32 * ns, (cudaStream_t)stream>>>(seed, index0, call, h->B, ns, hi, out);
+  k_random_actions<<<grid, 256, 8 * 32 * ns, (cudaStream_t)stream>>>(seed, index0, call, h->B, ns, hi, out,
+                                                                     nullptr);
   VY_CUDA(cudaGetLastError());
   ++h->launches;
+  return VY_OK;
+}
+
+int vy_random_actions_dev(vy_handle* h, uint64_t seed, int64_t index0, int64_t* call_counter, uint8_t* out,
+                          void* stream) {
+  if (!h || !out || !call_counter) return fail(VY_ERR_ARG, "null argument");
+  const int ns = h->t.n_ports + 1, hi = 2 * h->t.k + 1;
+  if (hi > 256) return fail(VY_ERR_UNSUPPORTED, "uint8 actions need 2k+1 <= 256");
+  const unsigned grid = (unsigned)((h->B + 255) / 256);
+  k_random_actions<<<grid, 256, 8 * 32 * ns, (cudaStream_t)stream>>>(seed, index0, 0, h->B, ns, hi, out,
+                                                                     call_counter);
+  k_bump<<<1, 1, 0, (cudaStream_t)stream>>>(call_counter);
+  VY_CUDA(cudaGetLastError());
+  h->launches += 2;
   return VY_OK;
 }
 

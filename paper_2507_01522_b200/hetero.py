@@ -105,6 +105,36 @@ class HeteroBatch:
 
         return self._fan_out(one)
 
+    def graph_random_step(self) -> None:
+        """random_step replayed from a captured CUDA graph: the group launches
+        and their stream fork/join cost one graph launch.  Actions come from the
+        device-counter RandomPolicy (vy_random_actions_dev), so every replay
+        draws the next call; the host-side lockstep clocks and call counters are
+        advanced here because a replay runs no host code."""
+        if getattr(self, "_graph", None) is None:
+            def one(i):
+                e = self.envs[i]
+                o, r, d, _ = e.step(self.policies[i].actions(e, device_counter=True), collect_infos=False)
+                return o, r, d
+
+            clocks = [e._t for e in self.envs]
+            # warm-up (creates the device counters) then capture
+            self._fan_out(one)
+            for p in self.policies:
+                p.calls += 1
+            clocks = [e._t for e in self.envs]
+            self._graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self._graph):
+                self._fan_out(one)
+            for e, c in zip(self.envs, clocks):
+                e._t = c  # capture did not execute
+        self._graph.replay()
+        for p in self.policies:
+            p.calls += 1
+        for e in self.envs:
+            if e._t is not None:
+                e._t = (e._t + 1) % e.tables.episode_steps
+
     def launch_count(self) -> int:
         return sum(e.launch_count() for e in self.envs)
 
