@@ -128,6 +128,7 @@ class HeteroBatch:
                 self._fan_out(one)
             for e, c in zip(self.envs, clocks):
                 e._t = c  # capture did not execute
+            return  # the warm-up was this call's step
         self._graph.replay()
         for p in self.policies:
             p.calls += 1
