@@ -196,6 +196,22 @@ def synthetic_vectors(vy):
     np.savez_compressed(OUT / "synthetic_vectors.npz", **out)
 
 
+def evaluate_vectors(vy):
+    """evaluate() reports of the three baseline policies (evaluate.py:78-142)."""
+    from voltyard.evaluate import evaluate
+
+    rc = vy.default_setup(vy.EnvConfig(episode_steps=96), days=40)
+    out = {}
+    for name in ("max_charge", "idle", "random"):
+        rep = evaluate(vy.make_policy(name, 16, 10, seed=3), rc.env, rc.station, rc.dataset, episodes=150, seed=7)
+        out[name] = rep.to_dict()
+    cfg4 = vy.EnvConfig(episode_steps=48, battery_enabled=True, alpha={"sat0": 1.0}, beta=0.1)
+    rc4 = vy.default_setup(cfg4, scenario="highway", traffic="high", days=20)
+    out["max_charge_battery"] = evaluate(vy.make_policy("max_charge", 16, 10), rc4.env, rc4.station, rc4.dataset,
+                                         episodes=40, seed=2).to_dict()
+    (OUT / "evaluate_reports.json").write_text(json.dumps(out, indent=1, sort_keys=True))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default=None)
@@ -213,6 +229,8 @@ def main():
         print("wrote", sc[0], "backend", be)
     synthetic_vectors(vy)
     print("wrote synthetic_vectors")
+    evaluate_vectors(vy)
+    print("wrote evaluate_reports")
 
 
 if __name__ == "__main__":

@@ -86,3 +86,14 @@ def test_tables_match_reference_build_tables(name):
         np.testing.assert_array_equal(got.astype(want.dtype) if want.dtype != object else got, want,
                                       err_msg=field)
     assert t.obs_len == ObsLayout(t.n_ports, t.horizon).length
+
+
+def test_fingerprint_matches_reference_reports():
+    import json
+
+    from paper_2507_01522_b200 import EnvConfig, default_setup
+    from paper_2507_01522_b200.evaluation import fingerprint
+
+    want = json.loads((GOLDEN / "evaluate_reports.json").read_text())
+    rc = default_setup(EnvConfig(episode_steps=96), days=40)
+    assert fingerprint(rc.env, rc.station, rc.dataset) == want["idle"]["config_fingerprint"]
