@@ -212,6 +212,24 @@ def evaluate_vectors(vy):
     (OUT / "evaluate_reports.json").write_text(json.dumps(out, indent=1, sort_keys=True))
 
 
+def bridge_vectors(vy):
+    """Observation-space bounds of the reference bridge (voltyard_gym :74-97)."""
+    sys.path.insert(0, "/root/reference/pkg/bridge/src")
+    from voltyard_gym import ChargingVectorEnv
+
+    out = {}
+    for tag, cfg, station, kw in (
+            ("default", vy.EnvConfig(), None, {}),
+            ("c4", vy.EnvConfig(battery_enabled=True), vy.preset_station("nested_splitters", ac_count=0, dc_count=64,
+                                                                         battery=vy.DEFAULT_BATTERY), {})):
+        rc = vy.default_setup(cfg, days=10, **kw)
+        env = ChargingVectorEnv(rc.env, station or rc.station, rc.dataset, num_envs=1, seed=0)
+        out[f"{tag}_low"] = env.observation_space.low
+        out[f"{tag}_high"] = env.observation_space.high
+        env.close()
+    np.savez_compressed(OUT / "bridge_spaces.npz", **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default=None)
@@ -230,6 +248,7 @@ def main():
     synthetic_vectors(vy)
     print("wrote synthetic_vectors")
     evaluate_vectors(vy)
+    bridge_vectors(vy)
     print("wrote evaluate_reports")
 
 

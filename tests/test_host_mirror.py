@@ -97,3 +97,21 @@ def test_fingerprint_matches_reference_reports():
     want = json.loads((GOLDEN / "evaluate_reports.json").read_text())
     rc = default_setup(EnvConfig(episode_steps=96), days=40)
     assert fingerprint(rc.env, rc.station, rc.dataset) == want["idle"]["config_fingerprint"]
+
+
+@pytest.mark.parametrize("tag", ["default", "c4"])
+def test_bridge_observation_space_matches_reference(tag):
+    from paper_2507_01522_b200 import DEFAULT_BATTERY, EnvConfig, default_setup, preset_station
+    from paper_2507_01522_b200.bridge import MultiDiscreteSpace, observation_space
+    from paper_2507_01522_b200.tables import build_tables
+
+    z = np.load(GOLDEN / "bridge_spaces.npz")
+    cfg = EnvConfig() if tag == "default" else EnvConfig(battery_enabled=True)
+    rc = default_setup(cfg, days=10)
+    st = rc.station if tag == "default" else preset_station("nested_splitters", ac_count=0, dc_count=64,
+                                                            battery=DEFAULT_BATTERY)
+    sp = observation_space(build_tables(cfg, st, rc.dataset))
+    np.testing.assert_array_equal(sp.low, z[f"{tag}_low"])
+    np.testing.assert_array_equal(sp.high, z[f"{tag}_high"])
+    ms = MultiDiscreteSpace(nvec=np.full(17, 21))
+    assert ms.contains(np.full(17, 20)) and not ms.contains(np.full(17, 21)) and not ms.contains(np.zeros(17))
