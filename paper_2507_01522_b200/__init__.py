@@ -9,6 +9,8 @@ from .errors import DataError, EpisodeDone, NativeError, SimError, StationError
 from .exogenous import (ArrivalProfile, AuxSeries, CarCatalog, CatalogEntry, Dataset, ExogenousFrame,
                         PriceSeries, UserScenarioModel, frame_at, generate_synthetic_defaults,
                         sample_arrival_count, sample_car, sample_user)
+from .ingest import (load_arrivals, load_aux, load_car_catalog, load_dataset, load_prices, load_station,
+                     save_arrivals, save_aux, save_car_catalog, save_dataset, save_prices, save_station)
 from .physics import (BatterySpec, BatteryState, CarProfile, CarState, UserProfile, charge_limit,
                       discharge_limit, integrate_battery, integrate_charge, power_to_current)
 from .station import (ArchNode, EvseSpec, StationParams, StationTree, build_station, default_station,

@@ -230,6 +230,58 @@ def bridge_vectors(vy):
     np.savez_compressed(OUT / "bridge_spaces.npz", **out)
 
 
+BAD_FILES = {
+    # name: (file, contents, loader)
+    "prices_gap": ("prices.csv", "timestamp,buy_eur_per_kwh\n2023-01-01T00:00,0.1\n2023-01-01T02:00,0.2\n", "load_prices"),
+    "prices_dup": ("prices.csv", "timestamp,buy_eur_per_kwh\n2023-01-01T00:00,0.1\n2023-01-01T00:00,0.2\n", "load_prices"),
+    "prices_offhour": ("prices.csv", "timestamp,buy_eur_per_kwh\n2023-01-01T00:30,0.1\n", "load_prices"),
+    "prices_col": ("prices.csv", "time,buy\n2023-01-01T00:00,0.1\n", "load_prices"),
+    "prices_empty": ("prices.csv", "timestamp,buy_eur_per_kwh\n", "load_prices"),
+    "prices_parse": ("prices.csv", "timestamp,buy_eur_per_kwh\n2023-01-01T00:00,abc\n", "load_prices"),
+    "arrivals_order": ("arrivals.csv", "step_of_day,lambda\n0,0.1\n2,0.2\n", "load_arrivals"),
+    "arrivals_neg": ("arrivals.csv", "step_of_day,lambda\n0,-0.1\n", "load_arrivals"),
+    "cars_tau": ("cars.csv", "name,capacity_kwh,r_max_ac_kw,r_max_dc_kw,tau,weight\nx,50,11,100,1.5,1\n",
+                 "load_car_catalog"),
+    "cars_cap": ("cars.csv", "name,capacity_kwh,r_max_ac_kw,r_max_dc_kw,tau,weight\nx,0,11,100,0.8,1\n",
+                 "load_car_catalog"),
+    "cars_zero": ("cars.csv", "name,capacity_kwh,r_max_ac_kw,r_max_dc_kw,tau,weight\nx,50,11,100,0.8,0\n",
+                  "load_car_catalog"),
+    "aux_cols": ("aux.csv", "timestamp,foo\n2023-01-01T00:00,1\n", "load_aux"),
+}
+
+
+def ingest_vectors(vy):
+    """Dataset directory + station JSON written by the reference, and its loader errors."""
+    import tempfile
+
+    from voltyard import data as vd
+    from voltyard import topology as vt
+
+    d = OUT / "ingest"
+    d.mkdir(exist_ok=True)
+    import dataclasses
+
+    ds = vy.generate_synthetic_defaults("work", "high", "us", seed=5, days=3)
+    ds = dataclasses.replace(ds, aux=vd.synthetic_aux(seed=1, days=3))
+    vd.save_dataset(ds, d / "dataset")
+    st = vy.preset_station("nested_splitters", ac_count=4, dc_count=6, battery=vy.DEFAULT_BATTERY)
+    obj = vt.station_to_dict(st)
+    obj["evse_order"] = list(reversed([e.id for e in st.evses]))
+    vt.save_station(vt.station_from_dict(obj), d / "station.json")
+    errs = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, (fname, text, loader) in BAD_FILES.items():
+            p = Path(tmp) / fname
+            p.write_text(text)
+            case = {"file": fname, "text": text, "loader": loader, "error": None}
+            try:
+                getattr(vd, loader)(p)
+            except vy.DataError as exc:
+                case["error"] = str(exc).replace(str(p), "<path>")
+            errs[name] = case
+    (d / "errors.json").write_text(json.dumps(errs, indent=1, sort_keys=True))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default=None)
@@ -249,6 +301,7 @@ def main():
     print("wrote synthetic_vectors")
     evaluate_vectors(vy)
     bridge_vectors(vy)
+    ingest_vectors(vy)
     print("wrote evaluate_reports")
 
 
