@@ -10,7 +10,11 @@ RandomPolicy writes uint8 actions, the fused step kernel advances all envs
 single-batch run); there is no data-path collective.  Time = max over ranks of
 CUDA-event time around exactly K steps with barrier + synchronize on both
 sides.  State + outputs are ~1.5 GB per rank, far above the 126 MB L2, so no
-L2 flush is needed between steps.
+L2 flush is needed between steps.  All envs move through the 288-step day in
+lockstep and the station load follows the arrival profile (empty at night,
+~94% of ports occupied mid-afternoon), so the timed window is centred on
+mid-day; the default K = 288 covers one whole day (every leg and both arms
+use the same rule, see window_start).
 
 Extra keys: roofline (dominant kernel: the fused step), e2e (same metric
 through the public API with host buffers: pinned actions H2D, step, obs /
@@ -20,8 +24,8 @@ cores, bounded sample), rollout (the fused T-step kernel, reported
 separately), clocks (nvidia-smi sampled during the timed region).
 
 Reference arm (--impl reference): the reference's compiled CPU kernel on all
-host cores, one step = one env-step of a bounded 2^18-env sample of the same
-workload; rank 0 only.
+host cores, one step = one env-step of a bounded 2^16-env sample of the same
+workload over the same window of the day; rank 0 only.
 """
 
 from __future__ import annotations
@@ -111,8 +115,18 @@ def load_peaks() -> dict:
         return {"hbm_gbs": 6650.0, "_fallback": True}
 
 
-def cpu_reference_rate(rc, B: int, steps: int, threads: int, prefer_ref: bool = True) -> dict:
-    """The reference's compiled kernel (oracle/_ref) or the C oracle on host cores."""
+def window_start(steps: int, warmup: int, episode_steps: int = 288) -> int:
+    """Untimed steps run before the warm-up so the timed window is centred on the
+    middle of the 288-step day.  All envs move in lockstep through the day
+    (reference semantics: every episode starts at step 0), and the station load
+    follows the arrival profile: nearly empty at night, ~94% of ports occupied
+    mid-afternoon (profiles/r1_day_profile.json).  K = 288 covers one whole day."""
+    return max(0, (episode_steps - steps) // 2 - warmup)
+
+
+def cpu_reference_rate(rc, B: int, advance: int, steps: int, threads: int, prefer_ref: bool = True) -> dict:
+    """The reference's compiled kernel (oracle/_ref) or the C oracle on host cores,
+    timed over the same window of the day as the GPU arm."""
     from oracle.harness import HostBatch, HostRandomPolicy, ref_available
     from paper_2507_01522_b200.tables import build_tables
 
@@ -121,15 +135,17 @@ def cpu_reference_rate(rc, B: int, steps: int, threads: int, prefer_ref: bool = 
     hb = HostBatch(t, B, master_seed=0, core="ref" if kind == "reference" else "oracle", threads=threads)
     pol = HostRandomPolicy(0, t.n_ports, t.k, range(B))
     hb.reset()
-    acts = [pol.actions() for _ in range(steps + 1)]
-    hb.core.step_all(acts[0])  # warm-up (page faults)
+    for _ in range(advance):
+        hb.core.step_all(pol.actions())
+    acts = [pol.actions() for _ in range(steps)]
     t0 = time.perf_counter()
     for s in range(steps):
-        hb.core.step_all(acts[s + 1])
+        hb.core.step_all(acts[s])
     dt = time.perf_counter() - t0
     return {"value": B * steps / dt, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"{B} envs x {steps} env-steps of the default station (core.step_range over {threads} threads, "
-                      f"actions pre-generated)", "seconds": dt}
+            "sample": f"{B} envs x {steps} env-steps (steps {advance}..{advance + steps - 1} of the day) of the "
+                      f"default station, core.step_range over {threads} threads, actions pre-generated",
+            "seconds": dt}
 
 
 def run_reference_arm(args) -> None:
@@ -140,14 +156,17 @@ def run_reference_arm(args) -> None:
 
     rc = default_setup()
     threads = len(os.sched_getaffinity(0))
-    B = 1 << 18
-    res = cpu_reference_rate(rc, B, args.steps + args.warmup, threads)
+    B = 1 << 16
+    res = cpu_reference_rate(rc, B, window_start(args.steps, args.warmup) + args.warmup, args.steps, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "C2 default 16-port station, random actions (bounded CPU sample)",
-                   "envs_per_step": B, "episode_steps": 288},
+                   "envs_per_step": B, "episode_steps": 288,
+                   "timed_window": f"steps {window_start(args.steps, args.warmup) + args.warmup}.."
+                                   f"{window_start(args.steps, args.warmup) + args.warmup + args.steps - 1} of the "
+                                   f"lockstep 288-step day (same window as the GPU arm)"},
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -157,7 +176,7 @@ def run_reference_arm(args) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=288)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--envs", type=int, default=B_PER_GPU)
@@ -190,6 +209,9 @@ def main() -> None:
     pol.bind(range(rank * B, rank * B + B))
     env.reset(as_numpy=False)
     stream = torch.cuda.current_stream()
+    advance = window_start(args.steps, args.warmup, rc.env.episode_steps)
+    for _ in range(advance):
+        env.step(pol.actions(env), collect_infos=False)
 
     def barrier():
         torch.cuda.synchronize()
@@ -247,7 +269,9 @@ def main() -> None:
                                "288-step episodes with in-kernel auto-reset",
                    "envs_per_gpu": B, "global_envs": B * world, "episode_steps": rc.env.episode_steps,
                    "parallelism": f"env-sharded x{world}", "l2": "inputs ~1.5 GB/GPU >> 126 MB L2 (no flush)",
-                   "obs_dtype": "f32", "actions": "u8 from device RandomPolicy"},
+                   "obs_dtype": "f32", "actions": "u8 from device RandomPolicy",
+                   "timed_window": f"steps {advance + args.warmup}..{advance + args.warmup + args.steps - 1} "
+                                   f"of the lockstep {rc.env.episode_steps}-step day (centred mid-day)"},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                      "frac": achieved / peaks.get("hbm_gbs"), "traffic": traffic,
@@ -285,6 +309,8 @@ def main() -> None:
         h_act.copy_(pol.actions(env).cpu())
         d_act = torch.empty_like(h_act, device=dev)
         e_steps = max(3, min(args.steps, 20))
+        while env._t != window_start(e_steps, 2, rc.env.episode_steps):  # centre this window mid-day too
+            env.step(pol.actions(env), collect_infos=False)
         for i in range(e_steps + 2):
             if i == 2:
                 barrier()
@@ -329,11 +355,11 @@ def main() -> None:
 
         hb = HeteroBatch(sweep_groups(B), master_seed=0, global_offset=rank * B, policy_seed=0)
         hb.reset()
-        for _ in range(3):
+        hsteps = max(3, min(args.steps, 20))
+        for _ in range(3 + window_start(hsteps, 3, rc.env.episode_steps)):  # window centred mid-day
             hb.graph_random_step()
         barrier()
         h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        hsteps = max(3, min(args.steps, 20))
         l0 = sum(e.launch_count() for e in hb.envs)
         h0.record(stream)
         for _ in range(hsteps):
@@ -349,8 +375,8 @@ def main() -> None:
 
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
-        result["cpu_baseline"] = {k: v for k, v in cpu_reference_rate(rc, 1 << 16, 8, threads).items()
-                                  if k != "seconds"}
+        result["cpu_baseline"] = {k: v for k, v in cpu_reference_rate(
+            rc, 1 << 16, advance + args.warmup, args.steps, threads).items() if k != "seconds"}
     env.close()
     if world > 1:
         dist.barrier()
