@@ -79,7 +79,17 @@ __global__ void k_selftest_div(const double* d, const double* y, int nd, int64_t
     const uint64_t mant = bits & 0xFFFFFFFFFFFFFull;
     const uint64_t ex = 1023 - 64 + ((bits >> 52) & 127);  // exponents 2^-64 .. 2^63
     const uint64_t sign = bits & 0x8000000000000000ull;
-    const double x = __longlong_as_double((long long)(sign | (ex << 52) | mant));
+    double x = __longlong_as_double((long long)(sign | (ex << 52) | mant));
+    // the first 64 dividends of every divisor are the special ones the model
+    // produces: signed zeros, small integers (dwell / episode_steps), exact
+    // multiples and halves
+    const int64_t j = s / nd;
+    if (j < 64) {
+      if (j < 2) x = j == 0 ? 0.0 : -0.0;
+      else if (j < 34) x = (double)(j - 17);
+      else if (j < 50) x = d[k] * (double)(j - 41);
+      else x = 0.5 * (double)(j - 56);
+    }
     const double want = __ddiv_rn(x, d[k]);
     const double got = div_rcp(x, d[k], y[k]);
     if (__double_as_longlong(want) != __double_as_longlong(got)) ++local;
@@ -287,6 +297,14 @@ int geometry(vy_handle* h, K kernel, const TileLayout& L, int n_profiles, Geomet
   const int64_t tiles = (h->B + 31) / 32;
   g.grid = (unsigned)((tiles + best_w - 1) / best_w);
   return VY_OK;
+}
+
+// Spec<true> (vy_device.cuh) applies: lean outputs, none of the optional
+// model features, a small identity-ordered tree and a shuffle-sized grid.
+bool lean_ok(const vy_handle* h, uint32_t flags, bool staged_actions) {
+  const vy_tables& t = h->t;
+  return (flags & ~VY_F_AUTO_RESET) == 0 && staged_actions && !t.battery_enabled && !t.has_moer && !t.has_dgrid &&
+         t.horizon == 0 && t.n_nodes <= kFastNodes && h->order_identity && 2 * t.k < 32;
 }
 
 Profile make_profile(double cap, double r_ac, double r_dc, double tau) {
@@ -515,8 +533,9 @@ int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride
   P.act_col = col_stride;
   if (inj) P.inj = *inj;
   Geometry g;
-  if (int rc = geometry(h, k_step, P.L, P.n_profiles, g)) return rc;
-  k_step<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P);
+  auto* kern = lean_ok(h, flags, acts) ? k_step<true> : k_step<false>;
+  if (int rc = geometry(h, kern, P.L, P.n_profiles, g)) return rc;
+  kern<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P);
   VY_CUDA(cudaGetLastError());
   ++h->launches;
   return VY_OK;
@@ -562,9 +581,10 @@ int vy_rollout(vy_handle* h, int32_t T, uint64_t policy_seed, int64_t index0, in
   P.out.reward = reward;
   P.out.done = done;
   Geometry g;
-  if (int rc = geometry(h, k_rollout, P.L, P.n_profiles, g)) return rc;
-  k_rollout<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P, T, policy_seed, index0, call0, obs_step_stride,
-                                                                   rew_step_stride);
+  auto* kern = lean_ok(h, flags, true) ? k_rollout<true> : k_rollout<false>;
+  if (int rc = geometry(h, kern, P.L, P.n_profiles, g)) return rc;
+  kern<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P, T, policy_seed, index0, call0, obs_step_stride,
+                                                              rew_step_stride);
   VY_CUDA(cudaGetLastError());
   ++h->launches;
   return VY_OK;

@@ -60,12 +60,14 @@ __device__ __forceinline__ int policy_action(uint64_t key, uint64_t j, int hi) {
 // RN(q + r*y) is the correctly rounded quotient (Markstein's theorem for a
 // correctly rounded reciprocal; no under/overflow in this model's ranges).
 // Bit-identical to IEEE x / d, checked exhaustively-by-sampling by
-// vy_selftest_div (tests/test_gpu_numerics.py).  Zeros keep their sign.
+// vy_selftest_div (tests/test_gpu_numerics.py).  The residual is formed as
+// -(q*d - x) rather than x - q*d: the same exact value, but a zero dividend
+// yields a -0 residual, so RN(q + (-0)*y) keeps the sign of a zero quotient
+// with no select or branch (three fp64 instructions in all).
 __device__ __forceinline__ double div_rcp(double x, double d, double y) {
   const double q = __dmul_rn(x, y);
-  const double r = __fma_rn(-q, d, x);
-  const double z = __fma_rn(r, y, q);
-  return x == 0.0 ? x : z;
+  const double r = __fma_rn(q, d, -x);
+  return __fma_rn(-r, y, q);
 }
 
 struct Profile {  // car profile: catalogue entry (or injected car)
@@ -133,6 +135,31 @@ struct Params {
   vy_draws inj;
   uint32_t* err;
   TileLayout L;
+};
+
+
+// Compile-time specialisation.  Spec<true> ("lean") is the step of the common
+// configuration: obs/reward/done only (no infos, no injected draws), float32
+// obs, no battery, no carbon / demand series, no price horizon, a tree of at
+// most kFastNodes nodes, identity parking order, staged uint8 actions, a
+// shuffle-sized action grid.  Everything it folds away is dead code the lean
+// kernel never carries (smaller hot loop, fewer i-cache misses, no uniform
+// branches); Spec<false> reads all of it at run time.  The host picks the
+// instantiation (lean_ok in vy_abi.cu).
+template <bool Lean>
+struct Spec {
+  static constexpr bool lean = Lean;
+  __device__ __forceinline__ static bool info(const Params& P) { return !Lean && (P.flags & VY_F_INFOS); }
+  __device__ __forceinline__ static bool inject(const Params& P) { return !Lean && (P.flags & VY_F_INJECT); }
+  __device__ __forceinline__ static bool f64(const Params& P) { return !Lean && (P.flags & VY_F_OUT_F64); }
+  __device__ __forceinline__ static bool battery(const Params& P) { return !Lean && P.battery; }
+  __device__ __forceinline__ static bool moer(const Params& P) { return !Lean && P.has_moer; }
+  __device__ __forceinline__ static bool dgrid(const Params& P) { return !Lean && P.has_dgrid; }
+  __device__ __forceinline__ static int horizon(const Params& P) { return Lean ? 0 : P.horizon; }
+  __device__ __forceinline__ static bool fast_tree(const Params& P) { return Lean || P.n_nodes <= kFastNodes; }
+  __device__ __forceinline__ static bool identity(const Params& P) { return Lean || P.order_identity; }
+  __device__ __forceinline__ static bool staged(const Params& P) { return Lean || P.act_tile; }
+  __device__ __forceinline__ static bool probe(const Params& P, uint32_t bit) { return !Lean && (P.flags & bit); }
 };
 
 }  // namespace vy

@@ -40,24 +40,26 @@ __device__ __forceinline__ void stage_tables(const Params& P, const Profile*& pr
 // One step of the 32 envs of the tile starting at env b0.  Every lane runs
 // the transition (padding lanes on their harmless padding columns, side
 // effects masked) because the fused port loop synchronises the warp.
+template <bool Lean>
 __device__ __forceinline__ void step_tile(const Params& P, const Profile* prof, const double* dtab, uint32_t tile,
                                           int64_t b0, int lane) {
+  using C = Spec<Lean>;
   const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
   EnvRegs E{};  // zero for padding lanes so table lookups stay in bounds
-  if (active) load_env(P, b, E);
-  tile_issue(P, tile, b0, lane, P.act_tile);
+  if (active) load_env<Lean>(P, b, E);
+  tile_issue(P, tile, b0, lane, C::staged(P));
   // exogenous inputs for this step and the obs globals of the next one, in
   // flight together with the tile copies
-  const Frame F = load_frame(P, E.step, E.day);
+  const Frame F = load_frame<Lean>(P, E.step, E.day);
   const ObsGlobals G = load_obs_globals(P, E.step + 1, E.day);
   tile_wait();
-  const ObsSink S = make_sink(P, T, b, P.out.obs, /*in_place=*/true);
+  const ObsSink S = make_sink<Lean>(P, T, b, P.out.obs, /*in_place=*/true);
   const int dt = P.act_dtype;
   const int64_t rs = P.act_row, cs = P.act_col;
   const uint8_t* arow = vy_smem + tile + P.L.acts + lane * (P.n_ports + 1);
-  const bool staged = P.act_tile;
+  const bool staged = C::staged(P);
   auto act = [&](int slot) -> int {
     if (staged) return arow[slot];
     if (!active) return P.k;
@@ -68,7 +70,7 @@ __device__ __forceinline__ void step_tile(const Params& P, const Profile* prof, 
     return v < INT_MIN ? INT_MIN : (v > INT_MAX ? INT_MAX : (int)v);
   };
   StepResult r{0.0, false};
-  if (!(P.flags & 0x200u)) r = tile_step(P, prof, dtab, T, E, b, F, S, active, act);  // 0x200: memory-only probe
+  if (!C::probe(P, 0x200u)) r = tile_step<Lean>(P, prof, dtab, T, E, b, F, S, active, act);  // 0x200: memory-only probe
   bool reset = false;
   if (r.done && (P.flags & VY_F_AUTO_RESET)) {
     // in-kernel auto-reset (engine.py:460-462): the terminal reward/done/infos
@@ -83,19 +85,20 @@ __device__ __forceinline__ void step_tile(const Params& P, const Profile* prof, 
     reset = true;
   }
   if (active) {
-    if (!(P.flags & 0x800u)) store_env(P, b, E, reset);
-    if (P.flags & VY_F_OUT_F64)
+    if (!C::probe(P, 0x800u)) store_env<Lean>(P, b, E, reset);
+    if (C::f64(P))
       reinterpret_cast<double*>(P.out.reward)[b] = r.reward;
     else
       reinterpret_cast<float*>(P.out.reward)[b] = (float)r.reward;
     P.out.done[b] = r.done;
   }
-  emit_tail(P, T, E, G, S, b0, active, P.out.obs);
+  emit_tail<Lean>(P, T, E, G, S, b0, active, P.out.obs);
 }
 
 // One warp per tile.  (A persistent variant with L2 bulk prefetch of the next
 // tile measured slower: the kernel is bound by per-warp latency, not by DRAM
 // requests in flight.)
+template <bool Lean>
 __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) {
   const Profile* prof;
   const double* dtab;
@@ -103,12 +106,14 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
   if (b0 >= P.B) return;  // whole warp leaves together
-  step_tile(P, prof, dtab, tables_bytes(P.n_profiles, P.k) + warp * P.L.bytes, b0, lane);
+  step_tile<Lean>(P, prof, dtab, tables_bytes(P.n_profiles, P.k) + warp * P.L.bytes, b0, lane);
 }
 
+template <bool Lean>
 __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params P, int T_steps, uint64_t policy_seed,
                                                  int64_t index0, int64_t call0, int64_t obs_stride,
                                                  int64_t rew_stride) {
+  using C = Spec<Lean>;
   const Profile* prof;
   const double* dtab;
   stage_tables(P, prof, dtab);
@@ -125,21 +130,21 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
   uint64_t pkey = 0, seed = 0;
   int episode = 0;
   if (active) {
-    load_env(P, b, E);
+    load_env<Lean>(P, b, E);
     pkey = fold(fold(fold(kKey0, policy_seed), (uint64_t)(index0 + b)), 2);
     episode = P.st.episode[b];
     seed = P.st.env_seed[b];
   }
   const int ns = P.n_ports + 1, hi = 2 * P.k + 1;
-  const bool f64 = P.flags & VY_F_OUT_F64;
+  const bool f64 = C::f64(P);
   for (int t = 0; t < T_steps; ++t) {
     void* obs_t = f64 ? (void*)(reinterpret_cast<double*>(P.out.obs) + t * obs_stride)
                       : (void*)(reinterpret_cast<float*>(P.out.obs) + t * obs_stride);
-    const ObsSink S = make_sink(P, T, b, obs_t, /*in_place=*/false);
+    const ObsSink S = make_sink<Lean>(P, T, b, obs_t, /*in_place=*/false);
     const uint64_t j0 = (uint64_t)(call0 + t) * (uint64_t)ns;
     auto act = [&](int slot) -> int { return policy_action(pkey, j0 + slot + 1, hi); };
-    const Frame F = load_frame(P, E.step, E.day);
-    const StepResult r = tile_step(P, prof, dtab, T, E, b, F, S, active, act);
+    const Frame F = load_frame<Lean>(P, E.step, E.day);
+    const StepResult r = tile_step<Lean>(P, prof, dtab, T, E, b, F, S, active, act);
     if (r.done) {
       ++episode;
       reset_scalars(P, E, seed, episode, 0, false);
@@ -153,11 +158,11 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
         reinterpret_cast<float*>(P.out.reward)[t * rew_stride + b] = (float)r.reward;
       P.out.done[t * rew_stride + b] = r.done;
     }
-    emit_tail(P, T, E, load_obs_globals(P, E.step, E.day), S, b0, active, obs_t);
+    emit_tail<Lean>(P, T, E, load_obs_globals(P, E.step, E.day), S, b0, active, obs_t);
   }
-  if (!(P.flags & 0x800u)) tile_store(P, T.t, b0, lane);
+  if (!C::probe(P, 0x800u)) tile_store(P, T.t, b0, lane);
   if (active) {
-    store_env(P, b, E, true);
+    store_env<Lean>(P, b, E, true);
     P.st.episode[b] = episode;
   }
 }
@@ -179,13 +184,13 @@ __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P,
   tile_wait();
   const bool mine = active && (!mask || mask[b]);
   EnvRegs E{};  // zero for padding lanes so the obs path stays in bounds
-  if (active) load_env(P, b, E);
+  if (active) load_env<false>(P, b, E);
   if (mine) {
     const int ep = episode_mode ? P.st.episode[b] + 1 : 0;
     reset_scalars(P, E, P.st.env_seed[b], ep, inj_day ? inj_day[b] : 0, inj_day != nullptr);
     clear_tile_ports(P, T);
     P.st.episode[b] = ep;
-    store_env(P, b, E, true);
+    store_env<false>(P, b, E, true);
   }
   // masked-out rows still get their (unchanged) obs rewritten, which is idempotent
   emit_obs(P, prof, T, E, load_obs_globals(P, E.step, E.day), b0, active, P.out.obs, /*store_state=*/true);

@@ -22,6 +22,7 @@
 
 #include "vy_device.cuh"
 
+
 namespace vy {
 
 // Dynamic shared memory of every kernel in this library.  Tile data is
@@ -194,13 +195,15 @@ __device__ __forceinline__ void tile_wait() {
   __syncwarp();
 }
 
+template <bool Lean>
 __device__ __forceinline__ void load_env(const Params& P, int64_t b, EnvRegs& E) {
+  using C = Spec<Lean>;
   const vy_state& s = P.st;
   E.step = ldg_s32(s.step + b);
   E.day = ldg_s32(s.day + b);
   E.akey = ldg_u64(s.akey + b);
-  E.b_i = P.battery ? ldg_f64(s.b_i + b) : 0.0;
-  E.b_soc = P.battery ? ldg_f64(s.b_soc + b) : 0.0;
+  E.b_i = C::battery(P) ? ldg_f64(s.b_i + b) : 0.0;
+  E.b_soc = C::battery(P) ? ldg_f64(s.b_soc + b) : 0.0;
   E.ep_profit = ldg_f64(s.ep_profit + b);
   E.ep_reward = ldg_f64(s.ep_reward + b);
   E.ep_missing = ldg_f64(s.ep_missing + b);
@@ -210,10 +213,11 @@ __device__ __forceinline__ void load_env(const Params& P, int64_t b, EnvRegs& E)
   E.ep_departures = ldg_s32(s.ep_departures + b);
 }
 
+template <bool Lean>
 __device__ __forceinline__ void store_env(const Params& P, int64_t b, const EnvRegs& E, bool reset_too) {
   const vy_state& s = P.st;
   s.step[b] = E.step;
-  if (P.battery) {
+  if (Spec<Lean>::battery(P)) {
     s.b_i[b] = E.b_i;
     s.b_soc[b] = E.b_soc;
   }
@@ -232,7 +236,8 @@ __device__ __forceinline__ void store_env(const Params& P, int64_t b, const EnvR
 
 // charge envelope (vehicles.py:22-35): rbar below tau, then (1-soc)*rbar/(1-tau)
 __device__ __forceinline__ double envelope(double soc, double tau, double omt, double rcp_omt, double rbar) {
-  return soc <= tau ? rbar : div_rcp((1.0 - soc) * rbar, omt, rcp_omt);
+  const double taper = div_rcp((1.0 - soc) * rbar, omt, rcp_omt);  // five fp64 ops: cheaper than a branch
+  return soc <= tau ? rbar : taper;
 }
 
 // Clip a requested current (_kernel.pyx:309-325 ports, :329-345 battery).  Charging
@@ -336,6 +341,7 @@ struct Frame {
   double p_buy, p_sg, moer, dgrid, pthr;
   int hidx, lam_idx, pfull;
 };
+template <bool Lean>
 __device__ __forceinline__ Frame load_frame(const Params& P, int t, int day) {
   Frame F;
   const int64_t minutes = (int64_t)t * P.dt_min;
@@ -343,8 +349,8 @@ __device__ __forceinline__ Frame load_frame(const Params& P, int t, int day) {
   F.hidx = eff_day * 24 + (int)((minutes / 60) % 24);
   F.p_buy = ldg_nc_f64(P.buy + F.hidx);
   F.p_sg = ldg_nc_f64(P.sellg + F.hidx);
-  F.moer = P.has_moer ? ldg_nc_f64(P.moer + F.hidx) : 0.0;
-  F.dgrid = P.has_dgrid ? ldg_nc_f64(P.dgrid + F.hidx) : 0.0;
+  F.moer = Spec<Lean>::moer(P) ? ldg_nc_f64(P.moer + F.hidx) : 0.0;
+  F.dgrid = Spec<Lean>::dgrid(P) ? ldg_nc_f64(P.dgrid + F.hidx) : 0.0;
   F.lam_idx = (ldg_nc_s8(P.weekday + eff_day) ? 0 : P.lam_len) + t % P.lam_len;
   F.pfull = ldg_nc_s32(P.pois_full + F.lam_idx);
   F.pthr = ldg_nc_f64(P.pois_thr + F.lam_idx);
@@ -422,13 +428,15 @@ __device__ __forceinline__ void store_port(const Params& P, int64_t b, int i, ui
 
 // One transition of one env (_kernel.pyx:283-571).  `act(slot)` returns the
 // action index of a slot; `b` is the global env index (infos / injected draws).
-template <class Act>
+template <bool Lean, class Act>
 __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* __restrict__ prof,
                                                 const double* __restrict__ dtab, const Lane& T, EnvRegs& E,
                                                 int64_t b, const Frame& F, const ObsSink& S, bool active, Act act) {
   const int n = P.n_ports;
   const int64_t ld = P.ld;
-  const bool info = P.flags & VY_F_INFOS;
+  using C = Spec<Lean>;
+  const bool info = C::info(P);
+  const bool battery = C::battery(P);
   const vy_outputs& O = P.out;
   const int t = E.step;
 
@@ -442,17 +450,17 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   // (a-k)/k: with 2k+1 <= 32 the grid lives one entry per lane and a warp
   // shuffle fetches it (a random-index shared-memory lookup bank-conflicts);
   // otherwise the staged table, else the IEEE division.
-  const bool shfl_grid = hi_a < 32;
-  const double grid_lane = shfl_grid && dtab ? dtab[T.lane <= hi_a ? T.lane : 0] : 0.0;
+  const bool shfl_grid = C::lean || (hi_a < 32 && dtab);
+  const double grid_lane = shfl_grid ? dtab[T.lane <= hi_a ? T.lane : 0] : 0.0;
+  // out-of-range actions are clamped and flagged once per step (lazy error word)
+  bool bad_action = false;
   auto delta_of = [&](int a) -> double {
-    if ((unsigned)a > (unsigned)hi_a) {
-      atomicOr(P.err, 1u);
-      a = a < 0 ? 0 : hi_a;
-    }
-    if (shfl_grid && dtab) return __shfl_sync(0xffffffffu, grid_lane, a);
+    bad_action |= (unsigned)a > (unsigned)hi_a;
+    a = min(max(a, 0), hi_a);
+    if (shfl_grid) return __shfl_sync(0xffffffffu, grid_lane, a);
     return dtab ? dtab[a] : (double)(a - P.k) / (double)P.k;
   };
-  const bool fast = P.n_nodes <= kFastNodes;
+  const bool fast = C::fast_tree(P);
   double nsum[kFastNodes];
 #pragma unroll
   for (int m = 0; m < kFastNodes; ++m) nsum[m] = 0.0;
@@ -460,13 +468,18 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   for (int i = 0; i < n; ++i) {
     const double d = delta_of(act(i));
     const uint32_t mt = T.meta(i);
+    const double idr_i = T.idr(i), soc_i = T.soc(i);
+    // A port no lane of the warp occupies is skipped (one vote, uniform
+    // branch); otherwise branch-free: an empty port (meta 0 -> profile 0,
+    // zero slots) runs the same arithmetic and the select discards it.
     double c = 0.0;
-    if (mt & 1u) {
-      double tgt = T.idr(i) + d * P.imax_c[i];
+    if (__any_sync(0xffffffffu, mt & 1u)) {
+      double tgt = idr_i + d * P.imax_c[i];
       if (!P.allow_discharge && tgt < 0.0) tgt = 0.0;
       const Profile& pr = prof[mt >> 2];
-      c = clip_current(tgt, T.soc(i), pr.tau, pr.omt, pr.rcp_omt, P.kind[i] ? pr.r_dc : pr.r_ac, P.volt[i],
+      c = clip_current(tgt, soc_i, pr.tau, pr.omt, pr.rcp_omt, P.kind[i] ? pr.r_dc : pr.r_ac, P.volt[i],
                        P.rcp_volt[i], P.imax_c[i], P.imax_d[i]);
+      c = (mt & 1u) ? c : 0.0;
     }
     T.idr(i) = c;
     if (info) O.i_att[i * ld + b] = c;
@@ -479,7 +492,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   {
     // the battery slot is validated even when the battery is disabled (engine.py:440-442)
     const double d = delta_of(act(n));
-    if (P.battery) {
+    if (battery) {
       const double tgt = E.b_i + d * P.b_imax;
       cb = clip_current(tgt, E.b_soc, P.b_tau, P.b_omt, P.b_rcp_omt, P.b_rmax, P.b_volt, P.b_rcp_volt, P.b_imax,
                         P.b_imax);
@@ -489,6 +502,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
         if (P.battery_node_mask & (1 << m)) nsum[m] += cb;
     }
   }
+  if (bad_action) atomicOr(P.err, 1u);
   // tree: excess on the requested currents (_kernel.pyx:611-624), then rescale
   double excess = 0.0;
   if (fast) {
@@ -509,9 +523,9 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   if (excess > 0.0) fit_tree(P, T, cb);
   if (info) {
     for (int i = 0; i < n; ++i) O.i_used[i * ld + b] = T.idr(i);
-    if (P.battery) O.i_used[n * ld + b] = cb;
+    if (battery) O.i_used[n * ld + b] = cb;
   }
-  if (P.battery) E.b_i = cb;
+  if (battery) E.b_i = cb;
 
   // phases 2+3: charge (_kernel.pyx:358-424), dwell countdown (:420-422) and
   // departures (:426-458) fused into one pass in port order; the same pass
@@ -527,57 +541,64 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
     uint32_t mt = T.meta(i);
     double cur = T.idr(i), soc = T.soc(i), de = T.de(i);
     int dt = T.dtrem(i);
+    // Ports no lane of the warp occupies are skipped (one vote, uniform
+    // branch).  Otherwise branch-free: an empty port holds meta 0 and zero
+    // slots, its current is 0 (phase 1), so the arithmetic below yields
+    // got = +0, soc = de = 0 for it; only the dwell countdown and the
+    // departure test are gated.  Sums that start at +0 never become -0, so
+    // the +0 terms of empty / staying ports leave them bit-identical to the
+    // reference's conditional adds.
+    const bool occ = mt & 1u;
     double got = 0.0;
-    if (mt & 1u) {
+    bool dep = false;
+    if (__any_sync(0xffffffffu, occ)) {
       const Profile& pr = prof[mt >> 2];
       const double raw = div_rcp(P.dtv[i] * cur, 1000.0, P.rcp_1000);
-      got = raw;
-      if (raw >= 0.0) {
-        if (de < got) got = de;
+      {
+        double gc = raw;
+        if (de < gc) gc = de;
         const double room = pr.cap * (1.0 - soc);
-        if (room < got) got = room;
-      } else {
+        if (room < gc) gc = room;
         const double fl = -pr.cap * soc;
-        if (got < fl) got = fl;
+        const double gd = raw < fl ? fl : raw;
+        got = raw >= 0.0 ? gc : gd;
       }
       soc = soc + div_rcp(got, pr.cap, pr.rcp_cap);
       soc = soc < 0.0 ? 0.0 : (soc > 1.0 ? 1.0 : soc);
       de = de - got;
       de = de < 0.0 ? 0.0 : de;
       e_net += got;
-      if (got > 0.0)
-        e_in += P.eta_c[i] == 1.0 ? got : div_rcp(got, P.eta_c[i], P.rcp_eta_c[i]);
-      else if (got < 0.0)
-        e_out += got * P.eta_d[i];
-      dt -= 1;
+      const double gin = P.eta_c[i] == 1.0 ? got : div_rcp(got, P.eta_c[i], P.rcp_eta_c[i]);
+      e_in += got > 0.0 ? gin : 0.0;
+      e_out += got < 0.0 ? got * P.eta_d[i] : 0.0;
+      dt -= occ ? 1 : 0;
       const int p = (mt >> 1) & 1u;
-      if ((p == 0 && dt <= 0) || (p == 1 && de == 0.0)) {
-        const int over = dt < 0 ? -dt : 0, early = dt > 0 ? dt : 0;
-        if (info) {
-          const int64_t at = (int64_t)nd * ld + b;
-          O.dep_port[at] = i;
-          O.dep_missing[at] = de;
-          O.dep_overtime[at] = over;
-          O.dep_early[at] = early;
-          O.dep_pref[at] = p;
-          O.dep_cap[at] = pr.cap;
-          O.dep_soc[at] = soc;
-        }
-        if (p == 0)
-          sat0 += de;
-        else
-          sat1 += (double)over - P.beta * (double)early;
-        E.ep_missing += de;
-        E.ep_overtime += over;
-        E.ep_departures += 1;
-        mt = 0;
-        cur = soc = de = 0.0;
-        dt = 0;
-        ++nd;
-      } else {
-        occm |= 1ull << i;
-        if (last && p == 1 && dt < 0) tover += -dt;  // _kernel.pyx:559-561 (arrivals add dt > 0 only)
+      dep = occ && ((p == 0 && dt <= 0) || (p == 1 && de == 0.0));
+      const int over = dt < 0 ? -dt : 0, early = dt > 0 ? dt : 0;
+      if (info && dep) {
+        const int64_t at = (int64_t)nd * ld + b;
+        O.dep_port[at] = i;
+        O.dep_missing[at] = de;
+        O.dep_overtime[at] = over;
+        O.dep_early[at] = early;
+        O.dep_pref[at] = p;
+        O.dep_cap[at] = pr.cap;
+        O.dep_soc[at] = soc;
       }
+      sat0 += dep && p == 0 ? de : 0.0;
+      sat1 += dep && p == 1 ? (double)over - P.beta * (double)early : 0.0;
+      E.ep_missing += dep ? de : 0.0;
+      E.ep_overtime += dep ? over : 0;
+      E.ep_departures += dep ? 1 : 0;
+      nd += dep ? 1 : 0;
+      // _kernel.pyx:559-561 (arrivals add dt > 0 only)
+      tover += !dep && last && p == 1 && dt < 0 ? -dt : 0;
+      occm |= (uint64_t)(occ && !dep) << i;
+    }
+    if (dep) {
+      mt = 0;
+      cur = soc = de = 0.0;
+      dt = 0;
     }
     if (info) O.delivered[i * ld + b] = got;
     if (S.in_place) {
@@ -593,7 +614,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
     stage_port_obs(P, prof, S, T.lane, active, i, mt, cur, soc, de, dt);
   }
   double e_b = 0.0, bgot = 0.0;
-  if (P.battery) {
+  if (battery) {
     bgot = div_rcp(P.b_dtv * E.b_i, 1000.0, P.rcp_1000);
     if (bgot >= 0.0) {
       const double room = P.b_cap * (1.0 - E.b_soc);
@@ -614,7 +635,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
 
   // phase 4: arrivals (_kernel.pyx:460-509); draws of Stream(key4(seed, ep, 1, t))
   uint64_t st = fold(E.akey, (uint64_t)(int64_t)t);
-  const bool inj = P.flags & VY_F_INJECT;
+  const bool inj = C::inject(P);
   int m = 0;
   int64_t inj0 = 0;
   if (inj) {
@@ -658,7 +679,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
     if (j >= admitted) continue;
     const uint64_t freem = ~occm & (n == 64 ? ~0ull : ((1ull << n) - 1));
     int port = 0;
-    if (P.order_identity) {
+    if (C::identity(P)) {
       port = __ffsll((long long)freem) - 1;
     } else {
       for (int q = 0; q < n; ++q)
@@ -694,11 +715,11 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   c[0] = excess;
   c[1] = sat0;
   c[2] = sat1;
-  c[3] = P.has_moer ? F.moer * e_grid_net : 0.0;
+  c[3] = C::moer(P) ? F.moer * e_grid_net : 0.0;
   c[4] = (double)declined;
   c[5] = e_b < 0.0 ? -e_b : 0.0;
   c[6] = e_out < 0.0 ? -e_out : 0.0;
-  if (P.has_dgrid) {
+  if (C::dgrid(P)) {
     const double d = e_net - F.dgrid;
     c[7] = d >= 0.0 ? d : -d;
   } else {
@@ -780,16 +801,18 @@ __device__ __forceinline__ void tile_store(const Params& P, uint32_t toff, int64
   __syncwarp();
 }
 
+template <bool Lean>
 __device__ __forceinline__ ObsSink make_sink(const Params& P, const Lane& T, int64_t b, void* obs_base,
                                              bool in_place) {
   ObsSink S;
   S.cells = smem_base() + T.t + P.L.obs;
-  S.row64 = (P.flags & VY_F_OUT_F64) ? reinterpret_cast<double*>(obs_base) + b * P.obs_len : nullptr;
+  S.row64 = Spec<Lean>::f64(P) ? reinterpret_cast<double*>(obs_base) + b * P.obs_len : nullptr;
   S.in_place = in_place;
   return S;
 }
 
 // Global obs columns and the coalesced read-out of the staged [rows][OL] block.
+template <bool Lean>
 __device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const EnvRegs& E, ObsGlobals G,
                                           const ObsSink& S, int64_t b0, bool active, void* obs_base) {
   const int n = P.n_ports;
@@ -816,7 +839,7 @@ __device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const 
       sts_f32(S.cells + (c0 + k) * 132 + lane * 4, (float)gv[k]);
     }
   }
-  for (int h = 0; h < P.horizon; ++h) {
+  for (int h = 0; h < Spec<Lean>::horizon(P); ++h) {
     const int64_t fmin = (int64_t)(E.step + 1 + h) * P.dt_min;
     const int64_t fday = ((int64_t)E.day + fmin / 1440) % P.n_days;
     const double v = __ldg(P.buy + fday * 24 + (fmin / 60) % 24);
@@ -828,14 +851,28 @@ __device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const 
   }
   if (S.row64) return;
   __syncwarp();
-  if (P.flags & 0x400u) return;  // probe: no obs stores
+  if (Spec<Lean>::probe(P, 0x400u)) return;  // probe: no obs stores
   // Row-major read-out: row r, column c = lane + 32 j lives at
   // cells + c*132 + r*4 = cells + lane*132 + r*4 + j*4224; bank (lane + r) % 32.
   float* g = reinterpret_cast<float*>(obs_base) + b0 * OL + lane;
   const int64_t left = P.B - b0;
   const int rows = left >= 32 ? 32 : (int)left;
   const uint32_t lbase = S.cells + lane * 132;
-  if (OL <= 128) {
+  if (OL > 96 && OL <= 128) {
+    // three whole 32-column chunks (no predicates, no zero-filled temporaries)
+    // and a ragged fourth (the 16-port station: OL = 105)
+    const bool p3 = lane + 96 < OL;
+#pragma unroll 4
+    for (int r = 0; r < rows; ++r) {
+      const uint32_t a = lbase + r * 4;
+      const float v0 = lds_f32(a), v1 = lds_f32(a + 4224), v2 = lds_f32(a + 8448);
+      g[0] = v0;
+      g[32] = v1;
+      g[64] = v2;
+      if (p3) g[96] = lds_f32(a + 12672);
+      g += OL;
+    }
+  } else if (OL <= 128) {
     const bool p0 = lane < OL, p1 = lane + 32 < OL, p2 = lane + 64 < OL, p3 = lane + 96 < OL;
 #pragma unroll 2
     for (int r = 0; r < rows; ++r) {
@@ -868,7 +905,7 @@ __device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const 
 __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, const Lane& T, const EnvRegs& E,
                                          ObsGlobals G, int64_t b0, bool active, void* obs_base, bool store_state) {
   const int64_t b = b0 + T.lane;
-  const ObsSink S = make_sink(P, T, b, obs_base, P.L.obs == 0);
+  const ObsSink S = make_sink<false>(P, T, b, obs_base, P.L.obs == 0);
   if (store_state && !(P.flags & 0x800u)) tile_store(P, T.t, b0, T.lane);
 #pragma unroll 2
   for (int i = 0; i < P.n_ports; ++i) {
@@ -878,7 +915,7 @@ __device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, c
     if (S.in_place) __syncwarp();  // every lane has read port i before its slots are reused
     stage_port_obs(P, prof, S, T.lane, active, i, mt, idr, soc, de, dt);
   }
-  emit_tail(P, T, E, G, S, b0, active, obs_base);
+  emit_tail<false>(P, T, E, G, S, b0, active, obs_base);
 }
 
 }  // namespace vy
