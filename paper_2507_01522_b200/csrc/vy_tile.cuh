@@ -464,7 +464,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   double nsum[kFastNodes];
 #pragma unroll
   for (int m = 0; m < kFastNodes; ++m) nsum[m] = 0.0;
-#pragma unroll 2
+#pragma unroll 1  // rolled: smaller hot loop measured faster than unroll 2 or 4
   for (int i = 0; i < n; ++i) {
     const double d = delta_of(act(i));
     const uint32_t mt = T.meta(i);
@@ -536,7 +536,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
   int nd = 0, tover = 0;
   uint64_t occm = 0;
   const bool last = t + 1 == P.episode_steps;
-#pragma unroll 2
+#pragma unroll 1  // rolled: smaller hot loop measured faster than unroll 2 or 4
   for (int i = 0; i < n; ++i) {
     uint32_t mt = T.meta(i);
     double cur = T.idr(i), soc = T.soc(i), de = T.de(i);
