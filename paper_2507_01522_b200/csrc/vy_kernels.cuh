@@ -23,7 +23,7 @@ __host__ __device__ inline int tables_bytes(int n_profiles, int k) {
   return (n_profiles * (int)sizeof(Profile) + nd * 8 + 127) & ~127;
 }
 
-__device__ __forceinline__ void stage_tables(const Params& P, const Profile*& prof, const double*& dtab) {
+__device__ __forceinline__ void stage_tables(const Params& P, Prof& prof, const double*& dtab) {
   unsigned char* smem = vy_smem;
   double* spd = reinterpret_cast<double*>(smem);
   const double* gp = reinterpret_cast<const double*>(P.profiles);
@@ -33,7 +33,7 @@ __device__ __forceinline__ void stage_tables(const Params& P, const Profile*& pr
   if (nd <= 256)
     for (int i = threadIdx.x; i < nd; i += blockDim.x) sd[i] = __ldg(P.delta_tab + i);
   __syncthreads();
-  prof = reinterpret_cast<const Profile*>(smem);
+  prof = Prof{smem_base()};
   dtab = nd <= 256 ? sd : nullptr;
 }
 
@@ -41,7 +41,7 @@ __device__ __forceinline__ void stage_tables(const Params& P, const Profile*& pr
 // the transition (padding lanes on their harmless padding columns, side
 // effects masked) because the fused port loop synchronises the warp.
 template <bool Lean>
-__device__ __forceinline__ void step_tile(const Params& P, const Profile* prof, const double* dtab, uint32_t tile,
+__device__ __forceinline__ void step_tile(const Params& P, Prof prof, const double* dtab, uint32_t tile,
                                           int64_t b0, int lane) {
   using C = Spec<Lean>;
   const Lane T = make_lane(P, tile, lane);
@@ -100,7 +100,7 @@ __device__ __forceinline__ void step_tile(const Params& P, const Profile* prof, 
 // requests in flight.)
 template <bool Lean>
 __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) {
-  const Profile* prof;
+  Prof prof;
   const double* dtab;
   stage_tables(P, prof, dtab);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
                                                  int64_t index0, int64_t call0, int64_t obs_stride,
                                                  int64_t rew_stride) {
   using C = Spec<Lean>;
-  const Profile* prof;
+  Prof prof;
   const double* dtab;
   stage_tables(P, prof, dtab);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
 
 __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P, const uint8_t* mask,
                                                int episode_mode, const int32_t* inj_day) {
-  const Profile* prof;
+  Prof prof;
   const double* dtab;
   stage_tables(P, prof, dtab);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

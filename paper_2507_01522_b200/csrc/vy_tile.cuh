@@ -66,6 +66,26 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
 }
 __device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v)); }
 
+// The per-CTA car-profile table in shared memory, addressed through an
+// explicit 32-bit shared-window address (a generic Profile* made the compiler
+// re-derive the window base, S2UR SR_CgaCtaId + LEA, at every lookup).  Loads
+// are non-volatile: the table is read-only after staging.
+struct Prof {
+  uint32_t a;  // shared address of profile 0
+  __device__ __forceinline__ double at(int c, int w) const {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a + (uint32_t)c * (uint32_t)sizeof(Profile) + 8u * w));
+    return v;
+  }
+  __device__ __forceinline__ double cap(int c) const { return at(c, 0); }
+  __device__ __forceinline__ double r_ac(int c) const { return at(c, 1); }
+  __device__ __forceinline__ double r_dc(int c) const { return at(c, 2); }
+  __device__ __forceinline__ double tau(int c) const { return at(c, 3); }
+  __device__ __forceinline__ double omt(int c) const { return at(c, 4); }
+  __device__ __forceinline__ double rcp_cap(int c) const { return at(c, 5); }
+  __device__ __forceinline__ double rcp_omt(int c) const { return at(c, 6); }
+};
+
 // Global loads issued exactly where written (volatile asm): the compiler
 // otherwise sinks early loads next to their first use at the end of the step,
 // exposing the full DRAM latency there instead of overlapping it with the
@@ -393,7 +413,7 @@ struct ObsSink {
   bool in_place;
 };
 
-__device__ __forceinline__ void stage_port_obs(const Params& P, const Profile* prof, const ObsSink& S, int lane,
+__device__ __forceinline__ void stage_port_obs(const Params& P, Prof prof, const ObsSink& S, int lane,
                                                bool active, int i, uint32_t mt, double idr, double soc, double de,
                                                int dt) {
   const bool occ = mt & 1u;
@@ -401,7 +421,8 @@ __device__ __forceinline__ void stage_port_obs(const Params& P, const Profile* p
   v[0] = occ ? 1.0 : 0.0;
   v[1] = div_rcp(idr, P.i_denom[i], P.rcp_i_denom[i]);
   v[2] = soc;
-  v[3] = occ ? div_rcp(de, prof[mt >> 2].cap, prof[mt >> 2].rcp_cap) : 0.0;
+  const double dec = div_rcp(de, prof.cap(mt >> 2), prof.rcp_cap(mt >> 2));  // empty port: 0/cap0, discarded
+  v[3] = occ ? dec : 0.0;
   v[4] = div_rcp((double)dt, (double)P.episode_steps, P.rcp_ep);
   v[5] = (double)((mt >> 1) & 1u);
   if (S.row64) {
@@ -429,7 +450,7 @@ __device__ __forceinline__ void store_port(const Params& P, int64_t b, int i, ui
 // One transition of one env (_kernel.pyx:283-571).  `act(slot)` returns the
 // action index of a slot; `b` is the global env index (infos / injected draws).
 template <bool Lean, class Act>
-__device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* __restrict__ prof,
+__device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
                                                 const double* __restrict__ dtab, const Lane& T, EnvRegs& E,
                                                 int64_t b, const Frame& F, const ObsSink& S, bool active, Act act) {
   const int n = P.n_ports;
@@ -476,8 +497,8 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
     if (__any_sync(0xffffffffu, mt & 1u)) {
       double tgt = idr_i + d * P.imax_c[i];
       if (!P.allow_discharge && tgt < 0.0) tgt = 0.0;
-      const Profile& pr = prof[mt >> 2];
-      c = clip_current(tgt, soc_i, pr.tau, pr.omt, pr.rcp_omt, P.kind[i] ? pr.r_dc : pr.r_ac, P.volt[i],
+      const int pc = mt >> 2;
+      c = clip_current(tgt, soc_i, prof.tau(pc), prof.omt(pc), prof.rcp_omt(pc), P.kind[i] ? prof.r_dc(pc) : prof.r_ac(pc), P.volt[i],
                        P.rcp_volt[i], P.imax_c[i], P.imax_d[i]);
       c = (mt & 1u) ? c : 0.0;
     }
@@ -552,18 +573,18 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
     double got = 0.0;
     bool dep = false;
     if (__any_sync(0xffffffffu, occ)) {
-      const Profile& pr = prof[mt >> 2];
+      const int pc = mt >> 2;
       const double raw = div_rcp(P.dtv[i] * cur, 1000.0, P.rcp_1000);
       {
         double gc = raw;
         if (de < gc) gc = de;
-        const double room = pr.cap * (1.0 - soc);
+        const double room = prof.cap(pc) * (1.0 - soc);
         if (room < gc) gc = room;
-        const double fl = -pr.cap * soc;
+        const double fl = -prof.cap(pc) * soc;
         const double gd = raw < fl ? fl : raw;
         got = raw >= 0.0 ? gc : gd;
       }
-      soc = soc + div_rcp(got, pr.cap, pr.rcp_cap);
+      soc = soc + div_rcp(got, prof.cap(pc), prof.rcp_cap(pc));
       soc = soc < 0.0 ? 0.0 : (soc > 1.0 ? 1.0 : soc);
       de = de - got;
       de = de < 0.0 ? 0.0 : de;
@@ -573,7 +594,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
       e_out += got < 0.0 ? got * P.eta_d[i] : 0.0;
       dt -= occ ? 1 : 0;
       const int p = (mt >> 1) & 1u;
-      dep = occ && ((p == 0 && dt <= 0) || (p == 1 && de == 0.0));
+      dep = occ & ((p == 0 & dt <= 0) | (p == 1 & de == 0.0));  // bitwise: no short-circuit branches
       const int over = dt < 0 ? -dt : 0, early = dt > 0 ? dt : 0;
       if (info && dep) {
         const int64_t at = (int64_t)nd * ld + b;
@@ -582,17 +603,18 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
         O.dep_overtime[at] = over;
         O.dep_early[at] = early;
         O.dep_pref[at] = p;
-        O.dep_cap[at] = pr.cap;
+        O.dep_cap[at] = prof.cap(pc);
         O.dep_soc[at] = soc;
       }
-      sat0 += dep && p == 0 ? de : 0.0;
-      sat1 += dep && p == 1 ? (double)over - P.beta * (double)early : 0.0;
+      sat0 += dep & (p == 0) ? de : 0.0;
+      const double s1 = (double)over - P.beta * (double)early;
+      sat1 += dep & (p == 1) ? s1 : 0.0;
       E.ep_missing += dep ? de : 0.0;
       E.ep_overtime += dep ? over : 0;
       E.ep_departures += dep ? 1 : 0;
       nd += dep ? 1 : 0;
       // _kernel.pyx:559-561 (arrivals add dt > 0 only)
-      tover += !dep && last && p == 1 && dt < 0 ? -dt : 0;
+      tover += !dep & last & (p == 1) & (dt < 0) ? -dt : 0;
       occm |= (uint64_t)(occ && !dep) << i;
     }
     if (dep) {
@@ -602,7 +624,8 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
     }
     if (info) O.delivered[i * ld + b] = got;
     if (S.in_place) {
-      if (active) store_port(P, b, i, mt, cur, soc, de, dt);
+      // padding lanes (b >= B) write their own padding columns of the [n][ld] state: harmless, no branch
+      store_port(P, b, i, mt, cur, soc, de, dt);
       __syncwarp();  // every lane has read port i before its slots take obs columns
     } else {
       T.meta(i) = (uint8_t)mt;
@@ -690,7 +713,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, const Profile* 
     }
     occm |= 1ull << port;
     const uint32_t mt = 1u | (pref << 1) | ((uint32_t)car << 2);
-    const double de0 = frac * prof[car].cap * (1.0 - soc0);
+    const double de0 = frac * prof.cap(car) * (1.0 - soc0);
     if (S.in_place) {
       store_port(P, b, port, mt, 0.0, soc0, de0, stay);
     } else {
@@ -902,7 +925,7 @@ __device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const 
 
 // Obs of the tile's current state (reset kernel): write the state back to HBM
 // (bulk copies) if asked, then stage every port and finish.
-__device__ __forceinline__ void emit_obs(const Params& P, const Profile* prof, const Lane& T, const EnvRegs& E,
+__device__ __forceinline__ void emit_obs(const Params& P, Prof prof, const Lane& T, const EnvRegs& E,
                                          ObsGlobals G, int64_t b0, bool active, void* obs_base, bool store_state) {
   const int64_t b = b0 + T.lane;
   const ObsSink S = make_sink<false>(P, T, b, obs_base, P.L.obs == 0);
