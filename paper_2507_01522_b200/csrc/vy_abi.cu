@@ -120,6 +120,7 @@ struct vy_handle {
   int* d_pfull = nullptr;
   Profile* d_prof = nullptr;
   uint32_t* d_err = nullptr;
+  unsigned long long* d_tile_ctr = nullptr;
   double thr32 = 0.0;
   vy_state st{};
   vy_outputs out{};
@@ -256,6 +257,7 @@ void fill(vy_handle* h, Params& P, bool rollout, bool acts) {
   P.st = h->st;
   P.out = h->out;
   P.err = h->d_err;
+  P.tile_ctr = h->d_tile_ctr;
   P.act_tile = acts;
   P.n_profiles = (int)h->profiles.size();
   P.L = tile_layout(t, rollout, acts);
@@ -418,6 +420,8 @@ int vy_create(const vy_tables* t, int64_t batch, int device, vy_handle** out) {
   if (!rc) rc = upload<Profile>(&h->d_prof, nullptr, kMaxProfiles);
   if (!rc) rc = upload<uint32_t>(&h->d_err, nullptr, 1);
   if (!rc && cudaMemset(h->d_err, 0, 4) != cudaSuccess) rc = fail(VY_ERR_CUDA, "memset");
+  if (!rc) rc = upload<unsigned long long>(&h->d_tile_ctr, nullptr, 2);
+  if (!rc && cudaMemset(h->d_tile_ctr, 0, 16) != cudaSuccess) rc = fail(VY_ERR_CUDA, "memset");
   if (!rc) rc = upload_profiles(h);
   if (rc) {
     vy_destroy(h);
@@ -430,7 +434,7 @@ int vy_create(const vy_tables* t, int64_t batch, int device, vy_handle** out) {
 int vy_destroy(vy_handle* h) {
   if (!h) return VY_OK;
   void* ptrs[] = {h->d_buy, h->d_sellg, h->d_moer, h->d_dgrid, h->d_sin, h->d_cos, h->d_catcum,
-                  h->d_pthr, h->d_dtab, h->d_wk, h->d_pfull, h->d_prof, h->d_err};
+                  h->d_pthr, h->d_dtab, h->d_wk, h->d_pfull, h->d_prof, h->d_err, h->d_tile_ctr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete h;
@@ -535,7 +539,10 @@ int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride
   Geometry g;
   auto* kern = lean_ok(h, flags, acts) ? k_step<true> : k_step<false>;
   if (int rc = geometry(h, kern, P.L, P.n_profiles, g)) return rc;
-  kern<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P);
+  // persistent grid: every resident CTA slot, never more CTAs than tiles need
+  const unsigned resident = (unsigned)h->num_sms * (unsigned)(h->smem_per_sm / (g.smem + 1024));
+  const unsigned grid = g.grid < resident ? g.grid : resident;
+  kern<<<grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P);
   VY_CUDA(cudaGetLastError());
   ++h->launches;
   return VY_OK;

@@ -134,6 +134,7 @@ struct Params {
   int64_t act_row, act_col;
   vy_draws inj;
   uint32_t* err;
+  unsigned long long* tile_ctr;  // [2] work-stealing tile counter, finished-warp counter (k_step)
   TileLayout L;
 };
 

@@ -95,18 +95,35 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
   emit_tail<Lean>(P, T, E, G, S, b0, active, P.out.obs);
 }
 
-// One warp per tile.  (A persistent variant with L2 bulk prefetch of the next
-// tile measured slower: the kernel is bound by per-warp latency, not by DRAM
-// requests in flight.)
+// Persistent: one CTA per resident slot (tables staged once per CTA); each
+// warp claims 32-env tiles from a global counter until none are left, so no
+// warp idles waiting for the slowest warp of its CTA and the tail is balanced
+// dynamically.  The last warp to finish resets the counters, which keeps the
+// launch replayable inside CUDA graphs.
 template <bool Lean>
 __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) {
   Prof prof;
   const double* dtab;
   stage_tables(P, prof, dtab);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
-  if (b0 >= P.B) return;  // whole warp leaves together
-  step_tile<Lean>(P, prof, dtab, tables_bytes(P.n_profiles, P.k) + warp * P.L.bytes, b0, lane);
+  const uint32_t toff = tables_bytes(P.n_profiles, P.k) + warp * P.L.bytes;
+  const unsigned long long ntiles = (unsigned long long)((P.B + 31) >> 5);
+  for (;;) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(P.tile_ctr, 1ull);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= ntiles) break;
+    step_tile<Lean>(P, prof, dtab, toff, (int64_t)t * 32, lane);
+    __syncwarp();
+  }
+  if (lane == 0) {
+    __threadfence();  // this warp's last claim is ordered before its exit count
+    const unsigned long long warps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(P.tile_ctr + 1, 1ull) == warps - 1) {
+      P.tile_ctr[0] = 0;
+      P.tile_ctr[1] = 0;
+    }
+  }
 }
 
 template <bool Lean>
