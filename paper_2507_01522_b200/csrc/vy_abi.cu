@@ -64,7 +64,13 @@ __global__ void k_random_actions(uint64_t seed, int64_t index0, int64_t call, in
   const int64_t left = B - b0;
   const int bytes = (left >= 32 ? 32 : (int)left) * ns;
   uint8_t* g = out + b0 * ns;
-  for (int o = lane; o < bytes; o += 32) g[o] = rows[o];
+  if ((bytes & 15) == 0 && ((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(rows)) & 15) == 0) {
+    // a full 32-row tile is 32*ns bytes, a multiple of 16: 16-byte stores
+    for (int o = lane * 16; o < bytes; o += 512)
+      *reinterpret_cast<uint4*>(g + o) = *reinterpret_cast<const uint4*>(rows + o);
+  } else {
+    for (int o = lane; o < bytes; o += 32) g[o] = rows[o];
+  }
 }
 
 // div_rcp vs IEEE division on random dividends spread over 2^-64..2^64
