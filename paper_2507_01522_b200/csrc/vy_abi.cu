@@ -307,12 +307,15 @@ int geometry(vy_handle* h, K kernel, const TileLayout& L, int n_profiles, Geomet
   return VY_OK;
 }
 
-// Spec<true> (vy_device.cuh) applies: lean outputs, none of the optional
-// model features, a small identity-ordered tree and a shuffle-sized grid.
-bool lean_ok(const vy_handle* h, uint32_t flags, bool staged_actions) {
+// Which Spec<M> (vy_device.cuh) a call runs: 1 or 2 (lean, small or large
+// tree) for lean outputs without any of the optional model features, an
+// identity-ordered station and a shuffle-sized grid; 0 (generic) otherwise.
+int step_mode(const vy_handle* h, uint32_t flags, bool staged_actions) {
   const vy_tables& t = h->t;
-  return (flags & ~VY_F_AUTO_RESET) == 0 && staged_actions && !t.battery_enabled && !t.has_moer && !t.has_dgrid &&
-         t.horizon == 0 && t.n_nodes <= kFastNodes && h->order_identity && 2 * t.k < 32;
+  const bool lean = (flags & ~VY_F_AUTO_RESET) == 0 && staged_actions && !t.battery_enabled && !t.has_moer &&
+                    !t.has_dgrid && t.horizon == 0 && h->order_identity && 2 * t.k < 32;
+  if (!lean) return 0;
+  return t.n_nodes <= kFastNodes ? 1 : 2;
 }
 
 Profile make_profile(double cap, double r_ac, double r_dc, double tau) {
@@ -543,7 +546,8 @@ int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride
   P.act_col = col_stride;
   if (inj) P.inj = *inj;
   Geometry g;
-  auto* kern = lean_ok(h, flags, acts) ? k_step<true> : k_step<false>;
+  const int mode = step_mode(h, flags, acts);
+  auto* kern = mode == 1 ? k_step<1> : mode == 2 ? k_step<2> : k_step<0>;
   if (int rc = geometry(h, kern, P.L, P.n_profiles, g)) return rc;
   // persistent grid: every resident CTA slot, never more CTAs than tiles need
   const unsigned resident = (unsigned)h->num_sms * (unsigned)(h->smem_per_sm / (g.smem + 1024));
@@ -594,7 +598,8 @@ int vy_rollout(vy_handle* h, int32_t T, uint64_t policy_seed, int64_t index0, in
   P.out.reward = reward;
   P.out.done = done;
   Geometry g;
-  auto* kern = lean_ok(h, flags, true) ? k_rollout<true> : k_rollout<false>;
+  const int mode = step_mode(h, flags, true);
+  auto* kern = mode == 1 ? k_rollout<1> : mode == 2 ? k_rollout<2> : k_rollout<0>;
   if (int rc = geometry(h, kern, P.L, P.n_profiles, g)) return rc;
   kern<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P, T, policy_seed, index0, call0, obs_step_stride,
                                                               rew_step_stride);

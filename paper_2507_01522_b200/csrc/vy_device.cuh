@@ -139,28 +139,31 @@ struct Params {
 };
 
 
-// Compile-time specialisation.  Spec<true> ("lean") is the step of the common
-// configuration: obs/reward/done only (no infos, no injected draws), float32
-// obs, no battery, no carbon / demand series, no price horizon, a tree of at
-// most kFastNodes nodes, identity parking order, staged uint8 actions, a
-// shuffle-sized action grid.  Everything it folds away is dead code the lean
-// kernel never carries (smaller hot loop, fewer i-cache misses, no uniform
-// branches); Spec<false> reads all of it at run time.  The host picks the
-// instantiation (lean_ok in vy_abi.cu).
-template <bool Lean>
+// Compile-time specialisation.  Spec<M>, M = 1 ("lean") is the step of the
+// common configuration: obs/reward/done only (no infos, no injected draws),
+// float32 obs, no battery, no carbon / demand series, no price horizon, a
+// tree of at most kFastNodes nodes, identity parking order, staged uint8
+// actions, a shuffle-sized action grid.  M = 2 is the same with a larger tree
+// (node loads summed from the tile, vy_tile.cuh node_sum).  Everything a lean
+// mode folds away is dead code its kernel never carries (smaller hot loop,
+// fewer i-cache misses, no uniform branches); M = 0 reads all of it at run
+// time.  The host picks the instantiation (step_mode in vy_abi.cu).
+template <int M>
 struct Spec {
-  static constexpr bool lean = Lean;
-  __device__ __forceinline__ static bool info(const Params& P) { return !Lean && (P.flags & VY_F_INFOS); }
-  __device__ __forceinline__ static bool inject(const Params& P) { return !Lean && (P.flags & VY_F_INJECT); }
-  __device__ __forceinline__ static bool f64(const Params& P) { return !Lean && (P.flags & VY_F_OUT_F64); }
-  __device__ __forceinline__ static bool battery(const Params& P) { return !Lean && P.battery; }
-  __device__ __forceinline__ static bool moer(const Params& P) { return !Lean && P.has_moer; }
-  __device__ __forceinline__ static bool dgrid(const Params& P) { return !Lean && P.has_dgrid; }
-  __device__ __forceinline__ static int horizon(const Params& P) { return Lean ? 0 : P.horizon; }
-  __device__ __forceinline__ static bool fast_tree(const Params& P) { return Lean || P.n_nodes <= kFastNodes; }
-  __device__ __forceinline__ static bool identity(const Params& P) { return Lean || P.order_identity; }
-  __device__ __forceinline__ static bool staged(const Params& P) { return Lean || P.act_tile; }
-  __device__ __forceinline__ static bool probe(const Params& P, uint32_t bit) { return !Lean && (P.flags & bit); }
+  static constexpr bool lean = M != 0;
+  __device__ __forceinline__ static bool info(const Params& P) { return !lean && (P.flags & VY_F_INFOS); }
+  __device__ __forceinline__ static bool inject(const Params& P) { return !lean && (P.flags & VY_F_INJECT); }
+  __device__ __forceinline__ static bool f64(const Params& P) { return !lean && (P.flags & VY_F_OUT_F64); }
+  __device__ __forceinline__ static bool battery(const Params& P) { return !lean && P.battery; }
+  __device__ __forceinline__ static bool moer(const Params& P) { return !lean && P.has_moer; }
+  __device__ __forceinline__ static bool dgrid(const Params& P) { return !lean && P.has_dgrid; }
+  __device__ __forceinline__ static int horizon(const Params& P) { return lean ? 0 : P.horizon; }
+  __device__ __forceinline__ static bool fast_tree(const Params& P) {
+    return M == 1 || (M == 0 && P.n_nodes <= kFastNodes);
+  }
+  __device__ __forceinline__ static bool identity(const Params& P) { return lean || P.order_identity; }
+  __device__ __forceinline__ static bool staged(const Params& P) { return lean || P.act_tile; }
+  __device__ __forceinline__ static bool probe(const Params& P, uint32_t bit) { return !lean && (P.flags & bit); }
 };
 
 }  // namespace vy

@@ -40,22 +40,22 @@ __device__ __forceinline__ void stage_tables(const Params& P, Prof& prof, const 
 // One step of the 32 envs of the tile starting at env b0.  Every lane runs
 // the transition (padding lanes on their harmless padding columns, side
 // effects masked) because the fused port loop synchronises the warp.
-template <bool Lean>
+template <int M>
 __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const double* dtab, uint32_t tile,
                                           int64_t b0, int lane) {
-  using C = Spec<Lean>;
+  using C = Spec<M>;
   const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
   EnvRegs E{};  // zero for padding lanes so table lookups stay in bounds
-  if (active) load_env<Lean>(P, b, E);
+  if (active) load_env<M>(P, b, E);
   tile_issue(P, tile, b0, lane, C::staged(P));
   // exogenous inputs for this step and the obs globals of the next one, in
   // flight together with the tile copies
-  const Frame F = load_frame<Lean>(P, E.step, E.day);
+  const Frame F = load_frame<M>(P, E.step, E.day);
   const ObsGlobals G = load_obs_globals(P, E.step + 1, E.day);
   tile_wait();
-  const ObsSink S = make_sink<Lean>(P, T, b, P.out.obs, /*in_place=*/true);
+  const ObsSink S = make_sink<M>(P, T, b, P.out.obs, /*in_place=*/true);
   const int dt = P.act_dtype;
   const int64_t rs = P.act_row, cs = P.act_col;
   const uint8_t* arow = vy_smem + tile + P.L.acts + lane * (P.n_ports + 1);
@@ -70,7 +70,7 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
     return v < INT_MIN ? INT_MIN : (v > INT_MAX ? INT_MAX : (int)v);
   };
   StepResult r{0.0, false};
-  if (!C::probe(P, 0x200u)) r = tile_step<Lean>(P, prof, dtab, T, E, b, F, S, active, act);  // 0x200: memory-only probe
+  if (!C::probe(P, 0x200u)) r = tile_step<M>(P, prof, dtab, T, E, b, F, S, active, act);  // 0x200: memory-only probe
   bool reset = false;
   if (r.done && (P.flags & VY_F_AUTO_RESET)) {
     // in-kernel auto-reset (engine.py:460-462): the terminal reward/done/infos
@@ -85,14 +85,14 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
     reset = true;
   }
   if (active) {
-    if (!C::probe(P, 0x800u)) store_env<Lean>(P, b, E, reset);
+    if (!C::probe(P, 0x800u)) store_env<M>(P, b, E, reset);
     if (C::f64(P))
       reinterpret_cast<double*>(P.out.reward)[b] = r.reward;
     else
       reinterpret_cast<float*>(P.out.reward)[b] = (float)r.reward;
     P.out.done[b] = r.done;
   }
-  emit_tail<Lean>(P, T, E, G, S, b0, active, P.out.obs);
+  emit_tail<M>(P, T, E, G, S, b0, active, P.out.obs);
 }
 
 // Persistent: one CTA per resident slot (tables staged once per CTA); each
@@ -100,7 +100,7 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
 // warp idles waiting for the slowest warp of its CTA and the tail is balanced
 // dynamically.  The last warp to finish resets the counters, which keeps the
 // launch replayable inside CUDA graphs.
-template <bool Lean>
+template <int M>
 __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) {
   Prof prof;
   const double* dtab;
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
     if (lane == 0) t = atomicAdd(P.tile_ctr, 1ull);
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= ntiles) break;
-    step_tile<Lean>(P, prof, dtab, toff, (int64_t)t * 32, lane);
+    step_tile<M>(P, prof, dtab, toff, (int64_t)t * 32, lane);
     __syncwarp();
   }
   if (lane == 0) {
@@ -126,11 +126,11 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
   }
 }
 
-template <bool Lean>
+template <int M>
 __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params P, int T_steps, uint64_t policy_seed,
                                                  int64_t index0, int64_t call0, int64_t obs_stride,
                                                  int64_t rew_stride) {
-  using C = Spec<Lean>;
+  using C = Spec<M>;
   Prof prof;
   const double* dtab;
   stage_tables(P, prof, dtab);
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
   uint64_t pkey = 0, seed = 0;
   int episode = 0;
   if (active) {
-    load_env<Lean>(P, b, E);
+    load_env<M>(P, b, E);
     pkey = fold(fold(fold(kKey0, policy_seed), (uint64_t)(index0 + b)), 2);
     episode = P.st.episode[b];
     seed = P.st.env_seed[b];
@@ -157,11 +157,11 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
   for (int t = 0; t < T_steps; ++t) {
     void* obs_t = f64 ? (void*)(reinterpret_cast<double*>(P.out.obs) + t * obs_stride)
                       : (void*)(reinterpret_cast<float*>(P.out.obs) + t * obs_stride);
-    const ObsSink S = make_sink<Lean>(P, T, b, obs_t, /*in_place=*/false);
+    const ObsSink S = make_sink<M>(P, T, b, obs_t, /*in_place=*/false);
     const uint64_t j0 = (uint64_t)(call0 + t) * (uint64_t)ns;
     auto act = [&](int slot) -> int { return policy_action(pkey, j0 + slot + 1, hi); };
-    const Frame F = load_frame<Lean>(P, E.step, E.day);
-    const StepResult r = tile_step<Lean>(P, prof, dtab, T, E, b, F, S, active, act);
+    const Frame F = load_frame<M>(P, E.step, E.day);
+    const StepResult r = tile_step<M>(P, prof, dtab, T, E, b, F, S, active, act);
     if (r.done) {
       ++episode;
       reset_scalars(P, E, seed, episode, 0, false);
@@ -175,11 +175,11 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
         reinterpret_cast<float*>(P.out.reward)[t * rew_stride + b] = (float)r.reward;
       P.out.done[t * rew_stride + b] = r.done;
     }
-    emit_tail<Lean>(P, T, E, load_obs_globals(P, E.step, E.day), S, b0, active, obs_t);
+    emit_tail<M>(P, T, E, load_obs_globals(P, E.step, E.day), S, b0, active, obs_t);
   }
   if (!C::probe(P, 0x800u)) tile_store(P, T.t, b0, lane);
   if (active) {
-    store_env<Lean>(P, b, E, true);
+    store_env<M>(P, b, E, true);
     P.st.episode[b] = episode;
   }
 }
@@ -201,13 +201,13 @@ __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P,
   tile_wait();
   const bool mine = active && (!mask || mask[b]);
   EnvRegs E{};  // zero for padding lanes so the obs path stays in bounds
-  if (active) load_env<false>(P, b, E);
+  if (active) load_env<0>(P, b, E);
   if (mine) {
     const int ep = episode_mode ? P.st.episode[b] + 1 : 0;
     reset_scalars(P, E, P.st.env_seed[b], ep, inj_day ? inj_day[b] : 0, inj_day != nullptr);
     clear_tile_ports(P, T);
     P.st.episode[b] = ep;
-    store_env<false>(P, b, E, true);
+    store_env<0>(P, b, E, true);
   }
   // masked-out rows still get their (unchanged) obs rewritten, which is idempotent
   emit_obs(P, prof, T, E, load_obs_globals(P, E.step, E.day), b0, active, P.out.obs, /*store_state=*/true);

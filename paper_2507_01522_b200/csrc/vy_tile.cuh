@@ -215,9 +215,9 @@ __device__ __forceinline__ void tile_wait() {
   __syncwarp();
 }
 
-template <bool Lean>
+template <int M>
 __device__ __forceinline__ void load_env(const Params& P, int64_t b, EnvRegs& E) {
-  using C = Spec<Lean>;
+  using C = Spec<M>;
   const vy_state& s = P.st;
   E.step = ldg_s32(s.step + b);
   E.day = ldg_s32(s.day + b);
@@ -233,11 +233,11 @@ __device__ __forceinline__ void load_env(const Params& P, int64_t b, EnvRegs& E)
   E.ep_departures = ldg_s32(s.ep_departures + b);
 }
 
-template <bool Lean>
+template <int M>
 __device__ __forceinline__ void store_env(const Params& P, int64_t b, const EnvRegs& E, bool reset_too) {
   const vy_state& s = P.st;
   s.step[b] = E.step;
-  if (Spec<Lean>::battery(P)) {
+  if (Spec<M>::battery(P)) {
     s.b_i[b] = E.b_i;
     s.b_soc[b] = E.b_soc;
   }
@@ -361,7 +361,7 @@ struct Frame {
   double p_buy, p_sg, moer, dgrid, pthr;
   int hidx, lam_idx, pfull;
 };
-template <bool Lean>
+template <int M>
 __device__ __forceinline__ Frame load_frame(const Params& P, int t, int day) {
   Frame F;
   const int64_t minutes = (int64_t)t * P.dt_min;
@@ -369,8 +369,8 @@ __device__ __forceinline__ Frame load_frame(const Params& P, int t, int day) {
   F.hidx = eff_day * 24 + (int)((minutes / 60) % 24);
   F.p_buy = ldg_nc_f64(P.buy + F.hidx);
   F.p_sg = ldg_nc_f64(P.sellg + F.hidx);
-  F.moer = Spec<Lean>::moer(P) ? ldg_nc_f64(P.moer + F.hidx) : 0.0;
-  F.dgrid = Spec<Lean>::dgrid(P) ? ldg_nc_f64(P.dgrid + F.hidx) : 0.0;
+  F.moer = Spec<M>::moer(P) ? ldg_nc_f64(P.moer + F.hidx) : 0.0;
+  F.dgrid = Spec<M>::dgrid(P) ? ldg_nc_f64(P.dgrid + F.hidx) : 0.0;
   F.lam_idx = (ldg_nc_s8(P.weekday + eff_day) ? 0 : P.lam_len) + t % P.lam_len;
   F.pfull = ldg_nc_s32(P.pois_full + F.lam_idx);
   F.pthr = ldg_nc_f64(P.pois_thr + F.lam_idx);
@@ -449,13 +449,13 @@ __device__ __forceinline__ void store_port(const Params& P, int64_t b, int i, ui
 
 // One transition of one env (_kernel.pyx:283-571).  `act(slot)` returns the
 // action index of a slot; `b` is the global env index (infos / injected draws).
-template <bool Lean, class Act>
+template <int M, class Act>
 __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
                                                 const double* __restrict__ dtab, const Lane& T, EnvRegs& E,
                                                 int64_t b, const Frame& F, const ObsSink& S, bool active, Act act) {
   const int n = P.n_ports;
   const int64_t ld = P.ld;
-  using C = Spec<Lean>;
+  using C = Spec<M>;
   const bool info = C::info(P);
   const bool battery = C::battery(P);
   const vy_outputs& O = P.out;
@@ -824,18 +824,18 @@ __device__ __forceinline__ void tile_store(const Params& P, uint32_t toff, int64
   __syncwarp();
 }
 
-template <bool Lean>
+template <int M>
 __device__ __forceinline__ ObsSink make_sink(const Params& P, const Lane& T, int64_t b, void* obs_base,
                                              bool in_place) {
   ObsSink S;
   S.cells = smem_base() + T.t + P.L.obs;
-  S.row64 = Spec<Lean>::f64(P) ? reinterpret_cast<double*>(obs_base) + b * P.obs_len : nullptr;
+  S.row64 = Spec<M>::f64(P) ? reinterpret_cast<double*>(obs_base) + b * P.obs_len : nullptr;
   S.in_place = in_place;
   return S;
 }
 
 // Global obs columns and the coalesced read-out of the staged [rows][OL] block.
-template <bool Lean>
+template <int M>
 __device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const EnvRegs& E, ObsGlobals G,
                                           const ObsSink& S, int64_t b0, bool active, void* obs_base) {
   const int n = P.n_ports;
@@ -862,7 +862,7 @@ __device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const 
       sts_f32(S.cells + (c0 + k) * 132 + lane * 4, (float)gv[k]);
     }
   }
-  for (int h = 0; h < Spec<Lean>::horizon(P); ++h) {
+  for (int h = 0; h < Spec<M>::horizon(P); ++h) {
     const int64_t fmin = (int64_t)(E.step + 1 + h) * P.dt_min;
     const int64_t fday = ((int64_t)E.day + fmin / 1440) % P.n_days;
     const double v = __ldg(P.buy + fday * 24 + (fmin / 60) % 24);
@@ -874,7 +874,7 @@ __device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const 
   }
   if (S.row64) return;
   __syncwarp();
-  if (Spec<Lean>::probe(P, 0x400u)) return;  // probe: no obs stores
+  if (Spec<M>::probe(P, 0x400u)) return;  // probe: no obs stores
   // Row-major read-out: row r, column c = lane + 32 j lives at
   // cells + c*132 + r*4 = cells + lane*132 + r*4 + j*4224; bank (lane + r) % 32.
   float* g = reinterpret_cast<float*>(obs_base) + b0 * OL + lane;
@@ -928,7 +928,7 @@ __device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const 
 __device__ __forceinline__ void emit_obs(const Params& P, Prof prof, const Lane& T, const EnvRegs& E,
                                          ObsGlobals G, int64_t b0, bool active, void* obs_base, bool store_state) {
   const int64_t b = b0 + T.lane;
-  const ObsSink S = make_sink<false>(P, T, b, obs_base, P.L.obs == 0);
+  const ObsSink S = make_sink<0>(P, T, b, obs_base, P.L.obs == 0);
   if (store_state && !(P.flags & 0x800u)) tile_store(P, T.t, b0, T.lane);
 #pragma unroll 2
   for (int i = 0; i < P.n_ports; ++i) {
@@ -938,7 +938,7 @@ __device__ __forceinline__ void emit_obs(const Params& P, Prof prof, const Lane&
     if (S.in_place) __syncwarp();  // every lane has read port i before its slots are reused
     stage_port_obs(P, prof, S, T.lane, active, i, mt, idr, soc, de, dt);
   }
-  emit_tail<false>(P, T, E, G, S, b0, active, obs_base);
+  emit_tail<0>(P, T, E, G, S, b0, active, obs_base);
 }
 
 }  // namespace vy
