@@ -355,7 +355,7 @@ def main() -> None:
 
         hb = HeteroBatch(sweep_groups(B), master_seed=0, global_offset=rank * B, policy_seed=0)
         hb.reset()
-        hsteps = max(3, min(args.steps, 20))
+        hsteps = args.steps  # the same day window as the main leg (K = 288: one whole day)
         for _ in range(3 + window_start(hsteps, 3, rc.env.episode_steps)):  # window centred mid-day
             hb.graph_random_step()
         barrier()
