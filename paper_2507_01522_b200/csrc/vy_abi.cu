@@ -121,7 +121,7 @@ struct vy_handle {
   bool order_identity = true;
   std::vector<Profile> profiles;
   double *d_buy = nullptr, *d_sellg = nullptr, *d_moer = nullptr, *d_dgrid = nullptr, *d_sin = nullptr,
-         *d_cos = nullptr, *d_catcum = nullptr, *d_pthr = nullptr, *d_dtab = nullptr;
+         *d_cos = nullptr, *d_catcum = nullptr, *d_pthr = nullptr, *d_dtab = nullptr, *d_portc = nullptr;
   int8_t* d_wk = nullptr;
   int* d_pfull = nullptr;
   Profile* d_prof = nullptr;
@@ -260,6 +260,7 @@ void fill(vy_handle* h, Params& P, bool rollout, bool acts) {
   P.pois_full = h->d_pfull;
   P.profiles = h->d_prof;
   P.delta_tab = h->d_dtab;
+  P.portc = h->d_portc;
   P.st = h->st;
   P.out = h->out;
   P.err = h->d_err;
@@ -281,7 +282,7 @@ struct Geometry {
 template <typename K>
 int geometry(vy_handle* h, K kernel, const TileLayout& L, int n_profiles, Geometry& g) {
   const int per_sm = h->smem_per_sm;
-  const int tb = tables_bytes(n_profiles, h->t.k);
+  const int tb = tables_bytes(n_profiles, h->t.k, h->t.n_ports);
   int best_w = 1, best_total = 0;
   for (int w = 1; w <= 8; ++w) {  // __launch_bounds__(256)
     const int bytes = tb + w * L.bytes;
@@ -426,6 +427,22 @@ int vy_create(const vy_tables* t, int64_t batch, int device, vy_handle** out) {
   if (!rc) rc = upload(&h->d_pthr, pthr.data(), pthr.size());
   if (!rc) rc = upload(&h->d_pfull, pfull.data(), pfull.size());
   if (!rc) rc = upload(&h->d_dtab, dtab.data(), dtab.size());
+  {
+    // per-port constant records (PortC, vy_tile.cuh)
+    std::vector<double> pcv((size_t)n * kPortWords);
+    for (int i = 0; i < n; ++i) {
+      double* r = pcv.data() + (size_t)i * kPortWords;
+      uint32_t mask = 0;
+      for (int m = 0; m < t->n_nodes && m < kFastNodes; ++m)
+        if (h->node_lo[m] <= i && i < h->node_hi[m]) mask |= 1u << m;
+      const double dtv = t->dt_h * t->volt[i];
+      r[0] = t->imax_c[i], r[1] = t->imax_d[i], r[2] = t->volt[i], r[3] = rcp(t->volt[i]);
+      r[4] = t->kind[i] ? 1.0 : 0.0, r[5] = t->n_nodes <= kFastNodes ? (double)mask : 0.0;
+      r[6] = dtv, r[7] = t->eta_d[i], r[8] = t->eta_c[i], r[9] = rcp(t->eta_c[i]);
+      r[10] = t->i_denom[i], r[11] = rcp(t->i_denom[i]);
+    }
+    if (!rc) rc = upload(&h->d_portc, pcv.data(), pcv.size());
+  }
   if (!rc) rc = upload<Profile>(&h->d_prof, nullptr, kMaxProfiles);
   if (!rc) rc = upload<uint32_t>(&h->d_err, nullptr, 1);
   if (!rc && cudaMemset(h->d_err, 0, 4) != cudaSuccess) rc = fail(VY_ERR_CUDA, "memset");
@@ -443,7 +460,7 @@ int vy_create(const vy_tables* t, int64_t batch, int device, vy_handle** out) {
 int vy_destroy(vy_handle* h) {
   if (!h) return VY_OK;
   void* ptrs[] = {h->d_buy, h->d_sellg, h->d_moer, h->d_dgrid, h->d_sin, h->d_cos, h->d_catcum,
-                  h->d_pthr, h->d_dtab, h->d_wk, h->d_pfull, h->d_prof, h->d_err, h->d_tile_ctr};
+                  h->d_pthr, h->d_dtab, h->d_portc, h->d_wk, h->d_pfull, h->d_prof, h->d_err, h->d_tile_ctr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete h;

@@ -21,6 +21,9 @@ constexpr int kMaxPorts = 64;
 constexpr int kMaxNodes = 2 * kMaxPorts + 2;
 constexpr int kMaxProfiles = 64;  // 6 bits of port_meta
 constexpr int kFastNodes = 4;     // trees up to this many nodes keep node loads in registers
+// per-port constant record (PortC in vy_tile.cuh), 16-byte pairs in the order the step uses them:
+// {imax_c, imax_d} {volt, rcp_volt} {kind, node mask} {dtv, eta_d} {eta_c, rcp_eta_c} {i_denom, rcp_i_denom}
+constexpr int kPortWords = 12;
 constexpr uint32_t kFlagStageObs = 0x100u;
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -126,6 +129,7 @@ struct Params {
   const int* pois_full;     // [2][lam_len] number of full 32-chunks; -1 => lambda <= 0
   const Profile* profiles;  // [kMaxProfiles]
   const double* delta_tab;  // [2k+1] (a-k)/k
+  const double* portc;      // [n_ports][kPortWords] per-port constants, staged into shared memory (PortC)
   // state / outputs / actions
   vy_state st;
   vy_outputs out;

@@ -86,6 +86,16 @@ struct Prof {
   __device__ __forceinline__ double rcp_omt(int c) const { return at(c, 6); }
 };
 
+// Per-port constants staged in shared memory (one 96-byte record per port):
+// every lane reads the same address (broadcast), two doubles per 16-byte
+// load, instead of one indexed constant-bank load per value.
+struct PortC {
+  uint32_t a;  // shared address of port 0's record
+  __device__ __forceinline__ void pair(int i, int w, double& x, double& y) const {
+    asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a + (uint32_t)i * (8u * kPortWords) + 16u * w));
+  }
+};
+
 // Global loads issued exactly where written (volatile asm): the compiler
 // otherwise sinks early loads next to their first use at the end of the step,
 // exposing the full DRAM latency there instead of overlapping it with the
@@ -415,11 +425,11 @@ struct ObsSink {
 
 __device__ __forceinline__ void stage_port_obs(const Params& P, Prof prof, const ObsSink& S, int lane,
                                                bool active, int i, uint32_t mt, double idr, double soc, double de,
-                                               int dt) {
+                                               int dt, double i_denom, double rcp_i_denom) {
   const bool occ = mt & 1u;
   double v[6];
   v[0] = occ ? 1.0 : 0.0;
-  v[1] = div_rcp(idr, P.i_denom[i], P.rcp_i_denom[i]);
+  v[1] = div_rcp(idr, i_denom, rcp_i_denom);
   v[2] = soc;
   const double dec = div_rcp(de, prof.cap(mt >> 2), prof.rcp_cap(mt >> 2));  // empty port: 0/cap0, discarded
   v[3] = occ ? dec : 0.0;
@@ -434,6 +444,10 @@ __device__ __forceinline__ void stage_port_obs(const Params& P, Prof prof, const
 #pragma unroll
     for (int f = 0; f < 6; ++f) sts_f32(col + f * 132, (float)v[f]);
   }
+}
+__device__ __forceinline__ void stage_port_obs(const Params& P, Prof prof, const ObsSink& S, int lane, bool active,
+                                               int i, uint32_t mt, double idr, double soc, double de, int dt) {
+  stage_port_obs(P, prof, S, lane, active, i, mt, idr, soc, de, dt, P.i_denom[i], P.rcp_i_denom[i]);
 }
 
 __device__ __forceinline__ void store_port(const Params& P, int64_t b, int i, uint32_t mt, double idr, double soc,
@@ -451,7 +465,7 @@ __device__ __forceinline__ void store_port(const Params& P, int64_t b, int i, ui
 // action index of a slot; `b` is the global env index (infos / injected draws).
 template <int M, class Act>
 __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
-                                                const double* __restrict__ dtab, const Lane& T, EnvRegs& E,
+                                                const double* __restrict__ dtab, PortC pc, const Lane& T, EnvRegs& E,
                                                 int64_t b, const Frame& F, const ObsSink& S, bool active, Act act) {
   const int n = P.n_ports;
   const int64_t ld = P.ld;
@@ -494,17 +508,22 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
     // branch); otherwise branch-free: an empty port (meta 0 -> profile 0,
     // zero slots) runs the same arithmetic and the select discards it.
     double c = 0.0;
+    double kind_nodes[2];
+    pc.pair(i, 2, kind_nodes[0], kind_nodes[1]);
     if (__any_sync(0xffffffffu, mt & 1u)) {
-      double tgt = idr_i + d * P.imax_c[i];
+      double imax_c, imax_d, volt, rcp_volt;
+      pc.pair(i, 0, imax_c, imax_d);
+      pc.pair(i, 1, volt, rcp_volt);
+      double tgt = idr_i + d * imax_c;
       if (!P.allow_discharge && tgt < 0.0) tgt = 0.0;
-      const int pc = mt >> 2;
-      c = clip_current(tgt, soc_i, prof.tau(pc), prof.omt(pc), prof.rcp_omt(pc), P.kind[i] ? prof.r_dc(pc) : prof.r_ac(pc), P.volt[i],
-                       P.rcp_volt[i], P.imax_c[i], P.imax_d[i]);
+      const int pf = mt >> 2;
+      c = clip_current(tgt, soc_i, prof.tau(pf), prof.omt(pf), prof.rcp_omt(pf),
+                       kind_nodes[0] != 0.0 ? prof.r_dc(pf) : prof.r_ac(pf), volt, rcp_volt, imax_c, imax_d);
       c = (mt & 1u) ? c : 0.0;
     }
     T.idr(i) = c;
     if (info) O.i_att[i * ld + b] = c;
-    const uint32_t pm = P.port_nodes[i];
+    const uint32_t pm = (uint32_t)kind_nodes[1];
 #pragma unroll
     for (int m = 0; m < kFastNodes; ++m)
       if (pm & (1u << m)) nsum[m] += c;
@@ -573,25 +592,28 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
     double got = 0.0;
     bool dep = false;
     if (__any_sync(0xffffffffu, occ)) {
-      const int pc = mt >> 2;
-      const double raw = div_rcp(P.dtv[i] * cur, 1000.0, P.rcp_1000);
+      const int pf = mt >> 2;
+      double dtv, eta_d, eta_c, rcp_eta_c;
+      pc.pair(i, 3, dtv, eta_d);
+      pc.pair(i, 4, eta_c, rcp_eta_c);
+      const double raw = div_rcp(dtv * cur, 1000.0, P.rcp_1000);
       {
         double gc = raw;
         if (de < gc) gc = de;
-        const double room = prof.cap(pc) * (1.0 - soc);
+        const double room = prof.cap(pf) * (1.0 - soc);
         if (room < gc) gc = room;
-        const double fl = -prof.cap(pc) * soc;
+        const double fl = -prof.cap(pf) * soc;
         const double gd = raw < fl ? fl : raw;
         got = raw >= 0.0 ? gc : gd;
       }
-      soc = soc + div_rcp(got, prof.cap(pc), prof.rcp_cap(pc));
+      soc = soc + div_rcp(got, prof.cap(pf), prof.rcp_cap(pf));
       soc = soc < 0.0 ? 0.0 : (soc > 1.0 ? 1.0 : soc);
       de = de - got;
       de = de < 0.0 ? 0.0 : de;
       e_net += got;
-      const double gin = P.eta_c[i] == 1.0 ? got : div_rcp(got, P.eta_c[i], P.rcp_eta_c[i]);
+      const double gin = eta_c == 1.0 ? got : div_rcp(got, eta_c, rcp_eta_c);
       e_in += got > 0.0 ? gin : 0.0;
-      e_out += got < 0.0 ? got * P.eta_d[i] : 0.0;
+      e_out += got < 0.0 ? got * eta_d : 0.0;
       dt -= occ ? 1 : 0;
       const int p = (mt >> 1) & 1u;
       dep = occ & ((p == 0 & dt <= 0) | (p == 1 & de == 0.0));  // bitwise: no short-circuit branches
@@ -603,7 +625,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
         O.dep_overtime[at] = over;
         O.dep_early[at] = early;
         O.dep_pref[at] = p;
-        O.dep_cap[at] = prof.cap(pc);
+        O.dep_cap[at] = prof.cap(pf);
         O.dep_soc[at] = soc;
       }
       sat0 += dep & (p == 0) ? de : 0.0;
@@ -634,7 +656,11 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
       T.de(i) = de;
       T.dtrem(i) = (int16_t)dt;
     }
-    stage_port_obs(P, prof, S, T.lane, active, i, mt, cur, soc, de, dt);
+    {
+      double i_denom, rcp_i_denom;
+      pc.pair(i, 5, i_denom, rcp_i_denom);
+      stage_port_obs(P, prof, S, T.lane, active, i, mt, cur, soc, de, dt, i_denom, rcp_i_denom);
+    }
   }
   double e_b = 0.0, bgot = 0.0;
   if (battery) {
