@@ -87,7 +87,7 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
     reset_scalars(P, E, active ? P.st.env_seed[b] : 0ull, ep, 0, false);
     for (int i = 0; i < P.n_ports; ++i) {
       if (active) store_port(P, b, i, 0u, 0.0, 0.0, 0.0, 0);
-      stage_port_obs(P, prof, S, lane, active, i, 0u, 0.0, 0.0, 0.0, 0);
+      stage_port_obs(P, prof, S, lane, active, i, 0u, 0.0, 0.0, 0.0, 0, 1.0, 1.0);  // I = 0: any denominator
     }
     if (active) P.st.episode[b] = ep;
     reset = true;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
       ++episode;
       reset_scalars(P, E, seed, episode, 0, false);
       clear_tile_ports(P, T);
-      for (int i = 0; i < P.n_ports; ++i) stage_port_obs(P, prof, S, lane, active, i, 0u, 0.0, 0.0, 0.0, 0);
+      for (int i = 0; i < P.n_ports; ++i) stage_port_obs(P, prof, S, lane, active, i, 0u, 0.0, 0.0, 0.0, 0, 1.0, 1.0);
     }
     if (active) {
       if (f64)

@@ -749,7 +749,8 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
       T.de(port) = de0;
       T.dtrem(port) = (int16_t)stay;
     }
-    stage_port_obs(P, prof, S, T.lane, active, port, mt, 0.0, soc0, de0, stay);
+    // a new car draws no current yet: I / i_denom = 0 for any denominator
+    stage_port_obs(P, prof, S, T.lane, active, port, mt, 0.0, soc0, de0, stay, 1.0, 1.0);
   }
   E.ep_declined += declined;
   if (info) {
