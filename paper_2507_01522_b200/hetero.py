@@ -56,7 +56,7 @@ def sweep_groups(total_envs: int, days: int = 365, seed: int = 0) -> list[Group]
 
 class HeteroBatch:
     def __init__(self, groups: list[Group], master_seed: int = 0, global_offset: int = 0, device=None,
-                 policy_seed: int | None = None, n_streams: int = 4):
+                 policy_seed: int | None = None, n_streams: int = 8):
         self.groups = groups
         self.streams = [torch.cuda.Stream(device=device) for _ in range(max(1, n_streams))]
         self.envs: list[BatchEnv] = []
