@@ -57,8 +57,9 @@ __global__ void k_random_actions(uint64_t seed, int64_t index0, int64_t call, in
   const int64_t b = b0 + lane;
   if (b < B) {
     const uint64_t key = fold(fold(fold(kKey0, seed), (uint64_t)(index0 + b)), 2);
-    const uint64_t j0 = (uint64_t)call * (uint64_t)ns;
-    for (int s = 0; s < ns; ++s) rows[lane * ns + s] = (uint8_t)policy_action(key, j0 + s + 1, hi);
+    // draw j = call*ns + s + 1 of the row's stream is mix64(key + j*GOLDEN): step the argument by GOLDEN
+    uint64_t kj = key + ((uint64_t)call * (uint64_t)ns + 1) * kGolden;
+    for (int s = 0; s < ns; ++s, kj += kGolden) rows[lane * ns + s] = (uint8_t)policy_action(kj, 0, hi);
   }
   __syncwarp();
   const int64_t left = B - b0;
