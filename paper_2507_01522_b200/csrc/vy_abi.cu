@@ -122,7 +122,7 @@ struct vy_handle {
   bool order_identity = true;
   std::vector<Profile> profiles;
   double *d_buy = nullptr, *d_sellg = nullptr, *d_moer = nullptr, *d_dgrid = nullptr, *d_sin = nullptr,
-         *d_cos = nullptr, *d_catcum = nullptr, *d_pthr = nullptr, *d_dtab = nullptr, *d_portc = nullptr;
+         *d_cos = nullptr, *d_catcum = nullptr, *d_pthr = nullptr, *d_dtab = nullptr, *d_portc = nullptr, *d_treec = nullptr;
   int8_t* d_wk = nullptr;
   int* d_pfull = nullptr;
   Profile* d_prof = nullptr;
@@ -262,6 +262,7 @@ void fill(vy_handle* h, Params& P, bool rollout, bool acts) {
   P.profiles = h->d_prof;
   P.delta_tab = h->d_dtab;
   P.portc = h->d_portc;
+  P.treec = h->d_treec;
   P.st = h->st;
   P.out = h->out;
   P.err = h->d_err;
@@ -283,7 +284,7 @@ struct Geometry {
 template <typename K>
 int geometry(vy_handle* h, K kernel, const TileLayout& L, int n_profiles, Geometry& g) {
   const int per_sm = h->smem_per_sm;
-  const int tb = tables_bytes(n_profiles, h->t.k, h->t.n_ports);
+  const int tb = tables_bytes(n_profiles, h->t.k, h->t.n_ports, h->t.n_nodes);
   int best_w = 1, best_total = 0;
   for (int w = 1; w <= 8; ++w) {  // __launch_bounds__(256)
     const int bytes = tb + w * L.bytes;
@@ -443,6 +444,16 @@ int vy_create(const vy_tables* t, int64_t batch, int device, vy_handle** out) {
       r[10] = t->i_denom[i], r[11] = rcp(t->i_denom[i]);
     }
     if (!rc) rc = upload(&h->d_portc, pcv.data(), pcv.size());
+    // tree records in the deepest-first rescale order (TreeC, vy_tile.cuh)
+    std::vector<double> tcv((size_t)(t->n_nodes > 0 ? t->n_nodes : 1) * 4, 0.0);
+    for (int q = 0; q < t->n_nodes; ++q) {
+      const int m = h->node_order[q];
+      double* r = tcv.data() + (size_t)q * 4;
+      r[0] = h->node_cap[m], r[1] = h->node_eta[m], r[2] = rcp(h->node_eta[m]);
+      const int32_t lohi[2] = {h->node_lo[m], h->node_hi[m]};
+      std::memcpy(&r[3], lohi, 8);
+    }
+    if (!rc) rc = upload(&h->d_treec, tcv.data(), tcv.size());
   }
   if (!rc) rc = upload<Profile>(&h->d_prof, nullptr, kMaxProfiles);
   if (!rc) rc = upload<uint32_t>(&h->d_err, nullptr, 1);
@@ -461,7 +472,7 @@ int vy_create(const vy_tables* t, int64_t batch, int device, vy_handle** out) {
 int vy_destroy(vy_handle* h) {
   if (!h) return VY_OK;
   void* ptrs[] = {h->d_buy, h->d_sellg, h->d_moer, h->d_dgrid, h->d_sin, h->d_cos, h->d_catcum,
-                  h->d_pthr, h->d_dtab, h->d_portc, h->d_wk, h->d_pfull, h->d_prof, h->d_err, h->d_tile_ctr};
+                  h->d_pthr, h->d_dtab, h->d_portc, h->d_treec, h->d_wk, h->d_pfull, h->d_prof, h->d_err, h->d_tile_ctr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete h;

@@ -130,6 +130,7 @@ struct Params {
   const Profile* profiles;  // [kMaxProfiles]
   const double* delta_tab;  // [2k+1] (a-k)/k
   const double* portc;      // [n_ports][kPortWords] per-port constants, staged into shared memory (PortC)
+  const double* treec;      // [n_nodes][4] tree nodes in deepest-first order, staged into shared memory (TreeC)
   // state / outputs / actions
   vy_state st;
   vy_outputs out;

@@ -23,11 +23,15 @@ __host__ __device__ inline int portc_off(int n_profiles, int k) {
   const int nd = (2 * k + 1) <= 256 ? (2 * k + 1) : 0;
   return (grid_table_off(n_profiles) + nd * 8 + 15) & ~15;
 }
-__host__ __device__ inline int tables_bytes(int n_profiles, int k, int n_ports) {
-  return (portc_off(n_profiles, k) + n_ports * 8 * kPortWords + 127) & ~127;
+__host__ __device__ inline int treec_off(int n_profiles, int k, int n_ports) {
+  return portc_off(n_profiles, k) + n_ports * 8 * kPortWords;
+}
+__host__ __device__ inline int tables_bytes(int n_profiles, int k, int n_ports, int n_nodes) {
+  return (treec_off(n_profiles, k, n_ports) + n_nodes * 32 + 127) & ~127;
 }
 
-__device__ __forceinline__ void stage_tables(const Params& P, Prof& prof, const double*& dtab, PortC& pc) {
+__device__ __forceinline__ void stage_tables(const Params& P, Prof& prof, const double*& dtab, PortC& pc,
+                                             TreeC& tc) {
   unsigned char* smem = vy_smem;
   double* spd = reinterpret_cast<double*>(smem);
   const double* gp = reinterpret_cast<const double*>(P.profiles);
@@ -39,9 +43,13 @@ __device__ __forceinline__ void stage_tables(const Params& P, Prof& prof, const 
   const int po = portc_off(P.n_profiles, P.k);
   double* sp = reinterpret_cast<double*>(smem + po);
   for (int i = threadIdx.x; i < P.n_ports * kPortWords; i += blockDim.x) sp[i] = __ldg(P.portc + i);
+  const int to = treec_off(P.n_profiles, P.k, P.n_ports);
+  double* st = reinterpret_cast<double*>(smem + to);
+  for (int i = threadIdx.x; i < P.n_nodes * 4; i += blockDim.x) st[i] = __ldg(P.treec + i);
   __syncthreads();
   prof = Prof{smem_base()};
   pc = PortC{smem_base() + (uint32_t)po};
+  tc = TreeC{smem_base() + (uint32_t)to};
   dtab = nd <= 256 ? sd : nullptr;
 }
 
@@ -49,7 +57,8 @@ __device__ __forceinline__ void stage_tables(const Params& P, Prof& prof, const 
 // the transition (padding lanes on their harmless padding columns, side
 // effects masked) because the fused port loop synchronises the warp.
 template <int M>
-__device__ __forceinline__ void step_tile(const Params& P, Prof prof, const double* dtab, PortC pc, uint32_t tile,
+__device__ __forceinline__ void step_tile(const Params& P, Prof prof, const double* dtab, PortC pc, TreeC tc,
+                                          uint32_t tile,
                                           int64_t b0, int lane) {
   using C = Spec<M>;
   const Lane T = make_lane(P, tile, lane);
@@ -78,7 +87,7 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
     return v < INT_MIN ? INT_MIN : (v > INT_MAX ? INT_MAX : (int)v);
   };
   StepResult r{0.0, false};
-  if (!C::probe(P, 0x200u)) r = tile_step<M>(P, prof, dtab, pc, T, E, b, F, S, active, act);  // 0x200: memory-only probe
+  if (!C::probe(P, 0x200u)) r = tile_step<M>(P, prof, dtab, pc, tc, T, E, b, F, S, active, act);  // 0x200: memory-only probe
   bool reset = false;
   if (r.done && (P.flags & VY_F_AUTO_RESET)) {
     // in-kernel auto-reset (engine.py:460-462): the terminal reward/done/infos
@@ -112,17 +121,18 @@ template <int M>
 __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) {
   Prof prof;
   PortC pc;
+  TreeC tc;
   const double* dtab;
-  stage_tables(P, prof, dtab, pc);
+  stage_tables(P, prof, dtab, pc, tc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t toff = tables_bytes(P.n_profiles, P.k, P.n_ports) + warp * P.L.bytes;
+  const uint32_t toff = tables_bytes(P.n_profiles, P.k, P.n_ports, P.n_nodes) + warp * P.L.bytes;
   const unsigned long long ntiles = (unsigned long long)((P.B + 31) >> 5);
   for (;;) {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(P.tile_ctr, 1ull);
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= ntiles) break;
-    step_tile<M>(P, prof, dtab, pc, toff, (int64_t)t * 32, lane);
+    step_tile<M>(P, prof, dtab, pc, tc, toff, (int64_t)t * 32, lane);
     __syncwarp();
   }
   if (lane == 0) {
@@ -142,12 +152,13 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
   using C = Spec<M>;
   Prof prof;
   PortC pc;
+  TreeC tc;
   const double* dtab;
-  stage_tables(P, prof, dtab, pc);
+  stage_tables(P, prof, dtab, pc, tc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
   if (b0 >= P.B) return;
-  const uint32_t tile = tables_bytes(P.n_profiles, P.k, P.n_ports) + warp * P.L.bytes;
+  const uint32_t tile = tables_bytes(P.n_profiles, P.k, P.n_ports, P.n_nodes) + warp * P.L.bytes;
   const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
@@ -171,7 +182,7 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
     const uint64_t j0 = (uint64_t)(call0 + t) * (uint64_t)ns;
     auto act = [&](int slot) -> int { return policy_action(pkey, j0 + slot + 1, hi); };
     const Frame F = load_frame<M>(P, E.step, E.day);
-    const StepResult r = tile_step<M>(P, prof, dtab, pc, T, E, b, F, S, active, act);
+    const StepResult r = tile_step<M>(P, prof, dtab, pc, tc, T, E, b, F, S, active, act);
     if (r.done) {
       ++episode;
       reset_scalars(P, E, seed, episode, 0, false);
@@ -198,12 +209,13 @@ __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P,
                                                int episode_mode, const int32_t* inj_day) {
   Prof prof;
   PortC pc;
+  TreeC tc;
   const double* dtab;
-  stage_tables(P, prof, dtab, pc);
+  stage_tables(P, prof, dtab, pc, tc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
   if (b0 >= P.B) return;
-  const uint32_t tile = tables_bytes(P.n_profiles, P.k, P.n_ports) + warp * P.L.bytes;
+  const uint32_t tile = tables_bytes(P.n_profiles, P.k, P.n_ports, P.n_nodes) + warp * P.L.bytes;
   const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
   const bool active = b < P.B;

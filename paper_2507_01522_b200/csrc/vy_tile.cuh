@@ -96,6 +96,20 @@ struct PortC {
   }
 };
 
+// The capacity tree staged in shared memory, one 32-byte record per node in
+// the deepest-first order of the rescale (_kernel.pyx:626-649):
+// {cap, eta, RN(1/eta), (lo, hi) slot range}.  Read at a uniform address
+// (broadcast) instead of register-indexed constant-bank loads.
+struct TreeC {
+  uint32_t a;
+  __device__ __forceinline__ void rec(int q, double& cap, double& eta, double& rcp_eta, int& lo, int& hi) const {
+    const uint32_t r = a + (uint32_t)q * 32u;
+    asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(cap), "=d"(eta) : "r"(r));
+    asm("ld.shared.f64 %0, [%1];" : "=d"(rcp_eta) : "r"(r + 16u));
+    asm("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(r + 24u));
+  }
+};
+
 // Global loads issued exactly where written (volatile asm): the compiler
 // otherwise sinks early loads next to their first use at the end of the step,
 // exposing the full DRAM latency there instead of overlapping it with the
@@ -287,14 +301,16 @@ __device__ __forceinline__ double clip_current(double tgt, double soc, double ta
   return chg ? v : -v;
 }
 
+__device__ __forceinline__ double node_load(double s, double eta, double rcp_eta) {
+  if (s > 0.0) return eta == 1.0 ? s : div_rcp(s, eta, rcp_eta);
+  return s * eta;
+}
 __device__ __forceinline__ double node_load(const Params& P, double s, int m) {
-  if (s > 0.0) return P.node_eta[m] == 1.0 ? s : div_rcp(s, P.node_eta[m], P.node_rcp_eta[m]);
-  return s * P.node_eta[m];
+  return node_load(s, P.node_eta[m], P.node_rcp_eta[m]);
 }
 
-// node m's load sum over its slot range, sequentially in leaf order
-__device__ __forceinline__ double node_sum(const Params& P, const Lane& T, double cb, int m) {
-  const int lo = P.node_lo[m], hi = P.node_hi[m];
+// a node's load sum over its slot range [lo, hi), sequentially in leaf order
+__device__ __forceinline__ double node_sum(const Params& P, const Lane& T, double cb, int lo, int hi) {
   const int hp = hi < P.n_ports ? hi : P.n_ports;
   double s = 0.0;
   for (int j = lo; j < hp; ++j) s += T.idr(j);
@@ -304,15 +320,16 @@ __device__ __forceinline__ double node_sum(const Params& P, const Lane& T, doubl
 
 // _kernel.pyx:626-649: deepest-first proportional scaling to a fixed point.
 // Currents live in the i_drawn slots (they become i_drawn after the rescale).
-__device__ __noinline__ void fit_tree(const Params& P, const Lane& T, double& cb) {
+__device__ __noinline__ void fit_tree(const Params& P, TreeC tc, const Lane& T, double& cb) {
   for (int pass = 0; pass < P.max_passes; ++pass) {
     bool moved = false;
     for (int q = 0; q < P.n_nodes; ++q) {
-      const int m = P.node_order[q];
-      const double mag = fabs(node_load(P, node_sum(P, T, cb, m), m));
-      if (mag > P.node_cap[m]) {
-        const double f = P.node_cap[m] / mag;
-        const int lo = P.node_lo[m], hi = P.node_hi[m];
+      double cap, eta, rcp_eta;
+      int lo, hi;
+      tc.rec(q, cap, eta, rcp_eta, lo, hi);
+      const double mag = fabs(node_load(node_sum(P, T, cb, lo, hi), eta, rcp_eta));
+      if (mag > cap) {
+        const double f = cap / mag;
         const int hp = hi < P.n_ports ? hi : P.n_ports;
         for (int j = lo; j < hp; ++j) {
           const double old = T.idr(j);
@@ -465,7 +482,8 @@ __device__ __forceinline__ void store_port(const Params& P, int64_t b, int i, ui
 // action index of a slot; `b` is the global env index (infos / injected draws).
 template <int M, class Act>
 __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
-                                                const double* __restrict__ dtab, PortC pc, const Lane& T, EnvRegs& E,
+                                                const double* __restrict__ dtab, PortC pc, TreeC tc, const Lane& T,
+                                                EnvRegs& E,
                                                 int64_t b, const Frame& F, const ObsSink& S, bool active, Act act) {
   const int n = P.n_ports;
   const int64_t ld = P.ld;
@@ -554,13 +572,16 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
       }
     }
   } else {
-    for (int m = 0; m < P.n_nodes; ++m) {
-      const double over = fabs(node_load(P, node_sum(P, T, cb, m), m)) - P.node_cap[m];
+    for (int q = 0; q < P.n_nodes; ++q) {  // max over the nodes: any order
+      double cap, eta, rcp_eta;
+      int lo, hi;
+      tc.rec(q, cap, eta, rcp_eta, lo, hi);
+      const double over = fabs(node_load(node_sum(P, T, cb, lo, hi), eta, rcp_eta)) - cap;
       if (over > excess) excess = over;
     }
   }
   // no node over capacity => the reference's first rescale pass changes nothing and returns
-  if (excess > 0.0) fit_tree(P, T, cb);
+  if (excess > 0.0) fit_tree(P, tc, T, cb);
   if (info) {
     for (int i = 0; i < n; ++i) O.i_used[i * ld + b] = T.idr(i);
     if (battery) O.i_used[n * ld + b] = cb;
