@@ -211,6 +211,12 @@ int vy_poll_error(vy_handle *h, int clear, void *stream, uint32_t *out);
 /* Number of kernel launches issued through this handle (for bench accounting). */
 int64_t vy_launch_count(vy_handle *h);
 
+/* Diagnostics: which instantiation of the step kernel the last vy_step ran:
+ * 1 / 2 = lean (obs/reward/done only, none of the optional model features,
+ * staged uint8 actions; small / large capacity tree), 0 = generic, -1 = none
+ * yet.  Results never depend on it (tests/test_gpu_parity.py runs both). */
+int32_t vy_last_step_mode(vy_handle *h);
+
 /* PPO support (config C3): generalised advantage estimation as a reverse
  * scan over a [T][B] rollout (float32 values/rewards, uint8 dones, last_value
  * [B]); writes advantages and returns [T][B].  Not part of the reference

@@ -395,6 +395,10 @@ class BatchEnv:
     def launch_count(self) -> int:
         return int(self._lib.vy_launch_count(self._h))
 
+    def last_step_mode(self) -> int:
+        """Step-kernel instantiation of the last step (1/2 lean, 0 generic; diagnostics)."""
+        return int(self._lib.vy_last_step_mode(self._h))
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             torch.cuda.synchronize(self.device)

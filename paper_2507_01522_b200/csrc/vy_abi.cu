@@ -134,6 +134,7 @@ struct vy_handle {
   bool bound = false;
   int64_t launches = 0;
   int smem_per_sm = 0, num_sms = 0;
+  int last_mode = -1;  // Spec<M> of the last vy_step launch (diagnostics)
 };
 
 namespace {
@@ -576,6 +577,7 @@ int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride
   if (inj) P.inj = *inj;
   Geometry g;
   const int mode = step_mode(h, flags, acts);
+  h->last_mode = mode;
   auto* kern = mode == 1 ? k_step<1> : mode == 2 ? k_step<2> : k_step<0>;
   if (int rc = geometry(h, kern, P.L, P.n_profiles, g)) return rc;
   // persistent grid: every resident CTA slot, never more CTAs than tiles need
@@ -646,6 +648,7 @@ int vy_poll_error(vy_handle* h, int clear, void* stream, uint32_t* out) {
 }
 
 int64_t vy_launch_count(vy_handle* h) { return h ? h->launches : -1; }
+int32_t vy_last_step_mode(vy_handle* h) { return h ? h->last_mode : -1; }
 
 int vy_selftest_div(const double* divisors, int32_t nd, int64_t samples_per_divisor, uint64_t seed,
                     int64_t* mismatches) {

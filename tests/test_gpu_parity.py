@@ -75,6 +75,38 @@ def test_golden_trajectory_f32_device_path(name):
     env.close()
 
 
+LEAN = {"bp_coarse_dt": 1, "bp_default": 1, "bp_no_discharge": 1, "c1_default": 1, "default_maxcharge": 1,
+        "bp_random_tree": 2}
+
+
+@pytest.mark.parametrize("name", sorted(LEAN))
+def test_golden_trajectory_lean_kernel(name):
+    """The lean step instantiations (vy_device.cuh Spec<1> / Spec<2>) need
+    staged uint8 actions for whole 32-env tiles: the fixture's envs are rows
+    0..B-1 of a 32-env batch (same seeds), extra rows get the fixture's first
+    row of actions; rows 0..B-1 must reproduce the reference bit for bit."""
+    fx = Fixture(name)
+    from paper_2507_01522_b200.batch import BatchEnv
+
+    env = BatchEnv(fx.config, fx.station, fx.dataset, batch_size=32, master_seed=fx.master_seed)
+    obs = env.reset(as_numpy=False)
+    np.testing.assert_array_equal(obs[: fx.B].cpu().numpy(), fx["obs0"].astype(np.float32))
+    acts = np.repeat(fx["actions"][:, :1, :], 32, axis=1)
+    acts[:, : fx.B] = fx["actions"]
+    acts = torch.as_tensor(acts.astype(np.uint8), device="cuda")
+    for t in range(fx.steps):
+        obs, r, d, _ = env.step(acts[t], collect_infos=False)
+        assert env.last_step_mode() == LEAN[name]
+        np.testing.assert_array_equal(obs[: fx.B].cpu().numpy(), fx["obs"][t].astype(np.float32), err_msg=f"t={t}")
+        np.testing.assert_array_equal(r[: fx.B].cpu().numpy(), fx["reward"][t].astype(np.float32))
+        np.testing.assert_array_equal(d[: fx.B].cpu().numpy(), fx["done"][t].astype(np.uint8))
+    st = env.reference_state()
+    for k in STATE_KEYS:
+        np.testing.assert_array_equal(st[k][: fx.B], fx[f"final_{k}"], err_msg=k)
+    env.check_errors()
+    env.close()
+
+
 def test_device_random_policy_matches_reference():
     from paper_2507_01522_b200.batch import DeviceRandomPolicy
 
