@@ -217,6 +217,13 @@ int64_t vy_launch_count(vy_handle *h);
  * yet.  Results never depend on it (tests/test_gpu_parity.py runs both). */
 int32_t vy_last_step_mode(vy_handle *h);
 
+/* Launch shaping for batches that share the GPU with other handles (the
+ * heterogeneous C5 batch runs one handle per station config on concurrent
+ * streams): the persistent step kernel launches at most
+ * ceil(tiles / (warps per CTA * k)) CTAs, so each warp steps about k 32-env
+ * tiles.  Default 1 (as many CTAs as fit).  Results never depend on it. */
+int vy_set_tiles_per_warp(vy_handle *h, int32_t k);
+
 /* PPO support (config C3): generalised advantage estimation as a reverse
  * scan over a [T][B] rollout (float32 values/rewards, uint8 dones, last_value
  * [B]); writes advantages and returns [T][B].  Not part of the reference

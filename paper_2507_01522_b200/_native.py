@@ -60,6 +60,7 @@ _SIGS = {
     "vy_poll_error": (C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_uint32)]),
     "vy_launch_count": (C.c_int64, [_P]),
     "vy_last_step_mode": (C.c_int32, [_P]),
+    "vy_set_tiles_per_warp": (C.c_int, [_P, C.c_int32]),
     "vy_gae": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_int64, C.c_float, C.c_float, _P, _P, _P]),
     "vy_selftest_div": (C.c_int, [C.POINTER(C.c_double), C.c_int32, C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),
 }

@@ -395,6 +395,11 @@ class BatchEnv:
     def launch_count(self) -> int:
         return int(self._lib.vy_launch_count(self._h))
 
+    def set_tiles_per_warp(self, k: int) -> None:
+        """Shape the persistent step grid for a batch that shares the GPU with
+        other batches (HeteroBatch): about k 32-env tiles per warp."""
+        nat.check(self._lib.vy_set_tiles_per_warp(self._h, int(k)), "vy_set_tiles_per_warp")
+
     def last_step_mode(self) -> int:
         """Step-kernel instantiation of the last step (1/2 lean, 0 generic; diagnostics)."""
         return int(self._lib.vy_last_step_mode(self._h))

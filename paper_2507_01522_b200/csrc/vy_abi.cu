@@ -135,6 +135,7 @@ struct vy_handle {
   int64_t launches = 0;
   int smem_per_sm = 0, num_sms = 0;
   int last_mode = -1;  // Spec<M> of the last vy_step launch (diagnostics)
+  int tiles_per_warp = 1;  // persistent k_step grid: at most ceil(tiles / (warps per CTA * this)) CTAs
 };
 
 namespace {
@@ -582,7 +583,11 @@ int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride
   if (int rc = geometry(h, kern, P.L, P.n_profiles, g)) return rc;
   // persistent grid: every resident CTA slot, never more CTAs than tiles need
   const unsigned resident = (unsigned)h->num_sms * (unsigned)(h->smem_per_sm / (g.smem + 1024));
-  const unsigned grid = g.grid < resident ? g.grid : resident;
+  unsigned grid = g.grid < resident ? g.grid : resident;
+  if (h->tiles_per_warp > 1) {  // fewer, longer-lived warps (batches sharing the GPU)
+    const unsigned k = (unsigned)h->tiles_per_warp, want = (g.grid + k - 1) / k;
+    grid = want < grid ? want : grid;
+  }
   kern<<<grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P);
   VY_CUDA(cudaGetLastError());
   ++h->launches;
@@ -649,6 +654,12 @@ int vy_poll_error(vy_handle* h, int clear, void* stream, uint32_t* out) {
 
 int64_t vy_launch_count(vy_handle* h) { return h ? h->launches : -1; }
 int32_t vy_last_step_mode(vy_handle* h) { return h ? h->last_mode : -1; }
+
+int vy_set_tiles_per_warp(vy_handle* h, int32_t k) {
+  if (!h || k < 1) return fail(VY_ERR_ARG, "tiles per warp must be >= 1");
+  h->tiles_per_warp = k;
+  return VY_OK;
+}
 
 int vy_selftest_div(const double* divisors, int32_t nd, int64_t samples_per_divisor, uint64_t seed,
                     int64_t* mismatches) {

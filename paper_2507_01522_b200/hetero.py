@@ -2,10 +2,12 @@
 
 The reference requires one (config, station, dataset) per batch
 (engine.py:370).  ``HeteroBatch`` batches many: each group is a
-regular BatchEnv (own tables, own handle; the generic kernel serves every
-station size), groups are spread round-robin over a few CUDA streams so the small
-per-group grids run concurrently and fill the GPU (each group's launches stay
-ordered on its stream; a step joins all streams back into the caller's).  Env seeds and
+regular BatchEnv (own tables, own handle; the lean step kernel when the
+group's config allows it — group sizes are whole 32-env tiles for that),
+groups are spread round-robin over CUDA streams so the per-group grids run
+concurrently and fill the GPU (each group's launches stay ordered on its
+stream; a step joins all streams back into the caller's), and each group's
+persistent grid is shaped for sharing (``tiles_per_warp``).  Env seeds and
 RandomPolicy rows use one global index space across groups (group g's envs
 are global indices offset_g .. offset_g + B_g - 1), so a group's trajectory is
 bit-identical to a standalone BatchEnv with that global_offset — which is
@@ -44,7 +46,11 @@ _LAYOUTS = (("single_type", 0, 8), ("multi_type", 6, 10), ("nested_splitters", 4
 def sweep_groups(total_envs: int, days: int = 365, seed: int = 0) -> list[Group]:
     """36 (region, scenario, traffic) combinations splitting ``total_envs``."""
     combos = list(itertools.product(REGIONS, SCENARIOS, TRAFFIC_FACTORS))
+    # whole 32-env warp tiles per group (when the total allows): the lean step
+    # kernel stages each tile's uint8 action rows, which needs B % 32 == 0
     per = total_envs // len(combos)
+    if per >= 32:
+        per -= per % 32
     groups = []
     for gi, (region, scen, traffic) in enumerate(combos):
         layout, ac, dc = _LAYOUTS[gi % len(_LAYOUTS)]
@@ -56,7 +62,7 @@ def sweep_groups(total_envs: int, days: int = 365, seed: int = 0) -> list[Group]
 
 class HeteroBatch:
     def __init__(self, groups: list[Group], master_seed: int = 0, global_offset: int = 0, device=None,
-                 policy_seed: int | None = None, n_streams: int = 8):
+                 policy_seed: int | None = None, n_streams: int = 16, tiles_per_warp: int = 2):
         self.groups = groups
         self.streams = [torch.cuda.Stream(device=device) for _ in range(max(1, n_streams))]
         self.envs: list[BatchEnv] = []
@@ -65,6 +71,7 @@ class HeteroBatch:
         for g in groups:
             env = BatchEnv(g.config, g.station, g.dataset, batch_size=g.batch_size, master_seed=master_seed,
                            global_offset=off, device=device)
+            env.set_tiles_per_warp(tiles_per_warp)  # groups overlap on streams: fewer, longer-lived warps each
             self.envs.append(env)
             if policy_seed is not None:
                 pol = DeviceRandomPolicy(policy_seed, env.n_ports, g.config.discretization_k)
