@@ -58,8 +58,8 @@ __device__ __forceinline__ void stage_tables(const Params& P, Prof& prof, const 
 // effects masked) because the fused port loop synchronises the warp.
 template <int M>
 __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const double* dtab, PortC pc, TreeC tc,
-                                          uint32_t tile,
-                                          int64_t b0, int lane) {
+                                          uint32_t tile, int64_t b0, int lane,
+                                          unsigned long long* claim = nullptr) {
   using C = Spec<M>;
   const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
@@ -109,6 +109,10 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
       reinterpret_cast<float*>(P.out.reward)[b] = (float)r.reward;
     P.out.done[b] = r.done;
   }
+  // the next tile is claimed before the obs read-out so the atomic's round
+  // trip overlaps it (and not earlier: a claim held across a whole step
+  // lengthens the tail of the launch)
+  if (claim && lane == 0) *claim = atomicAdd(P.tile_ctr, 1ull);
   emit_tail<M>(P, T, E, G, S, b0, active, P.out.obs);
 }
 
@@ -127,12 +131,12 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t toff = tables_bytes(P.n_profiles, P.k, P.n_ports, P.n_nodes) + warp * P.L.bytes;
   const unsigned long long ntiles = (unsigned long long)((P.B + 31) >> 5);
+  unsigned long long nxt = 0;  // lane 0: this warp's next tile (claimed inside step_tile)
+  if (lane == 0) nxt = atomicAdd(P.tile_ctr, 1ull);
   for (;;) {
-    unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(P.tile_ctr, 1ull);
-    t = __shfl_sync(0xffffffffu, t, 0);
+    const unsigned long long t = __shfl_sync(0xffffffffu, nxt, 0);
     if (t >= ntiles) break;
-    step_tile<M>(P, prof, dtab, pc, tc, toff, (int64_t)t * 32, lane);
+    step_tile<M>(P, prof, dtab, pc, tc, toff, (int64_t)t * 32, lane, &nxt);
     __syncwarp();
   }
   if (lane == 0) {

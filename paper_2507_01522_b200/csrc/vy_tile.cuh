@@ -23,6 +23,7 @@
 #include "vy_device.cuh"
 
 
+
 namespace vy {
 
 // Dynamic shared memory of every kernel in this library.  Tile data is
