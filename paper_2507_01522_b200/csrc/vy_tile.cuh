@@ -468,6 +468,19 @@ __device__ __forceinline__ void stage_port_obs(const Params& P, Prof prof, const
   stage_port_obs(P, prof, S, lane, active, i, mt, idr, soc, de, dt, P.i_denom[i], P.rcp_i_denom[i]);
 }
 
+// the six obs columns of a port that is empty (all-zero state): +0
+__device__ __forceinline__ void stage_zero_obs(const ObsSink& S, int lane, bool active, int i) {
+  if (S.row64) {
+    if (active)
+#pragma unroll
+      for (int f = 0; f < 6; ++f) S.row64[6 * i + f] = 0.0;
+  } else {
+    const uint32_t col = S.cells + 6 * i * 132 + lane * 4;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) sts_f32(col + f * 132, 0.0f);
+  }
+}
+
 __device__ __forceinline__ void store_port(const Params& P, int64_t b, int i, uint32_t mt, double idr, double soc,
                                            double de, int dt) {
   const vy_state& s = P.st;
@@ -613,7 +626,8 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
     const bool occ = mt & 1u;
     double got = 0.0;
     bool dep = false;
-    if (__any_sync(0xffffffffu, occ)) {
+    const bool any_occ = __any_sync(0xffffffffu, occ);
+    if (any_occ) {
       const int pf = mt >> 2;
       double dtv, eta_d, eta_c, rcp_eta_c;
       pc.pair(i, 3, dtv, eta_d);
@@ -661,27 +675,34 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
       tover += !dep & last & (p == 1) & (dt < 0) ? -dt : 0;
       occm |= (uint64_t)(occ && !dep) << i;
     }
-    if (dep) {
-      mt = 0;
-      cur = soc = de = 0.0;
-      dt = 0;
-    }
     if (info) O.delivered[i * ld + b] = got;
-    if (S.in_place) {
-      // padding lanes (b >= B) write their own padding columns of the [n][ld] state: harmless, no branch
-      store_port(P, b, i, mt, cur, soc, de, dt);
-      __syncwarp();  // every lane has read port i before its slots take obs columns
-    } else {
-      T.meta(i) = (uint8_t)mt;
-      T.idr(i) = cur;
-      T.soc(i) = soc;
-      T.de(i) = de;
-      T.dtrem(i) = (int16_t)dt;
-    }
-    {
+    if (any_occ) {
+      if (dep) {
+        mt = 0;
+        cur = soc = de = 0.0;
+        dt = 0;
+      }
+      if (S.in_place) {
+        // padding lanes (b >= B) write their own padding columns of the [n][ld] state: harmless, no branch
+        store_port(P, b, i, mt, cur, soc, de, dt);
+        __syncwarp();  // every lane has read port i before its slots take obs columns
+      } else {
+        T.meta(i) = (uint8_t)mt;
+        T.idr(i) = cur;
+        T.soc(i) = soc;
+        T.de(i) = de;
+        T.dtrem(i) = (int16_t)dt;
+      }
       double i_denom, rcp_i_denom;
       pc.pair(i, 5, i_denom, rcp_i_denom);
       stage_port_obs(P, prof, S, T.lane, active, i, mt, cur, soc, de, dt, i_denom, rcp_i_denom);
+    } else {
+      // A port empty in every lane of the warp stays empty and all-zero (a
+      // departure or reset stored zeros, phase 1 set its current to 0): its
+      // HBM copy already holds this state, so it is not rewritten, and its
+      // six obs columns are +0.  Arrivals below store the ports they fill.
+      if (S.in_place) __syncwarp();  // every lane has read port i before its slots take obs columns
+      stage_zero_obs(S, T.lane, active, i);
     }
   }
   double e_b = 0.0, bgot = 0.0;
