@@ -66,11 +66,17 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
   const bool active = b < P.B;
   EnvRegs E{};  // zero for padding lanes so table lookups stay in bounds
   if (active) load_env<M>(P, b, E);
-  tile_issue(P, tile, b0, lane, C::staged(P));
+  // Two-stage tile load (tile_issue_meta / tile_issue_ports): the meta bytes
+  // and action rows first, then the slots of the ports some env of the tile
+  // occupies.  At night most ports are empty in every lane and are neither
+  // read nor written (-12% step time); at the afternoon peak every port is
+  // occupied somewhere and the extra round trip costs ~3% (day average -1.5%).
+  tile_issue_meta(P, tile, b0, lane, C::staged(P));
   // exogenous inputs for this step and the obs globals of the next one, in
   // flight together with the tile copies
   const Frame F = load_frame<M>(P, E.step, E.day);
   const ObsGlobals G = load_obs_globals(P, E.step + 1, E.day);
+  tile_issue_ports(P, tile, b0, lane);
   tile_wait();
   const ObsSink S = make_sink<M>(P, T, b, P.out.obs, /*in_place=*/true);
   const int dt = P.act_dtype;

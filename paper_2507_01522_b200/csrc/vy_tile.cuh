@@ -235,6 +235,72 @@ __device__ __forceinline__ void tile_issue(const Params& P, uint32_t toff, int64
   }
 }
 
+// Two-stage tile load (step kernel): the meta bytes (and action rows) first;
+// once they arrive the warp votes which ports any of its 32 envs occupies and
+// copies the float64 slots and dwell times of those ports only.  A port empty
+// in every lane is never read (its slots are not used: phase 1 zeroes its
+// current slot, phase 2 stages +0 obs and does not store it).
+__device__ __forceinline__ void tile_issue_meta(const Params& P, uint32_t toff, int64_t b0, int lane,
+                                                bool with_acts) {
+  unsigned char* t = vy_smem + toff;
+  const int n = P.n_ports;
+  const int64_t ld = P.ld;
+  const TileLayout& L = P.L;
+  const char* msrc = reinterpret_cast<const char*>(P.st.port_meta);
+  for (int c = lane >> 1; c < n; c += 16)
+    cp_async16(t + L.meta + c * 32 + (lane & 1) * 16, msrc + ((int64_t)c * ld + b0) + (lane & 1) * 16);
+  if (with_acts) {
+    const int bytes = 32 * (n + 1);
+    const char* asrc = reinterpret_cast<const char*>(P.actions) + b0 * (n + 1);
+    for (int o = lane * 16; o < bytes; o += 512) cp_async16(t + L.acts + o, asrc + o);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+// warp-uniform mask of the ports any env of the tile occupies (meta staged):
+// port c's 32 meta bytes are words 8c..8c+7 of the meta area, word w is read
+// by lane w % 32 in round w / 32
+__device__ __forceinline__ uint64_t occupied_ports(const Params& P, uint32_t toff, int lane) {
+  const int n = P.n_ports;
+  const uint32_t* mw = reinterpret_cast<const uint32_t*>(vy_smem + toff + P.L.meta);
+  uint64_t mask = 0;
+  for (int r = 0; r * 32 < 8 * n; ++r) {
+    const int w = r * 32 + lane;
+    const bool occ = w < 8 * n && (mw[w] & 0x01010101u);
+    const uint32_t bal = __ballot_sync(0xffffffffu, occ);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (bal & (0xFFu << (8 * q))) mask |= 1ull << (4 * r + q);
+  }
+  return mask;
+}
+
+// after tile_issue_meta: wait for the meta bytes, vote the occupied ports and
+// issue their slot copies; returns the warp-uniform port mask
+__device__ __forceinline__ uint64_t tile_issue_ports(const Params& P, uint32_t toff, int64_t b0, int lane) {
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncwarp();
+  unsigned char* t = vy_smem + toff;
+  const int n = P.n_ports;
+  const int64_t ld = P.ld;
+  const TileLayout& L = P.L;
+  const uint64_t mask = occupied_ports(P, toff, lane);
+  const int q16 = (lane & 15) * 16;
+  for (int i = lane >> 4; i < n; i += 2) {
+    if (!((mask >> i) & 1ull)) continue;
+    const int64_t g = ((int64_t)i * ld + b0) * 8 + q16;
+    unsigned char* d = t + L.ports + i * 768 + q16;
+    cp_async16(d, reinterpret_cast<const char*>(P.st.port_i) + g);
+    cp_async16(d + 256, reinterpret_cast<const char*>(P.st.port_soc) + g);
+    cp_async16(d + 512, reinterpret_cast<const char*>(P.st.port_de) + g);
+  }
+  const char* dsrc = reinterpret_cast<const char*>(P.st.port_dtrem);
+  for (int c = lane >> 2; c < n; c += 8)
+    if ((mask >> c) & 1ull)
+      cp_async16(t + L.dtrem + c * 64 + (lane & 3) * 16, dsrc + ((int64_t)c * ld + b0) * 2 + (lane & 3) * 16);
+  return mask;
+}
+
 __device__ __forceinline__ void tile_wait() {
   cp_async_wait_all();
   __syncwarp();
