@@ -252,13 +252,19 @@ def main() -> None:
     ab = algorithmic_bytes(env.tables)
     peaks = load_peaks()
     achieved = ab["per_env_step"] * B / (step_kernel_ms / 1e3) / 1e9
-    traffic = None
+    traffic = dram = None
     tpath = os.path.join(ROOT, "profiles", "step_kernel_dram_bytes.json")
-    if os.path.exists(tpath) and B == B_PER_GPU:
-        # dram__bytes_read.sum + dram__bytes_write.sum of one k_step launch at this workload
-        # (ncu --set full capture, summarised by scripts/summarize_ncu.py)
+    if os.path.exists(tpath) and B == B_PER_GPU and args.steps == 288:
+        # dram__bytes_read.sum + dram__bytes_write.sum per k_step launch, averaged over
+        # the 288 launches of this same day window (ncu, scripts/day_dram.sh).  The
+        # kernel neither reads nor rewrites ports that are empty in a whole 32-env
+        # tile, so its real traffic is below the step contract's 1414 B/env-step;
+        # dram_frac is that real traffic over the measured time.
         with open(tpath) as fh:
             traffic = json.load(fh).get("bytes_per_launch")
+        dram = {"bytes_per_env_step": traffic / B, "achieved": traffic / (step_kernel_ms / 1e3) / 1e9,
+                "frac": traffic / (step_kernel_ms / 1e3) / 1e9 / peaks.get("hbm_gbs"),
+                "source": "profiles/step_kernel_dram_bytes.json"}
 
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -277,6 +283,8 @@ def main() -> None:
                      "frac": achieved / peaks.get("hbm_gbs"), "traffic": traffic,
                      "kernel": "vy::k_step", "kernel_ms": step_kernel_ms,
                      "bytes_per_env_step": ab["per_env_step"],
+                     "bytes_note": "step contract: full f64 port state read + written, u8 actions, f32 obs",
+                     "dram": dram,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not peaks.get("_fallback") else "fallback"},
         "clocks": clocks.summary(),
     }
