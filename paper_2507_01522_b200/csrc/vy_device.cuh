@@ -51,10 +51,13 @@ __device__ __forceinline__ int knuth(uint64_t& st, double thr) {
     ++k;
   }
 }
-// RandomPolicy draw: row key k, overall draw number j (1-based), hi = 2K+1
+// RandomPolicy draw: row key k, overall draw number j (1-based), hi = 2K+1.
+// The reference's u * hi with u = m * 2^-53 (m = x >> 11, exact) is the single
+// rounding RN(m * hi * 2^-53) = RN(m * (hi * 2^-53)): one multiply by the
+// exact constant hi * 2^-53.
 __device__ __forceinline__ int policy_action(uint64_t key, uint64_t j, int hi) {
-  const double u = __dmul_rn((double)(mix64(key + j * kGolden) >> 11), 1.0 / 9007199254740992.0);
-  const int a = (int)__double2ll_rz(__dmul_rn(u, (double)hi));
+  const double uh = __dmul_rn((double)(mix64(key + j * kGolden) >> 11), (double)hi * (1.0 / 9007199254740992.0));
+  const int a = (int)__double2int_rz(uh);
   return a >= hi ? hi - 1 : a;
 }
 
