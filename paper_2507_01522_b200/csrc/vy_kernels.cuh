@@ -76,7 +76,7 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
   // flight together with the tile copies
   const Frame F = load_frame<M>(P, E.step, E.day);
   const ObsGlobals G = load_obs_globals(P, E.step + 1, E.day);
-  tile_issue_ports(P, tile, b0, lane);
+  const uint64_t occ_ports = tile_issue_ports(P, tile, b0, lane);
   tile_wait();
   const ObsSink S = make_sink<M>(P, T, b, P.out.obs, /*in_place=*/true);
   const int dt = P.act_dtype;
@@ -93,7 +93,7 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
     return v < INT_MIN ? INT_MIN : (v > INT_MAX ? INT_MAX : (int)v);
   };
   StepResult r{0.0, false};
-  if (!C::probe(P, 0x200u)) r = tile_step<M>(P, prof, dtab, pc, tc, T, E, b, F, S, active, act);  // 0x200: memory-only probe
+  if (!C::probe(P, 0x200u)) r = tile_step<M>(P, prof, dtab, pc, tc, T, E, b, F, S, active, act, &occ_ports);  // 0x200: probe
   bool reset = false;
   if (r.done && (P.flags & VY_F_AUTO_RESET)) {
     // in-kernel auto-reset (engine.py:460-462): the terminal reward/done/infos
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
     const uint64_t j0 = (uint64_t)(call0 + t) * (uint64_t)ns;
     auto act = [&](int slot) -> int { return policy_action(pkey, j0 + slot + 1, hi); };
     const Frame F = load_frame<M>(P, E.step, E.day);
-    const StepResult r = tile_step<M>(P, prof, dtab, pc, tc, T, E, b, F, S, active, act);
+    const StepResult r = tile_step<M>(P, prof, dtab, pc, tc, T, E, b, F, S, active, act, nullptr);
     if (r.done) {
       ++episode;
       reset_scalars(P, E, seed, episode, 0, false);

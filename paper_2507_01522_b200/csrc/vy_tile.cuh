@@ -563,8 +563,8 @@ __device__ __forceinline__ void store_port(const Params& P, int64_t b, int i, ui
 template <int M, class Act>
 __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
                                                 const double* __restrict__ dtab, PortC pc, TreeC tc, const Lane& T,
-                                                EnvRegs& E,
-                                                int64_t b, const Frame& F, const ObsSink& S, bool active, Act act) {
+                                                EnvRegs& E, int64_t b, const Frame& F, const ObsSink& S, bool active,
+                                                Act act, const uint64_t* occ_ports) {
   const int n = P.n_ports;
   const int64_t ld = P.ld;
   using C = Spec<M>;
@@ -602,13 +602,16 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
     const double d = delta_of(act(i));
     const uint32_t mt = T.meta(i);
     const double idr_i = T.idr(i), soc_i = T.soc(i);
-    // A port no lane of the warp occupies is skipped (one vote, uniform
-    // branch); otherwise branch-free: an empty port (meta 0 -> profile 0,
-    // zero slots) runs the same arithmetic and the select discards it.
+    // A port no lane of the warp occupies is skipped (a bit of the tile's
+    // warp-uniform port mask, one uniform branch); otherwise branch-free: an
+    // empty port (meta 0 -> profile 0, zero slots) runs the same arithmetic
+    // and the select discards it.
     double c = 0.0;
     double kind_nodes[2];
     pc.pair(i, 2, kind_nodes[0], kind_nodes[1]);
-    if (__any_sync(0xffffffffu, mt & 1u)) {
+    // some lane occupies port i: the tile's warp-uniform port mask when the
+    // caller has one (step kernel), else a vote (rollout)
+    if (occ_ports ? (*occ_ports >> i) & 1ull : __any_sync(0xffffffffu, mt & 1u)) {
       double imax_c, imax_d, volt, rcp_volt;
       pc.pair(i, 0, imax_c, imax_d);
       pc.pair(i, 1, volt, rcp_volt);
@@ -682,7 +685,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
     uint32_t mt = T.meta(i);
     double cur = T.idr(i), soc = T.soc(i), de = T.de(i);
     int dt = T.dtrem(i);
-    // Ports no lane of the warp occupies are skipped (one vote, uniform
+    // Ports no lane of the warp occupies are skipped (port mask, uniform
     // branch).  Otherwise branch-free: an empty port holds meta 0 and zero
     // slots, its current is 0 (phase 1), so the arithmetic below yields
     // got = +0, soc = de = 0 for it; only the dwell countdown and the
@@ -692,7 +695,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
     const bool occ = mt & 1u;
     double got = 0.0;
     bool dep = false;
-    const bool any_occ = __any_sync(0xffffffffu, occ);
+    const bool any_occ = occ_ports ? (*occ_ports >> i) & 1ull : __any_sync(0xffffffffu, occ);  // meta unchanged since phase 1
     if (any_occ) {
       const int pf = mt >> 2;
       double dtv, eta_d, eta_c, rcp_eta_c;
