@@ -814,7 +814,11 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
   const int nfree = n - __popcll(occm);
   const int admitted = m < nfree ? m : nfree;
   const int declined = m - admitted;
-  for (int j = 0; j < m; ++j) {
+  // Only the admitted cars (the first min(M, free) of the M arrivals) are
+  // drawn: the declined cars' draws come after them in this step's own
+  // stream key4(seed, ep, 1, t), which nothing else reads, so skipping them
+  // changes no output (M and `declined` are counts).
+  for (int j = 0; j < admitted; ++j) {
     int car, stay;
     double soc0, frac;
     uint32_t pref;
@@ -837,7 +841,6 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
       frac = P.frac_lo + unit(st) * P.frac_span;
       pref = unit(st) < P.p_charge ? 1u : 0u;
     }
-    if (j >= admitted) continue;
     const uint64_t freem = ~occm & (n == 64 ? ~0ull : ((1ull << n) - 1));
     int port = 0;
     if (C::identity(P)) {
