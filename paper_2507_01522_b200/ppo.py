@@ -56,6 +56,7 @@ class PPOConfig:
     hidden: int = 64
     seed: int = 0
     use_graph: bool = True
+    fused_head: bool = True  # vy_ppo_sample / vy_ppo_head_* kernels instead of the torch op chain
 
 
 def _ortho(layer: nn.Linear, gain: float) -> nn.Linear:
@@ -79,6 +80,45 @@ class ActorCritic(nn.Module):
     def forward(self, obs: torch.Tensor):
         logits = self.actor(obs).view(-1, self.n_slots, self.n_actions).float()
         return logits, self.critic(obs).squeeze(-1).float()
+
+
+class PolicyHead(torch.autograd.Function):
+    """Per-sample log-probability of stored multi-discrete actions and entropy
+    (both summed over slots) from float32 logits [N, S, A]: vy_ppo_head_fwd /
+    vy_ppo_head_bwd, one pass over the logits each way."""
+
+    @staticmethod
+    def forward(ctx, logits: torch.Tensor, actions: torch.Tensor):
+        logits = logits.contiguous()
+        N, S, A = logits.shape
+        lp = torch.empty(N, device=logits.device)
+        ent = torch.empty(N, device=logits.device)
+        nat.check(nat.lib().vy_ppo_head_fwd(logits.data_ptr(), actions.data_ptr(), N, S, A, lp.data_ptr(),
+                                            ent.data_ptr(), torch.cuda.current_stream().cuda_stream),
+                  "vy_ppo_head_fwd")
+        ctx.save_for_backward(logits, actions)
+        return lp, ent
+
+    @staticmethod
+    def backward(ctx, g_lp, g_ent):
+        logits, actions = ctx.saved_tensors
+        N, S, A = logits.shape
+        grad = torch.empty_like(logits)
+        g_lp = g_lp.contiguous() if g_lp is not None else None
+        g_ent = g_ent.contiguous() if g_ent is not None else None
+        nat.check(nat.lib().vy_ppo_head_bwd(logits.data_ptr(), actions.data_ptr(), N, S, A,
+                                            g_lp.data_ptr() if g_lp is not None else None,
+                                            g_ent.data_ptr() if g_ent is not None else None, grad.data_ptr(),
+                                            torch.cuda.current_stream().cuda_stream), "vy_ppo_head_bwd")
+        return grad, None
+
+
+def head_reference(logits: torch.Tensor, actions: torch.Tensor):
+    """Plain torch restatement of PolicyHead (tests only)."""
+    lsm = torch.log_softmax(logits, dim=-1)
+    lp = lsm.gather(-1, actions.long().unsqueeze(-1)).squeeze(-1).sum(-1)
+    ent = -(lsm.exp() * lsm).sum(-1).sum(-1)
+    return lp, ent
 
 
 def gae(values, rewards, dones, last_value, gamma, lam):
@@ -139,11 +179,19 @@ class PPOTrainer:
     def _policy_step(self, t: int) -> None:
         with torch.autocast("cuda", dtype=torch.bfloat16):
             logits, v = self.net(self.obs[t])
-        g = -torch.log(-torch.log(torch.rand_like(logits).clamp_(1e-20, 1.0)))  # Gumbel-max sampling
-        a = torch.argmax(logits + g, dim=-1)
-        lp = torch.log_softmax(logits, dim=-1).gather(-1, a.unsqueeze(-1)).squeeze(-1).sum(-1)
-        self.actions[t].copy_(a)
-        self.logp[t].copy_(lp)
+        noise = torch.rand_like(logits)
+        if self.cfg.fused_head:
+            # Gumbel-max sampling + log-probability in one kernel, straight into the rollout buffers
+            B, S, A = logits.shape
+            nat.check(nat.lib().vy_ppo_sample(logits.data_ptr(), noise.data_ptr(), B, S, A,
+                                              self.actions[t].data_ptr(), self.logp[t].data_ptr(),
+                                              torch.cuda.current_stream().cuda_stream), "vy_ppo_sample")
+        else:
+            g = -torch.log(-torch.log(noise.clamp_(1e-20, 1.0)))  # Gumbel-max sampling
+            a = torch.argmax(logits + g, dim=-1)
+            lp = torch.log_softmax(logits, dim=-1).gather(-1, a.unsqueeze(-1)).squeeze(-1).sum(-1)
+            self.actions[t].copy_(a)
+            self.logp[t].copy_(lp)
         self.values[t].copy_(v)
         # the env writes the next obs / reward / done straight into the rollout buffers
         self.env.set_outputs(obs=self.obs[t + 1], reward=self.rewards[t], done=self.dones[t])
@@ -200,7 +248,7 @@ class PPOTrainer:
             for g in self.opt.param_groups:
                 g["lr"] = cfg.lr * max(frac, 0.0)
         obs = self.obs[:T].reshape(T * B, -1)
-        act = self.actions.reshape(T * B, -1).long()
+        act = self.actions.reshape(T * B, -1)
         old_lp, old_v = self.logp.reshape(-1), self.values[:T].reshape(-1)
         adv, ret = adv.reshape(-1), ret.reshape(-1)
         n = T * B
@@ -212,9 +260,11 @@ class PPOTrainer:
                 idx = perm[k * mb:(k + 1) * mb]
                 with torch.autocast("cuda", dtype=torch.bfloat16):
                     logits, v = self.net(obs[idx])
-                lsm = torch.log_softmax(logits, dim=-1)
-                lp = lsm.gather(-1, act[idx].unsqueeze(-1)).squeeze(-1).sum(-1)
-                ent = -(lsm.exp() * lsm).sum(-1).sum(-1).mean()
+                if cfg.fused_head:
+                    lp, ent = PolicyHead.apply(logits, act[idx])
+                else:
+                    lp, ent = head_reference(logits, act[idx])
+                ent = ent.mean()
                 a = adv[idx]
                 a = (a - a.mean()) / (a.std() + 1e-8)
                 ratio = torch.exp(lp - old_lp[idx])
@@ -261,4 +311,5 @@ def seconds_per_100k(trainer: PPOTrainer, iters: int, warmup: int = 1) -> dict:
             "seconds": dt, "steps": steps}
 
 
-__all__ = ["PPOConfig", "ActorCritic", "PPOTrainer", "gae", "gae_reference", "seconds_per_100k", "np"]
+__all__ = ["PPOConfig", "ActorCritic", "PPOTrainer", "PolicyHead", "head_reference", "gae", "gae_reference",
+           "seconds_per_100k", "np"]
