@@ -14,6 +14,7 @@
 //   g_lp * lp + g_ent * ent with respect to the logits, each one read of the
 //   [N][S][A] logits (the unfused torch graph made ~10 passes over them).
 //   One warp per sample, lanes over slots.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -42,14 +43,17 @@ __global__ void k_gae(const float* __restrict__ values, const float* __restrict_
   }
 }
 
-// per-slot softmax statistics of A logits: max, log-sum-exp
-__device__ __forceinline__ void slot_lse(const float* __restrict__ z, int A, float& m, float& lse) {
-  m = -INFINITY;
-  for (int k = 0; k < A; ++k) m = fmaxf(m, z[k]);
-  float sum = 0.f;
-  for (int k = 0; k < A; ++k) sum += __expf(z[k] - m);
-  lse = m + __logf(sum);
-}
+// One warp per sample: the sample's S*A logits are staged in shared memory
+// with coalesced loads (float32, or bf16 straight from the autocast GEMM),
+// then lane s owns slot s (slots start A words apart: bank-conflict free for
+// odd A such as the 21-action head), and gradients leave through the same
+// staging row with coalesced stores.
+
+__device__ __forceinline__ float to_f(float v) { return v; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <class T> __device__ __forceinline__ T from_f(float v);
+template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -57,17 +61,39 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-__global__ void k_ppo_sample(const float* __restrict__ logits, const float* __restrict__ noise, int64_t N, int S,
-                             int A, uint8_t* __restrict__ actions, float* __restrict__ logp) {
+// per-slot max and log-sum-exp of A staged logits
+__device__ __forceinline__ void slot_lse(const float* z, int A, float& lse) {
+  float m = -INFINITY;
+  for (int k = 0; k < A; ++k) m = fmaxf(m, z[k]);
+  float sum = 0.f;
+  for (int k = 0; k < A; ++k) sum += __expf(z[k] - m);
+  lse = m + __logf(sum);
+}
+
+template <class T>
+__device__ __forceinline__ float* stage_row(const T* __restrict__ src, int64_t n, int SA, int lane) {
+  extern __shared__ float ppo_smem[];
+  float* row = ppo_smem + (threadIdx.x >> 5) * SA;
+  const T* g = src + n * SA;
+  for (int e = lane; e < SA; e += 32) row[e] = to_f(g[e]);
+  __syncwarp();
+  return row;
+}
+
+template <class T>
+__global__ void k_ppo_sample(const T* __restrict__ logits, const float* __restrict__ noise, int64_t N, int S, int A,
+                             uint8_t* __restrict__ actions, float* __restrict__ logp) {
   const int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (n >= N) return;
+  const int SA = S * A;
+  float* row = stage_row(logits, n, SA, lane);
   float acc = 0.f;
   for (int s = lane; s < S; s += 32) {
-    const float* z = logits + (n * S + s) * A;
+    const float* z = row + s * A;
     const float* u = noise + (n * S + s) * A;
-    float m, lse;
-    slot_lse(z, A, m, lse);
+    float lse;
+    slot_lse(z, A, lse);
     int best = 0;
     float bv = -INFINITY;
     for (int k = 0; k < A; ++k) {
@@ -85,16 +111,18 @@ __global__ void k_ppo_sample(const float* __restrict__ logits, const float* __re
   if (lane == 0) logp[n] = acc;
 }
 
-__global__ void k_ppo_head_fwd(const float* __restrict__ logits, const uint8_t* __restrict__ actions, int64_t N,
-                               int S, int A, float* __restrict__ lp, float* __restrict__ ent) {
+template <class T>
+__global__ void k_ppo_head_fwd(const T* __restrict__ logits, const uint8_t* __restrict__ actions, int64_t N, int S,
+                               int A, float* __restrict__ lp, float* __restrict__ ent) {
   const int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (n >= N) return;
+  float* row = stage_row(logits, n, S * A, lane);
   float alp = 0.f, aent = 0.f;
   for (int s = lane; s < S; s += 32) {
-    const float* z = logits + (n * S + s) * A;
-    float m, lse;
-    slot_lse(z, A, m, lse);
+    const float* z = row + s * A;
+    float lse;
+    slot_lse(z, A, lse);
     float h = 0.f;
     for (int k = 0; k < A; ++k) {
       const float l = z[k] - lse;
@@ -112,56 +140,86 @@ __global__ void k_ppo_head_fwd(const float* __restrict__ logits, const uint8_t* 
 }
 
 // d(g_lp * lp + g_ent * ent) / dz_k = g_lp (1[k = a] - p_k) - g_ent p_k (log p_k + H), H = slot entropy
-__global__ void k_ppo_head_bwd(const float* __restrict__ logits, const uint8_t* __restrict__ actions, int64_t N,
-                               int S, int A, const float* __restrict__ g_lp, const float* __restrict__ g_ent,
-                               float* __restrict__ grad) {
+template <class T>
+__global__ void k_ppo_head_bwd(const T* __restrict__ logits, const uint8_t* __restrict__ actions, int64_t N, int S,
+                               int A, const float* __restrict__ g_lp, const float* __restrict__ g_ent,
+                               T* __restrict__ grad) {
   const int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (n >= N) return;
+  const int SA = S * A;
+  float* row = stage_row(logits, n, SA, lane);
   const float gl = g_lp ? g_lp[n] : 0.f, ge = g_ent ? g_ent[n] : 0.f;
   for (int s = lane; s < S; s += 32) {
-    const float* z = logits + (n * S + s) * A;
-    float* d = grad + (n * S + s) * A;
-    float m, lse;
-    slot_lse(z, A, m, lse);
+    float* z = row + s * A;
+    float lse;
+    slot_lse(z, A, lse);
     float h = 0.f;
     for (int k = 0; k < A; ++k) {
       const float l = z[k] - lse;
       h -= __expf(l) * l;
     }
     const int a = actions[n * S + s];
-    for (int k = 0; k < A; ++k) {
+    for (int k = 0; k < A; ++k) {  // in place: this lane owns the slot's values
       const float l = z[k] - lse, p = __expf(l);
-      d[k] = gl * ((k == a ? 1.f : 0.f) - p) - ge * p * (l + h);
+      z[k] = gl * ((k == a ? 1.f : 0.f) - p) - ge * p * (l + h);
     }
   }
+  __syncwarp();
+  T* d = grad + n * SA;
+  for (int e = lane; e < SA; e += 32) d[e] = from_f<T>(row[e]);
 }
 
 constexpr int kWarpsPerBlock = 8;
 unsigned warp_grid(int64_t N) { return (unsigned)((N + kWarpsPerBlock - 1) / kWarpsPerBlock); }
+size_t row_smem(int S, int A) { return (size_t)kWarpsPerBlock * S * A * sizeof(float); }
 
 }  // namespace
 
-extern "C" int vy_ppo_sample(const float* logits, const float* noise, int64_t N, int32_t S, int32_t A,
-                             uint8_t* actions, float* logp, void* stream) {
-  if (!logits || !noise || !actions || !logp || N < 1 || S < 1 || A < 1 || A > 256) return VY_ERR_ARG;
-  k_ppo_sample<<<warp_grid(N), kWarpsPerBlock * 32, 0, (cudaStream_t)stream>>>(logits, noise, N, S, A, actions,
-                                                                                logp);
+// dtype: 0 = float32 logits (and gradient), 1 = bfloat16
+extern "C" int vy_ppo_sample(const void* logits, int32_t dtype, const float* noise, int64_t N, int32_t S,
+                             int32_t A, uint8_t* actions, float* logp, void* stream) {
+  if (!logits || !noise || !actions || !logp || N < 1 || S < 1 || A < 1 || A > 256 || (dtype != 0 && dtype != 1) ||
+      row_smem(S, A) > 48 * 1024)
+    return VY_ERR_ARG;
+  auto st = (cudaStream_t)stream;
+  if (dtype == 0)
+    k_ppo_sample<float><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
+        static_cast<const float*>(logits), noise, N, S, A, actions, logp);
+  else
+    k_ppo_sample<__nv_bfloat16><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
+        static_cast<const __nv_bfloat16*>(logits), noise, N, S, A, actions, logp);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 
-extern "C" int vy_ppo_head_fwd(const float* logits, const uint8_t* actions, int64_t N, int32_t S, int32_t A,
-                               float* lp, float* ent, void* stream) {
-  if (!logits || !actions || !lp || !ent || N < 1 || S < 1 || A < 1) return VY_ERR_ARG;
-  k_ppo_head_fwd<<<warp_grid(N), kWarpsPerBlock * 32, 0, (cudaStream_t)stream>>>(logits, actions, N, S, A, lp, ent);
+extern "C" int vy_ppo_head_fwd(const void* logits, int32_t dtype, const uint8_t* actions, int64_t N, int32_t S,
+                               int32_t A, float* lp, float* ent, void* stream) {
+  if (!logits || !actions || !lp || !ent || N < 1 || S < 1 || A < 1 || (dtype != 0 && dtype != 1) ||
+      row_smem(S, A) > 48 * 1024)
+    return VY_ERR_ARG;
+  auto st = (cudaStream_t)stream;
+  if (dtype == 0)
+    k_ppo_head_fwd<float><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
+        static_cast<const float*>(logits), actions, N, S, A, lp, ent);
+  else
+    k_ppo_head_fwd<__nv_bfloat16><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
+        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, lp, ent);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 
-extern "C" int vy_ppo_head_bwd(const float* logits, const uint8_t* actions, int64_t N, int32_t S, int32_t A,
-                               const float* g_lp, const float* g_ent, float* grad, void* stream) {
-  if (!logits || !actions || !grad || N < 1 || S < 1 || A < 1) return VY_ERR_ARG;
-  k_ppo_head_bwd<<<warp_grid(N), kWarpsPerBlock * 32, 0, (cudaStream_t)stream>>>(logits, actions, N, S, A, g_lp,
-                                                                                 g_ent, grad);
+extern "C" int vy_ppo_head_bwd(const void* logits, int32_t dtype, const uint8_t* actions, int64_t N, int32_t S,
+                               int32_t A, const float* g_lp, const float* g_ent, void* grad, void* stream) {
+  if (!logits || !actions || !grad || N < 1 || S < 1 || A < 1 || (dtype != 0 && dtype != 1) ||
+      row_smem(S, A) > 48 * 1024)
+    return VY_ERR_ARG;
+  auto st = (cudaStream_t)stream;
+  if (dtype == 0)
+    k_ppo_head_bwd<float><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
+        static_cast<const float*>(logits), actions, N, S, A, g_lp, g_ent, static_cast<float*>(grad));
+  else
+    k_ppo_head_bwd<__nv_bfloat16><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
+        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, g_lp, g_ent,
+        static_cast<__nv_bfloat16*>(grad));
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 

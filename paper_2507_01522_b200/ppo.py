@@ -77,9 +77,19 @@ class ActorCritic(nn.Module):
                                     _ortho(nn.Linear(hidden, hidden), g), nn.Tanh(),
                                     _ortho(nn.Linear(hidden, 1), 1.0))
 
-    def forward(self, obs: torch.Tensor):
-        logits = self.actor(obs).view(-1, self.n_slots, self.n_actions).float()
+    def forward(self, obs: torch.Tensor, logits_fp32: bool = True):
+        logits = self.actor(obs).view(-1, self.n_slots, self.n_actions)
+        if logits_fp32:  # the fused head kernels read the autocast GEMM's bf16 output directly
+            logits = logits.float()
         return logits, self.critic(obs).squeeze(-1).float()
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return 0
+    if t.dtype == torch.bfloat16:
+        return 1
+    raise TypeError(f"logits must be float32 or bfloat16, got {t.dtype}")
 
 
 class PolicyHead(torch.autograd.Function):
@@ -93,8 +103,8 @@ class PolicyHead(torch.autograd.Function):
         N, S, A = logits.shape
         lp = torch.empty(N, device=logits.device)
         ent = torch.empty(N, device=logits.device)
-        nat.check(nat.lib().vy_ppo_head_fwd(logits.data_ptr(), actions.data_ptr(), N, S, A, lp.data_ptr(),
-                                            ent.data_ptr(), torch.cuda.current_stream().cuda_stream),
+        nat.check(nat.lib().vy_ppo_head_fwd(logits.data_ptr(), _dtype_code(logits), actions.data_ptr(), N, S, A,
+                                            lp.data_ptr(), ent.data_ptr(), torch.cuda.current_stream().cuda_stream),
                   "vy_ppo_head_fwd")
         ctx.save_for_backward(logits, actions)
         return lp, ent
@@ -106,7 +116,7 @@ class PolicyHead(torch.autograd.Function):
         grad = torch.empty_like(logits)
         g_lp = g_lp.contiguous() if g_lp is not None else None
         g_ent = g_ent.contiguous() if g_ent is not None else None
-        nat.check(nat.lib().vy_ppo_head_bwd(logits.data_ptr(), actions.data_ptr(), N, S, A,
+        nat.check(nat.lib().vy_ppo_head_bwd(logits.data_ptr(), _dtype_code(logits), actions.data_ptr(), N, S, A,
                                             g_lp.data_ptr() if g_lp is not None else None,
                                             g_ent.data_ptr() if g_ent is not None else None, grad.data_ptr(),
                                             torch.cuda.current_stream().cuda_stream), "vy_ppo_head_bwd")
@@ -177,13 +187,15 @@ class PPOTrainer:
     # -- rollout -----------------------------------------------------------------
 
     def _policy_step(self, t: int) -> None:
+        fused = self.cfg.fused_head
         with torch.autocast("cuda", dtype=torch.bfloat16):
-            logits, v = self.net(self.obs[t])
-        noise = torch.rand_like(logits)
-        if self.cfg.fused_head:
+            logits, v = self.net(self.obs[t], logits_fp32=not fused)
+        noise = torch.rand(logits.shape, device=logits.device)
+        if fused:
             # Gumbel-max sampling + log-probability in one kernel, straight into the rollout buffers
+            logits = logits.contiguous()
             B, S, A = logits.shape
-            nat.check(nat.lib().vy_ppo_sample(logits.data_ptr(), noise.data_ptr(), B, S, A,
+            nat.check(nat.lib().vy_ppo_sample(logits.data_ptr(), _dtype_code(logits), noise.data_ptr(), B, S, A,
                                               self.actions[t].data_ptr(), self.logp[t].data_ptr(),
                                               torch.cuda.current_stream().cuda_stream), "vy_ppo_sample")
         else:
@@ -259,7 +271,7 @@ class PPOTrainer:
             for k in range(cfg.n_minibatches):
                 idx = perm[k * mb:(k + 1) * mb]
                 with torch.autocast("cuda", dtype=torch.bfloat16):
-                    logits, v = self.net(obs[idx])
+                    logits, v = self.net(obs[idx], logits_fp32=not cfg.fused_head)
                 if cfg.fused_head:
                     lp, ent = PolicyHead.apply(logits, act[idx])
                 else:

@@ -132,9 +132,31 @@ def test_fused_sampler_is_gumbel_max():
     u = torch.rand(N, S, A, device="cuda", generator=g)
     act = torch.empty(N, S, dtype=torch.uint8, device="cuda")
     lp = torch.empty(N, device="cuda")
-    nat.check(nat.lib().vy_ppo_sample(z.data_ptr(), u.data_ptr(), N, S, A, act.data_ptr(), lp.data_ptr(),
+    nat.check(nat.lib().vy_ppo_sample(z.data_ptr(), 0, u.data_ptr(), N, S, A, act.data_ptr(), lp.data_ptr(),
                                       torch.cuda.current_stream().cuda_stream), "vy_ppo_sample")
     ref = torch.argmax(z - torch.log(-torch.log(u.clamp(1e-20, 1.0))), dim=-1)
     assert (act.long() == ref).float().mean() > 0.9999  # fast-math log may flip exact near-ties only
     lp_r = torch.log_softmax(z, -1).gather(-1, act.long().unsqueeze(-1)).squeeze(-1).sum(-1)
     torch.testing.assert_close(lp, lp_r, rtol=1e-5, atol=1e-4)
+
+
+def test_fused_policy_head_bf16_logits():
+    """bf16 logits (the autocast GEMM output) go straight into the head: the
+    result equals the fp32 head on the upcast logits; the gradient comes back
+    in bf16 (what autograd's cast would have produced from the fp32 one)."""
+    from paper_2507_01522_b200.ppo import PolicyHead
+
+    g = torch.Generator(device="cuda").manual_seed(2)
+    N, S, A = 3000, 17, 21
+    zb = (torch.randn(N, S, A, device="cuda", generator=g) * 3).to(torch.bfloat16).requires_grad_(True)
+    zf = zb.detach().float().requires_grad_(True)
+    a = torch.randint(0, A, (N, S), device="cuda", generator=g).to(torch.uint8)
+    w1, w2 = torch.randn(N, device="cuda", generator=g), torch.randn(N, device="cuda", generator=g)
+    lpb, entb = PolicyHead.apply(zb, a)
+    (lpb * w1 + entb * w2).sum().backward()
+    lpf, entf = PolicyHead.apply(zf, a)
+    (lpf * w1 + entf * w2).sum().backward()
+    torch.testing.assert_close(lpb, lpf, rtol=0, atol=0)
+    torch.testing.assert_close(entb, entf, rtol=0, atol=0)
+    assert zb.grad.dtype == torch.bfloat16
+    torch.testing.assert_close(zb.grad, zf.grad.to(torch.bfloat16), rtol=0, atol=0)
