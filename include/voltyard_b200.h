@@ -231,20 +231,22 @@ int vy_set_tiles_per_warp(vy_handle *h, int32_t k);
 int vy_gae(const float *values, const float *rewards, const uint8_t *dones, const float *last_value, int32_t T,
            int64_t B, float gamma, float lam, float *adv, float *ret, void *stream);
 
-/* PPO head kernels (config C3), one warp per sample over [N][S][A] logits
- * (S slots of A actions; dtype 0 = float32, 1 = bfloat16):
- * vy_ppo_sample   Gumbel-max action per slot from `noise` ~ U[0,1) float32 of
- *                 the same shape -> actions uint8 [N][S], log-probability
- *                 float32 [N];
+/* PPO head kernels (config C3), one warp per sample over logits rows of S
+ * slots x A actions (dtype 0 = float32, 1 = bfloat16; row n starts at element
+ * n*ld, ld >= S*A, so a GEMM output padded to an aligned width is read in
+ * place):
+ * vy_ppo_sample   Gumbel-max action per slot from `noise` ~ U[0,1) float32
+ *                 [N][S][A] -> actions uint8 [N][S], log-probability float32 [N];
  * vy_ppo_head_fwd log-probability of `actions` and entropy, summed over slots;
- * vy_ppo_head_bwd gradient (logits' dtype) of g_lp*lp + g_ent*ent w.r.t. the
- *                 logits (either upstream gradient may be NULL = 0). */
-int vy_ppo_sample(const void *logits, int32_t dtype, const float *noise, int64_t N, int32_t S, int32_t A,
+ * vy_ppo_head_bwd gradient (logits' dtype and row stride, padding columns 0)
+ *                 of g_lp*lp + g_ent*ent w.r.t. the logits (either upstream
+ *                 gradient may be NULL = 0). */
+int vy_ppo_sample(const void *logits, int32_t dtype, int64_t ld, const float *noise, int64_t N, int32_t S, int32_t A,
                   uint8_t *actions, float *logp, void *stream);
-int vy_ppo_head_fwd(const void *logits, int32_t dtype, const uint8_t *actions, int64_t N, int32_t S, int32_t A,
-                    float *lp, float *ent, void *stream);
-int vy_ppo_head_bwd(const void *logits, int32_t dtype, const uint8_t *actions, int64_t N, int32_t S, int32_t A,
-                    const float *g_lp, const float *g_ent, void *grad, void *stream);
+int vy_ppo_head_fwd(const void *logits, int32_t dtype, int64_t ld, const uint8_t *actions, int64_t N, int32_t S,
+                    int32_t A, float *lp, float *ent, void *stream);
+int vy_ppo_head_bwd(const void *logits, int32_t dtype, int64_t ld, const uint8_t *actions, int64_t N, int32_t S,
+                    int32_t A, const float *g_lp, const float *g_ent, void *grad, void *stream);
 
 /* Diagnostics: compare the kernels' reciprocal-based division (div_rcp in
  * csrc/vy_device.cuh) with IEEE x / d on `samples_per_divisor` random

@@ -71,10 +71,10 @@ __device__ __forceinline__ void slot_lse(const float* z, int A, float& lse) {
 }
 
 template <class T>
-__device__ __forceinline__ float* stage_row(const T* __restrict__ src, int64_t n, int SA, int lane) {
+__device__ __forceinline__ float* stage_row(const T* __restrict__ src, int64_t n, int SA, int64_t ld, int lane) {
   extern __shared__ float ppo_smem[];
   float* row = ppo_smem + (threadIdx.x >> 5) * SA;
-  const T* g = src + n * SA;
+  const T* g = src + n * ld;
   for (int e = lane; e < SA; e += 32) row[e] = to_f(g[e]);
   __syncwarp();
   return row;
@@ -82,12 +82,12 @@ __device__ __forceinline__ float* stage_row(const T* __restrict__ src, int64_t n
 
 template <class T>
 __global__ void k_ppo_sample(const T* __restrict__ logits, const float* __restrict__ noise, int64_t N, int S, int A,
-                             uint8_t* __restrict__ actions, float* __restrict__ logp) {
+                             int64_t ld, uint8_t* __restrict__ actions, float* __restrict__ logp) {
   const int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (n >= N) return;
   const int SA = S * A;
-  float* row = stage_row(logits, n, SA, lane);
+  float* row = stage_row(logits, n, SA, ld, lane);
   float acc = 0.f;
   for (int s = lane; s < S; s += 32) {
     const float* z = row + s * A;
@@ -113,11 +113,11 @@ __global__ void k_ppo_sample(const T* __restrict__ logits, const float* __restri
 
 template <class T>
 __global__ void k_ppo_head_fwd(const T* __restrict__ logits, const uint8_t* __restrict__ actions, int64_t N, int S,
-                               int A, float* __restrict__ lp, float* __restrict__ ent) {
+                               int A, int64_t ld, float* __restrict__ lp, float* __restrict__ ent) {
   const int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (n >= N) return;
-  float* row = stage_row(logits, n, S * A, lane);
+  float* row = stage_row(logits, n, S * A, ld, lane);
   float alp = 0.f, aent = 0.f;
   for (int s = lane; s < S; s += 32) {
     const float* z = row + s * A;
@@ -142,13 +142,13 @@ __global__ void k_ppo_head_fwd(const T* __restrict__ logits, const uint8_t* __re
 // d(g_lp * lp + g_ent * ent) / dz_k = g_lp (1[k = a] - p_k) - g_ent p_k (log p_k + H), H = slot entropy
 template <class T>
 __global__ void k_ppo_head_bwd(const T* __restrict__ logits, const uint8_t* __restrict__ actions, int64_t N, int S,
-                               int A, const float* __restrict__ g_lp, const float* __restrict__ g_ent,
+                               int A, int64_t ld, const float* __restrict__ g_lp, const float* __restrict__ g_ent,
                                T* __restrict__ grad) {
   const int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (n >= N) return;
   const int SA = S * A;
-  float* row = stage_row(logits, n, SA, lane);
+  float* row = stage_row(logits, n, SA, ld, lane);
   const float gl = g_lp ? g_lp[n] : 0.f, ge = g_ent ? g_ent[n] : 0.f;
   for (int s = lane; s < S; s += 32) {
     float* z = row + s * A;
@@ -166,8 +166,8 @@ __global__ void k_ppo_head_bwd(const T* __restrict__ logits, const uint8_t* __re
     }
   }
   __syncwarp();
-  T* d = grad + n * SA;
-  for (int e = lane; e < SA; e += 32) d[e] = from_f<T>(row[e]);
+  T* d = grad + n * ld;
+  for (int e = lane; e < ld; e += 32) d[e] = from_f<T>(e < SA ? row[e] : 0.f);  // padding columns: 0
 }
 
 constexpr int kWarpsPerBlock = 8;
@@ -177,48 +177,48 @@ size_t row_smem(int S, int A) { return (size_t)kWarpsPerBlock * S * A * sizeof(f
 }  // namespace
 
 // dtype: 0 = float32 logits (and gradient), 1 = bfloat16
-extern "C" int vy_ppo_sample(const void* logits, int32_t dtype, const float* noise, int64_t N, int32_t S,
+extern "C" int vy_ppo_sample(const void* logits, int32_t dtype, int64_t ld, const float* noise, int64_t N, int32_t S,
                              int32_t A, uint8_t* actions, float* logp, void* stream) {
   if (!logits || !noise || !actions || !logp || N < 1 || S < 1 || A < 1 || A > 256 || (dtype != 0 && dtype != 1) ||
-      row_smem(S, A) > 48 * 1024)
+      row_smem(S, A) > 48 * 1024 || ld < (int64_t)S * A)
     return VY_ERR_ARG;
   auto st = (cudaStream_t)stream;
   if (dtype == 0)
     k_ppo_sample<float><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
-        static_cast<const float*>(logits), noise, N, S, A, actions, logp);
+        static_cast<const float*>(logits), noise, N, S, A, ld, actions, logp);
   else
     k_ppo_sample<__nv_bfloat16><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
-        static_cast<const __nv_bfloat16*>(logits), noise, N, S, A, actions, logp);
+        static_cast<const __nv_bfloat16*>(logits), noise, N, S, A, ld, actions, logp);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 
-extern "C" int vy_ppo_head_fwd(const void* logits, int32_t dtype, const uint8_t* actions, int64_t N, int32_t S,
-                               int32_t A, float* lp, float* ent, void* stream) {
+extern "C" int vy_ppo_head_fwd(const void* logits, int32_t dtype, int64_t ld, const uint8_t* actions, int64_t N,
+                               int32_t S, int32_t A, float* lp, float* ent, void* stream) {
   if (!logits || !actions || !lp || !ent || N < 1 || S < 1 || A < 1 || (dtype != 0 && dtype != 1) ||
-      row_smem(S, A) > 48 * 1024)
+      row_smem(S, A) > 48 * 1024 || ld < (int64_t)S * A)
     return VY_ERR_ARG;
   auto st = (cudaStream_t)stream;
   if (dtype == 0)
     k_ppo_head_fwd<float><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
-        static_cast<const float*>(logits), actions, N, S, A, lp, ent);
+        static_cast<const float*>(logits), actions, N, S, A, ld, lp, ent);
   else
     k_ppo_head_fwd<__nv_bfloat16><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
-        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, lp, ent);
+        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, lp, ent);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 
-extern "C" int vy_ppo_head_bwd(const void* logits, int32_t dtype, const uint8_t* actions, int64_t N, int32_t S,
-                               int32_t A, const float* g_lp, const float* g_ent, void* grad, void* stream) {
+extern "C" int vy_ppo_head_bwd(const void* logits, int32_t dtype, int64_t ld, const uint8_t* actions, int64_t N,
+                               int32_t S, int32_t A, const float* g_lp, const float* g_ent, void* grad, void* stream) {
   if (!logits || !actions || !grad || N < 1 || S < 1 || A < 1 || (dtype != 0 && dtype != 1) ||
-      row_smem(S, A) > 48 * 1024)
+      row_smem(S, A) > 48 * 1024 || ld < (int64_t)S * A)
     return VY_ERR_ARG;
   auto st = (cudaStream_t)stream;
   if (dtype == 0)
     k_ppo_head_bwd<float><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
-        static_cast<const float*>(logits), actions, N, S, A, g_lp, g_ent, static_cast<float*>(grad));
+        static_cast<const float*>(logits), actions, N, S, A, ld, g_lp, g_ent, static_cast<float*>(grad));
   else
     k_ppo_head_bwd<__nv_bfloat16><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
-        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, g_lp, g_ent,
+        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, g_lp, g_ent,
         static_cast<__nv_bfloat16*>(grad));
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }

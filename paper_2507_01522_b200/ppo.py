@@ -65,23 +65,42 @@ def _ortho(layer: nn.Linear, gain: float) -> nn.Linear:
     return layer
 
 
+def _ceil8(x: int) -> int:
+    return (x + 7) // 8 * 8
+
+
 class ActorCritic(nn.Module):
+    """Actor-critic MLP.  The observation width (6n+9, odd) and the head width
+    (S*A = 357) are padded to multiples of 8 — zero input columns, unused
+    output columns — so the bf16 GEMMs have 16-byte aligned rows (cuBLAS
+    otherwise falls back to sm75 kernels, 3-7x slower at these shapes,
+    scripts/micro/gemm_align.py)."""
+
     def __init__(self, obs_dim: int, n_slots: int, n_actions: int, hidden: int = 64):
         super().__init__()
         self.n_slots, self.n_actions = n_slots, n_actions
+        self.obs_dim, self.in_dim = obs_dim, _ceil8(obs_dim)
+        self.n_out, self.out_dim = n_slots * n_actions, _ceil8(n_slots * n_actions)
         g = math.sqrt(2.0)
-        self.actor = nn.Sequential(_ortho(nn.Linear(obs_dim, hidden), g), nn.Tanh(),
+        self.actor = nn.Sequential(_ortho(nn.Linear(self.in_dim, hidden), g), nn.Tanh(),
                                    _ortho(nn.Linear(hidden, hidden), g), nn.Tanh(),
-                                   _ortho(nn.Linear(hidden, n_slots * n_actions), 0.01))
-        self.critic = nn.Sequential(_ortho(nn.Linear(obs_dim, hidden), g), nn.Tanh(),
+                                   _ortho(nn.Linear(hidden, self.out_dim), 0.01))
+        self.critic = nn.Sequential(_ortho(nn.Linear(self.in_dim, hidden), g), nn.Tanh(),
                                     _ortho(nn.Linear(hidden, hidden), g), nn.Tanh(),
                                     _ortho(nn.Linear(hidden, 1), 1.0))
 
+    def pad_obs(self, obs: torch.Tensor) -> torch.Tensor:
+        w = obs.shape[-1]
+        return obs if w == self.in_dim else nn.functional.pad(obs, (0, self.in_dim - w))
+
     def forward(self, obs: torch.Tensor, logits_fp32: bool = True):
-        logits = self.actor(obs).view(-1, self.n_slots, self.n_actions)
-        if logits_fp32:  # the fused head kernels read the autocast GEMM's bf16 output directly
-            logits = logits.float()
-        return logits, self.critic(obs).squeeze(-1).float()
+        """-> (logits, value).  logits_fp32: float32 [M, S, A] (torch head);
+        else the raw padded head output [M, out_dim] (autocast dtype) that the
+        fused head kernels read in place with row stride out_dim."""
+        x = self.pad_obs(obs)
+        out = self.actor(x)
+        logits = out[:, : self.n_out].float().view(-1, self.n_slots, self.n_actions) if logits_fp32 else out
+        return logits, self.critic(x).squeeze(-1).float()
 
 
 def _dtype_code(t: torch.Tensor) -> int:
@@ -94,33 +113,38 @@ def _dtype_code(t: torch.Tensor) -> int:
 
 class PolicyHead(torch.autograd.Function):
     """Per-sample log-probability of stored multi-discrete actions and entropy
-    (both summed over slots) from float32 logits [N, S, A]: vy_ppo_head_fwd /
-    vy_ppo_head_bwd, one pass over the logits each way."""
+    (both summed over slots) from logits rows of S x A values (float32 or
+    bf16; row n starts at n * logits.stride(0), so the padded head output is
+    read in place): vy_ppo_head_fwd / vy_ppo_head_bwd, one pass each way."""
 
     @staticmethod
-    def forward(ctx, logits: torch.Tensor, actions: torch.Tensor):
-        logits = logits.contiguous()
-        N, S, A = logits.shape
+    def forward(ctx, logits: torch.Tensor, actions: torch.Tensor, S: int, A: int):
+        N = logits.shape[0]
+        ld = logits.stride(0)
+        if logits.stride(-1) != 1 or logits[0].numel() < S * A or (logits.dim() > 2 and not logits[0].is_contiguous()):
+            raise ValueError("logits rows must be contiguous with at least S*A values")
         lp = torch.empty(N, device=logits.device)
         ent = torch.empty(N, device=logits.device)
-        nat.check(nat.lib().vy_ppo_head_fwd(logits.data_ptr(), _dtype_code(logits), actions.data_ptr(), N, S, A,
+        nat.check(nat.lib().vy_ppo_head_fwd(logits.data_ptr(), _dtype_code(logits), ld, actions.data_ptr(), N, S, A,
                                             lp.data_ptr(), ent.data_ptr(), torch.cuda.current_stream().cuda_stream),
                   "vy_ppo_head_fwd")
         ctx.save_for_backward(logits, actions)
+        ctx.S, ctx.A = S, A
         return lp, ent
 
     @staticmethod
     def backward(ctx, g_lp, g_ent):
         logits, actions = ctx.saved_tensors
-        N, S, A = logits.shape
+        N, S, A = logits.shape[0], ctx.S, ctx.A
         grad = torch.empty_like(logits)
         g_lp = g_lp.contiguous() if g_lp is not None else None
         g_ent = g_ent.contiguous() if g_ent is not None else None
-        nat.check(nat.lib().vy_ppo_head_bwd(logits.data_ptr(), _dtype_code(logits), actions.data_ptr(), N, S, A,
+        nat.check(nat.lib().vy_ppo_head_bwd(logits.data_ptr(), _dtype_code(logits), logits.stride(0),
+                                            actions.data_ptr(), N, S, A,
                                             g_lp.data_ptr() if g_lp is not None else None,
                                             g_ent.data_ptr() if g_ent is not None else None, grad.data_ptr(),
                                             torch.cuda.current_stream().cuda_stream), "vy_ppo_head_bwd")
-        return grad, None
+        return grad, None, None, None
 
 
 def head_reference(logits: torch.Tensor, actions: torch.Tensor):
@@ -190,12 +214,12 @@ class PPOTrainer:
         fused = self.cfg.fused_head
         with torch.autocast("cuda", dtype=torch.bfloat16):
             logits, v = self.net(self.obs[t], logits_fp32=not fused)
-        noise = torch.rand(logits.shape, device=logits.device)
+        noise = torch.rand(logits.shape[0], self.net.n_slots, self.net.n_actions, device=logits.device)
         if fused:
             # Gumbel-max sampling + log-probability in one kernel, straight into the rollout buffers
-            logits = logits.contiguous()
-            B, S, A = logits.shape
-            nat.check(nat.lib().vy_ppo_sample(logits.data_ptr(), _dtype_code(logits), noise.data_ptr(), B, S, A,
+            B, S, A = logits.shape[0], self.net.n_slots, self.net.n_actions
+            nat.check(nat.lib().vy_ppo_sample(logits.data_ptr(), _dtype_code(logits), logits.stride(0),
+                                              noise.data_ptr(), B, S, A,
                                               self.actions[t].data_ptr(), self.logp[t].data_ptr(),
                                               torch.cuda.current_stream().cuda_stream), "vy_ppo_sample")
         else:
@@ -259,7 +283,7 @@ class PPOTrainer:
             frac = 1.0 - self.iterations / self.n_iters
             for g in self.opt.param_groups:
                 g["lr"] = cfg.lr * max(frac, 0.0)
-        obs = self.obs[:T].reshape(T * B, -1)
+        obs = self.net.pad_obs(self.obs[:T].reshape(T * B, -1))  # aligned rows once; minibatches gather them
         act = self.actions.reshape(T * B, -1)
         old_lp, old_v = self.logp.reshape(-1), self.values[:T].reshape(-1)
         adv, ret = adv.reshape(-1), ret.reshape(-1)
@@ -273,7 +297,7 @@ class PPOTrainer:
                 with torch.autocast("cuda", dtype=torch.bfloat16):
                     logits, v = self.net(obs[idx], logits_fp32=not cfg.fused_head)
                 if cfg.fused_head:
-                    lp, ent = PolicyHead.apply(logits, act[idx])
+                    lp, ent = PolicyHead.apply(logits, act[idx], self.net.n_slots, self.net.n_actions)
                 else:
                     lp, ent = head_reference(logits, act[idx])
                 ent = ent.mean()

@@ -110,7 +110,7 @@ def test_fused_policy_head_matches_torch_fp32():
     z = (torch.randn(N, S, A, device="cuda", generator=g) * 3).requires_grad_(True)
     a = torch.randint(0, A, (N, S), device="cuda", generator=g).to(torch.uint8)
     w1, w2 = torch.randn(N, device="cuda", generator=g), torch.randn(N, device="cuda", generator=g)
-    lp, ent = PolicyHead.apply(z, a)
+    lp, ent = PolicyHead.apply(z, a, S, A)
     (lp * w1 + ent * w2).sum().backward()
     gz = z.grad.clone()
     z.grad = None
@@ -132,7 +132,7 @@ def test_fused_sampler_is_gumbel_max():
     u = torch.rand(N, S, A, device="cuda", generator=g)
     act = torch.empty(N, S, dtype=torch.uint8, device="cuda")
     lp = torch.empty(N, device="cuda")
-    nat.check(nat.lib().vy_ppo_sample(z.data_ptr(), 0, u.data_ptr(), N, S, A, act.data_ptr(), lp.data_ptr(),
+    nat.check(nat.lib().vy_ppo_sample(z.data_ptr(), 0, S * A, u.data_ptr(), N, S, A, act.data_ptr(), lp.data_ptr(),
                                       torch.cuda.current_stream().cuda_stream), "vy_ppo_sample")
     ref = torch.argmax(z - torch.log(-torch.log(u.clamp(1e-20, 1.0))), dim=-1)
     assert (act.long() == ref).float().mean() > 0.9999  # fast-math log may flip exact near-ties only
@@ -152,11 +152,31 @@ def test_fused_policy_head_bf16_logits():
     zf = zb.detach().float().requires_grad_(True)
     a = torch.randint(0, A, (N, S), device="cuda", generator=g).to(torch.uint8)
     w1, w2 = torch.randn(N, device="cuda", generator=g), torch.randn(N, device="cuda", generator=g)
-    lpb, entb = PolicyHead.apply(zb, a)
+    lpb, entb = PolicyHead.apply(zb, a, S, A)
     (lpb * w1 + entb * w2).sum().backward()
-    lpf, entf = PolicyHead.apply(zf, a)
+    lpf, entf = PolicyHead.apply(zf, a, S, A)
     (lpf * w1 + entf * w2).sum().backward()
     torch.testing.assert_close(lpb, lpf, rtol=0, atol=0)
     torch.testing.assert_close(entb, entf, rtol=0, atol=0)
     assert zb.grad.dtype == torch.bfloat16
     torch.testing.assert_close(zb.grad, zf.grad.to(torch.bfloat16), rtol=0, atol=0)
+
+
+def test_fused_policy_head_padded_rows():
+    """Logits read in place from a GEMM output padded to an aligned width: the
+    same values as the packed rows, zero gradient in the padding columns."""
+    from paper_2507_01522_b200.ppo import PolicyHead
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    N, S, A, W = 2000, 17, 21, 360
+    full = (torch.randn(N, W, device="cuda", generator=g)).to(torch.bfloat16).requires_grad_(True)
+    packed = full.detach()[:, : S * A].contiguous().requires_grad_(True)
+    a = torch.randint(0, A, (N, S), device="cuda", generator=g).to(torch.uint8)
+    w1 = torch.randn(N, device="cuda", generator=g)
+    lp1, e1 = PolicyHead.apply(full, a, S, A)
+    (lp1 * w1 + e1).sum().backward()
+    lp2, e2 = PolicyHead.apply(packed, a, S, A)
+    (lp2 * w1 + e2).sum().backward()
+    torch.testing.assert_close(lp1, lp2, rtol=0, atol=0)
+    torch.testing.assert_close(full.grad[:, : S * A], packed.grad, rtol=0, atol=0)
+    assert (full.grad[:, S * A:] == 0).all()
