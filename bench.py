@@ -382,7 +382,8 @@ def main() -> None:
                          "env_steps_per_s": res["env_steps_per_s"], "envs_per_gpu": 4096,
                          "rollout_steps": cfg.rollout_steps, "epochs": cfg.update_epochs,
                          "minibatches": cfg.n_minibatches, "hidden": cfg.hidden, "timed_iterations": args.ppo_iters,
-                         "rollout": "CUDA graph (policy fwd bf16 + Gumbel-max sampling + k_step) x 300",
+                         "rollout": "CUDA graph (policy fwd bf16 + vy_ppo_sample Gumbel-max kernel + k_step) x 300",
+                         "update": "bf16 GEMMs at 8-aligned widths + vy_ppo_head_fwd/_bwd fused log-prob/entropy head",
                          "grad_allreduce": "NCCL all_reduce(AVG) per minibatch" if world > 1 else "none (1 GPU)",
                          "paper_reference": "Chargax PPO(16) 0.65 s / 100k on RTX 4000 Ada (PAPER.md:239)"}
         penv.close()
