@@ -211,6 +211,45 @@ def test_rollout_kernel_equals_stepwise():
     b.close()
 
 
+def test_rollout_equals_stepwise_large_tree_lean():
+    """Lean instantiations for a large capacity tree (mode 2, nested splitters):
+    the fused rollout equals single steps, and a scattered subset of the
+    single-step trajectory equals the CPU oracle."""
+    from paper_2507_01522_b200 import EnvConfig
+    from paper_2507_01522_b200.batch import BatchEnv, DeviceRandomPolicy
+    from paper_2507_01522_b200.exogenous import generate_synthetic_defaults
+    from paper_2507_01522_b200.station import preset_station
+
+    cfg = EnvConfig()
+    st = preset_station("nested_splitters", 4, 12)
+    ds = generate_synthetic_defaults("highway", "high", "eu", seed=0, days=30)
+    B, T, master, pseed = 3072, 300, 4, 6
+    a = BatchEnv(cfg, st, ds, batch_size=B, master_seed=master)
+    b = BatchEnv(cfg, st, ds, batch_size=B, master_seed=master)
+    a.reset(as_numpy=False)
+    b.reset(as_numpy=False)
+    pol = DeviceRandomPolicy(pseed, a.n_ports, cfg.discretization_k)
+    pol.bind(range(B))
+    rows = [0, 31, 32, 1000, B - 1]
+    obs_s, rew_s = [], []
+    for _ in range(T):
+        o, r, _, _ = a.step(pol.actions(a), collect_infos=False)
+        assert a.last_step_mode() == 2
+        obs_s.append(o.clone())
+        rew_s.append(r.clone())
+    obs_r = torch.empty(T, B, b.obs_length, device="cuda")
+    rew_r = torch.empty(T, B, device="cuda")
+    done_r = torch.empty(T, B, dtype=torch.uint8, device="cuda")
+    b.rollout(T, pseed, 0, obs_r, rew_r, done_r)
+    torch.testing.assert_close(obs_r, torch.stack(obs_s), rtol=0, atol=0)
+    torch.testing.assert_close(rew_r, torch.stack(rew_s), rtol=0, atol=0)
+    ref_obs, ref_r, _ = _oracle_subset(a.tables, B, master, rows, pseed, T, cfg.episode_steps)
+    np.testing.assert_array_equal(torch.stack(obs_s)[:, rows].cpu().numpy(), ref_obs[1:].astype(np.float32))
+    np.testing.assert_array_equal(torch.stack(rew_s)[:, rows].cpu().numpy(), ref_r.astype(np.float32))
+    a.close()
+    b.close()
+
+
 def test_injected_draws_reproduce_reference_stream():
     """Arrival draws replayed on the host (the reference's own recipe,
     tests/test_env.py:251-278) and injected through vy_draws give the same
