@@ -1,7 +1,8 @@
 """k_step throughput across station configurations (profiles/r1_configs.json).
 
 Not the headline bench (bench.py measures config C2); this records how the
-single generic kernel scales with station size: the default 16-port station,
+step kernel scales with station size, each timed over one whole 288-step day
+(mean of per-step CUDA events, like bench.py): the default 16-port station,
 the config-C4 station (64 DC ports, 3-level splitter tree, battery, highway /
 high traffic, satisfaction penalties), and a small single-node station.
 """
@@ -18,29 +19,30 @@ from paper_2507_01522_b200.batch import BatchEnv, DeviceRandomPolicy  # noqa: E4
 from bench import algorithmic_bytes, load_peaks  # noqa: E402
 
 
-def measure(name, cfg, station, ds, B, steps=20):
+def measure(name, cfg, station, ds, B, steps=288):
     env = BatchEnv(cfg, station, ds, batch_size=B)
     pol = DeviceRandomPolicy(0, env.n_ports, cfg.discretization_k)
     pol.bind(range(B))
     env.reset(as_numpy=False)
-    for _ in range(3):
+    for _ in range(5):
         env.step(pol.actions(env), collect_infos=False)
-    ts = []
+    ev = []
     for _ in range(steps):
         a = pol.actions(env)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         env.step(a, collect_infos=False)
         e.record()
-        torch.cuda.synchronize()
-        ts.append(s.elapsed_time(e))
-    ms = sorted(ts)[len(ts) // 2]
+        ev.append((s, e))
+    torch.cuda.synchronize()
+    ms = sum(s.elapsed_time(e) for s, e in ev) / len(ev)
+    mode = env.last_step_mode()
     ab = algorithmic_bytes(env.tables)["per_env_step"]
     gbs = ab * B / (ms / 1e3) / 1e9
     env.close()
     return {"config": name, "n_ports": station.n_ports, "obs_len": env.obs_length, "envs": B, "k_step_ms": ms,
             "env_steps_per_s": B / (ms / 1e3), "bytes_per_env_step": ab, "achieved_gbs": gbs,
-            "hbm_frac": gbs / load_peaks()["hbm_gbs"]}
+            "hbm_frac": gbs / load_peaks()["hbm_gbs"], "kernel_mode": mode, "steps": steps}
 
 
 def main():
