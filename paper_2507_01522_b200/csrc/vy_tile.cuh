@@ -1031,10 +1031,11 @@ __device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const 
     for (int r = 0; r < rows; ++r) {
       const uint32_t a = lbase + r * 4;
       const float v0 = lds_f32(a), v1 = lds_f32(a + 4224), v2 = lds_f32(a + 8448);
-      g[0] = v0;
-      g[32] = v1;
-      g[64] = v2;
-      if (p3) g[96] = lds_f32(a + 12672);
+      // streaming stores (evict-first): obs are not re-read by the kernel
+      __stcs(g, v0);
+      __stcs(g + 32, v1);
+      __stcs(g + 64, v2);
+      if (p3) __stcs(g + 96, lds_f32(a + 12672));
       g += OL;
     }
   } else if (OL <= 128) {
@@ -1047,10 +1048,10 @@ __device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const 
       const float v1 = p1 ? lds_f32(a + 4224) : 0.f;
       const float v2 = p2 ? lds_f32(a + 8448) : 0.f;
       const float v3 = p3 ? lds_f32(a + 12672) : 0.f;
-      if (p0) g[0] = v0;
-      if (p1) g[32] = v1;
-      if (p2) g[64] = v2;
-      if (p3) g[96] = v3;
+      if (p0) __stcs(g, v0);
+      if (p1) __stcs(g + 32, v1);
+      if (p2) __stcs(g + 64, v2);
+      if (p3) __stcs(g + 96, v3);
       g += OL;
     }
   } else {
@@ -1058,7 +1059,7 @@ __device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const 
     for (int r = 0; r < rows; ++r) {
       const uint32_t a = lbase + r * 4;
       for (int j = 0; j < J; ++j)
-        if (lane + 32 * j < OL) g[32 * j] = lds_f32(a + j * 4224);
+        if (lane + 32 * j < OL) __stcs(g + 32 * j, lds_f32(a + j * 4224));
       g += OL;
     }
   }
