@@ -24,6 +24,7 @@
 
 
 
+
 namespace vy {
 
 // Dynamic shared memory of every kernel in this library.  Tile data is
@@ -114,10 +115,11 @@ struct TreeC {
 // Global loads issued exactly where written (volatile asm): the compiler
 // otherwise sinks early loads next to their first use at the end of the step,
 // exposing the full DRAM latency there instead of overlapping it with the
-// tile copies.
+// tile copies.  The per-env state scalars are read once per step (.lu, last
+// use); the read-only series go through the non-coherent path (.nc).
 __device__ __forceinline__ double ldg_f64(const double* p) {
   double v;
-  asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  asm volatile("ld.global.lu.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ double ldg_nc_f64(const double* p) {
@@ -127,7 +129,7 @@ __device__ __forceinline__ double ldg_nc_f64(const double* p) {
 }
 __device__ __forceinline__ int ldg_s32(const int32_t* p) {
   int v;
-  asm volatile("ld.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile("ld.global.lu.s32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ int ldg_nc_s32(const int* p) {
@@ -137,7 +139,7 @@ __device__ __forceinline__ int ldg_nc_s32(const int* p) {
 }
 __device__ __forceinline__ uint64_t ldg_u64(const uint64_t* p) {
   uint64_t v;
-  asm volatile("ld.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  asm volatile("ld.global.lu.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ int ldg_nc_s8(const int8_t* p) {
