@@ -314,12 +314,14 @@ int geometry(vy_handle* h, K kernel, const TileLayout& L, int n_profiles, Geomet
 
 // Which Spec<M> (vy_device.cuh) a call runs: 1 or 2 (lean, small or large
 // tree) for lean outputs without any of the optional model features, an
-// identity-ordered station and a shuffle-sized grid; 0 (generic) otherwise.
+// identity-ordered station and a shuffle-sized grid; 3 the same with a
+// battery; 0 (generic) otherwise.
 int step_mode(const vy_handle* h, uint32_t flags, bool staged_actions) {
   const vy_tables& t = h->t;
-  const bool lean = (flags & ~VY_F_AUTO_RESET) == 0 && staged_actions && !t.battery_enabled && !t.has_moer &&
-                    !t.has_dgrid && t.horizon == 0 && h->order_identity && 2 * t.k < 32;
+  const bool lean = (flags & ~VY_F_AUTO_RESET) == 0 && staged_actions && !t.has_moer && !t.has_dgrid &&
+                    t.horizon == 0 && h->order_identity && 2 * t.k < 32;
   if (!lean) return 0;
+  if (t.battery_enabled) return 3;
   return t.n_nodes <= kFastNodes ? 1 : 2;
 }
 
@@ -579,7 +581,7 @@ int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride
   Geometry g;
   const int mode = step_mode(h, flags, acts);
   h->last_mode = mode;
-  auto* kern = mode == 1 ? k_step<1> : mode == 2 ? k_step<2> : k_step<0>;
+  auto* kern = mode == 1 ? k_step<1> : mode == 2 ? k_step<2> : mode == 3 ? k_step<3> : k_step<0>;
   if (int rc = geometry(h, kern, P.L, P.n_profiles, g)) return rc;
   // persistent grid: every resident CTA slot, never more CTAs than tiles need
   const unsigned resident = (unsigned)h->num_sms * (unsigned)(h->smem_per_sm / (g.smem + 1024));
@@ -635,7 +637,7 @@ int vy_rollout(vy_handle* h, int32_t T, uint64_t policy_seed, int64_t index0, in
   P.out.done = done;
   Geometry g;
   const int mode = step_mode(h, flags, true);
-  auto* kern = mode == 1 ? k_rollout<1> : mode == 2 ? k_rollout<2> : k_rollout<0>;
+  auto* kern = mode == 1 ? k_rollout<1> : mode == 2 ? k_rollout<2> : mode == 3 ? k_rollout<3> : k_rollout<0>;
   if (int rc = geometry(h, kern, P.L, P.n_profiles, g)) return rc;
   kern<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P, T, policy_seed, index0, call0, obs_step_stride,
                                                               rew_step_stride);

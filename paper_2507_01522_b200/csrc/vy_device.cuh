@@ -152,7 +152,8 @@ struct Params {
 // float32 obs, no battery, no carbon / demand series, no price horizon, a
 // tree of at most kFastNodes nodes, identity parking order, staged uint8
 // actions, a shuffle-sized action grid.  M = 2 is the same with a larger tree
-// (node loads summed from the tile, vy_tile.cuh node_sum).  Everything a lean
+// (node loads summed from the tile, vy_tile.cuh node_sum); M = 3 adds the
+// stationary battery (any tree) — the config-C4 station.  Everything a lean
 // mode folds away is dead code its kernel never carries (smaller hot loop,
 // fewer i-cache misses, no uniform branches); M = 0 reads all of it at run
 // time.  The host picks the instantiation (step_mode in vy_abi.cu).
@@ -162,12 +163,12 @@ struct Spec {
   __device__ __forceinline__ static bool info(const Params& P) { return !lean && (P.flags & VY_F_INFOS); }
   __device__ __forceinline__ static bool inject(const Params& P) { return !lean && (P.flags & VY_F_INJECT); }
   __device__ __forceinline__ static bool f64(const Params& P) { return !lean && (P.flags & VY_F_OUT_F64); }
-  __device__ __forceinline__ static bool battery(const Params& P) { return !lean && P.battery; }
+  __device__ __forceinline__ static bool battery(const Params& P) { return (M == 0 || M == 3) && P.battery; }
   __device__ __forceinline__ static bool moer(const Params& P) { return !lean && P.has_moer; }
   __device__ __forceinline__ static bool dgrid(const Params& P) { return !lean && P.has_dgrid; }
   __device__ __forceinline__ static int horizon(const Params& P) { return lean ? 0 : P.horizon; }
   __device__ __forceinline__ static bool fast_tree(const Params& P) {
-    return M == 1 || (M == 0 && P.n_nodes <= kFastNodes);
+    return M == 1 || ((M == 0 || M == 3) && P.n_nodes <= kFastNodes);
   }
   __device__ __forceinline__ static bool identity(const Params& P) { return lean || P.order_identity; }
   __device__ __forceinline__ static bool staged(const Params& P) { return lean || P.act_tile; }

@@ -76,12 +76,12 @@ def test_golden_trajectory_f32_device_path(name):
 
 
 LEAN = {"bp_coarse_dt": 1, "bp_default": 1, "bp_no_discharge": 1, "c1_default": 1, "default_maxcharge": 1,
-        "bp_random_tree": 2}
+        "bp_random_tree": 2, "c4_highway64": 3}
 
 
 @pytest.mark.parametrize("name", sorted(LEAN))
 def test_golden_trajectory_lean_kernel(name):
-    """The lean step instantiations (vy_device.cuh Spec<1> / Spec<2>) need
+    """The lean step instantiations (vy_device.cuh Spec<1> / <2> / <3>) need
     staged uint8 actions for whole 32-env tiles: the fixture's envs are rows
     0..B-1 of a 32-env batch (same seeds), extra rows get the fixture's first
     row of actions; rows 0..B-1 must reproduce the reference bit for bit."""
