@@ -250,6 +250,32 @@ def test_rollout_equals_stepwise_large_tree_lean():
     b.close()
 
 
+def test_results_invariant_to_launch_shape():
+    """The reference's worker-count contract (tests/test_engine.py:78-86) on the
+    GPU: the persistent step kernel's grid shape (tiles per warp) does not
+    change any output."""
+    from paper_2507_01522_b200 import default_setup
+    from paper_2507_01522_b200.batch import BatchEnv, DeviceRandomPolicy
+
+    rc = default_setup()
+    B = 8192
+    envs = [BatchEnv(rc.env, rc.station, rc.dataset, batch_size=B, master_seed=2) for _ in range(3)]
+    envs[1].set_tiles_per_warp(3)
+    envs[2].set_tiles_per_warp(64)
+    pol = DeviceRandomPolicy(5, envs[0].n_ports, 10)
+    pol.bind(range(B))
+    for e in envs:
+        e.reset(as_numpy=False)
+    for _ in range(60):
+        a = pol.actions(envs[0]).clone()
+        outs = [tuple(x.clone() for x in e.step(a, collect_infos=False)[:3]) for e in envs]
+        for o in outs[1:]:
+            for x, y in zip(outs[0], o):
+                torch.testing.assert_close(x, y, rtol=0, atol=0)
+    for e in envs:
+        e.close()
+
+
 def test_injected_draws_reproduce_reference_stream():
     """Arrival draws replayed on the host (the reference's own recipe,
     tests/test_env.py:251-278) and injected through vy_draws give the same
