@@ -409,7 +409,7 @@ def main() -> None:
         hms = max_over_ranks(h0.elapsed_time(h1))
         result["hetero"] = {"metric": METRIC, "value": hsteps * hb.total * world / (hms / 1e3), "unit": UNIT,
                             "groups": len(hb.groups), "envs_per_gpu": hb.total, "global_envs": hb.total * world,
-                            "kernels_per_step": 3 * len(hb.groups), "graph_launches_per_step": 1,
+                            "kernels_per_step": 2 * len(hb.groups), "graph_launches_per_step": 1,
                             "workload": "C5: regions x scenarios x traffic, single/multi/nested stations"}
         hb.close()
 

@@ -190,8 +190,10 @@ int vy_random_actions(vy_handle *h, uint64_t seed, int64_t index0, int64_t call,
                       uint8_t *out, void *stream);
 
 /* As vy_random_actions, with the call index read from (and then incremented
- * in) a device counter, so the pair of launches can be replayed from a CUDA
- * graph and still draw the next call's actions every replay. */
+ * in) a device counter, so the launch can be replayed from a CUDA graph and
+ * still draw the next call's actions every replay.  call_counter points to two
+ * int64: the call index and a scratch word (0 between launches) the kernel's
+ * blocks use to elect the one that advances the index. */
 int vy_random_actions_dev(vy_handle *h, uint64_t seed, int64_t index0, int64_t *call_counter, uint8_t *out,
                           void *stream);
 

@@ -538,7 +538,8 @@ class DeviceRandomPolicy:
             self._out = torch.empty(B, self.n_ports + 1, dtype=torch.uint8, device=env.device)
         if device_counter:
             if getattr(self, "_counter", None) is None:
-                self._counter = torch.tensor([self.calls], dtype=torch.int64, device=env.device)
+                # {call index, scratch}: see vy_random_actions_dev
+                self._counter = torch.tensor([self.calls, 0], dtype=torch.int64, device=env.device)
             rc = env._lib.vy_random_actions_dev(env._h, self.seed & ((1 << 64) - 1), self.index0,
                                                 self._counter.data_ptr(), self._out.data_ptr(), env._stream)
             nat.check(rc, "vy_random_actions_dev")

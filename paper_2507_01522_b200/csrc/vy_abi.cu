@@ -47,12 +47,30 @@ namespace vy {
 // RandomPolicy rows: thread per env computes its n+1 actions into a per-warp
 // smem row block, then the warp writes the contiguous [32][n+1] byte block
 // with coalesced stores (per-thread 17-byte rows would be strided byte stores).
+// Device-counter mode (call_dev = {call, blocks done}): every block reads the
+// call index at its start; the last block to finish advances it (and clears
+// the done count), so one launch per step is graph-replayable.
+__device__ __forceinline__ void bump_call(int64_t* call_dev) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    auto* done = reinterpret_cast<unsigned long long*>(call_dev + 1);
+    if (atomicAdd(done, 1ull) == (unsigned long long)gridDim.x - 1) {
+      call_dev[0] += 1;
+      *done = 0;
+    }
+  }
+}
+
 __global__ void k_random_actions(uint64_t seed, int64_t index0, int64_t call, int64_t B, int ns, int hi,
-                                 uint8_t* out, const int64_t* call_dev) {
-  if (call_dev) call += *call_dev;
+                                 uint8_t* out, int64_t* call_dev) {
+  if (call_dev) call += *(volatile int64_t*)call_dev;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
-  if (b0 >= B) return;
+  if (b0 >= B) {  // (warp 0 of every block is in range: grid = ceil(B / block))
+    if (call_dev) bump_call(call_dev);
+    return;
+  }
   unsigned char* rows = vy_smem + warp * 32 * ns;
   const int64_t b = b0 + lane;
   if (b < B) {
@@ -72,6 +90,7 @@ __global__ void k_random_actions(uint64_t seed, int64_t index0, int64_t call, in
   } else {
     for (int o = lane; o < bytes; o += 32) g[o] = rows[o];
   }
+  if (call_dev) bump_call(call_dev);
 }
 
 // div_rcp vs IEEE division on random dividends spread over 2^-64..2^64
@@ -104,7 +123,6 @@ __global__ void k_selftest_div(const double* d, const double* y, int nd, int64_t
   if (local) atomicAdd(bad, local);
 }
 
-__global__ void k_bump(int64_t* c) { *c += 1; }
 
 __global__ void k_seed_envs(uint64_t master, int64_t index0, int64_t B, uint64_t* env_seed) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -616,9 +634,8 @@ int vy_random_actions_dev(vy_handle* h, uint64_t seed, int64_t index0, int64_t* 
   const unsigned grid = (unsigned)((h->B + 255) / 256);
   k_random_actions<<<grid, 256, 8 * 32 * ns, (cudaStream_t)stream>>>(seed, index0, 0, h->B, ns, hi, out,
                                                                      call_counter);
-  k_bump<<<1, 1, 0, (cudaStream_t)stream>>>(call_counter);
   VY_CUDA(cudaGetLastError());
-  h->launches += 2;
+  ++h->launches;
   return VY_OK;
 }
 
