@@ -82,6 +82,16 @@ def scenarios(vy, helpers):
                                eta_charge=0.9, eta_discharge=0.85) for i in range(5))
     st_po = vy.build_station(vy.ArchNode(capacity_a=70.0, children=leaves), evse_order=[3, 1, 4, 0, 2])
     yield "parking_order", EnvConfig(episode_steps=48), st_po, mk(lam=1.5, days=4), 3, 21, 4, "random", 96
+    # whole 32-env tiles, so the GPU tests run these through the lean step
+    # instantiations as well: C5-style stations and markets (config C5 groups)
+    # and the C2 station, each crossing an episode boundary
+    cfg96 = EnvConfig(episode_steps=96)
+    yield "c5_nested_residential_us", cfg96, vy.preset_station("nested_splitters", 4, 12), \
+        vy.generate_synthetic_defaults("residential", "low", "us", seed=0, days=20), 32, 6, 8, "random", 150
+    yield "c5_single_highway_world", cfg96, vy.preset_station("single_type", 0, 8), \
+        vy.generate_synthetic_defaults("highway", "high", "world", seed=0, days=20), 32, 7, 9, "random", 150
+    yield "c2_default_tile", cfg96, rc.station, vy.generate_synthetic_defaults("shopping", "medium", "eu", seed=0,
+                                                                                 days=20), 32, 8, 10, "random", 150
 
 
 def dataset_dict(ds) -> dict:
@@ -285,6 +295,7 @@ def ingest_vectors(vy):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default=None)
+    ap.add_argument("--only", nargs="*", default=None, help="regenerate only these scenarios (no vectors)")
     args = ap.parse_args()
     sys.path.insert(0, ensure_ref(args.ref))
     sys.path.insert(0, "/root/reference/pkg/tests")
@@ -295,8 +306,12 @@ def main():
 
     print("reference backends:", vy.available_backends())
     for sc in scenarios(vy, helpers):
+        if args.only is not None and sc[0] not in args.only:
+            continue
         be = run(vy, *sc)
         print("wrote", sc[0], "backend", be)
+    if args.only is not None:
+        return
     synthetic_vectors(vy)
     print("wrote synthetic_vectors")
     evaluate_vectors(vy)
