@@ -389,14 +389,26 @@ __device__ __forceinline__ double node_sum(const Params& P, const Lane& T, doubl
 
 // _kernel.pyx:626-649: deepest-first proportional scaling to a fixed point.
 // Currents live in the i_drawn slots (they become i_drawn after the rescale).
-__device__ __noinline__ void fit_tree(const Params& P, TreeC tc, const Lane& T, double& cb) {
+// `clean` (trees of at most 64 nodes): bit q set = node q's leaves are
+// unchanged since it was last evaluated and that evaluation changed nothing,
+// so evaluating it again is a no-op and is skipped.  A node whose rescale
+// moves a current clears the bit of every node sharing a slot with it
+// (itself included).  The values, the pass in which the loop stops and the
+// max_passes bound are exactly the reference's: only no-op evaluations go.
+// The caller seeds `clean` with the nodes its excess check found within
+// capacity.
+__device__ __noinline__ void fit_tree(const Params& P, TreeC tc, const Lane& T, double& cb, uint64_t clean) {
+  const bool track = P.n_nodes <= 64;
+  if (!track) clean = 0;
   for (int pass = 0; pass < P.max_passes; ++pass) {
     bool moved = false;
     for (int q = 0; q < P.n_nodes; ++q) {
+      if ((clean >> q) & 1ull) continue;
       double cap, eta, rcp_eta;
       int lo, hi;
       tc.rec(q, cap, eta, rcp_eta, lo, hi);
       const double mag = fabs(node_load(node_sum(P, T, cb, lo, hi), eta, rcp_eta));
+      bool mq = false;
       if (mag > cap) {
         const double f = cap / mag;
         const int hp = hi < P.n_ports ? hi : P.n_ports;
@@ -405,16 +417,29 @@ __device__ __noinline__ void fit_tree(const Params& P, TreeC tc, const Lane& T, 
           const double v = old * f;
           if (v != old) {
             T.idr(j) = v;
-            moved = true;
+            mq = true;
           }
         }
         if (P.battery && lo <= P.n_ports && P.n_ports < hi) {
           const double v = cb * f;
           if (v != cb) {
             cb = v;
-            moved = true;
+            mq = true;
           }
         }
+      }
+      if (!track) {
+        moved |= mq;
+      } else if (mq) {
+        moved = true;
+        for (int r = 0; r < P.n_nodes; ++r) {
+          double c2, e2, re2;
+          int lo2, hi2;
+          tc.rec(r, c2, e2, re2, lo2, hi2);
+          if (lo2 < hi && lo < hi2) clean &= ~(1ull << r);
+        }
+      } else {
+        clean |= 1ull << q;
       }
     }
     if (!moved) return;
@@ -648,6 +673,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
   if (bad_action) atomicOr(P.err, 1u);
   // tree: excess on the requested currents (_kernel.pyx:611-624), then rescale
   double excess = 0.0;
+  uint64_t clean = 0;  // nodes the excess check found within capacity (fit_tree)
   if (fast) {
 #pragma unroll
     for (int m = 0; m < kFastNodes; ++m) {
@@ -663,10 +689,13 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
       tc.rec(q, cap, eta, rcp_eta, lo, hi);
       const double over = fabs(node_load(node_sum(P, T, cb, lo, hi), eta, rcp_eta)) - cap;
       if (over > excess) excess = over;
+      if (!(over > 0.0)) clean |= 1ull << (q & 63);  // within capacity (mag <= cap)
     }
   }
   // no node over capacity => the reference's first rescale pass changes nothing and returns
-  if (excess > 0.0) fit_tree(P, tc, T, cb);
+#ifndef VY_AB_NO_FIT
+  if (excess > 0.0) fit_tree(P, tc, T, cb, clean);
+#endif
   if (info) {
     for (int i = 0; i < n; ++i) O.i_used[i * ld + b] = T.idr(i);
     if (battery) O.i_used[n * ld + b] = cb;

@@ -62,7 +62,8 @@ def sweep_groups(total_envs: int, days: int = 365, seed: int = 0) -> list[Group]
 
 class HeteroBatch:
     def __init__(self, groups: list[Group], master_seed: int = 0, global_offset: int = 0, device=None,
-                 policy_seed: int | None = None, n_streams: int = 16, tiles_per_warp: int = 2):
+                 policy_seed: int | None = None, n_streams: int = 12, tiles_per_warp: int = 3,
+                 longest_first: bool = True):
         self.groups = groups
         self.streams = [torch.cuda.Stream(device=device) for _ in range(max(1, n_streams))]
         self.envs: list[BatchEnv] = []
@@ -79,6 +80,11 @@ class HeteroBatch:
                 self.policies.append(pol)
             off += g.batch_size
         self.total = off - global_offset
+        # launch order: the costliest groups first (bigger trees, then more
+        # ports, then more envs) so they do not form the step's tail
+        cost = [(e.tables.n_nodes, e.n_ports, g.batch_size) for e, g in zip(self.envs, groups)]
+        self._order = sorted(range(len(groups)), key=lambda i: cost[i], reverse=True) if longest_first \
+            else list(range(len(groups)))
 
     def reset(self) -> list[torch.Tensor]:
         return [e.reset(as_numpy=False) for e in self.envs]
@@ -88,10 +94,10 @@ class HeteroBatch:
         cur = torch.cuda.current_stream()
         for s in self.streams:
             s.wait_stream(cur)
-        out = []
-        for i in range(len(self.envs)):
-            with torch.cuda.stream(self.streams[i % len(self.streams)]):
-                out.append(fn(i))
+        out = [None] * len(self.envs)
+        for p, i in enumerate(self._order):
+            with torch.cuda.stream(self.streams[p % len(self.streams)]):
+                out[i] = fn(i)
         for s in self.streams:
             cur.wait_stream(s)
         return out

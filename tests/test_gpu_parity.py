@@ -340,6 +340,33 @@ def test_errors_match_reference_behaviour():
     env.close()
 
 
+def test_host_path_returns_fresh_arrays_and_accepts_any_int_actions():
+    """The numpy drop-in returns new float64/bool arrays every step (callers
+    keep them, as the reference's .copy() allows, engine.py:463-464) and takes
+    read-only or narrower integer action arrays like np.ascontiguousarray."""
+    fx = Fixture("bp_default")
+    env = make_env(fx, obs_dtype=torch.float64)
+    obs0 = env.reset()
+    a0 = fx["actions"][0].astype(np.int32)
+    a0.setflags(write=False)
+    obs1, r1, d1, _ = env.step(a0, collect_infos=False)
+    keep = obs1.copy(), r1.copy(), d1.copy()
+    obs2, r2, d2, _ = env.step(fx["actions"][1], collect_infos=False)
+    assert obs1.dtype == np.float64 and r1.dtype == np.float64 and d1.dtype == np.bool_
+    assert not np.shares_memory(obs1, obs2) and not np.shares_memory(obs0, obs1)
+    np.testing.assert_array_equal(obs1, keep[0])
+    np.testing.assert_array_equal(r1, keep[1])
+    np.testing.assert_array_equal(d1, keep[2])
+    np.testing.assert_array_equal(obs0, fx["obs0"])
+    np.testing.assert_array_equal(obs1, fx["obs"][0])
+    np.testing.assert_array_equal(obs2, fx["obs"][1])
+    neg = fx["actions"][2].copy()
+    neg[-1, -1] = -1
+    with pytest.raises(ValueError):
+        env.step(neg)
+    env.close()
+
+
 def test_no_auto_reset_raises_episode_done():
     from paper_2507_01522_b200.batch import BatchEnv
     from paper_2507_01522_b200.errors import EpisodeDone
