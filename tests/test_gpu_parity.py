@@ -251,6 +251,41 @@ def test_rollout_equals_stepwise_large_tree_lean():
     b.close()
 
 
+@pytest.mark.parametrize("obs_dtype", ["f32", "f64"])
+def test_tree_rescale_every_row_matches_oracle(obs_dtype):
+    """Nested splitters (11 nodes, 2-port caps) at high traffic: the tree
+    rescale runs multi-pass fixed points on most steps.  Every row and every
+    state slot of the kernel (lean mode 2 for f32 obs, the generic kernel for
+    f64) equals the CPU oracle over a whole episode and past its boundary."""
+    from paper_2507_01522_b200 import EnvConfig
+    from paper_2507_01522_b200.batch import BatchEnv, DeviceRandomPolicy
+    from paper_2507_01522_b200.exogenous import generate_synthetic_defaults
+    from paper_2507_01522_b200.station import preset_station
+
+    cfg = EnvConfig()
+    st = preset_station("nested_splitters", 4, 12)
+    ds = generate_synthetic_defaults("work", "high", "us", seed=2, days=20)
+    B, T, master, pseed = 256, 300, 13, 17
+    dt = torch.float32 if obs_dtype == "f32" else torch.float64
+    env = BatchEnv(cfg, st, ds, batch_size=B, master_seed=master, obs_dtype=dt)
+    pol = DeviceRandomPolicy(pseed, env.n_ports, cfg.discretization_k)
+    pol.bind(range(B))
+    obs = [env.reset(as_numpy=False).cpu().numpy()]
+    rews = []
+    for _ in range(T):
+        o, r, _, _ = env.step(pol.actions(env), collect_infos=False)
+        assert env.last_step_mode() == (2 if obs_dtype == "f32" else 0)
+        obs.append(o.cpu().numpy())
+        rews.append(r.cpu().numpy())
+    ref_obs, ref_r, hb = _oracle_subset(env.tables, B, master, list(range(B)), pseed, T, cfg.episode_steps)
+    np.testing.assert_array_equal(np.array(obs), ref_obs.astype(obs[0].dtype))
+    np.testing.assert_array_equal(np.array(rews), ref_r.astype(rews[0].dtype))
+    stt = env.reference_state()
+    for k in ("occ", "soc", "de", "i_drawn", "dtrem", "ep_reward", "ep_profit", "episode", "day"):
+        np.testing.assert_array_equal(stt[k], getattr(hb.states, k), err_msg=k)
+    env.close()
+
+
 def test_results_invariant_to_launch_shape():
     """The reference's worker-count contract (tests/test_engine.py:78-86) on the
     GPU: the persistent step kernel's grid shape (tiles per warp) does not
