@@ -693,9 +693,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
     }
   }
   // no node over capacity => the reference's first rescale pass changes nothing and returns
-#ifndef VY_AB_NO_FIT
   if (excess > 0.0) fit_tree(P, tc, T, cb, clean);
-#endif
   if (info) {
     for (int i = 0; i < n; ++i) O.i_used[i * ld + b] = T.idr(i);
     if (battery) O.i_used[n * ld + b] = cb;
