@@ -13,7 +13,8 @@
 //   the stored actions and entropy (sum over slots), and the gradient of
 //   g_lp * lp + g_ent * ent with respect to the logits, each one read of the
 //   [N][S][A] logits (the unfused torch graph made ~10 passes over them).
-//   One warp per sample, lanes over slots.
+//   Sampling: one warp per sample, lanes over slots; the head: one thread per
+//   (sample, slot), whole rows staged per block.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -111,64 +112,141 @@ __global__ void k_ppo_sample(const T* __restrict__ logits, const float* __restri
   if (lane == 0) logp[n] = acc;
 }
 
+// The update's head runs on minibatches of ~300k samples, so it is laid out
+// for bandwidth: a block stages G whole rows (G*ld values, contiguous in
+// memory) with 16-byte loads, then one thread per (sample, slot) — G*S of
+// the 256 threads, 255 for the 17-slot head — works on its slot's A values
+// (slots A words apart: conflict-free for odd A), and per-sample sums go
+// through shared memory.  The backward writes the gradient rows back the
+// same way (padding columns zero).
+constexpr int kHeadThreads = 256;
+
 template <class T>
-__global__ void k_ppo_head_fwd(const T* __restrict__ logits, const uint8_t* __restrict__ actions, int64_t N, int S,
-                               int A, int64_t ld, float* __restrict__ lp, float* __restrict__ ent) {
-  const int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (n >= N) return;
-  float* row = stage_row(logits, n, S * A, ld, lane);
-  float alp = 0.f, aent = 0.f;
-  for (int s = lane; s < S; s += 32) {
-    const float* z = row + s * A;
-    float lse;
-    slot_lse(z, A, lse);
-    float h = 0.f;
-    for (int k = 0; k < A; ++k) {
-      const float l = z[k] - lse;
-      h -= __expf(l) * l;
+__device__ __forceinline__ void stage_rows(const T* __restrict__ src, int64_t n, float* __restrict__ dst) {
+  constexpr int V = 16 / sizeof(T);
+  if ((reinterpret_cast<uintptr_t>(src) & 15u) == 0 && n % V == 0) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    for (int64_t i = threadIdx.x; i < n / V; i += blockDim.x) {
+      const uint4 u = __ldg(s4 + i);
+      const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+      for (int j = 0; j < V; ++j) dst[i * V + j] = to_f(e[j]);
     }
-    alp += z[actions[n * S + s]] - lse;
-    aent += h;
+  } else {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = to_f(src[i]);
   }
-  alp = warp_sum(alp);
-  aent = warp_sum(aent);
-  if (lane == 0) {
-    lp[n] = alp;
-    ent[n] = aent;
+}
+
+template <class T>
+__device__ __forceinline__ void store_rows(const float* __restrict__ src, int64_t n, T* __restrict__ dst) {
+  constexpr int V = 16 / sizeof(T);
+  if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && n % V == 0) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (int64_t i = threadIdx.x; i < n / V; i += blockDim.x) {
+      uint4 u;
+      T* e = reinterpret_cast<T*>(&u);
+#pragma unroll
+      for (int j = 0; j < V; ++j) e[j] = from_f<T>(src[i * V + j]);
+      d4[i] = u;
+    }
+  } else {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = from_f<T>(src[i]);
+  }
+}
+
+// One slot's softmax statistics from its A staged logits z, with a single
+// exp per value: m = max z, e_k = exp(z_k - m), sum = sum e_k,
+// logsum = log(sum), lse = m + logsum, and the entropy
+// H = -sum p_k (z_k - lse) = logsum - sum(e_k (z_k - m)) / sum.
+__device__ __forceinline__ void slot_stats(const float* z, int A, float& m, float& logsum, float& inv, float& h) {
+  m = -INFINITY;
+#pragma unroll 4
+  for (int k = 0; k < A; ++k) m = fmaxf(m, z[k]);
+  float sum = 0.f, ed = 0.f;
+#pragma unroll 4
+  for (int k = 0; k < A; ++k) {
+    const float d = z[k] - m, e = __expf(d);
+    sum += e;
+    ed += e * d;
+  }
+  inv = 1.f / sum;
+  logsum = __logf(sum);
+  h = logsum - ed * inv;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kHeadThreads) k_ppo_head_fwd(const T* __restrict__ logits,
+                                                               const uint8_t* __restrict__ actions, int64_t N, int S,
+                                                               int A, int64_t ld, int G, float* __restrict__ lp,
+                                                               float* __restrict__ ent) {
+  extern __shared__ float ppo_smem[];
+  const int64_t n0 = (int64_t)blockIdx.x * G;
+  const int gh = (int)min((int64_t)G, N - n0);
+  float* rows = ppo_smem;
+  float* part = ppo_smem + (size_t)G * ld;  // [2][G*S]
+  stage_rows(logits + n0 * ld, (int64_t)gh * ld, rows);
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < gh * S) {
+    const int r = t / S, s = t - r * S;
+    const float* z = rows + (size_t)r * ld + s * A;
+    float m, logsum, inv, h;
+    slot_stats(z, A, m, logsum, inv, h);
+    part[t] = (z[actions[(n0 + r) * S + s]] - m) - logsum;
+    part[G * S + t] = h;
+  }
+  __syncthreads();
+  if (t < gh) {
+    float alp = 0.f, aent = 0.f;
+    for (int s = 0; s < S; ++s) {  // slot order, as the warp version's lanes summed
+      alp += part[t * S + s];
+      aent += part[G * S + t * S + s];
+    }
+    lp[n0 + t] = alp;
+    ent[n0 + t] = aent;
   }
 }
 
 // d(g_lp * lp + g_ent * ent) / dz_k = g_lp (1[k = a] - p_k) - g_ent p_k (log p_k + H), H = slot entropy
 template <class T>
-__global__ void k_ppo_head_bwd(const T* __restrict__ logits, const uint8_t* __restrict__ actions, int64_t N, int S,
-                               int A, int64_t ld, const float* __restrict__ g_lp, const float* __restrict__ g_ent,
-                               T* __restrict__ grad) {
-  const int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (n >= N) return;
+__global__ void __launch_bounds__(kHeadThreads) k_ppo_head_bwd(const T* __restrict__ logits,
+                                                               const uint8_t* __restrict__ actions, int64_t N, int S,
+                                                               int A, int64_t ld, int G,
+                                                               const float* __restrict__ g_lp,
+                                                               const float* __restrict__ g_ent, T* __restrict__ grad) {
+  extern __shared__ float ppo_smem[];
+  const int64_t n0 = (int64_t)blockIdx.x * G;
+  const int gh = (int)min((int64_t)G, N - n0);
+  float* rows = ppo_smem;
   const int SA = S * A;
-  float* row = stage_row(logits, n, SA, ld, lane);
-  const float gl = g_lp ? g_lp[n] : 0.f, ge = g_ent ? g_ent[n] : 0.f;
-  for (int s = lane; s < S; s += 32) {
-    float* z = row + s * A;
-    float lse;
-    slot_lse(z, A, lse);
-    float h = 0.f;
-    for (int k = 0; k < A; ++k) {
-      const float l = z[k] - lse;
-      h -= __expf(l) * l;
-    }
-    const int a = actions[n * S + s];
-    for (int k = 0; k < A; ++k) {  // in place: this lane owns the slot's values
-      const float l = z[k] - lse, p = __expf(l);
+  stage_rows(logits + n0 * ld, (int64_t)gh * ld, rows);
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < gh * S) {
+    const int r = t / S, s = t - r * S;
+    float* z = rows + (size_t)r * ld + s * A;
+    float m, logsum, inv, h;
+    slot_stats(z, A, m, logsum, inv, h);
+    const float gl = g_lp ? g_lp[n0 + r] : 0.f, ge = g_ent ? g_ent[n0 + r] : 0.f;
+    const int a = actions[(n0 + r) * S + s];
+#pragma unroll 4
+    for (int k = 0; k < A; ++k) {  // in place: this thread owns the slot's values
+      const float d = z[k] - m, p = __expf(d) * inv, l = d - logsum;
       z[k] = gl * ((k == a ? 1.f : 0.f) - p) - ge * p * (l + h);
     }
   }
-  __syncwarp();
-  T* d = grad + n * ld;
-  for (int e = lane; e < ld; e += 32) d[e] = from_f<T>(e < SA ? row[e] : 0.f);  // padding columns: 0
+  const int pad = (int)(ld - SA);
+  for (int i = t; i < gh * pad; i += blockDim.x) rows[(size_t)(i / pad) * ld + SA + i % pad] = 0.f;
+  __syncthreads();
+  store_rows(rows, (int64_t)gh * ld, grad + n0 * ld);
 }
+
+int head_rows(int S) { return S <= kHeadThreads ? kHeadThreads / S : 0; }
+size_t head_smem(int S, int64_t ld) {
+  const int G = head_rows(S);
+  return (size_t)G * ld * sizeof(float) + 2 * (size_t)G * S * sizeof(float);
+}
+unsigned head_grid(int64_t N, int S) { return (unsigned)((N + head_rows(S) - 1) / head_rows(S)); }
 
 constexpr int kWarpsPerBlock = 8;
 unsigned warp_grid(int64_t N) { return (unsigned)((N + kWarpsPerBlock - 1) / kWarpsPerBlock); }
@@ -195,30 +273,32 @@ extern "C" int vy_ppo_sample(const void* logits, int32_t dtype, int64_t ld, cons
 extern "C" int vy_ppo_head_fwd(const void* logits, int32_t dtype, int64_t ld, const uint8_t* actions, int64_t N,
                                int32_t S, int32_t A, float* lp, float* ent, void* stream) {
   if (!logits || !actions || !lp || !ent || N < 1 || S < 1 || A < 1 || (dtype != 0 && dtype != 1) ||
-      row_smem(S, A) > 48 * 1024 || ld < (int64_t)S * A)
+      head_rows(S) < 1 || ld < (int64_t)S * A || head_smem(S, ld) > 48 * 1024)
     return VY_ERR_ARG;
   auto st = (cudaStream_t)stream;
+  const int G = head_rows(S);
   if (dtype == 0)
-    k_ppo_head_fwd<float><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
-        static_cast<const float*>(logits), actions, N, S, A, ld, lp, ent);
+    k_ppo_head_fwd<float><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+        static_cast<const float*>(logits), actions, N, S, A, ld, G, lp, ent);
   else
-    k_ppo_head_fwd<__nv_bfloat16><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
-        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, lp, ent);
+    k_ppo_head_fwd<__nv_bfloat16><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, lp, ent);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 
 extern "C" int vy_ppo_head_bwd(const void* logits, int32_t dtype, int64_t ld, const uint8_t* actions, int64_t N,
                                int32_t S, int32_t A, const float* g_lp, const float* g_ent, void* grad, void* stream) {
-  if (!logits || !actions || !grad || N < 1 || S < 1 || A < 1 || (dtype != 0 && dtype != 1) ||
-      row_smem(S, A) > 48 * 1024 || ld < (int64_t)S * A)
+  if (!logits || !actions || !grad || N < 1 || S < 1 || A < 1 || (dtype != 0 && dtype != 1) || head_rows(S) < 1 ||
+      ld < (int64_t)S * A || head_smem(S, ld) > 48 * 1024)
     return VY_ERR_ARG;
   auto st = (cudaStream_t)stream;
+  const int G = head_rows(S);
   if (dtype == 0)
-    k_ppo_head_bwd<float><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
-        static_cast<const float*>(logits), actions, N, S, A, ld, g_lp, g_ent, static_cast<float*>(grad));
+    k_ppo_head_bwd<float><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+        static_cast<const float*>(logits), actions, N, S, A, ld, G, g_lp, g_ent, static_cast<float*>(grad));
   else
-    k_ppo_head_bwd<__nv_bfloat16><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
-        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, g_lp, g_ent,
+    k_ppo_head_bwd<__nv_bfloat16><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, g_lp, g_ent,
         static_cast<__nv_bfloat16*>(grad));
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }

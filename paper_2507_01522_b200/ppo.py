@@ -65,6 +65,49 @@ def _ortho(layer: nn.Linear, gain: float) -> nn.Linear:
     return layer
 
 
+_ONES: dict = {}
+
+
+def _ones_row(m: int, like: torch.Tensor) -> torch.Tensor:
+    key = (m, like.dtype, like.device)
+    if key not in _ONES:
+        _ONES.clear()
+        _ONES[key] = torch.ones(1, m, dtype=like.dtype, device=like.device)
+    return _ONES[key]
+
+
+class _LinearFn(torch.autograd.Function):
+    """y = x W^T + b whose backward forms the bias gradient as a [1 x M] @ [M x N]
+    GEMM with a ones row instead of a column reduction: on the update's ~300k-row
+    minibatches torch's sum(0) ran 2.5-4x slower (scripts/micro/bias_grad.py)."""
+
+    @staticmethod
+    @torch.amp.custom_fwd(device_type="cuda", cast_inputs=torch.bfloat16)
+    def forward(ctx, x, w, b):
+        ctx.save_for_backward(x, w)
+        return nn.functional.linear(x, w, b)
+
+    @staticmethod
+    @torch.amp.custom_bwd(device_type="cuda")
+    def backward(ctx, g):
+        x, w = ctx.saved_tensors
+        g = g.contiguous()
+        dx = g @ w if ctx.needs_input_grad[0] else None
+        dw = g.t() @ x
+        db = (_ones_row(g.shape[0], g) @ g).view(-1)
+        return dx, dw, db
+
+
+class _Linear(nn.Linear):
+    """nn.Linear with the GEMM bias gradient while training (2-D inputs); the
+    plain layer otherwise, so inference keeps autocast's weight cache."""
+
+    def forward(self, x):
+        if torch.is_grad_enabled() and self.weight.requires_grad and x.dim() == 2 and x.is_cuda:
+            return _LinearFn.apply(x, self.weight, self.bias)
+        return super().forward(x)
+
+
 def _ceil8(x: int) -> int:
     return (x + 7) // 8 * 8
 
@@ -74,20 +117,27 @@ class ActorCritic(nn.Module):
     (S*A = 357) are padded to multiples of 8 — zero input columns, unused
     output columns — so the bf16 GEMMs have 16-byte aligned rows (cuBLAS
     otherwise falls back to sm75 kernels, 3-7x slower at these shapes,
-    scripts/micro/gemm_align.py)."""
+    scripts/micro/gemm_align.py).  The actor's and the critic's first layers
+    read the same observation, so they are one [2H x in] GEMM (rows 0..H-1
+    actor, H..2H-1 critic; each half initialised as its own orthogonal layer):
+    one pass over the observations and one launch instead of two."""
 
     def __init__(self, obs_dim: int, n_slots: int, n_actions: int, hidden: int = 64):
         super().__init__()
-        self.n_slots, self.n_actions = n_slots, n_actions
+        self.n_slots, self.n_actions, self.hidden = n_slots, n_actions, hidden
         self.obs_dim, self.in_dim = obs_dim, _ceil8(obs_dim)
         self.n_out, self.out_dim = n_slots * n_actions, _ceil8(n_slots * n_actions)
         g = math.sqrt(2.0)
-        self.actor = nn.Sequential(_ortho(nn.Linear(self.in_dim, hidden), g), nn.Tanh(),
-                                   _ortho(nn.Linear(hidden, hidden), g), nn.Tanh(),
-                                   _ortho(nn.Linear(hidden, self.out_dim), 0.01))
-        self.critic = nn.Sequential(_ortho(nn.Linear(self.in_dim, hidden), g), nn.Tanh(),
-                                    _ortho(nn.Linear(hidden, hidden), g), nn.Tanh(),
-                                    _ortho(nn.Linear(hidden, 1), 1.0))
+        self.inp = _Linear(self.in_dim, 2 * hidden)
+        with torch.no_grad():
+            for half in range(2):
+                layer = _ortho(nn.Linear(self.in_dim, hidden), g)
+                self.inp.weight[half * hidden:(half + 1) * hidden].copy_(layer.weight)
+                self.inp.bias[half * hidden:(half + 1) * hidden].copy_(layer.bias)
+        self.actor = nn.Sequential(_ortho(_Linear(hidden, hidden), g), nn.Tanh(),
+                                   _ortho(_Linear(hidden, self.out_dim), 0.01))
+        self.critic = nn.Sequential(_ortho(_Linear(hidden, hidden), g), nn.Tanh(),
+                                    _ortho(_Linear(hidden, 1), 1.0))
 
     def pad_obs(self, obs: torch.Tensor) -> torch.Tensor:
         w = obs.shape[-1]
@@ -96,11 +146,14 @@ class ActorCritic(nn.Module):
     def forward(self, obs: torch.Tensor, logits_fp32: bool = True):
         """-> (logits, value).  logits_fp32: float32 [M, S, A] (torch head);
         else the raw padded head output [M, out_dim] (autocast dtype) that the
-        fused head kernels read in place with row stride out_dim."""
-        x = self.pad_obs(obs)
-        out = self.actor(x)
+        fused head kernels read in place with row stride out_dim.  The value
+        comes back in the compute dtype ([M]); callers widen it where they use it."""
+        # split, not two slices: its backward is one concatenation of the two
+        # halves' gradients (two slice backwards each write a zero-filled full width)
+        ha, hc = torch.tanh(self.inp(self.pad_obs(obs))).split(self.hidden, dim=1)
+        out = self.actor(ha)
         logits = out[:, : self.n_out].float().view(-1, self.n_slots, self.n_actions) if logits_fp32 else out
-        return logits, self.critic(x).squeeze(-1).float()
+        return logits, self.critic(hc).squeeze(-1)
 
 
 def _dtype_code(t: torch.Tensor) -> int:
@@ -194,7 +247,7 @@ class PPOTrainer:
         if self.world > 1:  # identical initial weights on every rank
             for p in self.net.parameters():
                 dist.broadcast(p.data, 0)
-        self.opt = torch.optim.Adam(self.net.parameters(), lr=cfg.lr, eps=1e-5)
+        self.opt = torch.optim.Adam(self.net.parameters(), lr=cfg.lr, eps=1e-5, fused=True)
         T, B, L, A = cfg.rollout_steps, env.batch_size, env.obs_length, env.action_size
         self.obs = torch.zeros(T + 1, B, L, device=dev)
         self.actions = torch.zeros(T, B, A, dtype=torch.uint8, device=dev)
@@ -212,8 +265,7 @@ class PPOTrainer:
 
     def _policy_step(self, t: int) -> None:
         fused = self.cfg.fused_head
-        with torch.autocast("cuda", dtype=torch.bfloat16):
-            logits, v = self.net(self.obs[t], logits_fp32=not fused)
+        logits, v = self.net(self.obs[t], logits_fp32=not fused)
         noise = torch.rand(logits.shape[0], self.net.n_slots, self.net.n_actions, device=logits.device)
         if fused:
             # Gumbel-max sampling + log-probability in one kernel, straight into the rollout buffers
@@ -228,16 +280,20 @@ class PPOTrainer:
             lp = torch.log_softmax(logits, dim=-1).gather(-1, a.unsqueeze(-1)).squeeze(-1).sum(-1)
             self.actions[t].copy_(a)
             self.logp[t].copy_(lp)
-        self.values[t].copy_(v)
+        self.values[t].copy_(v)  # widened to float32 by the copy
         # the env writes the next obs / reward / done straight into the rollout buffers
         self.env.set_outputs(obs=self.obs[t + 1], reward=self.rewards[t], done=self.dones[t])
         self.env.step(self.actions[t], collect_infos=False)
 
     def _rollout_body(self) -> None:
-        for t in range(self.cfg.rollout_steps):
-            self._policy_step(t)
-        with torch.no_grad(), torch.autocast("cuda", dtype=torch.bfloat16):
-            _, self.values[-1] = self.net(self.obs[-1])
+        # one autocast region for the whole rollout: the bf16 copies of the
+        # weights are made once per rollout (autocast's weight cache), not once
+        # per policy step
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            for t in range(self.cfg.rollout_steps):
+                self._policy_step(t)
+            _, v = self.net(self.obs[-1])
+            self.values[-1].copy_(v)
 
     @torch.no_grad()
     def rollout(self) -> None:
@@ -283,7 +339,9 @@ class PPOTrainer:
             frac = 1.0 - self.iterations / self.n_iters
             for g in self.opt.param_groups:
                 g["lr"] = cfg.lr * max(frac, 0.0)
-        obs = self.net.pad_obs(self.obs[:T].reshape(T * B, -1))  # aligned rows once; minibatches gather them
+        # aligned bf16 rows once per update (the value autocast would cast each
+        # minibatch to anyway); minibatches gather half the bytes
+        obs = self.net.pad_obs(self.obs[:T].reshape(T * B, -1)).to(torch.bfloat16)
         act = self.actions.reshape(T * B, -1)
         old_lp, old_v = self.logp.reshape(-1), self.values[:T].reshape(-1)
         adv, ret = adv.reshape(-1), ret.reshape(-1)
@@ -296,6 +354,7 @@ class PPOTrainer:
                 idx = perm[k * mb:(k + 1) * mb]
                 with torch.autocast("cuda", dtype=torch.bfloat16):
                     logits, v = self.net(obs[idx], logits_fp32=not cfg.fused_head)
+                    v = v.float()
                 if cfg.fused_head:
                     lp, ent = PolicyHead.apply(logits, act[idx], self.net.n_slots, self.net.n_actions)
                 else:

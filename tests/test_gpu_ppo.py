@@ -180,3 +180,29 @@ def test_fused_policy_head_padded_rows():
     torch.testing.assert_close(lp1, lp2, rtol=0, atol=0)
     torch.testing.assert_close(full.grad[:, : S * A], packed.grad, rtol=0, atol=0)
     assert (full.grad[:, S * A:] == 0).all()
+
+
+@pytest.mark.parametrize("autocast", [False, True])
+def test_linear_gemm_bias_grad_matches_torch(autocast):
+    """The update's linear layers (bias gradient as a ones-row GEMM) give torch's
+    gradients: fp32 tightly, bf16 autocast within bf16 rounding."""
+    from paper_2507_01522_b200.ppo import _Linear
+
+    torch.manual_seed(0)
+    lin = _Linear(112, 360).cuda()
+    ref = torch.nn.Linear(112, 360).cuda()
+    ref.load_state_dict(lin.state_dict())
+    x = torch.randn(4099, 112, device="cuda", requires_grad=True)
+    x2 = x.detach().clone().requires_grad_(True)
+    g = torch.randn(4099, 360, device="cuda")
+    with torch.autocast("cuda", dtype=torch.bfloat16, enabled=autocast):
+        y = lin(x)
+        y2 = ref(x2)
+    (y.float() * g).sum().backward()
+    (y2.float() * g).sum().backward()
+    tol = dict(rtol=2e-2, atol=2e-2) if autocast else dict(rtol=1e-4, atol=1e-3)
+    torch.testing.assert_close(y.float(), y2.float(), **tol)
+    scale = lambda t: t / t.abs().max()  # noqa: E731
+    torch.testing.assert_close(scale(lin.weight.grad), scale(ref.weight.grad), **tol)
+    torch.testing.assert_close(scale(lin.bias.grad), scale(ref.bias.grad), **tol)
+    torch.testing.assert_close(scale(x.grad), scale(x2.grad), **tol)
