@@ -249,6 +249,9 @@ int vy_ppo_head_fwd(const void *logits, int32_t dtype, int64_t ld, const uint8_t
                     int32_t A, float *lp, float *ent, void *stream);
 int vy_ppo_head_bwd(const void *logits, int32_t dtype, int64_t ld, const uint8_t *actions, int64_t N, int32_t S,
                     int32_t A, const float *g_lp, const float *g_ent, void *grad, void *stream);
+/* PPO minibatch gather: dst row i = src row idx[i] for i < n, rows of
+ * row_bytes bytes (a multiple of 16; src and dst 16-byte aligned). */
+int vy_gather_rows(const void *src, int64_t row_bytes, const int64_t *idx, int64_t n, void *dst, void *stream);
 
 /* Diagnostics: compare the kernels' reciprocal-based division (div_rcp in
  * csrc/vy_device.cuh) with IEEE x / d on `samples_per_divisor` random

@@ -18,6 +18,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <string>
 
@@ -241,6 +242,18 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_head_bwd(const T* __restri
   store_rows(rows, (int64_t)gh * ld, grad + n0 * ld);
 }
 
+// Row gather with 16-byte vectors: a row's vectors go to consecutive threads
+// (coalesced reads of each random row, fully coalesced writes).
+// I = 32-bit element indices when the gathered block fits (cheap division).
+template <class I>
+__global__ void k_gather_rows(const uint4* __restrict__ src, I vpr, const int64_t* __restrict__ idx, I total,
+                              uint4* __restrict__ dst) {
+  for (I i = (I)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (I)gridDim.x * blockDim.x) {
+    const I r = i / vpr, v = i - r * vpr;
+    dst[i] = __ldg(src + idx[r] * (int64_t)vpr + v);
+  }
+}
+
 int head_rows(int S) { return S <= kHeadThreads ? kHeadThreads / S : 0; }
 size_t head_smem(int S, int64_t ld) {
   const int G = head_rows(S);
@@ -300,6 +313,24 @@ extern "C" int vy_ppo_head_bwd(const void* logits, int32_t dtype, int64_t ld, co
     k_ppo_head_bwd<__nv_bfloat16><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
         static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, g_lp, g_ent,
         static_cast<__nv_bfloat16*>(grad));
+  return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
+}
+
+extern "C" int vy_gather_rows(const void* src, int64_t row_bytes, const int64_t* idx, int64_t n, void* dst,
+                              void* stream) {
+  if (n < 0 || row_bytes < 16 || row_bytes % 16) return VY_ERR_ARG;
+  if (n == 0) return VY_OK;  // nothing to read or write (empty tensors may have null pointers)
+  if (!src || !idx || !dst || (reinterpret_cast<uintptr_t>(src) & 15u) || (reinterpret_cast<uintptr_t>(dst) & 15u))
+    return VY_ERR_ARG;
+  const int64_t vpr = row_bytes / 16, total = n * vpr;
+  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  auto st = (cudaStream_t)stream;
+  if (total < (int64_t)UINT32_MAX)
+    k_gather_rows<uint32_t><<<grid, 256, 0, st>>>(static_cast<const uint4*>(src), (uint32_t)vpr, idx,
+                                                  (uint32_t)total, static_cast<uint4*>(dst));
+  else
+    k_gather_rows<int64_t><<<grid, 256, 0, st>>>(static_cast<const uint4*>(src), vpr, idx, total,
+                                                 static_cast<uint4*>(dst));
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 

@@ -57,6 +57,7 @@ class PPOConfig:
     seed: int = 0
     use_graph: bool = True
     fused_head: bool = True  # vy_ppo_sample / vy_ppo_head_* kernels instead of the torch op chain
+    graph_update: bool = True  # the whole update (GAE + epochs x minibatches + Adam) as one CUDA graph (1 GPU)
 
 
 def _ortho(layer: nn.Linear, gain: float) -> nn.Linear:
@@ -70,10 +71,22 @@ _ONES: dict = {}
 
 def _ones_row(m: int, like: torch.Tensor) -> torch.Tensor:
     key = (m, like.dtype, like.device)
-    if key not in _ONES:
-        _ONES.clear()
+    if key not in _ONES:  # kept for the process: captured update graphs hold these pointers
         _ONES[key] = torch.ones(1, m, dtype=like.dtype, device=like.device)
     return _ONES[key]
+
+
+def gather_rows(src: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+    """src[idx] for a row-major [n, w] tensor with 16-byte rows (vy_gather_rows;
+    torch's indexing gathers these 224-byte rows at ~0.85 TB/s)."""
+    row_bytes = src.shape[1] * src.element_size()
+    if not (src.is_cuda and src.dim() == 2 and src.is_contiguous() and row_bytes % 16 == 0):
+        raise ValueError("gather_rows needs a contiguous 2-D CUDA tensor with 16-byte-multiple rows")
+    idx = idx.to(torch.int64).contiguous()
+    out = torch.empty(idx.shape[0], src.shape[1], dtype=src.dtype, device=src.device)
+    nat.check(nat.lib().vy_gather_rows(src.data_ptr(), row_bytes, idx.data_ptr(), idx.shape[0], out.data_ptr(),
+                                       torch.cuda.current_stream().cuda_stream), "vy_gather_rows")
+    return out
 
 
 class _LinearFn(torch.autograd.Function):
@@ -247,7 +260,17 @@ class PPOTrainer:
         if self.world > 1:  # identical initial weights on every rank
             for p in self.net.parameters():
                 dist.broadcast(p.data, 0)
-        self.opt = torch.optim.Adam(self.net.parameters(), lr=cfg.lr, eps=1e-5, fused=True)
+        # one graph replay per update on a single GPU (the update is launch-bound
+        # otherwise: ~300 kernels per minibatch); with a gradient all-reduce
+        # the update stays eager
+        self._graph_update = cfg.graph_update and cfg.use_graph and self.world == 1
+        if self._graph_update:
+            self._lr = torch.tensor(cfg.lr, device=dev)
+            self.opt = torch.optim.Adam(self.net.parameters(), lr=self._lr, eps=1e-5, fused=True, capturable=True)
+        else:
+            self.opt = torch.optim.Adam(self.net.parameters(), lr=cfg.lr, eps=1e-5, fused=True)
+        self._ugraph = None
+        self._ustats: dict = {}
         T, B, L, A = cfg.rollout_steps, env.batch_size, env.obs_length, env.action_size
         self.obs = torch.zeros(T + 1, B, L, device=dev)
         self.actions = torch.zeros(T, B, A, dtype=torch.uint8, device=dev)
@@ -333,12 +356,33 @@ class PPOTrainer:
 
     def update(self) -> dict:
         cfg = self.cfg
+        lr = cfg.lr * max(1.0 - self.iterations / self.n_iters, 0.0) if cfg.anneal_lr else cfg.lr
+        if not self._graph_update:
+            for g in self.opt.param_groups:
+                g["lr"] = lr
+            stats = self._update_body()
+        else:
+            self._lr.fill_(lr)
+            if self._ugraph is None:
+                cur = torch.cuda.current_stream()
+                s = torch.cuda.Stream()
+                s.wait_stream(cur)
+                with torch.cuda.stream(s):  # this iteration's update, eager (warms up autograd / cuBLAS)
+                    stats = self._update_body()
+                cur.wait_stream(s)
+                self._ugraph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(self._ugraph):  # captured, not executed
+                    self._ustats = self._update_body()
+            else:
+                self._ugraph.replay()
+                stats = {k: v.clone() for k, v in self._ustats.items()}
+        self.iterations += 1
+        return stats
+
+    def _update_body(self) -> dict:
+        cfg = self.cfg
         T, B = cfg.rollout_steps, self.env.batch_size
         adv, ret = gae(self.values[:T], self.rewards, self.dones, self.values[T], cfg.gamma, cfg.gae_lambda)
-        if cfg.anneal_lr:
-            frac = 1.0 - self.iterations / self.n_iters
-            for g in self.opt.param_groups:
-                g["lr"] = cfg.lr * max(frac, 0.0)
         # aligned bf16 rows once per update (the value autocast would cast each
         # minibatch to anyway); minibatches gather half the bytes
         obs = self.net.pad_obs(self.obs[:T].reshape(T * B, -1)).to(torch.bfloat16)
@@ -349,11 +393,11 @@ class PPOTrainer:
         mb = n // cfg.n_minibatches
         stats = {}
         for _ in range(cfg.update_epochs):
-            perm = torch.randperm(n, device=obs.device)
+            perm = torch.argsort(torch.rand(n, device=obs.device))  # a uniform permutation, capture-safe
             for k in range(cfg.n_minibatches):
                 idx = perm[k * mb:(k + 1) * mb]
                 with torch.autocast("cuda", dtype=torch.bfloat16):
-                    logits, v = self.net(obs[idx], logits_fp32=not cfg.fused_head)
+                    logits, v = self.net(gather_rows(obs, idx), logits_fp32=not cfg.fused_head)
                     v = v.float()
                 if cfg.fused_head:
                     lp, ent = PolicyHead.apply(logits, act[idx], self.net.n_slots, self.net.n_actions)
@@ -374,7 +418,6 @@ class PPOTrainer:
                 self.opt.step()
                 stats = {"loss": loss.detach(), "pg": pg.detach(), "vf": vl.detach(), "ent": ent.detach()}
         self.obs[0].copy_(self.obs[T])
-        self.iterations += 1
         return stats
 
     def iterate(self) -> dict:

@@ -6,7 +6,10 @@ n, w, mb = 1228800, 112, 307200
 obs = torch.randn(n, w, device="cuda").to(torch.bfloat16)
 idx = torch.randperm(n, device="cuda")[:mb]
 act = torch.randint(0, 21, (n, 17), device="cuda", dtype=torch.uint8)
-fns = {"obs[idx]": lambda: obs[idx], "index_select": lambda: obs.index_select(0, idx),
+import sys
+sys.path.insert(0, ".")
+from paper_2507_01522_b200.ppo import gather_rows  # noqa: E402
+fns = {"vy_gather_rows": lambda: gather_rows(obs, idx), "obs[idx]": lambda: obs[idx], "index_select": lambda: obs.index_select(0, idx),
        "act[idx]": lambda: act[idx], "act index_select": lambda: act.index_select(0, idx),
        "sorted idx obs[idx]": lambda: obs[idx.sort().values]}
 for name, f in fns.items():

@@ -206,3 +206,14 @@ def test_linear_gemm_bias_grad_matches_torch(autocast):
     torch.testing.assert_close(scale(lin.weight.grad), scale(ref.weight.grad), **tol)
     torch.testing.assert_close(scale(lin.bias.grad), scale(ref.bias.grad), **tol)
     torch.testing.assert_close(scale(x.grad), scale(x2.grad), **tol)
+
+
+def test_gather_rows_equals_indexing():
+    from paper_2507_01522_b200.ppo import gather_rows
+
+    src = torch.randn(5000, 112, device="cuda").to(torch.bfloat16)
+    idx = torch.randint(0, 5000, (3001,), device="cuda")
+    torch.testing.assert_close(gather_rows(src, idx), src[idx], rtol=0, atol=0)
+    assert gather_rows(src, idx[:0]).shape == (0, 112)
+    with pytest.raises(ValueError):
+        gather_rows(src[:, :7], idx)
