@@ -13,8 +13,9 @@
 //   the stored actions and entropy (sum over slots), and the gradient of
 //   g_lp * lp + g_ent * ent with respect to the logits, each one read of the
 //   [N][S][A] logits (the unfused torch graph made ~10 passes over them).
-//   Sampling: one warp per sample, lanes over slots; the head: one thread per
-//   (sample, slot), whole rows staged per block.
+//   Both: one thread per (sample, slot), whole rows staged per block.
+//   vy_ppo_sample_rng draws the sampler's uniforms in the kernel (no noise
+//   tensor), with a device call counter so graph replays need no host work.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -45,73 +46,11 @@ __global__ void k_gae(const float* __restrict__ values, const float* __restrict_
   }
 }
 
-// One warp per sample: the sample's S*A logits are staged in shared memory
-// with coalesced loads (float32, or bf16 straight from the autocast GEMM),
-// then lane s owns slot s (slots start A words apart: bank-conflict free for
-// odd A such as the 21-action head), and gradients leave through the same
-// staging row with coalesced stores.
-
 __device__ __forceinline__ float to_f(float v) { return v; }
 __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
 template <class T> __device__ __forceinline__ T from_f(float v);
 template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
 template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
-
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// per-slot max and log-sum-exp of A staged logits
-__device__ __forceinline__ void slot_lse(const float* z, int A, float& lse) {
-  float m = -INFINITY;
-  for (int k = 0; k < A; ++k) m = fmaxf(m, z[k]);
-  float sum = 0.f;
-  for (int k = 0; k < A; ++k) sum += __expf(z[k] - m);
-  lse = m + __logf(sum);
-}
-
-template <class T>
-__device__ __forceinline__ float* stage_row(const T* __restrict__ src, int64_t n, int SA, int64_t ld, int lane) {
-  extern __shared__ float ppo_smem[];
-  float* row = ppo_smem + (threadIdx.x >> 5) * SA;
-  const T* g = src + n * ld;
-  for (int e = lane; e < SA; e += 32) row[e] = to_f(g[e]);
-  __syncwarp();
-  return row;
-}
-
-template <class T>
-__global__ void k_ppo_sample(const T* __restrict__ logits, const float* __restrict__ noise, int64_t N, int S, int A,
-                             int64_t ld, uint8_t* __restrict__ actions, float* __restrict__ logp) {
-  const int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (n >= N) return;
-  const int SA = S * A;
-  float* row = stage_row(logits, n, SA, ld, lane);
-  float acc = 0.f;
-  for (int s = lane; s < S; s += 32) {
-    const float* z = row + s * A;
-    const float* u = noise + (n * S + s) * A;
-    float lse;
-    slot_lse(z, A, lse);
-    int best = 0;
-    float bv = -INFINITY;
-    for (int k = 0; k < A; ++k) {
-      const float g = -__logf(-__logf(fminf(fmaxf(u[k], 1e-20f), 1.f)));  // Gumbel(0, 1)
-      const float v = z[k] + g;
-      if (v > bv) {
-        bv = v;
-        best = k;
-      }
-    }
-    actions[n * S + s] = (uint8_t)best;
-    acc += z[best] - lse;
-  }
-  acc = warp_sum(acc);
-  if (lane == 0) logp[n] = acc;
-}
 
 // The update's head runs on minibatches of ~300k samples, so it is laid out
 // for bandwidth: a block stages G whole rows (G*ld values, contiguous in
@@ -254,6 +193,74 @@ __global__ void k_gather_rows(const uint4* __restrict__ src, I vpr, const int64_
   }
 }
 
+// Rollout sampling, laid out like the head: G rows staged per block, one
+// thread per (sample, slot) takes argmax_k z_k + Gumbel_k and adds the
+// action's log-probability; per-sample sums through shared memory.  Uniforms
+// come from `noise` [N][S][A] or, when it is NULL, from the splitmix64 stream
+// of (seed, call, element): call = counter[0], bumped by the last block to
+// finish (counter[1] counts finished blocks), so a CUDA-graph replay draws
+// fresh noise with no host involvement.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+template <class T>
+__global__ void __launch_bounds__(kHeadThreads) k_ppo_sample(const T* __restrict__ logits,
+                                                             const float* __restrict__ noise, uint64_t seed,
+                                                             unsigned long long* counter, int64_t N, int S, int A,
+                                                             int64_t ld, int G, uint8_t* __restrict__ actions,
+                                                             float* __restrict__ logp) {
+  extern __shared__ float ppo_smem[];
+  const int64_t n0 = (int64_t)blockIdx.x * G;
+  const int gh = (int)min((int64_t)G, N - n0);
+  float* rows = ppo_smem;
+  float* part = ppo_smem + (size_t)G * ld;
+  stage_rows(logits + n0 * ld, (int64_t)gh * ld, rows);
+  const uint64_t key = noise ? 0 : mix64(seed ^ mix64(counter[0] + 0x9E3779B97F4A7C15ULL));
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < gh * S) {
+    const int r = t / S, s = t - r * S;
+    const float* z = rows + (size_t)r * ld + s * A;
+    float m, logsum, inv, h;
+    slot_stats(z, A, m, logsum, inv, h);
+    const int64_t e0 = ((n0 + r) * S + s) * A;
+    int best = 0;
+    float bv = -INFINITY;
+    for (int k = 0; k < A; ++k) {
+      float u;
+      if (noise) {
+        u = fminf(fmaxf(noise[e0 + k], 1e-20f), 1.f);
+      } else {
+        u = ((float)(mix64(key + (uint64_t)(e0 + k) * 0x9E3779B97F4A7C15ULL) >> 40) + 0.5f) * (1.f / 16777216.f);
+      }
+      const float v = z[k] - __logf(-__logf(u));  // + Gumbel(0, 1)
+      if (v > bv) {
+        bv = v;
+        best = k;
+      }
+    }
+    actions[(n0 + r) * S + s] = (uint8_t)best;
+    part[t] = (z[best] - m) - logsum;
+  }
+  __syncthreads();
+  if (t < gh) {
+    float acc = 0.f;
+    for (int s = 0; s < S; ++s) acc += part[t * S + s];
+    logp[n0 + t] = acc;
+  }
+  if (!noise && t == 0) {
+    __threadfence();
+    if (atomicAdd(counter + 1, 1ull) == gridDim.x - 1) {  // last block: every block has read counter[0]
+      counter[1] = 0;
+      counter[0] += 1;
+      __threadfence();
+    }
+  }
+}
+
 int head_rows(int S) { return S <= kHeadThreads ? kHeadThreads / S : 0; }
 size_t head_smem(int S, int64_t ld) {
   const int G = head_rows(S);
@@ -261,26 +268,38 @@ size_t head_smem(int S, int64_t ld) {
 }
 unsigned head_grid(int64_t N, int S) { return (unsigned)((N + head_rows(S) - 1) / head_rows(S)); }
 
-constexpr int kWarpsPerBlock = 8;
-unsigned warp_grid(int64_t N) { return (unsigned)((N + kWarpsPerBlock - 1) / kWarpsPerBlock); }
-size_t row_smem(int S, int A) { return (size_t)kWarpsPerBlock * S * A * sizeof(float); }
-
 }  // namespace
 
 // dtype: 0 = float32 logits (and gradient), 1 = bfloat16
-extern "C" int vy_ppo_sample(const void* logits, int32_t dtype, int64_t ld, const float* noise, int64_t N, int32_t S,
-                             int32_t A, uint8_t* actions, float* logp, void* stream) {
-  if (!logits || !noise || !actions || !logp || N < 1 || S < 1 || A < 1 || A > 256 || (dtype != 0 && dtype != 1) ||
-      row_smem(S, A) > 48 * 1024 || ld < (int64_t)S * A)
+namespace {
+int launch_sample(const void* logits, int32_t dtype, int64_t ld, const float* noise, uint64_t seed, int64_t* counter,
+                  int64_t N, int32_t S, int32_t A, uint8_t* actions, float* logp, void* stream) {
+  if (!logits || !actions || !logp || N < 1 || S < 1 || A < 1 || A > 256 || (dtype != 0 && dtype != 1) ||
+      head_rows(S) < 1 || ld < (int64_t)S * A || head_smem(S, ld) > 48 * 1024)
     return VY_ERR_ARG;
   auto st = (cudaStream_t)stream;
+  const int G = head_rows(S);
+  auto ctr = reinterpret_cast<unsigned long long*>(counter);
   if (dtype == 0)
-    k_ppo_sample<float><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
-        static_cast<const float*>(logits), noise, N, S, A, ld, actions, logp);
+    k_ppo_sample<float><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+        static_cast<const float*>(logits), noise, seed, ctr, N, S, A, ld, G, actions, logp);
   else
-    k_ppo_sample<__nv_bfloat16><<<warp_grid(N), kWarpsPerBlock * 32, row_smem(S, A), st>>>(
-        static_cast<const __nv_bfloat16*>(logits), noise, N, S, A, ld, actions, logp);
+    k_ppo_sample<__nv_bfloat16><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+        static_cast<const __nv_bfloat16*>(logits), noise, seed, ctr, N, S, A, ld, G, actions, logp);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
+}
+}  // namespace
+
+extern "C" int vy_ppo_sample(const void* logits, int32_t dtype, int64_t ld, const float* noise, int64_t N, int32_t S,
+                             int32_t A, uint8_t* actions, float* logp, void* stream) {
+  if (!noise) return VY_ERR_ARG;
+  return launch_sample(logits, dtype, ld, noise, 0, nullptr, N, S, A, actions, logp, stream);
+}
+
+extern "C" int vy_ppo_sample_rng(const void* logits, int32_t dtype, int64_t ld, uint64_t seed, int64_t* counter,
+                                 int64_t N, int32_t S, int32_t A, uint8_t* actions, float* logp, void* stream) {
+  if (!counter) return VY_ERR_ARG;
+  return launch_sample(logits, dtype, ld, nullptr, seed, counter, N, S, A, actions, logp, stream);
 }
 
 extern "C" int vy_ppo_head_fwd(const void* logits, int32_t dtype, int64_t ld, const uint8_t* actions, int64_t N,

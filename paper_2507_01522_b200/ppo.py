@@ -271,6 +271,9 @@ class PPOTrainer:
             self.opt = torch.optim.Adam(self.net.parameters(), lr=cfg.lr, eps=1e-5, fused=True)
         self._ugraph = None
         self._ustats: dict = {}
+        # rollout sampler stream: per-rank seed, {call, scratch} counter on the device
+        self._sample_seed = (cfg.seed * 0x9E3779B1 + env.global_offset + 1) & ((1 << 64) - 1)
+        self._sample_ctr = torch.zeros(2, dtype=torch.int64, device=dev)
         T, B, L, A = cfg.rollout_steps, env.batch_size, env.obs_length, env.action_size
         self.obs = torch.zeros(T + 1, B, L, device=dev)
         self.actions = torch.zeros(T, B, A, dtype=torch.uint8, device=dev)
@@ -289,15 +292,16 @@ class PPOTrainer:
     def _policy_step(self, t: int) -> None:
         fused = self.cfg.fused_head
         logits, v = self.net(self.obs[t], logits_fp32=not fused)
-        noise = torch.rand(logits.shape[0], self.net.n_slots, self.net.n_actions, device=logits.device)
         if fused:
-            # Gumbel-max sampling + log-probability in one kernel, straight into the rollout buffers
+            # Gumbel-max sampling (uniforms drawn in the kernel, call counter on
+            # the device) + log-probability in one kernel, into the rollout buffers
             B, S, A = logits.shape[0], self.net.n_slots, self.net.n_actions
-            nat.check(nat.lib().vy_ppo_sample(logits.data_ptr(), _dtype_code(logits), logits.stride(0),
-                                              noise.data_ptr(), B, S, A,
-                                              self.actions[t].data_ptr(), self.logp[t].data_ptr(),
-                                              torch.cuda.current_stream().cuda_stream), "vy_ppo_sample")
+            nat.check(nat.lib().vy_ppo_sample_rng(logits.data_ptr(), _dtype_code(logits), logits.stride(0),
+                                                  self._sample_seed, self._sample_ctr.data_ptr(), B, S, A,
+                                                  self.actions[t].data_ptr(), self.logp[t].data_ptr(),
+                                                  torch.cuda.current_stream().cuda_stream), "vy_ppo_sample_rng")
         else:
+            noise = torch.rand(logits.shape[0], self.net.n_slots, self.net.n_actions, device=logits.device)
             g = -torch.log(-torch.log(noise.clamp_(1e-20, 1.0)))  # Gumbel-max sampling
             a = torch.argmax(logits + g, dim=-1)
             lp = torch.log_softmax(logits, dim=-1).gather(-1, a.unsqueeze(-1)).squeeze(-1).sum(-1)

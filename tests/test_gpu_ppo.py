@@ -217,3 +217,36 @@ def test_gather_rows_equals_indexing():
     assert gather_rows(src, idx[:0]).shape == (0, 112)
     with pytest.raises(ValueError):
         gather_rows(src[:, :7], idx)
+
+
+def test_in_kernel_rng_sampler_draws_the_softmax():
+    """vy_ppo_sample_rng: action frequencies follow softmax(logits), the
+    log-probability is that of the pick, the device call counter advances once
+    per launch, and (seed, call) reproduces the draw."""
+    from paper_2507_01522_b200 import _native as nat
+
+    N, S, A = 1 << 16, 3, 5
+    z = torch.tensor([0.0, 1.0, -1.0, 2.0, 0.5], device="cuda").repeat(N, S, 1).contiguous()
+    probs = torch.softmax(z[0, 0], -1)
+    ctr = torch.zeros(2, dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+
+    def draw():
+        act = torch.empty(N, S, dtype=torch.uint8, device="cuda")
+        lp = torch.empty(N, device="cuda")
+        nat.check(nat.lib().vy_ppo_sample_rng(z.data_ptr(), 0, S * A, 1234, ctr.data_ptr(), N, S, A,
+                                              act.data_ptr(), lp.data_ptr(), st), "vy_ppo_sample_rng")
+        return act, lp
+
+    a1, lp1 = draw()
+    assert ctr.tolist() == [1, 0]
+    a2, _ = draw()
+    assert ctr.tolist() == [2, 0]
+    assert (a1 != a2).float().mean() > 0.3
+    freq = torch.bincount(a1.long().reshape(-1), minlength=A).float() / (N * S)
+    torch.testing.assert_close(freq, probs, rtol=0, atol=6e-3)  # ~5 sigma at 196k draws
+    lp_r = torch.log_softmax(z, -1).gather(-1, a1.long().unsqueeze(-1)).squeeze(-1).sum(-1)
+    torch.testing.assert_close(lp1, lp_r, rtol=1e-5, atol=1e-4)
+    ctr.zero_()
+    a3, _ = draw()
+    assert torch.equal(a1, a3)
