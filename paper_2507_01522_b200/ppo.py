@@ -274,6 +274,7 @@ class PPOTrainer:
         # rollout sampler stream: per-rank seed, {call, scratch} counter on the device
         self._sample_seed = (cfg.seed * 0x9E3779B1 + env.global_offset + 1) & ((1 << 64) - 1)
         self._sample_ctr = torch.zeros(2, dtype=torch.int64, device=dev)
+        self._xin = torch.zeros(env.batch_size, self.net.in_dim, dtype=torch.bfloat16, device=dev)
         T, B, L, A = cfg.rollout_steps, env.batch_size, env.obs_length, env.action_size
         self.obs = torch.zeros(T + 1, B, L, device=dev)
         self.actions = torch.zeros(T, B, A, dtype=torch.uint8, device=dev)
@@ -291,7 +292,10 @@ class PPOTrainer:
 
     def _policy_step(self, t: int) -> None:
         fused = self.cfg.fused_head
-        logits, v = self.net(self.obs[t], logits_fp32=not fused)
+        # the padded bf16 network input in one copy (the zero padding columns of
+        # the persistent buffer are never written): no pad + cast pair per step
+        self._xin[:, : self.env.obs_length].copy_(self.obs[t])
+        logits, v = self.net(self._xin, logits_fp32=not fused)
         if fused:
             # Gumbel-max sampling (uniforms drawn in the kernel, call counter on
             # the device) + log-probability in one kernel, into the rollout buffers
@@ -319,7 +323,8 @@ class PPOTrainer:
         with torch.autocast("cuda", dtype=torch.bfloat16):
             for t in range(self.cfg.rollout_steps):
                 self._policy_step(t)
-            _, v = self.net(self.obs[-1])
+            self._xin[:, : self.env.obs_length].copy_(self.obs[-1])
+            _, v = self.net(self._xin)
             self.values[-1].copy_(v)
 
     @torch.no_grad()
