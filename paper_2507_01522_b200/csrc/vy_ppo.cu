@@ -94,17 +94,39 @@ __device__ __forceinline__ void store_rows(const float* __restrict__ src, int64_
   }
 }
 
-// One slot's softmax statistics from its A staged logits z, with a single
-// exp per value: m = max z, e_k = exp(z_k - m), sum = sum e_k,
-// logsum = log(sum), lse = m + logsum, and the entropy
-// H = -sum p_k (z_k - lse) = logsum - sum(e_k (z_k - m)) / sum.
-__device__ __forceinline__ void slot_stats(const float* z, int A, float& m, float& logsum, float& inv, float& h) {
+// One slot's A logits: in registers when A is a compile-time constant AC
+// (the 21-action head: one shared-memory read per logit instead of one per
+// pass — the kernels were bound by shared-memory instructions), else read
+// from the staged row.
+template <int AC>
+struct Slot {
+  float r[AC > 0 ? AC : 1];
+  const float* p;
+  int a;
+  __device__ __forceinline__ Slot(const float* src, int A) : p(src), a(A) {
+    if constexpr (AC > 0) {
+#pragma unroll
+      for (int k = 0; k < AC; ++k) r[k] = src[k];
+    }
+  }
+  __device__ __forceinline__ int size() const { return AC > 0 ? AC : a; }
+  __device__ __forceinline__ float operator[](int k) const {
+    if constexpr (AC > 0) return r[k];
+    else return p[k];
+  }
+};
+
+// One slot's softmax statistics with a single exp per value: m = max z,
+// e_k = exp(z_k - m), sum = sum e_k, logsum = log(sum), lse = m + logsum, and
+// the entropy H = -sum p_k (z_k - lse) = logsum - sum(e_k (z_k - m)) / sum.
+template <int AC>
+__device__ __forceinline__ void slot_stats(const Slot<AC>& z, float& m, float& logsum, float& inv, float& h) {
   m = -INFINITY;
-#pragma unroll 4
-  for (int k = 0; k < A; ++k) m = fmaxf(m, z[k]);
+#pragma unroll
+  for (int k = 0; k < z.size(); ++k) m = fmaxf(m, z[k]);
   float sum = 0.f, ed = 0.f;
-#pragma unroll 4
-  for (int k = 0; k < A; ++k) {
+#pragma unroll
+  for (int k = 0; k < z.size(); ++k) {
     const float d = z[k] - m, e = __expf(d);
     sum += e;
     ed += e * d;
@@ -114,7 +136,7 @@ __device__ __forceinline__ void slot_stats(const float* z, int A, float& m, floa
   h = logsum - ed * inv;
 }
 
-template <class T>
+template <class T, int AC>
 __global__ void __launch_bounds__(kHeadThreads) k_ppo_head_fwd(const T* __restrict__ logits,
                                                                const uint8_t* __restrict__ actions, int64_t N, int S,
                                                                int A, int64_t ld, int G, float* __restrict__ lp,
@@ -129,10 +151,11 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_head_fwd(const T* __restri
   const int t = threadIdx.x;
   if (t < gh * S) {
     const int r = t / S, s = t - r * S;
-    const float* z = rows + (size_t)r * ld + s * A;
+    const float* zs = rows + (size_t)r * ld + s * A;
+    const Slot<AC> z(zs, A);
     float m, logsum, inv, h;
-    slot_stats(z, A, m, logsum, inv, h);
-    part[t] = (z[actions[(n0 + r) * S + s]] - m) - logsum;
+    slot_stats(z, m, logsum, inv, h);
+    part[t] = (zs[actions[(n0 + r) * S + s]] - m) - logsum;
     part[G * S + t] = h;
   }
   __syncthreads();
@@ -148,7 +171,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_head_fwd(const T* __restri
 }
 
 // d(g_lp * lp + g_ent * ent) / dz_k = g_lp (1[k = a] - p_k) - g_ent p_k (log p_k + H), H = slot entropy
-template <class T>
+template <class T, int AC>
 __global__ void __launch_bounds__(kHeadThreads) k_ppo_head_bwd(const T* __restrict__ logits,
                                                                const uint8_t* __restrict__ actions, int64_t N, int S,
                                                                int A, int64_t ld, int G,
@@ -164,15 +187,16 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_head_bwd(const T* __restri
   const int t = threadIdx.x;
   if (t < gh * S) {
     const int r = t / S, s = t - r * S;
-    float* z = rows + (size_t)r * ld + s * A;
+    float* zs = rows + (size_t)r * ld + s * A;
+    const Slot<AC> z(zs, A);
     float m, logsum, inv, h;
-    slot_stats(z, A, m, logsum, inv, h);
+    slot_stats(z, m, logsum, inv, h);
     const float gl = g_lp ? g_lp[n0 + r] : 0.f, ge = g_ent ? g_ent[n0 + r] : 0.f;
     const int a = actions[(n0 + r) * S + s];
-#pragma unroll 4
-    for (int k = 0; k < A; ++k) {  // in place: this thread owns the slot's values
+#pragma unroll
+    for (int k = 0; k < z.size(); ++k) {  // in place: this thread owns the slot's values
       const float d = z[k] - m, p = __expf(d) * inv, l = d - logsum;
-      z[k] = gl * ((k == a ? 1.f : 0.f) - p) - ge * p * (l + h);
+      zs[k] = gl * ((k == a ? 1.f : 0.f) - p) - ge * p * (l + h);
     }
   }
   const int pad = (int)(ld - SA);
@@ -206,7 +230,7 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-template <class T>
+template <class T, int AC>
 __global__ void __launch_bounds__(kHeadThreads) k_ppo_sample(const T* __restrict__ logits,
                                                              const float* __restrict__ noise, uint64_t seed,
                                                              unsigned long long* counter, int64_t N, int S, int A,
@@ -223,13 +247,15 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_sample(const T* __restrict
   const int t = threadIdx.x;
   if (t < gh * S) {
     const int r = t / S, s = t - r * S;
-    const float* z = rows + (size_t)r * ld + s * A;
+    const float* zs = rows + (size_t)r * ld + s * A;
+    const Slot<AC> z(zs, A);
     float m, logsum, inv, h;
-    slot_stats(z, A, m, logsum, inv, h);
+    slot_stats(z, m, logsum, inv, h);
     const int64_t e0 = ((n0 + r) * S + s) * A;
     int best = 0;
     float bv = -INFINITY;
-    for (int k = 0; k < A; ++k) {
+#pragma unroll
+    for (int k = 0; k < z.size(); ++k) {
       float u;
       if (noise) {
         u = fminf(fmaxf(noise[e0 + k], 1e-20f), 1.f);
@@ -243,7 +269,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_sample(const T* __restrict
       }
     }
     actions[(n0 + r) * S + s] = (uint8_t)best;
-    part[t] = (z[best] - m) - logsum;
+    part[t] = (zs[best] - m) - logsum;
   }
   __syncthreads();
   if (t < gh) {
@@ -280,12 +306,21 @@ int launch_sample(const void* logits, int32_t dtype, int64_t ld, const float* no
   auto st = (cudaStream_t)stream;
   const int G = head_rows(S);
   auto ctr = reinterpret_cast<unsigned long long*>(counter);
-  if (dtype == 0)
-    k_ppo_sample<float><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+  if (dtype == 0) {
+    if (A == 21)
+      k_ppo_sample<float, 21><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
         static_cast<const float*>(logits), noise, seed, ctr, N, S, A, ld, G, actions, logp);
-  else
-    k_ppo_sample<__nv_bfloat16><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+    else
+      k_ppo_sample<float, 0><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+        static_cast<const float*>(logits), noise, seed, ctr, N, S, A, ld, G, actions, logp);
+  } else {
+    if (A == 21)
+      k_ppo_sample<__nv_bfloat16, 21><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
         static_cast<const __nv_bfloat16*>(logits), noise, seed, ctr, N, S, A, ld, G, actions, logp);
+    else
+      k_ppo_sample<__nv_bfloat16, 0><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+        static_cast<const __nv_bfloat16*>(logits), noise, seed, ctr, N, S, A, ld, G, actions, logp);
+  }
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 }  // namespace
@@ -309,12 +344,21 @@ extern "C" int vy_ppo_head_fwd(const void* logits, int32_t dtype, int64_t ld, co
     return VY_ERR_ARG;
   auto st = (cudaStream_t)stream;
   const int G = head_rows(S);
-  if (dtype == 0)
-    k_ppo_head_fwd<float><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+  if (dtype == 0) {
+    if (A == 21)
+      k_ppo_head_fwd<float, 21><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
         static_cast<const float*>(logits), actions, N, S, A, ld, G, lp, ent);
-  else
-    k_ppo_head_fwd<__nv_bfloat16><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+    else
+      k_ppo_head_fwd<float, 0><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+        static_cast<const float*>(logits), actions, N, S, A, ld, G, lp, ent);
+  } else {
+    if (A == 21)
+      k_ppo_head_fwd<__nv_bfloat16, 21><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
         static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, lp, ent);
+    else
+      k_ppo_head_fwd<__nv_bfloat16, 0><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, lp, ent);
+  }
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 
@@ -325,13 +369,23 @@ extern "C" int vy_ppo_head_bwd(const void* logits, int32_t dtype, int64_t ld, co
     return VY_ERR_ARG;
   auto st = (cudaStream_t)stream;
   const int G = head_rows(S);
-  if (dtype == 0)
-    k_ppo_head_bwd<float><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+  if (dtype == 0) {
+    if (A == 21)
+      k_ppo_head_bwd<float, 21><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
         static_cast<const float*>(logits), actions, N, S, A, ld, G, g_lp, g_ent, static_cast<float*>(grad));
-  else
-    k_ppo_head_bwd<__nv_bfloat16><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+    else
+      k_ppo_head_bwd<float, 0><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+        static_cast<const float*>(logits), actions, N, S, A, ld, G, g_lp, g_ent, static_cast<float*>(grad));
+  } else {
+    if (A == 21)
+      k_ppo_head_bwd<__nv_bfloat16, 21><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
         static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, g_lp, g_ent,
         static_cast<__nv_bfloat16*>(grad));
+    else
+      k_ppo_head_bwd<__nv_bfloat16, 0><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
+        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, g_lp, g_ent,
+        static_cast<__nv_bfloat16*>(grad));
+  }
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 
