@@ -384,8 +384,8 @@ def main() -> None:
                          "minibatches": cfg.n_minibatches, "hidden": cfg.hidden, "timed_iterations": args.ppo_iters,
                          "rollout": "CUDA graph (policy fwd bf16 + vy_ppo_sample_rng Gumbel-max kernel with in-kernel uniforms + k_step) x 300",
                          "update": ("one CUDA graph per update on 1 GPU (eager with the all-reduce): vy_gae, "
-                                    "vy_gather_rows minibatch gather, bf16 GEMMs at 8-aligned widths with GEMM bias "
-                                    "gradients, vy_ppo_head_fwd/_bwd fused log-prob/entropy head, fused Adam"),
+                                    "vy_gather_rows minibatch gather, bf16 GEMMs at 8-aligned widths with column-sum bias "
+                                    "gradients (vy_colsum), vy_ppo_head_fwd/_bwd fused log-prob/entropy head, fused Adam"),
                          "grad_allreduce": "NCCL all_reduce(AVG) per minibatch" if world > 1 else "none (1 GPU)",
                          "paper_reference": "Chargax PPO(16) 0.65 s / 100k on RTX 4000 Ada (PAPER.md:239)"}
         penv.close()

@@ -287,6 +287,31 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_sample(const T* __restrict
   }
 }
 
+// Column sums of a row-major [M][N] matrix (a linear layer's bias
+// gradient): each block walks a band of rows with one thread per column,
+// accumulating in float32 (rows are read whole and coalesced), then adds its
+// partial sums into out[N] with one atomic per column.  One pass over the
+// matrix at HBM rate, vs ~2.5-4x that for torch's sum(0) at these shapes.
+template <class T>
+__global__ void __launch_bounds__(512) k_colsum(const T* __restrict__ g, int64_t M, int N, int64_t ld, int64_t rows_per_block,
+                         float* __restrict__ out) {
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
+  const int64_t r1 = min(M, r0 + rows_per_block);
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    int64_t r = r0;
+    for (; r + 8 <= r1; r += 8) {  // eight independent loads in flight per thread
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = to_f(g[(r + j) * ld + c]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc += v[j];
+    }
+    for (; r < r1; ++r) acc += to_f(g[r * ld + c]);
+    atomicAdd(out + c, acc);
+  }
+}
+
 int head_rows(int S) { return S <= kHeadThreads ? kHeadThreads / S : 0; }
 size_t head_smem(int S, int64_t ld) {
   const int G = head_rows(S);
@@ -404,6 +429,25 @@ extern "C" int vy_gather_rows(const void* src, int64_t row_bytes, const int64_t*
   else
     k_gather_rows<int64_t><<<grid, 256, 0, st>>>(static_cast<const uint4*>(src), vpr, idx, total,
                                                  static_cast<uint4*>(dst));
+  return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
+}
+
+extern "C" int vy_colsum(const void* g, int32_t dtype, int64_t M, int64_t N, int64_t ld, float* out, void* stream) {
+  if (!out || M < 0 || N < 1 || N > (1 << 20) || ld < N || (dtype != 0 && dtype != 1)) return VY_ERR_ARG;
+  if (M == 0) return VY_OK;
+  if (!g) return VY_ERR_ARG;
+  const int threads = N >= 512 ? 512 : ((int)N + 31) / 32 * 32;  // one x-block up to 512 columns
+  const unsigned gx = (unsigned)((N + threads - 1) / threads);
+  // enough row bands to fill the GPU a few times over, at least 64 rows each
+  int64_t bands = std::max<int64_t>(1, 148 * 8 / (int64_t)gx);
+  int64_t rpb = std::max<int64_t>(64, (M + bands - 1) / bands);
+  bands = (M + rpb - 1) / rpb;
+  const dim3 grid(gx, (unsigned)bands);
+  auto st = (cudaStream_t)stream;
+  if (dtype == 0)
+    k_colsum<float><<<grid, threads, 0, st>>>(static_cast<const float*>(g), M, (int)N, ld, rpb, out);
+  else
+    k_colsum<__nv_bfloat16><<<grid, threads, 0, st>>>(static_cast<const __nv_bfloat16*>(g), M, (int)N, ld, rpb, out);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 

@@ -66,16 +66,6 @@ def _ortho(layer: nn.Linear, gain: float) -> nn.Linear:
     return layer
 
 
-_ONES: dict = {}
-
-
-def _ones_row(m: int, like: torch.Tensor) -> torch.Tensor:
-    key = (m, like.dtype, like.device)
-    if key not in _ONES:  # kept for the process: captured update graphs hold these pointers
-        _ONES[key] = torch.ones(1, m, dtype=like.dtype, device=like.device)
-    return _ONES[key]
-
-
 def gather_rows(src: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
     """src[idx] for a row-major [n, w] tensor with 16-byte rows (vy_gather_rows;
     torch's indexing gathers these 224-byte rows at ~0.85 TB/s)."""
@@ -89,10 +79,22 @@ def gather_rows(src: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def colsum(g: torch.Tensor) -> torch.Tensor:
+    """Float32 column sums of a 2-D CUDA tensor (float32 / bf16, unit column
+    stride) via vy_colsum: one pass at HBM rate."""
+    if g.dim() != 2 or g.stride(1) != 1:
+        raise ValueError("colsum needs a 2-D tensor with unit column stride")
+    out = torch.zeros(g.shape[1], dtype=torch.float32, device=g.device)
+    nat.check(nat.lib().vy_colsum(g.data_ptr(), _dtype_code(g), g.shape[0], g.shape[1], g.stride(0),
+                                  out.data_ptr(), torch.cuda.current_stream().cuda_stream), "vy_colsum")
+    return out
+
+
 class _LinearFn(torch.autograd.Function):
-    """y = x W^T + b whose backward forms the bias gradient as a [1 x M] @ [M x N]
-    GEMM with a ones row instead of a column reduction: on the update's ~300k-row
-    minibatches torch's sum(0) ran 2.5-4x slower (scripts/micro/bias_grad.py)."""
+    """y = x W^T + b whose backward forms the bias gradient with vy_colsum
+    (one pass over the output gradient) instead of torch's sum(0), which ran
+    2.5-4x slower on the update's ~300k-row minibatches
+    (scripts/micro/bias_grad.py)."""
 
     @staticmethod
     @torch.amp.custom_fwd(device_type="cuda", cast_inputs=torch.bfloat16)
@@ -107,7 +109,7 @@ class _LinearFn(torch.autograd.Function):
         g = g.contiguous()
         dx = g @ w if ctx.needs_input_grad[0] else None
         dw = g.t() @ x
-        db = (_ones_row(g.shape[0], g) @ g).view(-1)
+        db = colsum(g).to(g.dtype)
         return dx, dw, db
 
 

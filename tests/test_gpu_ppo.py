@@ -250,3 +250,13 @@ def test_in_kernel_rng_sampler_draws_the_softmax():
     ctr.zero_()
     a3, _ = draw()
     assert torch.equal(a1, a3)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_colsum_matches_torch(dtype):
+    from paper_2507_01522_b200.ppo import colsum
+
+    g = torch.randn(30001, 360, device="cuda").to(dtype)
+    torch.testing.assert_close(colsum(g), g.float().sum(0), rtol=1e-4, atol=1e-2)
+    torch.testing.assert_close(colsum(g[:, :357]), g[:, :357].float().sum(0), rtol=1e-4, atol=1e-2)
+    torch.testing.assert_close(colsum(g[:5, :1]), g[:5, :1].float().sum(0), rtol=1e-4, atol=1e-4)
