@@ -257,10 +257,13 @@ int vy_ppo_head_bwd(const void *logits, int32_t dtype, int64_t ld, const uint8_t
 /* PPO minibatch gather: dst row i = src row idx[i] for i < n, rows of
  * row_bytes bytes (a multiple of 16; src and dst 16-byte aligned). */
 int vy_gather_rows(const void *src, int64_t row_bytes, const int64_t *idx, int64_t n, void *dst, void *stream);
-/* Column sums (a linear layer's bias gradient): out[c] += sum over m < M of
- * g[m*ld + c], c < N; g float32 (dtype 0) or bfloat16 (1); out float32,
- * accumulated into (zero it first). */
-int vy_colsum(const void *g, int32_t dtype, int64_t M, int64_t N, int64_t ld, float *out, void *stream);
+/* Column sums (a linear layer's bias gradient): out[c] = sum over m < M of
+ * g[m*ld + c], c < N; g float32 (dtype 0) or bfloat16 (1); out float32.
+ * work: float32 scratch of VY_COLSUM_BANDS * N values.  Deterministic (no
+ * atomics: per-band partial sums, then the bands added in order). */
+#define VY_COLSUM_BANDS 512
+int vy_colsum(const void *g, int32_t dtype, int64_t M, int64_t N, int64_t ld, float *work, float *out,
+              void *stream);
 
 /* Diagnostics: compare the kernels' reciprocal-based division (div_rcp in
  * csrc/vy_device.cuh) with IEEE x / d on `samples_per_divisor` random

@@ -16,6 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libvoltyard_b200.so"
 
 VY_OK, VY_ERR_ARG, VY_ERR_CUDA, VY_ERR_UNSUPPORTED, VY_ERR_STATE = 0, 1, 2, 3, 4
 VY_ACT_U8, VY_ACT_I32, VY_ACT_I64 = 0, 1, 2
+COLSUM_BANDS = 512  # VY_COLSUM_BANDS
 F_AUTO_RESET, F_INFOS, F_INJECT, F_OUT_F64 = 1, 2, 4, 8
 
 _P = C.c_void_p
@@ -68,7 +69,7 @@ _SIGS = {
     "vy_ppo_head_fwd": (C.c_int, [_P, C.c_int32, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]),
     "vy_ppo_head_bwd": (C.c_int, [_P, C.c_int32, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P, _P]),
     "vy_gather_rows": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, _P]),
-    "vy_colsum": (C.c_int, [_P, C.c_int32, C.c_int64, C.c_int64, C.c_int64, _P, _P]),
+    "vy_colsum": (C.c_int, [_P, C.c_int32, C.c_int64, C.c_int64, C.c_int64, _P, _P, _P]),
     "vy_selftest_div": (C.c_int, [C.POINTER(C.c_double), C.c_int32, C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),
 }
 

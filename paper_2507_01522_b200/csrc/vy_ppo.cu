@@ -288,19 +288,22 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_sample(const T* __restrict
 }
 
 // Column sums of a row-major [M][N] matrix (a linear layer's bias
-// gradient): each block walks a band of rows with one thread per column,
-// accumulating in float32 (rows are read whole and coalesced), then adds its
-// partial sums into out[N] with one atomic per column.  One pass over the
-// matrix at HBM rate, vs ~2.5-4x that for torch's sum(0) at these shapes.
+// gradient) in two deterministic passes: each block of the first walks a
+// band of rows with one thread per column (rows read whole and coalesced,
+// eight loads in flight per thread) and writes its float32 partial sums to
+// work[band][N]; the second adds the bands in order.  No atomics, so the
+// result is the same on every run.
+constexpr int kColsumBands = VY_COLSUM_BANDS;
+
 template <class T>
-__global__ void __launch_bounds__(512) k_colsum(const T* __restrict__ g, int64_t M, int N, int64_t ld, int64_t rows_per_block,
-                         float* __restrict__ out) {
-  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
-  const int64_t r1 = min(M, r0 + rows_per_block);
+__global__ void __launch_bounds__(512) k_colsum_bands(const T* __restrict__ g, int64_t M, int N, int64_t ld,
+                                                      int64_t rows_per_band, float* __restrict__ work) {
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_band;
+  const int64_t r1 = min(M, r0 + rows_per_band);
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N; c += gridDim.x * blockDim.x) {
     float acc = 0.f;
     int64_t r = r0;
-    for (; r + 8 <= r1; r += 8) {  // eight independent loads in flight per thread
+    for (; r + 8 <= r1; r += 8) {
       float v[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) v[j] = to_f(g[(r + j) * ld + c]);
@@ -308,7 +311,37 @@ __global__ void __launch_bounds__(512) k_colsum(const T* __restrict__ g, int64_t
       for (int j = 0; j < 8; ++j) acc += v[j];
     }
     for (; r < r1; ++r) acc += to_f(g[r * ld + c]);
-    atomicAdd(out + c, acc);
+    work[(int64_t)blockIdx.y * N + c] = acc;
+  }
+}
+
+// 32 columns per block, eight band groups per column summed with eight loads
+// in flight each, then the eight group sums added in group order.
+__global__ void __launch_bounds__(256) k_colsum_reduce(const float* __restrict__ work, int bands, int N,
+                                                       float* __restrict__ out) {
+  __shared__ float grp[8][33];
+  const int lane = threadIdx.x & 31, gi = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  const int per = (bands + 7) / 8, b0 = gi * per, b1 = min(bands, b0 + per);
+  float acc = 0.f;
+  if (c < N) {
+    int b = b0;
+    for (; b + 8 <= b1; b += 8) {
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = work[(int64_t)(b + j) * N + c];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc += v[j];
+    }
+    for (; b < b1; ++b) acc += work[(int64_t)b * N + c];
+  }
+  grp[gi][lane] = acc;
+  __syncthreads();
+  if (gi == 0 && c < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t += grp[j][lane];
+    out[c] = t;
   }
 }
 
@@ -432,22 +465,27 @@ extern "C" int vy_gather_rows(const void* src, int64_t row_bytes, const int64_t*
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 
-extern "C" int vy_colsum(const void* g, int32_t dtype, int64_t M, int64_t N, int64_t ld, float* out, void* stream) {
-  if (!out || M < 0 || N < 1 || N > (1 << 20) || ld < N || (dtype != 0 && dtype != 1)) return VY_ERR_ARG;
-  if (M == 0) return VY_OK;
+extern "C" int vy_colsum(const void* g, int32_t dtype, int64_t M, int64_t N, int64_t ld, float* work, float* out,
+                         void* stream) {
+  if (!out || !work || M < 0 || N < 1 || N > (1 << 20) || ld < N || (dtype != 0 && dtype != 1)) return VY_ERR_ARG;
+  auto st = (cudaStream_t)stream;
+  if (M == 0) {
+    return cudaMemsetAsync(out, 0, (size_t)N * sizeof(float), st) == cudaSuccess ? VY_OK : VY_ERR_CUDA;
+  }
   if (!g) return VY_ERR_ARG;
   const int threads = N >= 512 ? 512 : ((int)N + 31) / 32 * 32;  // one x-block up to 512 columns
   const unsigned gx = (unsigned)((N + threads - 1) / threads);
   // enough row bands to fill the GPU a few times over, at least 64 rows each
-  int64_t bands = std::max<int64_t>(1, 148 * 8 / (int64_t)gx);
-  int64_t rpb = std::max<int64_t>(64, (M + bands - 1) / bands);
+  int64_t bands = std::min<int64_t>(kColsumBands, std::max<int64_t>(1, 148 * 8 / (int64_t)gx));
+  const int64_t rpb = std::max<int64_t>(64, (M + bands - 1) / bands);
   bands = (M + rpb - 1) / rpb;
   const dim3 grid(gx, (unsigned)bands);
-  auto st = (cudaStream_t)stream;
   if (dtype == 0)
-    k_colsum<float><<<grid, threads, 0, st>>>(static_cast<const float*>(g), M, (int)N, ld, rpb, out);
+    k_colsum_bands<float><<<grid, threads, 0, st>>>(static_cast<const float*>(g), M, (int)N, ld, rpb, work);
   else
-    k_colsum<__nv_bfloat16><<<grid, threads, 0, st>>>(static_cast<const __nv_bfloat16*>(g), M, (int)N, ld, rpb, out);
+    k_colsum_bands<__nv_bfloat16><<<grid, threads, 0, st>>>(static_cast<const __nv_bfloat16*>(g), M, (int)N, ld, rpb,
+                                                            work);
+  k_colsum_reduce<<<(unsigned)((N + 31) / 32), 256, 0, st>>>(work, (int)bands, (int)N, out);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 

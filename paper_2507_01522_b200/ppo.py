@@ -81,12 +81,14 @@ def gather_rows(src: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
 
 def colsum(g: torch.Tensor) -> torch.Tensor:
     """Float32 column sums of a 2-D CUDA tensor (float32 / bf16, unit column
-    stride) via vy_colsum: one pass at HBM rate."""
+    stride) via vy_colsum: one pass at HBM rate, deterministic."""
     if g.dim() != 2 or g.stride(1) != 1:
         raise ValueError("colsum needs a 2-D tensor with unit column stride")
-    out = torch.zeros(g.shape[1], dtype=torch.float32, device=g.device)
+    out = torch.empty(g.shape[1], dtype=torch.float32, device=g.device)
+    work = torch.empty(nat.COLSUM_BANDS, g.shape[1], dtype=torch.float32, device=g.device)
     nat.check(nat.lib().vy_colsum(g.data_ptr(), _dtype_code(g), g.shape[0], g.shape[1], g.stride(0),
-                                  out.data_ptr(), torch.cuda.current_stream().cuda_stream), "vy_colsum")
+                                  work.data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream),
+              "vy_colsum")
     return out
 
 

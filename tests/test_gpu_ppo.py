@@ -260,3 +260,5 @@ def test_colsum_matches_torch(dtype):
     torch.testing.assert_close(colsum(g), g.float().sum(0), rtol=1e-4, atol=1e-2)
     torch.testing.assert_close(colsum(g[:, :357]), g[:, :357].float().sum(0), rtol=1e-4, atol=1e-2)
     torch.testing.assert_close(colsum(g[:5, :1]), g[:5, :1].float().sum(0), rtol=1e-4, atol=1e-4)
+    assert torch.equal(colsum(g), colsum(g))  # no atomics: bit-identical run to run
+    assert torch.equal(colsum(g[:0]), torch.zeros(360, device="cuda"))
