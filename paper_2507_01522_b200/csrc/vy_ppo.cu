@@ -66,6 +66,7 @@ __device__ __forceinline__ void stage_rows(const T* __restrict__ src, int64_t n,
   constexpr int V = 16 / sizeof(T);
   if ((reinterpret_cast<uintptr_t>(src) & 15u) == 0 && n % V == 0) {
     const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll 4  // several vectors' loads in flight before the first conversion
     for (int64_t i = threadIdx.x; i < n / V; i += blockDim.x) {
       const uint4 u = __ldg(s4 + i);
       const T* e = reinterpret_cast<const T*>(&u);
@@ -146,16 +147,18 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_head_fwd(const T* __restri
   const int gh = (int)min((int64_t)G, N - n0);
   float* rows = ppo_smem;
   float* part = ppo_smem + (size_t)G * ld;  // [2][G*S]
+  const int t = threadIdx.x;
+  // this thread's action, loaded before the staging so its latency overlaps it
+  const int act = t < gh * S ? actions[n0 * S + t] : 0;
   stage_rows(logits + n0 * ld, (int64_t)gh * ld, rows);
   __syncthreads();
-  const int t = threadIdx.x;
   if (t < gh * S) {
     const int r = t / S, s = t - r * S;
     const float* zs = rows + (size_t)r * ld + s * A;
     const Slot<AC> z(zs, A);
     float m, logsum, inv, h;
     slot_stats(z, m, logsum, inv, h);
-    part[t] = (zs[actions[(n0 + r) * S + s]] - m) - logsum;
+    part[t] = (zs[act] - m) - logsum;
     part[G * S + t] = h;
   }
   __syncthreads();
@@ -182,17 +185,19 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_head_bwd(const T* __restri
   const int gh = (int)min((int64_t)G, N - n0);
   float* rows = ppo_smem;
   const int SA = S * A;
+  const int t = threadIdx.x;
+  // per-thread inputs loaded before the staging so their latency overlaps it
+  const bool live = t < gh * S;
+  const int r = live ? t / S : 0, s = t - r * S;
+  const int a = live ? actions[n0 * S + t] : 0;
+  const float gl = live && g_lp ? g_lp[n0 + r] : 0.f, ge = live && g_ent ? g_ent[n0 + r] : 0.f;
   stage_rows(logits + n0 * ld, (int64_t)gh * ld, rows);
   __syncthreads();
-  const int t = threadIdx.x;
-  if (t < gh * S) {
-    const int r = t / S, s = t - r * S;
+  if (live) {
     float* zs = rows + (size_t)r * ld + s * A;
     const Slot<AC> z(zs, A);
     float m, logsum, inv, h;
     slot_stats(z, m, logsum, inv, h);
-    const float gl = g_lp ? g_lp[n0 + r] : 0.f, ge = g_ent ? g_ent[n0 + r] : 0.f;
-    const int a = actions[(n0 + r) * S + s];
 #pragma unroll
     for (int k = 0; k < z.size(); ++k) {  // in place: this thread owns the slot's values
       const float d = z[k] - m, p = __expf(d) * inv, l = d - logsum;
