@@ -261,7 +261,7 @@ int vy_gather_rows(const void *src, int64_t row_bytes, const int64_t *idx, int64
  * g[m*ld + c], c < N; g float32 (dtype 0) or bfloat16 (1); out float32.
  * work: float32 scratch of VY_COLSUM_BANDS * N values.  Deterministic (no
  * atomics: per-band partial sums, then the bands added in order). */
-#define VY_COLSUM_BANDS 512
+#define VY_COLSUM_BANDS 2048
 int vy_colsum(const void *g, int32_t dtype, int64_t M, int64_t N, int64_t ld, float *work, float *out,
               void *stream);
 

@@ -16,7 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libvoltyard_b200.so"
 
 VY_OK, VY_ERR_ARG, VY_ERR_CUDA, VY_ERR_UNSUPPORTED, VY_ERR_STATE = 0, 1, 2, 3, 4
 VY_ACT_U8, VY_ACT_I32, VY_ACT_I64 = 0, 1, 2
-COLSUM_BANDS = 512  # VY_COLSUM_BANDS
+COLSUM_BANDS = 2048  # VY_COLSUM_BANDS
 F_AUTO_RESET, F_INFOS, F_INJECT, F_OUT_F64 = 1, 2, 4, 8
 
 _P = C.c_void_p
