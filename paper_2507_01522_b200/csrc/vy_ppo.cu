@@ -99,29 +99,29 @@ __device__ __forceinline__ void store_rows(const float* __restrict__ src, int64_
 // (the 21-action head: one shared-memory read per logit instead of one per
 // pass — the kernels were bound by shared-memory instructions), else read
 // from the staged row.
-template <int AC>
+template <int AC, class E = float>
 struct Slot {
   float r[AC > 0 ? AC : 1];
-  const float* p;
+  const E* p;
   int a;
-  __device__ __forceinline__ Slot(const float* src, int A) : p(src), a(A) {
+  __device__ __forceinline__ Slot(const E* src, int A) : p(src), a(A) {
     if constexpr (AC > 0) {
 #pragma unroll
-      for (int k = 0; k < AC; ++k) r[k] = src[k];
+      for (int k = 0; k < AC; ++k) r[k] = to_f(src[k]);
     }
   }
   __device__ __forceinline__ int size() const { return AC > 0 ? AC : a; }
   __device__ __forceinline__ float operator[](int k) const {
     if constexpr (AC > 0) return r[k];
-    else return p[k];
+    else return to_f(p[k]);
   }
 };
 
 // One slot's softmax statistics with a single exp per value: m = max z,
 // e_k = exp(z_k - m), sum = sum e_k, logsum = log(sum), lse = m + logsum, and
 // the entropy H = -sum p_k (z_k - lse) = logsum - sum(e_k (z_k - m)) / sum.
-template <int AC>
-__device__ __forceinline__ void slot_stats(const Slot<AC>& z, float& m, float& logsum, float& inv, float& h) {
+template <int AC, class E>
+__device__ __forceinline__ void slot_stats(const Slot<AC, E>& z, float& m, float& logsum, float& inv, float& h) {
   m = -INFINITY;
 #pragma unroll
   for (int k = 0; k < z.size(); ++k) m = fmaxf(m, z[k]);
@@ -137,40 +137,82 @@ __device__ __forceinline__ void slot_stats(const Slot<AC>& z, float& m, float& l
   h = logsum - ed * inv;
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory"); }
+
+// n raw elements src -> dst (shared): 16-byte cp.async when both are aligned,
+// else plain copies (complete on return)
+template <class T>
+__device__ __forceinline__ void issue_rows(const T* __restrict__ src, int64_t n, T* dst) {
+  constexpr int V = 16 / sizeof(T);
+  if ((reinterpret_cast<uintptr_t>(src) & 15u) == 0 && n % V == 0) {
+    for (int64_t i = threadIdx.x; i < n / V; i += blockDim.x) cp_async16(dst + i * V, src + i * V);
+  } else {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+template <class T>
+__host__ __device__ constexpr size_t raw_rows_bytes(int G, int64_t ld) {
+  return ((size_t)G * ld * sizeof(T) + 15) & ~(size_t)15;
+}
+
+// Persistent and double-buffered: each block walks chunks of G rows
+// (blockIdx.x, += gridDim.x) and copies the next chunk's raw rows into the
+// other buffer with cp.async while it works on the current one, so the row
+// loads overlap the softmax work (the one-chunk-per-block version stalled on
+// them: long-scoreboard was its top stall).
 template <class T, int AC>
 __global__ void __launch_bounds__(kHeadThreads) k_ppo_head_fwd(const T* __restrict__ logits,
                                                                const uint8_t* __restrict__ actions, int64_t N, int S,
                                                                int A, int64_t ld, int G, float* __restrict__ lp,
                                                                float* __restrict__ ent) {
-  extern __shared__ float ppo_smem[];
-  const int64_t n0 = (int64_t)blockIdx.x * G;
-  const int gh = (int)min((int64_t)G, N - n0);
-  float* rows = ppo_smem;
-  float* part = ppo_smem + (size_t)G * ld;  // [2][G*S]
+  extern __shared__ __align__(16) unsigned char ppo_raw[];
+  const size_t rb = raw_rows_bytes<T>(G, ld);
+  T* buf0 = reinterpret_cast<T*>(ppo_raw);
+  T* buf1 = reinterpret_cast<T*>(ppo_raw + rb);
+  float* part = reinterpret_cast<float*>(ppo_raw + 2 * rb);  // [2][G*S]
+  const int64_t nch = (N + G - 1) / G;
   const int t = threadIdx.x;
-  // this thread's action, loaded before the staging so its latency overlaps it
-  const int act = t < gh * S ? actions[n0 * S + t] : 0;
-  stage_rows(logits + n0 * ld, (int64_t)gh * ld, rows);
-  __syncthreads();
-  if (t < gh * S) {
-    const int r = t / S, s = t - r * S;
-    const float* zs = rows + (size_t)r * ld + s * A;
-    const Slot<AC> z(zs, A);
-    float m, logsum, inv, h;
-    slot_stats(z, m, logsum, inv, h);
-    part[t] = (zs[act] - m) - logsum;
-    part[G * S + t] = h;
-  }
-  __syncthreads();
-  if (t < gh) {
-    float alp = 0.f, aent = 0.f;
-    for (int s = 0; s < S; ++s) {  // slot order, as the warp version's lanes summed
-      alp += part[t * S + s];
-      aent += part[G * S + t * S + s];
+  int64_t c = blockIdx.x;
+  if (c < nch) issue_rows(logits + c * G * ld, (int64_t)min((int64_t)G, N - c * G) * ld, buf0);
+  cp_async_commit();
+  for (int i = 0; c < nch; c += gridDim.x, ++i) {
+    const int64_t cn = c + gridDim.x;
+    T* cur = (i & 1) ? buf1 : buf0;
+    if (cn < nch) issue_rows(logits + cn * G * ld, (int64_t)min((int64_t)G, N - cn * G) * ld, (i & 1) ? buf0 : buf1);
+    cp_async_commit();
+    const int64_t n0 = c * G;
+    const int gh = (int)min((int64_t)G, N - n0);
+    const int act = t < gh * S ? actions[n0 * S + t] : 0;
+    cp_async_wait<1>();  // every group but the one just issued: chunk c has landed
+    __syncthreads();
+    if (t < gh * S) {
+      const int r = t / S, s = t - r * S;
+      const T* zs = cur + (size_t)r * ld + s * A;
+      const Slot<AC, T> z(zs, A);
+      float m, logsum, inv, h;
+      slot_stats(z, m, logsum, inv, h);
+      part[t] = (to_f(zs[act]) - m) - logsum;
+      part[G * S + t] = h;
     }
-    lp[n0 + t] = alp;
-    ent[n0 + t] = aent;
+    __syncthreads();  // also frees `cur` for the copy issued next iteration
+    if (t < gh) {
+      float alp = 0.f, aent = 0.f;
+      for (int s = 0; s < S; ++s) {
+        alp += part[t * S + s];
+        aent += part[G * S + t * S + s];
+      }
+      lp[n0 + t] = alp;
+      ent[n0 + t] = aent;
+    }
   }
+  cp_async_wait<0>();
 }
 
 // d(g_lp * lp + g_ent * ent) / dz_k = g_lp (1[k = a] - p_k) - g_ent p_k (log p_k + H), H = slot entropy
@@ -403,24 +445,29 @@ extern "C" int vy_ppo_sample_rng(const void* logits, int32_t dtype, int64_t ld, 
 extern "C" int vy_ppo_head_fwd(const void* logits, int32_t dtype, int64_t ld, const uint8_t* actions, int64_t N,
                                int32_t S, int32_t A, float* lp, float* ent, void* stream) {
   if (!logits || !actions || !lp || !ent || N < 1 || S < 1 || A < 1 || (dtype != 0 && dtype != 1) ||
-      head_rows(S) < 1 || ld < (int64_t)S * A || head_smem(S, ld) > 48 * 1024)
+      head_rows(S) < 1 || ld < (int64_t)S * A)
     return VY_ERR_ARG;
   auto st = (cudaStream_t)stream;
   const int G = head_rows(S);
+  const size_t part = 2 * (size_t)G * S * sizeof(float);
+  const size_t smem = (dtype == 0 ? 2 * raw_rows_bytes<float>(G, ld) : 2 * raw_rows_bytes<__nv_bfloat16>(G, ld)) + part;
+  if (smem > 48 * 1024) return VY_ERR_ARG;
+  const int64_t nch = (N + G - 1) / G;
+  const unsigned grid = (unsigned)std::min<int64_t>(nch, 148 * 8);  // persistent: about one wave of resident blocks
   if (dtype == 0) {
     if (A == 21)
-      k_ppo_head_fwd<float, 21><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
-        static_cast<const float*>(logits), actions, N, S, A, ld, G, lp, ent);
+      k_ppo_head_fwd<float, 21><<<grid, kHeadThreads, smem, st>>>(static_cast<const float*>(logits), actions, N, S, A,
+                                                                  ld, G, lp, ent);
     else
-      k_ppo_head_fwd<float, 0><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
-        static_cast<const float*>(logits), actions, N, S, A, ld, G, lp, ent);
+      k_ppo_head_fwd<float, 0><<<grid, kHeadThreads, smem, st>>>(static_cast<const float*>(logits), actions, N, S, A,
+                                                                 ld, G, lp, ent);
   } else {
     if (A == 21)
-      k_ppo_head_fwd<__nv_bfloat16, 21><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
-        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, lp, ent);
+      k_ppo_head_fwd<__nv_bfloat16, 21><<<grid, kHeadThreads, smem, st>>>(
+          static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, lp, ent);
     else
-      k_ppo_head_fwd<__nv_bfloat16, 0><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
-        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, lp, ent);
+      k_ppo_head_fwd<__nv_bfloat16, 0><<<grid, kHeadThreads, smem, st>>>(
+          static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, lp, ent);
   }
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
