@@ -222,34 +222,49 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_head_bwd(const T* __restri
                                                                int A, int64_t ld, int G,
                                                                const float* __restrict__ g_lp,
                                                                const float* __restrict__ g_ent, T* __restrict__ grad) {
-  extern __shared__ float ppo_smem[];
-  const int64_t n0 = (int64_t)blockIdx.x * G;
-  const int gh = (int)min((int64_t)G, N - n0);
-  float* rows = ppo_smem;
-  const int SA = S * A;
+  // persistent and double-buffered like the forward; the gradient rows go
+  // through a float32 staging area and leave with 16-byte stores
+  extern __shared__ __align__(16) unsigned char ppo_raw[];
+  const size_t rb = raw_rows_bytes<T>(G, ld);
+  T* buf0 = reinterpret_cast<T*>(ppo_raw);
+  T* buf1 = reinterpret_cast<T*>(ppo_raw + rb);
+  float* out = reinterpret_cast<float*>(ppo_raw + 2 * rb);  // [G][ld]
+  const int SA = S * A, pad = (int)(ld - SA);
+  const int64_t nch = (N + G - 1) / G;
   const int t = threadIdx.x;
-  // per-thread inputs loaded before the staging so their latency overlaps it
-  const bool live = t < gh * S;
-  const int r = live ? t / S : 0, s = t - r * S;
-  const int a = live ? actions[n0 * S + t] : 0;
-  const float gl = live && g_lp ? g_lp[n0 + r] : 0.f, ge = live && g_ent ? g_ent[n0 + r] : 0.f;
-  stage_rows(logits + n0 * ld, (int64_t)gh * ld, rows);
-  __syncthreads();
-  if (live) {
-    float* zs = rows + (size_t)r * ld + s * A;
-    const Slot<AC> z(zs, A);
-    float m, logsum, inv, h;
-    slot_stats(z, m, logsum, inv, h);
+  int64_t c = blockIdx.x;
+  if (c < nch) issue_rows(logits + c * G * ld, (int64_t)min((int64_t)G, N - c * G) * ld, buf0);
+  cp_async_commit();
+  for (int i = 0; c < nch; c += gridDim.x, ++i) {
+    const int64_t cn = c + gridDim.x;
+    T* cur = (i & 1) ? buf1 : buf0;
+    if (cn < nch) issue_rows(logits + cn * G * ld, (int64_t)min((int64_t)G, N - cn * G) * ld, (i & 1) ? buf0 : buf1);
+    cp_async_commit();
+    const int64_t n0 = c * G;
+    const int gh = (int)min((int64_t)G, N - n0);
+    const bool live = t < gh * S;
+    const int r = live ? t / S : 0, s = t - r * S;
+    const int a = live ? actions[n0 * S + t] : 0;
+    const float gl = live && g_lp ? g_lp[n0 + r] : 0.f, ge = live && g_ent ? g_ent[n0 + r] : 0.f;
+    cp_async_wait<1>();
+    __syncthreads();  // chunk c landed; the previous chunk's gradient rows have left `out`
+    if (live) {
+      const T* zs = cur + (size_t)r * ld + s * A;
+      float* os = out + (size_t)r * ld + s * A;
+      const Slot<AC, T> z(zs, A);
+      float m, logsum, inv, h;
+      slot_stats(z, m, logsum, inv, h);
 #pragma unroll
-    for (int k = 0; k < z.size(); ++k) {  // in place: this thread owns the slot's values
-      const float d = z[k] - m, p = __expf(d) * inv, l = d - logsum;
-      zs[k] = gl * ((k == a ? 1.f : 0.f) - p) - ge * p * (l + h);
+      for (int k = 0; k < z.size(); ++k) {
+        const float d = z[k] - m, p = __expf(d) * inv, l = d - logsum;
+        os[k] = gl * ((k == a ? 1.f : 0.f) - p) - ge * p * (l + h);
+      }
     }
+    for (int j = t; j < gh * pad; j += blockDim.x) out[(size_t)(j / pad) * ld + SA + j % pad] = 0.f;
+    __syncthreads();
+    store_rows(out, (int64_t)gh * ld, grad + n0 * ld);
   }
-  const int pad = (int)(ld - SA);
-  for (int i = t; i < gh * pad; i += blockDim.x) rows[(size_t)(i / pad) * ld + SA + i % pad] = 0.f;
-  __syncthreads();
-  store_rows(rows, (int64_t)gh * ld, grad + n0 * ld);
+  cp_async_wait<0>();
 }
 
 // Row gather with 16-byte vectors: a row's vectors go to consecutive threads
@@ -475,26 +490,38 @@ extern "C" int vy_ppo_head_fwd(const void* logits, int32_t dtype, int64_t ld, co
 extern "C" int vy_ppo_head_bwd(const void* logits, int32_t dtype, int64_t ld, const uint8_t* actions, int64_t N,
                                int32_t S, int32_t A, const float* g_lp, const float* g_ent, void* grad, void* stream) {
   if (!logits || !actions || !grad || N < 1 || S < 1 || A < 1 || (dtype != 0 && dtype != 1) || head_rows(S) < 1 ||
-      ld < (int64_t)S * A || head_smem(S, ld) > 48 * 1024)
+      ld < (int64_t)S * A)
     return VY_ERR_ARG;
   auto st = (cudaStream_t)stream;
   const int G = head_rows(S);
+  const size_t smem = (dtype == 0 ? 2 * raw_rows_bytes<float>(G, ld) : 2 * raw_rows_bytes<__nv_bfloat16>(G, ld)) +
+                      (size_t)G * ld * sizeof(float);
+  if (smem > 200 * 1024) return VY_ERR_ARG;
+  const int64_t nch = (N + G - 1) / G;
+  const unsigned grid = (unsigned)std::min<int64_t>(nch, 148 * 8);
+  if (smem > 48 * 1024) {  // float32 rows of the 17 x 21 head: 64 KB (opt-in above the 48 KB default)
+    auto k = dtype == 0 ? (A == 21 ? (const void*)k_ppo_head_bwd<float, 21> : (const void*)k_ppo_head_bwd<float, 0>)
+                        : (A == 21 ? (const void*)k_ppo_head_bwd<__nv_bfloat16, 21>
+                                   : (const void*)k_ppo_head_bwd<__nv_bfloat16, 0>);
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return VY_ERR_CUDA;
+  }
   if (dtype == 0) {
     if (A == 21)
-      k_ppo_head_bwd<float, 21><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
-        static_cast<const float*>(logits), actions, N, S, A, ld, G, g_lp, g_ent, static_cast<float*>(grad));
+      k_ppo_head_bwd<float, 21><<<grid, kHeadThreads, smem, st>>>(static_cast<const float*>(logits), actions, N, S, A,
+                                                                  ld, G, g_lp, g_ent, static_cast<float*>(grad));
     else
-      k_ppo_head_bwd<float, 0><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
-        static_cast<const float*>(logits), actions, N, S, A, ld, G, g_lp, g_ent, static_cast<float*>(grad));
+      k_ppo_head_bwd<float, 0><<<grid, kHeadThreads, smem, st>>>(static_cast<const float*>(logits), actions, N, S, A,
+                                                                 ld, G, g_lp, g_ent, static_cast<float*>(grad));
   } else {
     if (A == 21)
-      k_ppo_head_bwd<__nv_bfloat16, 21><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
-        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, g_lp, g_ent,
-        static_cast<__nv_bfloat16*>(grad));
+      k_ppo_head_bwd<__nv_bfloat16, 21><<<grid, kHeadThreads, smem, st>>>(
+          static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, g_lp, g_ent,
+          static_cast<__nv_bfloat16*>(grad));
     else
-      k_ppo_head_bwd<__nv_bfloat16, 0><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
-        static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, g_lp, g_ent,
-        static_cast<__nv_bfloat16*>(grad));
+      k_ppo_head_bwd<__nv_bfloat16, 0><<<grid, kHeadThreads, smem, st>>>(
+          static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, g_lp, g_ent,
+          static_cast<__nv_bfloat16*>(grad));
   }
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
