@@ -377,14 +377,14 @@ __global__ void __launch_bounds__(512) k_colsum_bands(const T* __restrict__ g, i
   }
 }
 
-// 32 columns per block, eight band groups per column summed with eight loads
-// in flight each, then the eight group sums added in group order.
-__global__ void __launch_bounds__(256) k_colsum_reduce(const float* __restrict__ work, int bands, int N,
-                                                       float* __restrict__ out) {
-  __shared__ float grp[8][33];
+// 32 columns per block, 32 band groups per column summed with eight loads
+// in flight each, then the 32 group sums added in group order.
+__global__ void __launch_bounds__(1024) k_colsum_reduce(const float* __restrict__ work, int bands, int N,
+                                                        float* __restrict__ out) {
+  __shared__ float grp[32][33];
   const int lane = threadIdx.x & 31, gi = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
-  const int per = (bands + 7) / 8, b0 = gi * per, b1 = min(bands, b0 + per);
+  const int per = (bands + 31) / 32, b0 = gi * per, b1 = min(bands, b0 + per);
   float acc = 0.f;
   if (c < N) {
     int b = b0;
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(256) k_colsum_reduce(const float* __restrict__
   if (gi == 0 && c < N) {
     float t = 0.f;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) t += grp[j][lane];
+    for (int j = 0; j < 32; ++j) t += grp[j][lane];
     out[c] = t;
   }
 }
@@ -564,7 +564,7 @@ extern "C" int vy_colsum(const void* g, int32_t dtype, int64_t M, int64_t N, int
   else
     k_colsum_bands<__nv_bfloat16><<<grid, threads, 0, st>>>(static_cast<const __nv_bfloat16*>(g), M, (int)N, ld, rpb,
                                                             work);
-  k_colsum_reduce<<<(unsigned)((N + 31) / 32), 256, 0, st>>>(work, (int)bands, (int)N, out);
+  k_colsum_reduce<<<(unsigned)((N + 31) / 32), 1024, 0, st>>>(work, (int)bands, (int)N, out);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 
