@@ -400,8 +400,8 @@ class PPOTrainer:
         # minibatch to anyway); minibatches gather half the bytes
         obs = self.net.pad_obs(self.obs[:T].reshape(T * B, -1)).to(torch.bfloat16)
         act = self.actions.reshape(T * B, -1)
-        old_lp, old_v = self.logp.reshape(-1), self.values[:T].reshape(-1)
-        adv, ret = adv.reshape(-1), ret.reshape(-1)
+        # the four per-sample scalars side by side: one 16-byte-row gather per minibatch
+        scal = torch.stack([self.logp.reshape(-1), self.values[:T].reshape(-1), adv.reshape(-1), ret.reshape(-1)], 1)
         n = T * B
         mb = n // cfg.n_minibatches
         stats = {}
@@ -417,12 +417,12 @@ class PPOTrainer:
                 else:
                     lp, ent = head_reference(logits, act[idx])
                 ent = ent.mean()
-                a = adv[idx]
+                old_lp, old_v, a, r = gather_rows(scal, idx).unbind(1)
                 a = (a - a.mean()) / (a.std() + 1e-8)
-                ratio = torch.exp(lp - old_lp[idx])
+                ratio = torch.exp(lp - old_lp)
                 pg = -torch.min(ratio * a, torch.clamp(ratio, 1 - cfg.clip_eps, 1 + cfg.clip_eps) * a).mean()
-                v_clip = old_v[idx] + (v - old_v[idx]).clamp(-cfg.vf_clip, cfg.vf_clip)
-                vl = 0.5 * torch.max((v - ret[idx]) ** 2, (v_clip - ret[idx]) ** 2).mean()
+                v_clip = old_v + (v - old_v).clamp(-cfg.vf_clip, cfg.vf_clip)
+                vl = 0.5 * torch.max((v - r) ** 2, (v_clip - r) ** 2).mean()
                 loss = pg + cfg.vf_coef * vl - cfg.ent_coef * ent
                 self.opt.zero_grad(set_to_none=False)
                 loss.backward()
