@@ -4,8 +4,9 @@ The reference requires one (config, station, dataset) per batch
 (engine.py:370).  ``HeteroBatch`` batches many: each group is a
 regular BatchEnv (own tables, own handle; the lean step kernel when the
 group's config allows it — group sizes are whole 32-env tiles for that),
-groups are spread round-robin over CUDA streams so the per-group grids run
-concurrently and fill the GPU (each group's launches stay ordered on its
+groups are launched costliest first (largest tree, then most ports),
+round-robin over CUDA streams, so the per-group grids run concurrently, fill
+the GPU and the slowest groups do not form the step's tail (each group's launches stay ordered on its
 stream; a step joins all streams back into the caller's), and each group's
 persistent grid is shaped for sharing (``tiles_per_warp``).  Env seeds and
 RandomPolicy rows use one global index space across groups (group g's envs
