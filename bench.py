@@ -382,7 +382,7 @@ def main() -> None:
                          "env_steps_per_s": res["env_steps_per_s"], "envs_per_gpu": 4096,
                          "rollout_steps": cfg.rollout_steps, "epochs": cfg.update_epochs,
                          "minibatches": cfg.n_minibatches, "hidden": cfg.hidden, "timed_iterations": args.ppo_iters,
-                         "rollout": "CUDA graph (policy fwd bf16 + vy_ppo_sample_rng Gumbel-max kernel with in-kernel uniforms + k_step) x 300",
+                         "rollout": "CUDA graph (policy fwd bf16: 3 GEMMs with block-diagonal layer 2 and merged heads + vy_ppo_sample_rng Gumbel-max kernel with in-kernel uniforms + k_step) x 300",
                          "update": ("one CUDA graph per update on 1 GPU (eager with the all-reduce): vy_gae, "
                                     "vy_gather_rows minibatch gather, bf16 GEMMs at 8-aligned widths with column-sum bias "
                                     "gradients (vy_colsum), vy_ppo_head_fwd/_bwd fused log-prob/entropy head, fused Adam"),

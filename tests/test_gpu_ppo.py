@@ -262,3 +262,22 @@ def test_colsum_matches_torch(dtype):
     torch.testing.assert_close(colsum(g[:5, :1]), g[:5, :1].float().sum(0), rtol=1e-4, atol=1e-4)
     assert torch.equal(colsum(g), colsum(g))  # no atomics: bit-identical run to run
     assert torch.equal(colsum(g[:0]), torch.zeros(360, device="cuda"))
+
+
+def test_rollout_inference_weights_match_the_network():
+    """The rollout's three-GEMM forward (block-diagonal second layer, merged
+    heads) gives the network's logits and value to bf16 accuracy."""
+    from paper_2507_01522_b200.ppo import ActorCritic
+
+    torch.manual_seed(0)
+    net = ActorCritic(105, 17, 21).cuda()
+    for p in net.parameters():  # non-trivial biases and head weights
+        p.data.add_(0.05 * torch.randn_like(p))
+    x = torch.zeros(512, net.in_dim, device="cuda")
+    x[:, :105] = torch.randn(512, 105, device="cuda")
+    with torch.autocast("cuda", dtype=torch.bfloat16):
+        logits, v = net(x, logits_fp32=False)
+        out, v2 = net.infer(x.to(torch.bfloat16), net.inference_weights())
+    assert out.shape == (512, net.out_dim + 8) and out.stride(0) == net.out_dim + 8
+    torch.testing.assert_close(out[:, : net.n_out].float(), logits[:, : net.n_out].float(), rtol=2e-2, atol=2e-2)
+    torch.testing.assert_close(v2.float(), v.float(), rtol=2e-2, atol=2e-2)
