@@ -172,6 +172,31 @@ class ActorCritic(nn.Module):
         logits = out[:, : self.n_out].float().view(-1, self.n_slots, self.n_actions) if logits_fp32 else out
         return logits, self.critic(hc).squeeze(-1)
 
+    def merged_weights(self) -> tuple:
+        """Differentiable fp32 views of the second layers and heads as single
+        matrices (see `inference_weights`): gradients flow back to the
+        separate layers' parameters, the zero blocks get none."""
+        H = self.hidden
+        w2 = torch.block_diag(self.actor[0].weight, self.critic[0].weight)
+        b2 = torch.cat([self.actor[0].bias, self.critic[0].bias])
+        wh = torch.block_diag(self.actor[2].weight, self.critic[2].weight)  # [out_dim + 1, 2H]
+        bh = torch.cat([self.actor[2].bias, self.critic[2].bias])
+        pad = (-wh.shape[0]) % 8
+        wh = nn.functional.pad(wh, (0, 0, 0, pad))
+        bh = nn.functional.pad(bh, (0, pad))
+        return w2, b2, wh, bh
+
+    def forward_merged(self, x: torch.Tensor):
+        """Training forward with three GEMMs (block-diagonal second layer,
+        merged heads) on a padded input -> (head output [M, out_dim + 8]:
+        logits in columns < out_dim, value in column out_dim; the value)."""
+        w2, b2, wh, bh = self.merged_weights()
+        lin = _LinearFn.apply if x.is_cuda else nn.functional.linear
+        h = torch.tanh(self.inp(x))
+        h = torch.tanh(lin(h, w2, b2))
+        out = lin(h, wh, bh)
+        return out, out[:, self.out_dim]
+
     @torch.no_grad()
     def inference_weights(self) -> tuple:
         """bf16 weights for `infer`, built once per rollout: the second layers
@@ -443,7 +468,10 @@ class PPOTrainer:
             for k in range(cfg.n_minibatches):
                 idx = perm[k * mb:(k + 1) * mb]
                 with torch.autocast("cuda", dtype=torch.bfloat16):
-                    logits, v = self.net(gather_rows(obs, idx), logits_fp32=not cfg.fused_head)
+                    if cfg.fused_head:  # head output read in place by the fused head (row stride out_dim + 8)
+                        logits, v = self.net.forward_merged(gather_rows(obs, idx))
+                    else:
+                        logits, v = self.net(gather_rows(obs, idx), logits_fp32=True)
                     v = v.float()
                 if cfg.fused_head:
                     lp, ent = PolicyHead.apply(logits, act[idx], self.net.n_slots, self.net.n_actions)

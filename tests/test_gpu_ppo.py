@@ -281,3 +281,28 @@ def test_rollout_inference_weights_match_the_network():
     assert out.shape == (512, net.out_dim + 8) and out.stride(0) == net.out_dim + 8
     torch.testing.assert_close(out[:, : net.n_out].float(), logits[:, : net.n_out].float(), rtol=2e-2, atol=2e-2)
     torch.testing.assert_close(v2.float(), v.float(), rtol=2e-2, atol=2e-2)
+
+
+def test_merged_training_forward_matches_the_network():
+    """forward_merged (block-diagonal layer 2, merged heads) gives the same
+    outputs and parameter gradients as the layer-by-layer forward (fp32)."""
+    from paper_2507_01522_b200.ppo import ActorCritic
+
+    torch.manual_seed(1)
+    net = ActorCritic(105, 17, 21).cuda()
+    for p in net.parameters():
+        p.data.add_(0.05 * torch.randn_like(p))
+    x = torch.zeros(777, net.in_dim, device="cuda")
+    x[:, :105] = torch.randn(777, 105, device="cuda")
+    gl = torch.randn(777, net.n_out, device="cuda")
+    gv = torch.randn(777, device="cuda")
+    logits, v = net(x, logits_fp32=False)
+    ((logits[:, : net.n_out] * gl).sum() + (v * gv).sum()).backward()
+    ref = {n: p.grad.clone() for n, p in net.named_parameters()}
+    net.zero_grad()
+    out, v2 = net.forward_merged(x)
+    ((out[:, : net.n_out] * gl).sum() + (v2 * gv).sum()).backward()
+    torch.testing.assert_close(out[:, : net.n_out], logits[:, : net.n_out], rtol=1e-4, atol=1e-4)
+    torch.testing.assert_close(v2, v, rtol=1e-4, atol=1e-4)
+    for n, p in net.named_parameters():
+        torch.testing.assert_close(p.grad, ref[n], rtol=1e-3, atol=1e-3, msg=n)
