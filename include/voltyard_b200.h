@@ -242,7 +242,9 @@ int vy_gae(const float *values, const float *rewards, const uint8_t *dones, cons
  * vy_ppo_head_fwd log-probability of `actions` and entropy, summed over slots;
  * vy_ppo_head_bwd gradient (logits' dtype and row stride, padding columns 0)
  *                 of g_lp*lp + g_ent*ent w.r.t. the logits (either upstream
- *                 gradient may be NULL = 0). */
+ *                 gradient may be NULL = 0); with g_value non-NULL, padding
+ *                 column value_col (S*A <= value_col < ld: a value head
+ *                 sharing the GEMM) receives g_value[n] instead of 0. */
 int vy_ppo_sample(const void *logits, int32_t dtype, int64_t ld, const float *noise, int64_t N, int32_t S, int32_t A,
                   uint8_t *actions, float *logp, void *stream);
 /* vy_ppo_sample with the uniforms drawn in the kernel: element e of call c
@@ -253,7 +255,8 @@ int vy_ppo_sample_rng(const void *logits, int32_t dtype, int64_t ld, uint64_t se
 int vy_ppo_head_fwd(const void *logits, int32_t dtype, int64_t ld, const uint8_t *actions, int64_t N, int32_t S,
                     int32_t A, float *lp, float *ent, void *stream);
 int vy_ppo_head_bwd(const void *logits, int32_t dtype, int64_t ld, const uint8_t *actions, int64_t N, int32_t S,
-                    int32_t A, const float *g_lp, const float *g_ent, void *grad, void *stream);
+                    int32_t A, const float *g_lp, const float *g_ent, const float *g_value, int32_t value_col,
+                    void *grad, void *stream);
 /* PPO minibatch gather: dst row i = src row idx[i] for i < n, rows of
  * row_bytes bytes (a multiple of 16; src and dst 16-byte aligned). */
 int vy_gather_rows(const void *src, int64_t row_bytes, const int64_t *idx, int64_t n, void *dst, void *stream);

@@ -67,7 +67,8 @@ _SIGS = {
     "vy_ppo_sample_rng": (C.c_int, [_P, C.c_int32, C.c_int64, C.c_uint64, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P,
                                     _P]),
     "vy_ppo_head_fwd": (C.c_int, [_P, C.c_int32, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]),
-    "vy_ppo_head_bwd": (C.c_int, [_P, C.c_int32, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P, _P]),
+    "vy_ppo_head_bwd": (C.c_int, [_P, C.c_int32, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P,
+                                  C.c_int32, _P, _P]),
     "vy_gather_rows": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, _P]),
     "vy_colsum": (C.c_int, [_P, C.c_int32, C.c_int64, C.c_int64, C.c_int64, _P, _P, _P]),
     "vy_selftest_div": (C.c_int, [C.POINTER(C.c_double), C.c_int32, C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),

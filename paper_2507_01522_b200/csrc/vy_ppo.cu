@@ -221,7 +221,9 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_head_bwd(const T* __restri
                                                                const uint8_t* __restrict__ actions, int64_t N, int S,
                                                                int A, int64_t ld, int G,
                                                                const float* __restrict__ g_lp,
-                                                               const float* __restrict__ g_ent, T* __restrict__ grad) {
+                                                               const float* __restrict__ g_ent,
+                                                               const float* __restrict__ g_value, int value_col,
+                                                               T* __restrict__ grad) {
   // persistent and double-buffered like the forward; the gradient rows go
   // through a float32 staging area and leave with 16-byte stores
   extern __shared__ __align__(16) unsigned char ppo_raw[];
@@ -260,7 +262,10 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_head_bwd(const T* __restri
         os[k] = gl * ((k == a ? 1.f : 0.f) - p) - ge * p * (l + h);
       }
     }
-    for (int j = t; j < gh * pad; j += blockDim.x) out[(size_t)(j / pad) * ld + SA + j % pad] = 0.f;
+    for (int j = t; j < gh * pad; j += blockDim.x) {  // padding columns: 0, or the value head's gradient
+      const int rr = j / pad, col = SA + (j - rr * pad);
+      out[(size_t)rr * ld + col] = (g_value && col == value_col) ? g_value[n0 + rr] : 0.f;
+    }
     __syncthreads();
     store_rows(out, (int64_t)gh * ld, grad + n0 * ld);
   }
@@ -488,9 +493,10 @@ extern "C" int vy_ppo_head_fwd(const void* logits, int32_t dtype, int64_t ld, co
 }
 
 extern "C" int vy_ppo_head_bwd(const void* logits, int32_t dtype, int64_t ld, const uint8_t* actions, int64_t N,
-                               int32_t S, int32_t A, const float* g_lp, const float* g_ent, void* grad, void* stream) {
+                               int32_t S, int32_t A, const float* g_lp, const float* g_ent, const float* g_value,
+                               int32_t value_col, void* grad, void* stream) {
   if (!logits || !actions || !grad || N < 1 || S < 1 || A < 1 || (dtype != 0 && dtype != 1) || head_rows(S) < 1 ||
-      ld < (int64_t)S * A)
+      ld < (int64_t)S * A || (g_value && (value_col < S * A || value_col >= ld)))
     return VY_ERR_ARG;
   auto st = (cudaStream_t)stream;
   const int G = head_rows(S);
@@ -509,19 +515,19 @@ extern "C" int vy_ppo_head_bwd(const void* logits, int32_t dtype, int64_t ld, co
   if (dtype == 0) {
     if (A == 21)
       k_ppo_head_bwd<float, 21><<<grid, kHeadThreads, smem, st>>>(static_cast<const float*>(logits), actions, N, S, A,
-                                                                  ld, G, g_lp, g_ent, static_cast<float*>(grad));
+                                                                  ld, G, g_lp, g_ent, g_value, value_col, static_cast<float*>(grad));
     else
       k_ppo_head_bwd<float, 0><<<grid, kHeadThreads, smem, st>>>(static_cast<const float*>(logits), actions, N, S, A,
-                                                                 ld, G, g_lp, g_ent, static_cast<float*>(grad));
+                                                                 ld, G, g_lp, g_ent, g_value, value_col, static_cast<float*>(grad));
   } else {
     if (A == 21)
       k_ppo_head_bwd<__nv_bfloat16, 21><<<grid, kHeadThreads, smem, st>>>(
           static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, g_lp, g_ent,
-          static_cast<__nv_bfloat16*>(grad));
+          g_value, value_col, static_cast<__nv_bfloat16*>(grad));
     else
       k_ppo_head_bwd<__nv_bfloat16, 0><<<grid, kHeadThreads, smem, st>>>(
           static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G, g_lp, g_ent,
-          static_cast<__nv_bfloat16*>(grad));
+          g_value, value_col, static_cast<__nv_bfloat16*>(grad));
   }
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }

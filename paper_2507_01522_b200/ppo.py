@@ -238,36 +238,47 @@ class PolicyHead(torch.autograd.Function):
     """Per-sample log-probability of stored multi-discrete actions and entropy
     (both summed over slots) from logits rows of S x A values (float32 or
     bf16; row n starts at n * logits.stride(0), so the padded head output is
-    read in place): vy_ppo_head_fwd / vy_ppo_head_bwd, one pass each way."""
+    read in place): vy_ppo_head_fwd / vy_ppo_head_bwd, one pass each way.
+    With value_col >= 0 the rows also carry a value head in padding column
+    value_col (the merged head GEMM): it is returned as a third output and its
+    gradient is written by the same backward pass (a separate column select
+    would add two full-width passes over the gradient)."""
 
     @staticmethod
-    def forward(ctx, logits: torch.Tensor, actions: torch.Tensor, S: int, A: int):
+    def forward(ctx, logits: torch.Tensor, actions: torch.Tensor, S: int, A: int, value_col: int = -1):
         N = logits.shape[0]
         ld = logits.stride(0)
         if logits.stride(-1) != 1 or logits[0].numel() < S * A or (logits.dim() > 2 and not logits[0].is_contiguous()):
             raise ValueError("logits rows must be contiguous with at least S*A values")
+        if value_col >= 0 and not (S * A <= value_col < ld and logits.dim() == 2):
+            raise ValueError("value_col must be a padding column of 2-D logits rows")
         lp = torch.empty(N, device=logits.device)
         ent = torch.empty(N, device=logits.device)
         nat.check(nat.lib().vy_ppo_head_fwd(logits.data_ptr(), _dtype_code(logits), ld, actions.data_ptr(), N, S, A,
                                             lp.data_ptr(), ent.data_ptr(), torch.cuda.current_stream().cuda_stream),
                   "vy_ppo_head_fwd")
         ctx.save_for_backward(logits, actions)
-        ctx.S, ctx.A = S, A
+        ctx.S, ctx.A, ctx.value_col = S, A, value_col
+        if value_col >= 0:
+            return lp, ent, logits[:, value_col].float()
         return lp, ent
 
     @staticmethod
-    def backward(ctx, g_lp, g_ent):
+    def backward(ctx, g_lp, g_ent, g_v=None):
         logits, actions = ctx.saved_tensors
         N, S, A = logits.shape[0], ctx.S, ctx.A
         grad = torch.empty_like(logits)
         g_lp = g_lp.contiguous() if g_lp is not None else None
         g_ent = g_ent.contiguous() if g_ent is not None else None
+        g_v = g_v.float().contiguous() if (g_v is not None and ctx.value_col >= 0) else None
         nat.check(nat.lib().vy_ppo_head_bwd(logits.data_ptr(), _dtype_code(logits), logits.stride(0),
                                             actions.data_ptr(), N, S, A,
                                             g_lp.data_ptr() if g_lp is not None else None,
-                                            g_ent.data_ptr() if g_ent is not None else None, grad.data_ptr(),
-                                            torch.cuda.current_stream().cuda_stream), "vy_ppo_head_bwd")
-        return grad, None, None, None
+                                            g_ent.data_ptr() if g_ent is not None else None,
+                                            g_v.data_ptr() if g_v is not None else None, ctx.value_col,
+                                            grad.data_ptr(), torch.cuda.current_stream().cuda_stream),
+                  "vy_ppo_head_bwd")
+        return grad, None, None, None, None
 
 
 def head_reference(logits: torch.Tensor, actions: torch.Tensor):
@@ -469,12 +480,13 @@ class PPOTrainer:
                 idx = perm[k * mb:(k + 1) * mb]
                 with torch.autocast("cuda", dtype=torch.bfloat16):
                     if cfg.fused_head:  # head output read in place by the fused head (row stride out_dim + 8)
-                        logits, v = self.net.forward_merged(gather_rows(obs, idx))
+                        logits, _ = self.net.forward_merged(gather_rows(obs, idx))
                     else:
                         logits, v = self.net(gather_rows(obs, idx), logits_fp32=True)
-                    v = v.float()
-                if cfg.fused_head:
-                    lp, ent = PolicyHead.apply(logits, act[idx], self.net.n_slots, self.net.n_actions)
+                        v = v.float()
+                if cfg.fused_head:  # the value column rides through the head kernels too
+                    lp, ent, v = PolicyHead.apply(logits, act[idx], self.net.n_slots, self.net.n_actions,
+                                                  self.net.out_dim)
                 else:
                     lp, ent = head_reference(logits, act[idx])
                 ent = ent.mean()

@@ -306,3 +306,28 @@ def test_merged_training_forward_matches_the_network():
     torch.testing.assert_close(v2, v, rtol=1e-4, atol=1e-4)
     for n, p in net.named_parameters():
         torch.testing.assert_close(p.grad, ref[n], rtol=1e-3, atol=1e-3, msg=n)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_policy_head_value_column(dtype):
+    """PolicyHead with value_col: the value is column value_col of the rows and
+    its gradient lands there in the same backward pass; the logits gradient
+    equals the plain head plus a column select."""
+    from paper_2507_01522_b200.ppo import PolicyHead
+
+    torch.manual_seed(2)
+    N, S, A, ld, col = 3001, 17, 21, 368, 360
+    base = torch.randn(N, ld, device="cuda").to(dtype)
+    a = torch.randint(0, A, (N, S), device="cuda", dtype=torch.uint8)
+    g1, g2, g3 = (torch.randn(N, device="cuda") for _ in range(3))
+    z1 = base.clone().requires_grad_(True)
+    lp, ent, v = PolicyHead.apply(z1, a, S, A, col)
+    ((lp * g1).sum() + (ent * g2).sum() + (v * g3).sum()).backward()
+    z2 = base.clone().requires_grad_(True)
+    lp2, ent2 = PolicyHead.apply(z2, a, S, A)
+    v2 = z2[:, col].float()
+    ((lp2 * g1).sum() + (ent2 * g2).sum() + (v2 * g3).sum()).backward()
+    torch.testing.assert_close(v, v2, rtol=0, atol=0)
+    torch.testing.assert_close(lp, lp2, rtol=0, atol=0)
+    torch.testing.assert_close(z1.grad.float(), z2.grad.float(), rtol=1e-2, atol=1e-2)
+    assert torch.equal(z1.grad[:, col].float(), g3.to(dtype).float())
