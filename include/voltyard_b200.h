@@ -249,9 +249,12 @@ int vy_ppo_sample(const void *logits, int32_t dtype, int64_t ld, const float *no
                   uint8_t *actions, float *logp, void *stream);
 /* vy_ppo_sample with the uniforms drawn in the kernel: element e of call c
  * uses splitmix64(mix(seed, c) + e*golden); counter = int64[2] on the device,
- * {c, scratch = 0}, c advanced by the launch itself (CUDA-graph friendly). */
+ * {c, scratch = 0}, c advanced by the launch itself (CUDA-graph friendly).
+ * value (optional, float32 [N]) receives padding column value_col of each
+ * row (S*A <= value_col < ld): a value head sharing the GEMM. */
 int vy_ppo_sample_rng(const void *logits, int32_t dtype, int64_t ld, uint64_t seed, int64_t *counter, int64_t N,
-                      int32_t S, int32_t A, uint8_t *actions, float *logp, void *stream);
+                      int32_t S, int32_t A, uint8_t *actions, float *logp, float *value, int32_t value_col,
+                      void *stream);
 int vy_ppo_head_fwd(const void *logits, int32_t dtype, int64_t ld, const uint8_t *actions, int64_t N, int32_t S,
                     int32_t A, float *lp, float *ent, void *stream);
 int vy_ppo_head_bwd(const void *logits, int32_t dtype, int64_t ld, const uint8_t *actions, int64_t N, int32_t S,

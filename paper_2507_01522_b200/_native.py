@@ -65,7 +65,7 @@ _SIGS = {
     "vy_gae": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_int64, C.c_float, C.c_float, _P, _P, _P]),
     "vy_ppo_sample": (C.c_int, [_P, C.c_int32, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]),
     "vy_ppo_sample_rng": (C.c_int, [_P, C.c_int32, C.c_int64, C.c_uint64, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P,
-                                    _P]),
+                                    _P, C.c_int32, _P]),
     "vy_ppo_head_fwd": (C.c_int, [_P, C.c_int32, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]),
     "vy_ppo_head_bwd": (C.c_int, [_P, C.c_int32, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P,
                                   C.c_int32, _P, _P]),

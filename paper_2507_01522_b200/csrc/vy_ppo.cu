@@ -302,7 +302,8 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_sample(const T* __restrict
                                                              const float* __restrict__ noise, uint64_t seed,
                                                              unsigned long long* counter, int64_t N, int S, int A,
                                                              int64_t ld, int G, uint8_t* __restrict__ actions,
-                                                             float* __restrict__ logp) {
+                                                             float* __restrict__ logp, float* __restrict__ value,
+                                                             int value_col) {
   extern __shared__ float ppo_smem[];
   const int64_t n0 = (int64_t)blockIdx.x * G;
   const int gh = (int)min((int64_t)G, N - n0);
@@ -343,6 +344,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_sample(const T* __restrict
     float acc = 0.f;
     for (int s = 0; s < S; ++s) acc += part[t * S + s];
     logp[n0 + t] = acc;
+    if (value) value[n0 + t] = rows[(size_t)t * ld + value_col];  // a value head sharing the GEMM row
   }
   if (!noise && t == 0) {
     __threadfence();
@@ -424,9 +426,11 @@ unsigned head_grid(int64_t N, int S) { return (unsigned)((N + head_rows(S) - 1) 
 // dtype: 0 = float32 logits (and gradient), 1 = bfloat16
 namespace {
 int launch_sample(const void* logits, int32_t dtype, int64_t ld, const float* noise, uint64_t seed, int64_t* counter,
-                  int64_t N, int32_t S, int32_t A, uint8_t* actions, float* logp, void* stream) {
+                  int64_t N, int32_t S, int32_t A, uint8_t* actions, float* logp, float* value, int32_t value_col,
+                  void* stream) {
   if (!logits || !actions || !logp || N < 1 || S < 1 || A < 1 || A > 256 || (dtype != 0 && dtype != 1) ||
-      head_rows(S) < 1 || ld < (int64_t)S * A || head_smem(S, ld) > 48 * 1024)
+      head_rows(S) < 1 || ld < (int64_t)S * A || head_smem(S, ld) > 48 * 1024 ||
+      (value && (value_col < S * A || value_col >= ld)))
     return VY_ERR_ARG;
   auto st = (cudaStream_t)stream;
   const int G = head_rows(S);
@@ -434,17 +438,17 @@ int launch_sample(const void* logits, int32_t dtype, int64_t ld, const float* no
   if (dtype == 0) {
     if (A == 21)
       k_ppo_sample<float, 21><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
-        static_cast<const float*>(logits), noise, seed, ctr, N, S, A, ld, G, actions, logp);
+        static_cast<const float*>(logits), noise, seed, ctr, N, S, A, ld, G, actions, logp, value, value_col);
     else
       k_ppo_sample<float, 0><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
-        static_cast<const float*>(logits), noise, seed, ctr, N, S, A, ld, G, actions, logp);
+        static_cast<const float*>(logits), noise, seed, ctr, N, S, A, ld, G, actions, logp, value, value_col);
   } else {
     if (A == 21)
       k_ppo_sample<__nv_bfloat16, 21><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
-        static_cast<const __nv_bfloat16*>(logits), noise, seed, ctr, N, S, A, ld, G, actions, logp);
+        static_cast<const __nv_bfloat16*>(logits), noise, seed, ctr, N, S, A, ld, G, actions, logp, value, value_col);
     else
       k_ppo_sample<__nv_bfloat16, 0><<<head_grid(N, S), kHeadThreads, head_smem(S, ld), st>>>(
-        static_cast<const __nv_bfloat16*>(logits), noise, seed, ctr, N, S, A, ld, G, actions, logp);
+        static_cast<const __nv_bfloat16*>(logits), noise, seed, ctr, N, S, A, ld, G, actions, logp, value, value_col);
   }
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
@@ -453,13 +457,14 @@ int launch_sample(const void* logits, int32_t dtype, int64_t ld, const float* no
 extern "C" int vy_ppo_sample(const void* logits, int32_t dtype, int64_t ld, const float* noise, int64_t N, int32_t S,
                              int32_t A, uint8_t* actions, float* logp, void* stream) {
   if (!noise) return VY_ERR_ARG;
-  return launch_sample(logits, dtype, ld, noise, 0, nullptr, N, S, A, actions, logp, stream);
+  return launch_sample(logits, dtype, ld, noise, 0, nullptr, N, S, A, actions, logp, nullptr, 0, stream);
 }
 
 extern "C" int vy_ppo_sample_rng(const void* logits, int32_t dtype, int64_t ld, uint64_t seed, int64_t* counter,
-                                 int64_t N, int32_t S, int32_t A, uint8_t* actions, float* logp, void* stream) {
+                                 int64_t N, int32_t S, int32_t A, uint8_t* actions, float* logp, float* value,
+                                 int32_t value_col, void* stream) {
   if (!counter) return VY_ERR_ARG;
-  return launch_sample(logits, dtype, ld, nullptr, seed, counter, N, S, A, actions, logp, stream);
+  return launch_sample(logits, dtype, ld, nullptr, seed, counter, N, S, A, actions, logp, value, value_col, stream);
 }
 
 extern "C" int vy_ppo_head_fwd(const void* logits, int32_t dtype, int64_t ld, const uint8_t* actions, int64_t N,

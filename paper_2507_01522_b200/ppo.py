@@ -374,6 +374,7 @@ class PPOTrainer:
             nat.check(nat.lib().vy_ppo_sample_rng(logits.data_ptr(), _dtype_code(logits), logits.stride(0),
                                                   self._sample_seed, self._sample_ctr.data_ptr(), B, S, A,
                                                   self.actions[t].data_ptr(), self.logp[t].data_ptr(),
+                                                  self.values[t].data_ptr(), self.net.out_dim,  # value column too
                                                   torch.cuda.current_stream().cuda_stream), "vy_ppo_sample_rng")
         else:
             noise = torch.rand(logits.shape[0], self.net.n_slots, self.net.n_actions, device=logits.device)
@@ -382,7 +383,7 @@ class PPOTrainer:
             lp = torch.log_softmax(logits, dim=-1).gather(-1, a.unsqueeze(-1)).squeeze(-1).sum(-1)
             self.actions[t].copy_(a)
             self.logp[t].copy_(lp)
-        self.values[t].copy_(v)  # widened to float32 by the copy
+            self.values[t].copy_(v)
         # the env writes the next obs / reward / done straight into the rollout buffers
         self.env.set_outputs(obs=self.obs[t + 1], reward=self.rewards[t], done=self.dones[t])
         self.env.step(self.actions[t], collect_infos=False)

@@ -235,7 +235,7 @@ def test_in_kernel_rng_sampler_draws_the_softmax():
         act = torch.empty(N, S, dtype=torch.uint8, device="cuda")
         lp = torch.empty(N, device="cuda")
         nat.check(nat.lib().vy_ppo_sample_rng(z.data_ptr(), 0, S * A, 1234, ctr.data_ptr(), N, S, A,
-                                              act.data_ptr(), lp.data_ptr(), st), "vy_ppo_sample_rng")
+                                              act.data_ptr(), lp.data_ptr(), None, 0, st), "vy_ppo_sample_rng")
         return act, lp
 
     a1, lp1 = draw()
@@ -331,3 +331,18 @@ def test_policy_head_value_column(dtype):
     torch.testing.assert_close(lp, lp2, rtol=0, atol=0)
     torch.testing.assert_close(z1.grad.float(), z2.grad.float(), rtol=1e-2, atol=1e-2)
     assert torch.equal(z1.grad[:, col].float(), g3.to(dtype).float())
+
+
+def test_sampler_writes_the_value_column():
+    from paper_2507_01522_b200 import _native as nat
+
+    N, S, A, ld, col = 1000, 17, 21, 368, 360
+    z = torch.randn(N, ld, device="cuda").to(torch.bfloat16)
+    ctr = torch.zeros(2, dtype=torch.int64, device="cuda")
+    act = torch.empty(N, S, dtype=torch.uint8, device="cuda")
+    lp = torch.empty(N, device="cuda")
+    val = torch.empty(N, device="cuda")
+    nat.check(nat.lib().vy_ppo_sample_rng(z.data_ptr(), 1, ld, 7, ctr.data_ptr(), N, S, A, act.data_ptr(),
+                                          lp.data_ptr(), val.data_ptr(), col,
+                                          torch.cuda.current_stream().cuda_stream), "vy_ppo_sample_rng")
+    assert torch.equal(val, z[:, col].float())
