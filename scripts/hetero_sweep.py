@@ -3,8 +3,8 @@ sys.path.insert(0, ".")
 import torch
 from paper_2507_01522_b200.hetero import HeteroBatch, sweep_groups
 B = 1 << 20
-for tpw in (1, 2, 3):
-    for ns in (8, 12, 16, 24, 36):
+for tpw in (2, 3, 4):
+    for ns in (9, 12, 18, 24):
         hb = HeteroBatch(sweep_groups(B), master_seed=0, policy_seed=0, n_streams=ns, tiles_per_warp=tpw)
         hb.reset()
         for _ in range(3):
