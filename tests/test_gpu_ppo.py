@@ -346,3 +346,20 @@ def test_sampler_writes_the_value_column():
                                           lp.data_ptr(), val.data_ptr(), col,
                                           torch.cuda.current_stream().cuda_stream), "vy_ppo_sample_rng")
     assert torch.equal(val, z[:, col].float())
+
+
+@pytest.mark.parametrize("fused,graph", [(False, True), (False, False), (True, False)])
+def test_trainer_non_default_modes_run(fused, graph):
+    """The torch-head and eager (no CUDA graph) trainer paths still run and
+    give finite losses."""
+    from paper_2507_01522_b200 import default_setup
+    from paper_2507_01522_b200.batch import BatchEnv
+    from paper_2507_01522_b200.ppo import PPOConfig, PPOTrainer
+
+    rc = default_setup()
+    env = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=256, master_seed=1)
+    tr = PPOTrainer(env, PPOConfig(rollout_steps=20, fused_head=fused, use_graph=graph))
+    for _ in range(2):
+        st = tr.iterate()
+    assert all(torch.isfinite(v).all() for v in st.values())
+    env.close()
