@@ -384,6 +384,35 @@ __global__ void __launch_bounds__(512) k_colsum_bands(const T* __restrict__ g, i
   }
 }
 
+// bf16 rows with an even width: one thread per column pair (4-byte loads),
+// half the load instructions of the per-column kernel
+__global__ void __launch_bounds__(512) k_colsum_bands_bf2(const __nv_bfloat162* __restrict__ g, int64_t M, int N2,
+                                                          int64_t ld2, int64_t rows_per_band, float* __restrict__ work) {
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_band;
+  const int64_t r1 = min(M, r0 + rows_per_band);
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < N2; c += gridDim.x * blockDim.x) {
+    float a0 = 0.f, a1 = 0.f;
+    int64_t r = r0;
+    for (; r + 8 <= r1; r += 8) {
+      float2 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __bfloat1622float2(g[(r + j) * ld2 + c]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        a0 += v[j].x;
+        a1 += v[j].y;
+      }
+    }
+    for (; r < r1; ++r) {
+      const float2 v = __bfloat1622float2(g[r * ld2 + c]);
+      a0 += v.x;
+      a1 += v.y;
+    }
+    work[(int64_t)blockIdx.y * 2 * N2 + 2 * c] = a0;
+    work[(int64_t)blockIdx.y * 2 * N2 + 2 * c + 1] = a1;
+  }
+}
+
 // 32 columns per block, 32 band groups per column summed with eight loads
 // in flight each, then the 32 group sums added in group order.
 __global__ void __launch_bounds__(1024) k_colsum_reduce(const float* __restrict__ work, int bands, int N,
@@ -563,14 +592,19 @@ extern "C" int vy_colsum(const void* g, int32_t dtype, int64_t M, int64_t N, int
     return cudaMemsetAsync(out, 0, (size_t)N * sizeof(float), st) == cudaSuccess ? VY_OK : VY_ERR_CUDA;
   }
   if (!g) return VY_ERR_ARG;
-  const int threads = N >= 512 ? 512 : ((int)N + 31) / 32 * 32;  // one x-block up to 512 columns
-  const unsigned gx = (unsigned)((N + threads - 1) / threads);
+  const bool pairs = dtype == 1 && N % 2 == 0 && ld % 2 == 0 && (reinterpret_cast<uintptr_t>(g) & 3u) == 0;
+  const int64_t cols = pairs ? N / 2 : N;  // threads' columns (pairs for even-width bf16)
+  const int threads = cols >= 512 ? 512 : ((int)cols + 31) / 32 * 32;  // one x-block up to 512 columns
+  const unsigned gx = (unsigned)((cols + threads - 1) / threads);
   // enough row bands to fill the GPU a few times over, at least 64 rows each
   int64_t bands = std::min<int64_t>(kColsumBands, std::max<int64_t>(1, 148 * 8 / (int64_t)gx));
   const int64_t rpb = std::max<int64_t>(64, (M + bands - 1) / bands);
   bands = (M + rpb - 1) / rpb;
   const dim3 grid(gx, (unsigned)bands);
-  if (dtype == 0)
+  if (pairs)
+    k_colsum_bands_bf2<<<grid, threads, 0, st>>>(static_cast<const __nv_bfloat162*>(g), M, (int)(N / 2), ld / 2, rpb,
+                                                 work);
+  else if (dtype == 0)
     k_colsum_bands<float><<<grid, threads, 0, st>>>(static_cast<const float*>(g), M, (int)N, ld, rpb, work);
   else
     k_colsum_bands<__nv_bfloat16><<<grid, threads, 0, st>>>(static_cast<const __nv_bfloat16*>(g), M, (int)N, ld, rpb,
