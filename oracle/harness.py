@@ -62,6 +62,9 @@ def load_oracle() -> C.CDLL:
         lib.vyo_step_range.argtypes = [_P, _P, _P, C.c_int64, C.c_int64, _P]
         lib.vyo_step_parallel.argtypes = [_P, _P, _P, C.c_int64, _P, C.c_int]
         lib.vyo_random_actions.argtypes = [_P, C.c_int64, C.c_int32, C.c_int32, _P]
+        lib.vyo_reset_parallel.argtypes = [_P, _P, _P, C.c_int64, C.c_int, C.c_int]
+        lib.vyo_step_parallel_autoreset.argtypes = [_P, _P, _P, C.c_int64, _P, C.c_int]
+        lib.vyo_random_actions_parallel.argtypes = [_P, C.c_int64, C.c_int32, C.c_int32, _P, C.c_int]
         _lib = lib
     return _lib
 
@@ -130,6 +133,14 @@ class _OracleCore:
         self.lib.vyo_step_parallel(C.byref(self.tc), C.byref(self.sc), C.byref(self.oc), len(a),
                                    a.ctypes.data, self.threads)
 
+    def reset_all(self, first: bool) -> None:
+        self.lib.vyo_reset_parallel(C.byref(self.tc), C.byref(self.sc), C.byref(self.oc), len(self.s.step),
+                                    int(first), self.threads)
+
+    def step_all_autoreset(self, a: np.ndarray) -> None:
+        self.lib.vyo_step_parallel_autoreset(C.byref(self.tc), C.byref(self.sc), C.byref(self.oc), len(a),
+                                             a.ctypes.data, self.threads)
+
 
 class _RefCore:
     """The reference's CySimCore on our arrays; worker threads like engine.py:446-456."""
@@ -171,8 +182,8 @@ class HostBatch:
         self.t = tables
         self.batch_size = B = batch_size
         self.auto_reset = auto_reset
-        if env_seeds is None:
-            env_seeds = [split_seed(master_seed, i) for i in range(B)]
+        if env_seeds is None:  # split_seed(master, i) for every row, vectorised
+            env_seeds = vstream_key(master_seed, np.arange(B, dtype=np.int64))
         self.states = allocate_state(B, tables.n_ports, env_seeds)
         self.outs = allocate_outs(B, tables.n_ports, tables.n_slots, tables.obs_len)
         cls = {"oracle": _OracleCore, "ref": _RefCore}[core]
@@ -189,8 +200,11 @@ class HostBatch:
         return self.reset()
 
     def reset(self) -> np.ndarray:
-        for b in range(self.batch_size):
-            self.core.reset_env(b, 0 if self._needs_reset else int(self.states.episode[b]) + 1)
+        if hasattr(self.core, "reset_all"):
+            self.core.reset_all(self._needs_reset)
+        else:
+            for b in range(self.batch_size):
+                self.core.reset_env(b, 0 if self._needs_reset else int(self.states.episode[b]) + 1)
         self._needs_reset = False
         return self.outs.obs.copy()
 
@@ -211,16 +225,31 @@ class HostBatch:
                 self.core.reset_env(int(b), int(self.states.episode[b]) + 1)
         return self.outs.obs.copy(), self.outs.reward.copy(), dones
 
+    def step_inplace(self, actions: np.ndarray) -> None:
+        """step() for large batches: int64 [B, N+1] actions, no validation and no
+        copies (outputs stay in self.outs); done rows are reset inside the
+        oracle's worker threads (core="oracle" only)."""
+        if self.auto_reset:
+            self.core.step_all_autoreset(actions)
+        else:
+            self.core.step_all(actions)
+
 
 class HostRandomPolicy:
     """RandomPolicy (policies.py:51-73) with the oracle's C draw loop."""
 
-    def __init__(self, seed: int, n_ports: int, k: int, rows):
+    def __init__(self, seed: int, n_ports: int, k: int, rows, threads: int = 1):
         self.n_slots, self.hi = n_ports + 1, 2 * k + 1
-        self.keys = vstream_key(seed, np.asarray(list(rows), dtype=np.int64), PHASE_POLICY)
+        rows = rows if isinstance(rows, range) else list(rows)
+        self.keys = vstream_key(seed, np.asarray(rows, dtype=np.int64), PHASE_POLICY)
+        self.threads = threads
+        self._out = None
 
-    def actions(self) -> np.ndarray:
-        out = np.empty((len(self.keys), self.n_slots), dtype=np.int64)
-        load_oracle().vyo_random_actions(self.keys.ctypes.data, len(self.keys), self.n_slots, self.hi,
-                                         out.ctypes.data)
+    def actions(self, reuse: bool = False) -> np.ndarray:
+        """Next call's actions; reuse=True writes into one persistent buffer."""
+        out = self._out if reuse and self._out is not None else np.empty((len(self.keys), self.n_slots), np.int64)
+        if reuse:
+            self._out = out
+        load_oracle().vyo_random_actions_parallel(self.keys.ctypes.data, len(self.keys), self.n_slots, self.hi,
+                                                  out.ctypes.data, self.threads)
         return out

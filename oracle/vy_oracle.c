@@ -453,26 +453,98 @@ typedef struct slice_job {
   vyo_outs *o;
   int64_t b0, b1;
   const int64_t *a;
+  int auto_reset;
 } slice_job;
 
 static void *run_slice(void *p) {
   slice_job *j = (slice_job *)p;
   vyo_step_range(j->t, j->s, j->o, j->b0, j->b1, j->a);
+  /* engine.py:459-462: done rows start episode + 1 after the step (rows are
+   * independent, so resetting inside the slice equals the engine's loop) */
+  if (j->auto_reset)
+    for (int64_t b = j->b0; b < j->b1; ++b)
+      if (j->o->done[b]) vyo_reset_env(j->t, j->s, j->o, b, j->s->episode[b] + 1);
   return NULL;
 }
 
-void vyo_step_parallel(const vy_tables *t, vyo_state *s, vyo_outs *o, int64_t B, const int64_t *actions,
-                       int threads) {
-  if (threads <= 1 || B < 2) {
-    vyo_step_range(t, s, o, 0, B, actions);
-    return;
-  }
+static void step_slices(const vy_tables *t, vyo_state *s, vyo_outs *o, int64_t B, const int64_t *actions,
+                        int threads, int auto_reset) {
+  if (threads < 1 || B < 2) threads = 1;
   if (threads > 256) threads = 256;
   pthread_t th[256];
   slice_job jobs[256];
   for (int w = 0; w < threads; ++w) {
-    jobs[w] = (slice_job){t, s, o, B * w / threads, B * (w + 1) / threads, actions};
-    pthread_create(&th[w], NULL, run_slice, &jobs[w]);
+    jobs[w] = (slice_job){t, s, o, B * w / threads, B * (w + 1) / threads, actions, auto_reset};
+    if (threads == 1)
+      run_slice(&jobs[w]);
+    else
+      pthread_create(&th[w], NULL, run_slice, &jobs[w]);
+  }
+  if (threads > 1)
+    for (int w = 0; w < threads; ++w) pthread_join(th[w], NULL);
+}
+
+void vyo_step_parallel(const vy_tables *t, vyo_state *s, vyo_outs *o, int64_t B, const int64_t *actions,
+                       int threads) {
+  step_slices(t, s, o, B, actions, threads, 0);
+}
+
+void vyo_step_parallel_autoreset(const vy_tables *t, vyo_state *s, vyo_outs *o, int64_t B,
+                                 const int64_t *actions, int threads) {
+  step_slices(t, s, o, B, actions, threads, 1);
+}
+
+/* BatchEnv.reset over rows [0, B) (engine.py:414-424): episode 0 when `first`,
+ * else each row's episode + 1; rows are independent, so slices run in parallel */
+typedef struct reset_job {
+  const vy_tables *t;
+  vyo_state *s;
+  vyo_outs *o;
+  int64_t b0, b1;
+  int first;
+} reset_job;
+
+static void *run_reset(void *p) {
+  reset_job *j = (reset_job *)p;
+  for (int64_t b = j->b0; b < j->b1; ++b) vyo_reset_env(j->t, j->s, j->o, b, j->first ? 0 : j->s->episode[b] + 1);
+  return NULL;
+}
+
+void vyo_reset_parallel(const vy_tables *t, vyo_state *s, vyo_outs *o, int64_t B, int first, int threads) {
+  if (threads < 1 || B < 2) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  reset_job jobs[256];
+  for (int w = 0; w < threads; ++w) {
+    jobs[w] = (reset_job){t, s, o, B * w / threads, B * (w + 1) / threads, first};
+    pthread_create(&th[w], NULL, run_reset, &jobs[w]);
+  }
+  for (int w = 0; w < threads; ++w) pthread_join(th[w], NULL);
+}
+
+/* RandomPolicy.actions over rows [0, B) on `threads` threads (row-independent streams) */
+typedef struct pol_job {
+  uint64_t *keys;
+  int64_t b0, b1;
+  int32_t n_slots, hi;
+  int64_t *out;
+} pol_job;
+
+static void *run_pol(void *p) {
+  pol_job *j = (pol_job *)p;
+  vyo_random_actions(j->keys + j->b0, j->b1 - j->b0, j->n_slots, j->hi, j->out + j->b0 * j->n_slots);
+  return NULL;
+}
+
+void vyo_random_actions_parallel(uint64_t *keys, int64_t B, int32_t n_slots, int32_t hi, int64_t *out,
+                                 int threads) {
+  if (threads < 1 || B < 2) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  pol_job jobs[256];
+  for (int w = 0; w < threads; ++w) {
+    jobs[w] = (pol_job){keys, B * w / threads, B * (w + 1) / threads, n_slots, hi, out};
+    pthread_create(&th[w], NULL, run_pol, &jobs[w]);
   }
   for (int w = 0; w < threads; ++w) pthread_join(th[w], NULL);
 }

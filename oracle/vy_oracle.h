@@ -54,9 +54,17 @@ void vyo_step_range(const vy_tables *t, vyo_state *s, vyo_outs *o, int64_t b0, i
  * worker split, engine.py:446-456); results are identical for any count. */
 void vyo_step_parallel(const vy_tables *t, vyo_state *s, vyo_outs *o, int64_t B,
                        const int64_t *actions, int threads);
+/* The same with the engine's auto-reset of done rows (episode + 1,
+ * engine.py:459-462) done inside each slice. */
+void vyo_step_parallel_autoreset(const vy_tables *t, vyo_state *s, vyo_outs *o, int64_t B,
+                                 const int64_t *actions, int threads);
+/* BatchEnv.reset of rows [0, B): episode 0 if `first`, else episode + 1. */
+void vyo_reset_parallel(const vy_tables *t, vyo_state *s, vyo_outs *o, int64_t B, int first, int threads);
 /* RandomPolicy.actions for rows [0,B): keys[b] is the row's stream state,
  * advanced in place (policies.py:69-73, rng.py:154-170). */
 void vyo_random_actions(uint64_t *keys, int64_t B, int32_t n_slots, int32_t hi, int64_t *out);
+void vyo_random_actions_parallel(uint64_t *keys, int64_t B, int32_t n_slots, int32_t hi, int64_t *out,
+                                 int threads);
 uint64_t vyo_stream_key2(uint64_t a, uint64_t b);
 uint64_t vyo_stream_key3(uint64_t a, uint64_t b, uint64_t c);
 

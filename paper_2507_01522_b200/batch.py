@@ -461,22 +461,24 @@ class BatchEnv:
         occ = (meta & 1).astype(np.int8)
         pref = ((meta >> 1) & 1).astype(np.int8)
         prof = meta >> 2
-        profs = {int(p): self.profile(int(p)) for p in np.unique(prof[occ == 1])}
-        cap = np.zeros(meta.shape)
-        rbar = np.zeros(meta.shape)
-        tau = np.zeros(meta.shape)
-        for (b, i) in zip(*np.nonzero(occ)):
-            c, rac, rdc, ta = profs[int(prof[b, i])]
-            cap[b, i] = c
-            rbar[b, i] = rdc if t.kind[i] == 1 else rac
-            tau[b, i] = ta
+        # per-profile lookup tables (cap, r_ac, r_dc, tau), vectorised over [B, N]
+        ids = np.unique(prof[occ == 1])
+        lut = np.zeros((int(ids.max()) + 1 if ids.size else 1, 4))
+        for p in ids:
+            lut[int(p)] = self.profile(int(p))
+        on = occ == 1
+        dc = (np.asarray(t.kind)[None, :] == 1)
+        cap = np.where(on, lut[prof, 0], 0.0)
+        rbar = np.where(on, np.where(dc, lut[prof, 2], lut[prof, 1]), 0.0)
+        tau = np.where(on, lut[prof, 3], 0.0)
         soc = s.port_soc.cpu().numpy().T.copy()
-        rhat = np.zeros(meta.shape)
-        for (b, i) in zip(*np.nonzero(occ)):
-            rhat[b, i] = rbar[b, i] if soc[b, i] <= tau[b, i] else (1.0 - soc[b, i]) * rbar[b, i] / (1.0 - tau[b, i])
+        with np.errstate(divide="ignore", invalid="ignore"):
+            # charge_limit (vehicles.py:22-35) with the reference's operation order
+            taper = (1.0 - soc) * rbar / (1.0 - tau)
+        rhat = np.where(on, np.where(soc <= tau, rbar, taper), 0.0)
         b_soc = s.b_soc.cpu().numpy().copy()
         if t.battery_enabled:
-            b_rhat = np.array([t.b_rmax if x <= t.b_tau else (1.0 - x) * t.b_rmax / (1.0 - t.b_tau) for x in b_soc])
+            b_rhat = np.where(b_soc <= t.b_tau, t.b_rmax, (1.0 - b_soc) * t.b_rmax / (1.0 - t.b_tau))
         else:
             b_rhat = np.zeros_like(b_soc)
         return dict(

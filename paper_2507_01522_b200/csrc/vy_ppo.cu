@@ -328,7 +328,9 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_sample(const T* __restrict
       if (noise) {
         u = fminf(fmaxf(noise[e0 + k], 1e-20f), 1.f);
       } else {
-        u = ((float)(mix64(key + (uint64_t)(e0 + k) * 0x9E3779B97F4A7C15ULL) >> 40) + 0.5f) * (1.f / 16777216.f);
+        // 23 bits: (x + 0.5) * 2^-23 is exact in float and lies in (0, 1), so
+        // the double log stays finite (24 bits rounded the top draw to 1.0)
+        u = ((float)(mix64(key + (uint64_t)(e0 + k) * 0x9E3779B97F4A7C15ULL) >> 41) + 0.5f) * (1.f / 8388608.f);
       }
       const float v = z[k] - __logf(-__logf(u));  // + Gumbel(0, 1)
       if (v > bv) {
@@ -575,7 +577,9 @@ extern "C" int vy_gather_rows(const void* src, int64_t row_bytes, const int64_t*
   const int64_t vpr = row_bytes / 16, total = n * vpr;
   const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
   auto st = (cudaStream_t)stream;
-  if (total < (int64_t)UINT32_MAX)
+  // 32-bit indexing only when the grid-stride loop cannot wrap past 2^32
+  // (idx values must lie in [0, rows of src); they are not bounds-checked)
+  if (total + (int64_t)grid * 256 <= (int64_t)UINT32_MAX)
     k_gather_rows<uint32_t><<<grid, 256, 0, st>>>(static_cast<const uint4*>(src), (uint32_t)vpr, idx,
                                                   (uint32_t)total, static_cast<uint4*>(dst));
   else

@@ -405,6 +405,7 @@ class PPOTrainer:
     def rollout(self) -> None:
         T = self.cfg.rollout_steps
         t0 = self.env._t
+        executed = 1  # rollouts the GPU runs in this call
         if not self.cfg.use_graph:
             self._rollout_body()
         else:
@@ -416,11 +417,12 @@ class PPOTrainer:
                 torch.cuda.current_stream().wait_stream(s)
                 self.obs[0].copy_(self.obs[-1])
                 self._graph = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(self._graph):
+                with torch.cuda.graph(self._graph):  # captured, not executed (env.step still ticks the host clock)
                     self._rollout_body()
+                executed = 2  # the warm-up rollout, then the first replay below
             self._graph.replay()
-        if t0 is not None:  # the host mirror of the lockstep clock is not advanced by a graph replay
-            self.env._t = (t0 + T) % self.env.tables.episode_steps
+        if t0 is not None:  # the host mirror of the lockstep clock: a graph replay runs no host code
+            self.env._t = (t0 + executed * T) % self.env.tables.episode_steps
         self.env.restore_outputs()
 
     # -- update -------------------------------------------------------------------

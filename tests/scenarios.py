@@ -79,3 +79,47 @@ def single_node_station(n_ports: int = 2, cap_a: float = 1e9, voltage_v: float =
                             i_max_discharge_a=i_max if i_max_discharge is None else i_max_discharge,
                             eta_charge=eta_charge, eta_discharge=eta_discharge, kind=kind) for i in range(n_ports))
     return build_station(ArchNode(capacity_a=cap_a, eta=node_eta, children=leaves), battery=battery)
+
+
+def random_station(rng: np.random.Generator, max_depth: int = 3, max_leaves: int = 8, battery=None):
+    """A random capacity tree with binding capacities — the generator of the
+    reference's constraint suite (tests/helpers.py:104-160) restated: up to
+    ``max_leaves`` ports (AC or DC, 230-800 V, 16-400 A, 30% charge-only,
+    eta 0.85-1), internal nodes of 2-3 children at capacity 0.2-1.2x their
+    subtree's charge current, half of them lossy (eta 0.8-1)."""
+    from paper_2507_01522_b200.station import ArchNode, EvseSpec, build_station
+
+    ids = iter(range(1 << 20))
+    budget = [int(rng.integers(1, max_leaves + 1))]
+
+    def port():
+        budget[0] -= 1
+        dc = rng.random() < 0.5
+        imax = float(rng.uniform(16, 400))
+        return EvseSpec(id=next(ids), voltage_v=float(rng.uniform(230, 800)), i_max_charge_a=imax,
+                        i_max_discharge_a=imax if rng.random() < 0.7 else 0.0,
+                        eta_charge=float(rng.uniform(0.85, 1.0)), eta_discharge=float(rng.uniform(0.85, 1.0)),
+                        kind="dc" if dc else "ac")
+
+    def amps(nodes):
+        return sum(n.i_max_charge_a if isinstance(n, EvseSpec) else amps(n.children) for n in nodes)
+
+    def subtree(depth):
+        if depth >= max_depth or budget[0] <= 1 or rng.random() < 0.3:
+            return port()
+        kids = []
+        for _ in range(int(rng.integers(2, 4))):
+            if budget[0] <= 0:
+                break
+            kids.append(subtree(depth + 1))
+        if not kids:
+            return port()
+        eta = float(rng.uniform(0.8, 1.0)) if rng.random() < 0.5 else 1.0
+        return ArchNode(capacity_a=float(rng.uniform(0.2, 1.2) * max(amps(kids), 1.0)), eta=eta,
+                        children=tuple(kids))
+
+    top = [subtree(1)]
+    while budget[0] > 0:
+        top.append(subtree(1))
+    root = ArchNode(capacity_a=float(rng.uniform(0.2, 1.2) * max(amps(top), 1.0)), eta=1.0, children=tuple(top))
+    return build_station(root, battery=battery)

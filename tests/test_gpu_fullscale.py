@@ -1,0 +1,229 @@
+"""Parity at the headline scales, and the kernel paths small fixtures miss.
+
+Every check is bit-exact against the CPU oracle (oracle/vy_oracle.c, pinned to
+the reference's golden trajectories by tests/test_oracle_golden.py), run on
+all of the box's host cores:
+
+* C2 at full size: 2^20 envs of the default station over a whole 288-step
+  episode and across the auto-reset — every row's reward and done every step,
+  the RandomPolicy actions of every row every 8th step, the episode
+  statistics of every row at the episode end, obs on a rotating 4096-row slab
+  (all rows covered), and every state slot of every row at the end.
+* C4 at 2^18 envs (64 DC ports, 34-node tree, battery, satisfaction
+  penalties) over 300 steps: rewards every step, every final state slot.
+* C5: the 36-group heterogeneous batch at 2^20 envs, stepped through its CUDA
+  graph: every group's rewards every step and final state.
+* 500 random capacity trees (the generator of the reference's constraint
+  suite, tests/helpers.py:104-160 / test_acceptance.py:130-166), lean and
+  generic kernels, with the tree-rescale currents (i_att / i_used) compared.
+* Poisson arrivals with lambda > 32 per step (the chunked Knuth sampler,
+  rng.py:93-115, _kernel.pyx:55-73).
+* Episodes longer than a day with the reset day drawn near the end of the
+  calendar, so eff_day wraps (_kernel.pyx:289-295, 577-581).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.harness import HostBatch, HostRandomPolicy  # noqa: E402
+from scenarios import make_dataset, random_station, single_node_station  # noqa: E402
+
+THREADS = max(1, len(os.sched_getaffinity(0)))
+STATE_KEYS = ("occ", "i_drawn", "soc", "de", "dtrem", "cap", "rbar", "tau", "pref", "rhat", "b_i", "b_soc",
+              "b_rhat", "step", "day", "episode", "env_seed", "ep_profit", "ep_reward", "ep_missing", "ep_energy",
+              "ep_overtime", "ep_declined", "ep_departures")
+INFO_KEYS = ("breakdown", "flows", "declined", "arrivals_m", "dep_n", "i_att", "i_used", "delivered",
+             "b_delivered", "term_overtime")
+
+
+def _f32(x):
+    return x.astype(np.float32)
+
+
+def _assert_state(env, hb, rows=None):
+    st = env.reference_state()
+    for k in STATE_KEYS:
+        got = st[k] if rows is None else st[k][rows]
+        np.testing.assert_array_equal(got, getattr(hb.states, k), err_msg=f"final state {k}")
+
+
+def _paired(rc, B, master, pseed, offset=0):
+    from paper_2507_01522_b200.batch import BatchEnv, DeviceRandomPolicy
+    from paper_2507_01522_b200.streams import vstream_key
+
+    env = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=B, master_seed=master, global_offset=offset)
+    pol = DeviceRandomPolicy(pseed, env.n_ports, rc.env.discretization_k)
+    pol.bind(range(offset, offset + B))
+    seeds = vstream_key(master, np.arange(offset, offset + B, dtype=np.int64))
+    hb = HostBatch(env.tables, B, env_seeds=seeds, threads=THREADS)
+    hp = HostRandomPolicy(pseed, env.n_ports, rc.env.discretization_k, range(offset, offset + B), threads=THREADS)
+    return env, pol, hb, hp
+
+
+def _run_full(env, pol, hb, hp, steps, slab, action_every=8, mode=None):
+    B = env.batch_size
+    obs0 = env.reset(as_numpy=False)
+    hb.reset()
+    np.testing.assert_array_equal(obs0[:slab].cpu().numpy(), _f32(hb.outs.obs[:slab]))
+    E = env.tables.episode_steps
+    for t in range(steps):
+        a_d = pol.actions(env)
+        a_h = hp.actions(reuse=True)
+        obs, r, d, _ = env.step(a_d, collect_infos=False)
+        hb.step_inplace(a_h)  # overlaps the GPU step
+        if mode is not None:
+            assert env.last_step_mode() == mode
+        if t % action_every == 0:
+            np.testing.assert_array_equal(a_d.cpu().numpy(), a_h, err_msg=f"actions t={t}")
+        np.testing.assert_array_equal(r.cpu().numpy(), _f32(hb.outs.reward), err_msg=f"reward t={t}")
+        np.testing.assert_array_equal(d.cpu().numpy(), hb.outs.done.astype(np.uint8), err_msg=f"done t={t}")
+        lo = (t * slab) % B
+        np.testing.assert_array_equal(obs[lo:lo + slab].cpu().numpy(), _f32(hb.outs.obs[lo:lo + slab]),
+                                      err_msg=f"obs rows {lo}.. t={t}")
+        if (t + 1) % E == 0:  # the lockstep episode end: statistics of every row
+            es = env.outs.ep_stats[:, :B].cpu().numpy().T
+            np.testing.assert_array_equal(es, hb.outs.ep_stats, err_msg=f"ep_stats t={t}")
+    _assert_state(env, hb)
+
+
+def test_c2_full_scale_every_row():
+    """Config C2 as benchmarked: 2^20 envs x (288 + 12) steps, lean kernel."""
+    from paper_2507_01522_b200.workloads import c2_setup
+
+    rc = c2_setup()
+    env, pol, hb, hp = _paired(rc, 1 << 20, master=0, pseed=0)
+    _run_full(env, pol, hb, hp, steps=300, slab=4096, mode=1)
+    env.close()
+
+
+def test_c4_full_scale_every_row():
+    """Config C4 (64 DC ports, 3-level tree, battery): 2^18 envs x 300 steps."""
+    from paper_2507_01522_b200.workloads import c4_setup
+
+    rc = c4_setup()
+    env, pol, hb, hp = _paired(rc, 1 << 18, master=3, pseed=5)
+    _run_full(env, pol, hb, hp, steps=300, slab=1024, mode=3)
+    env.close()
+
+
+def test_c5_heterogeneous_full_scale_every_group():
+    """Config C5: 36 (region, scenario, traffic, layout) groups, 2^20 envs in
+    all, stepped through the captured CUDA graph; every group against its own
+    oracle batch with the same global env indices."""
+    from paper_2507_01522_b200.hetero import HeteroBatch, sweep_groups
+    from paper_2507_01522_b200.streams import vstream_key
+
+    groups = sweep_groups(1 << 20)
+    master, pseed = 0, 0
+    hbat = HeteroBatch(groups, master_seed=master, policy_seed=pseed)
+    oracles = []
+    off = 0
+    for g, e in zip(groups, hbat.envs):
+        seeds = vstream_key(master, np.arange(off, off + g.batch_size, dtype=np.int64))
+        hb = HostBatch(e.tables, g.batch_size, env_seeds=seeds, threads=THREADS)
+        hp = HostRandomPolicy(pseed, e.n_ports, g.config.discretization_k, range(off, off + g.batch_size),
+                              threads=THREADS)
+        hb.reset()
+        oracles.append((hb, hp))
+        off += g.batch_size
+    obs0 = hbat.reset()
+    for o, (hb, _) in zip(obs0, oracles):
+        np.testing.assert_array_equal(o[:64].cpu().numpy(), _f32(hb.outs.obs[:64]))
+    for t in range(300):
+        hbat.graph_random_step()
+        for gi, (e, (hb, hp)) in enumerate(zip(hbat.envs, oracles)):
+            hb.step_inplace(hp.actions(reuse=True))
+            np.testing.assert_array_equal(e.outs.reward.cpu().numpy(), _f32(hb.outs.reward),
+                                          err_msg=f"group {groups[gi].name} reward t={t}")
+            np.testing.assert_array_equal(e.outs.done.cpu().numpy(), hb.outs.done.astype(np.uint8))
+            if t % 37 == gi % 37:  # a rotating obs check
+                np.testing.assert_array_equal(e.outs.obs[:256].cpu().numpy(), _f32(hb.outs.obs[:256]),
+                                              err_msg=f"group {groups[gi].name} obs t={t}")
+    for e, (hb, _) in zip(hbat.envs, oracles):
+        _assert_state(e, hb)
+    hbat.close()
+
+
+def _small_run(rc, B, steps, master, pseed, obs_dtype, infos, mode=None):
+    """Every output of every row every step (infos: the generic kernel's info block too)."""
+    from paper_2507_01522_b200.batch import BatchEnv, DeviceRandomPolicy
+
+    env = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=B, master_seed=master, obs_dtype=obs_dtype)
+    pol = DeviceRandomPolicy(pseed, env.n_ports, rc.env.discretization_k)
+    pol.bind(range(B))
+    hb = HostBatch(env.tables, B, master_seed=master)
+    hp = HostRandomPolicy(pseed, env.n_ports, rc.env.discretization_k, range(B))
+    cast = _f32 if obs_dtype == torch.float32 else (lambda x: x)
+    np.testing.assert_array_equal(env.reset(as_numpy=False).cpu().numpy(), cast(hb.reset()))
+    for t in range(steps):
+        a = pol.actions(env)
+        obs, r, d, _ = env.step(a, collect_infos=infos)
+        if mode is not None:
+            assert env.last_step_mode() == mode
+        hb.step_inplace(hp.actions())
+        np.testing.assert_array_equal(obs.cpu().numpy(), cast(hb.outs.obs), err_msg=f"obs t={t}")
+        np.testing.assert_array_equal(r.cpu().numpy(), cast(hb.outs.reward), err_msg=f"reward t={t}")
+        np.testing.assert_array_equal(d.cpu().numpy(), hb.outs.done.astype(np.uint8))
+        if infos:
+            o = env.reference_outputs()
+            for k in INFO_KEYS:
+                np.testing.assert_array_equal(o[k], getattr(hb.outs, k), err_msg=f"{k} t={t}")
+    _assert_state(env, hb)
+    env.close()
+    return hb
+
+
+def test_random_trees_rescale_lean_and_generic():
+    """500 random capacity trees (depth <= 3, <= 8 ports, binding capacities,
+    lossy nodes, charge-only ports) at heavy traffic: the tree rescale runs
+    on most steps.  Even trees run the lean f32 kernel, odd trees the generic
+    kernel with infos (pre- and post-rescale currents compared exactly)."""
+    from paper_2507_01522_b200 import EnvConfig
+    from types import SimpleNamespace
+
+    rng = np.random.default_rng(77)
+    ds = make_dataset(lam=1.5, days=3)
+    cfg = EnvConfig(episode_steps=24)
+    rescaled = 0
+    for i in range(500):
+        st = random_station(rng, max_depth=3, max_leaves=8)
+        rc = SimpleNamespace(env=cfg, station=st, dataset=ds)
+        f32 = i % 2 == 0
+        hb = _small_run(rc, 32, 30, master=i, pseed=1000 + i, obs_dtype=torch.float32 if f32 else torch.float64,
+                        infos=not f32, mode=None)
+        rescaled += int((hb.outs.i_att != hb.outs.i_used).any())
+    assert rescaled > 100  # the sweep really exercises the rescale
+
+
+@pytest.mark.parametrize("lam", [31.9, 32.0, 33.0, 70.3])
+@pytest.mark.parametrize("kernel", ["lean", "generic"])
+def test_poisson_chunks_above_32(lam, kernel):
+    """lambda > 32 arrivals per step: M is the sum of Knuth draws over chunks of
+    32 (rng.py:93-115); declined cars are penalised so M reaches the reward."""
+    from paper_2507_01522_b200 import EnvConfig
+    from types import SimpleNamespace
+
+    cfg = EnvConfig(episode_steps=20, alpha={"declined": 0.01})
+    rc = SimpleNamespace(env=cfg, station=single_node_station(n_ports=8, cap_a=900.0), dataset=make_dataset(lam=lam))
+    hb = _small_run(rc, 64, 25, master=2, pseed=3, obs_dtype=torch.float32 if kernel == "lean" else torch.float64,
+                    infos=kernel == "generic", mode=1 if kernel == "lean" else 0)
+    assert hb.outs.declined.max() > 0
+
+
+@pytest.mark.parametrize("kernel", ["lean", "generic"])
+def test_multi_day_episodes_wrap_the_calendar(kernel):
+    """700-step episodes (2.4 days) on a 3-day calendar: reset days drawn at
+    n_days - 1 make eff_day wrap mid-episode (_kernel.pyx:290); the generic
+    run also observes a 4-hour price horizon across the wrap (:577-581)."""
+    from paper_2507_01522_b200 import EnvConfig, default_setup
+
+    H = 0 if kernel == "lean" else 4
+    rc = default_setup(EnvConfig(episode_steps=700, observe_price_horizon=H), days=3)
+    hb = _small_run(rc, 128, 720, master=6, pseed=8, obs_dtype=torch.float32 if kernel == "lean" else torch.float64,
+                    infos=False, mode=1 if kernel == "lean" else 0)
+    assert (hb.states.episode == 1).all()

@@ -68,9 +68,12 @@ def test_graph_rollout_continues_env_exactly():
     env = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=B, master_seed=8)
     tr = PPOTrainer(env, PPOConfig(rollout_steps=T, use_graph=True, total_timesteps=10 * T * B))
     tr.rollout()  # warm-up + capture + first replay
+    # the host lockstep clock follows the GPU's step counter (warm-up included)
+    assert env._t == int(env.states.view("step")[0])
     tr.obs[0].copy_(tr.obs[T])
     before = env.reference_state()
     tr.rollout()  # second replay
+    assert env._t == int(env.states.view("step")[0])
     acts = tr.actions.cpu().numpy().astype(np.int64)
     # CPU oracle started from the device state snapshot
     ref = HostBatch(env.tables, B, master_seed=8)
