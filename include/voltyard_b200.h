@@ -173,6 +173,13 @@ int vy_bind(vy_handle *h, const vy_state *s, const vy_outputs *o);
 int vy_reset(vy_handle *h, const uint8_t *mask, int32_t episode_mode,
              const int32_t *inj_day, uint32_t flags, void *stream);
 
+/* Reset the envs selected by `mask` (device uint8 [B], NULL = all) to the
+ * explicit episode numbers `episodes` (device int32 [B]) — the per-env call
+ * core.reset_env(b, episode) of the reference's plugin protocol
+ * (_kernel.pyx:239-261; BatchEnv.reset / auto-reset, engine.py:414-424,
+ * 459-462), batched into one launch.  Writes the reset observations. */
+int vy_reset_episodes(vy_handle *h, const uint8_t *mask, const int32_t *episodes, uint32_t flags, void *stream);
+
 /* Set the seed of every env: env_seed[b] = split_seed(master, b + index0)
  * (engine.py:371-372, 407-412).  Does not reset. */
 int vy_seed_envs(vy_handle *h, int64_t master_seed, int64_t index0, void *stream);

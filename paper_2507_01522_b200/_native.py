@@ -52,6 +52,7 @@ _SIGS = {
     "vy_get_profile": (C.c_int, [_P, C.c_int, C.POINTER(C.c_double)]),
     "vy_bind": (C.c_int, [_P, C.POINTER(VyState), C.POINTER(VyOutputs)]),
     "vy_reset": (C.c_int, [_P, _P, C.c_int32, _P, C.c_uint32, _P]),
+    "vy_reset_episodes": (C.c_int, [_P, _P, _P, C.c_uint32, _P]),
     "vy_seed_envs": (C.c_int, [_P, C.c_int64, C.c_int64, _P]),
     "vy_step": (C.c_int, [_P, _P, C.c_int32, C.c_int64, C.c_int64, C.c_uint32, C.POINTER(VyDraws), _P]),
     "vy_random_actions": (C.c_int, [_P, C.c_uint64, C.c_int64, C.c_int64, _P, _P]),

@@ -155,7 +155,8 @@ class BatchEnv:
 
     def __init__(self, config: EnvConfig, station: StationTree, dataset: Dataset, batch_size: int = 1,
                  master_seed: int = 0, env_seeds=None, auto_reset: bool = True, backend: str | None = None,
-                 workers: int = 1, device=None, obs_dtype=torch.float32, global_offset: int = 0):
+                 workers: int = 1, device=None, obs_dtype=torch.float32, global_offset: int = 0,
+                 tables: StepTables | None = None):
         if batch_size < 1:
             raise ValueError("batch_size must be >= 1")
         if workers < 1:
@@ -172,7 +173,8 @@ class BatchEnv:
         if obs_dtype not in (torch.float32, torch.float64):
             raise ValueError("obs_dtype must be torch.float32 or torch.float64")
         self.obs_dtype = obs_dtype
-        self.tables: StepTables = build_tables(config, station, dataset)
+        # prebuilt tables: the reference plugin path receives the engine's KernelTables (plugin.py)
+        self.tables: StepTables = tables if tables is not None else build_tables(config, station, dataset)
         t = self.tables
         if env_seeds is not None and len(env_seeds) != B:
             raise ValueError("env_seeds length must equal batch_size")
@@ -190,8 +192,7 @@ class BatchEnv:
         if env_seeds is None:
             self._seed_from_master(master_seed)
         else:
-            seeds = np.array([int(s) & ((1 << 64) - 1) for s in env_seeds], dtype=np.uint64)
-            self.states.env_seed[:B].copy_(torch.from_numpy(seeds.view(np.int64)).to(self.device))
+            self.set_env_seeds(env_seeds)
         self._needs_reset = True
         self._t = None  # common step counter while all envs move in lockstep
         self.profile_base = t.n_cat
@@ -210,6 +211,16 @@ class BatchEnv:
     def _seed_from_master(self, master_seed: int) -> None:
         nat.check(self._lib.vy_seed_envs(self._h, int(master_seed), self.global_offset, self._stream),
                   "vy_seed_envs")
+
+    def set_env_seeds(self, env_seeds) -> None:
+        """Per-env seeds (uint64; BatchEnv(env_seeds=...), engine.py:371-374)."""
+        if isinstance(env_seeds, np.ndarray) and env_seeds.dtype == np.uint64:
+            seeds = np.ascontiguousarray(env_seeds)
+        else:
+            seeds = np.array([int(s) & ((1 << 64) - 1) for s in env_seeds], dtype=np.uint64)
+        if seeds.shape != (self.batch_size,):
+            raise ValueError("env_seeds length must equal batch_size")
+        self.states.env_seed[: self.batch_size].copy_(torch.from_numpy(seeds.view(np.int64)).to(self.device))
 
     def set_outputs(self, obs: torch.Tensor | None = None, reward: torch.Tensor | None = None,
                     done: torch.Tensor | None = None) -> None:

@@ -558,7 +558,21 @@ int vy_reset(vy_handle* h, const uint8_t* mask, int32_t episode_mode, const int3
   P.flags = flags;
   Geometry g;
   if (int rc = geometry(h, k_reset, P.L, P.n_profiles, g)) return rc;
-  k_reset<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P, mask, episode_mode, inj_day);
+  k_reset<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P, mask, episode_mode, inj_day, nullptr);
+  VY_CUDA(cudaGetLastError());
+  ++h->launches;
+  return VY_OK;
+}
+
+int vy_reset_episodes(vy_handle* h, const uint8_t* mask, const int32_t* episodes, uint32_t flags, void* stream) {
+  if (!h || !h->bound) return fail(VY_ERR_STATE, "handle not bound");
+  if (!episodes) return fail(VY_ERR_ARG, "null episodes");
+  Params P;
+  fill(h, P, false, false);
+  P.flags = flags;
+  Geometry g;
+  if (int rc = geometry(h, k_reset, P.L, P.n_profiles, g)) return rc;
+  k_reset<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P, mask, 0, nullptr, episodes);
   VY_CUDA(cudaGetLastError());
   ++h->launches;
   return VY_OK;

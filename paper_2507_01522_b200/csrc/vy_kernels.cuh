@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
 }
 
 __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P, const uint8_t* mask,
-                                               int episode_mode, const int32_t* inj_day) {
+                                               int episode_mode, const int32_t* inj_day,
+                                               const int32_t* episodes) {
   Prof prof;
   PortC pc;
   TreeC tc;
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P,
   EnvRegs E{};  // zero for padding lanes so the obs path stays in bounds
   if (active) load_env<0>(P, b, E);
   if (mine) {
-    const int ep = episode_mode ? P.st.episode[b] + 1 : 0;
+    const int ep = episodes ? episodes[b] : (episode_mode ? P.st.episode[b] + 1 : 0);
     reset_scalars(P, E, P.st.env_seed[b], ep, inj_day ? inj_day[b] : 0, inj_day != nullptr);
     clear_tile_ports(P, T);
     P.st.episode[b] = ep;

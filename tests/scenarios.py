@@ -81,13 +81,17 @@ def single_node_station(n_ports: int = 2, cap_a: float = 1e9, voltage_v: float =
     return build_station(ArchNode(capacity_a=cap_a, eta=node_eta, children=leaves), battery=battery)
 
 
-def random_station(rng: np.random.Generator, max_depth: int = 3, max_leaves: int = 8, battery=None):
+def random_station(rng: np.random.Generator, max_depth: int = 3, max_leaves: int = 8, battery=None, types=None):
     """A random capacity tree with binding capacities — the generator of the
     reference's constraint suite (tests/helpers.py:104-160) restated: up to
     ``max_leaves`` ports (AC or DC, 230-800 V, 16-400 A, 30% charge-only,
     eta 0.85-1), internal nodes of 2-3 children at capacity 0.2-1.2x their
-    subtree's charge current, half of them lossy (eta 0.8-1)."""
-    from paper_2507_01522_b200.station import ArchNode, EvseSpec, build_station
+    subtree's charge current, half of them lossy (eta 0.8-1).  ``types``: a
+    namespace with ArchNode / EvseSpec / build_station (default: this
+    package's; ref_scenarios passes the reference's)."""
+    if types is None:
+        from paper_2507_01522_b200 import station as types
+    ArchNode, EvseSpec, build_station = types.ArchNode, types.EvseSpec, types.build_station
 
     ids = iter(range(1 << 20))
     budget = [int(rng.integers(1, max_leaves + 1))]
