@@ -3,9 +3,10 @@
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
   (N > 1: torchrun --nproc-per-node N ... bench.py --gpus N)
 
-Our arm.  A "step" is one BatchEnv.step of every env on the GPU: the device
-RandomPolicy writes uint8 actions, the fused step kernel advances all envs
-(auto-reset included) and emits obs/reward/done.  Each rank owns 2^20 envs
+Our arm.  A "step" is one pass of the throughput_probe loop body
+(engine.py:541-545) over every env on the GPU: BatchEnv.step_random draws the
+RandomPolicy rows inside the fused step kernel, which advances all envs
+(auto-reset included) and emits obs/reward/done — one launch per step.  Each rank owns 2^20 envs
 (weak scaling, global env indices rank*2^20 + i, so the union of shards is the
 single-batch run); there is no data-path collective.  Time = max over ranks of
 CUDA-event time around exactly K steps with barrier + synchronize on both
@@ -16,16 +17,20 @@ lockstep and the station load follows the arrival profile (empty at night,
 mid-day; the default K = 288 covers one whole day (every leg and both arms
 use the same rule, see window_start).
 
-Extra keys: roofline (dominant kernel: the fused step), e2e (same metric
+Extra keys: roofline (the fused step on SURVEY §8(d)'s 1010 B/env-step, with
+the ncu-measured DRAM bytes of the same day window as `traffic`), e2e (same metric
 through the public API with host buffers: pinned actions H2D, step, obs /
 reward / done D2H every step), cpu_baseline (the reference's own compiled
 kernel from oracle/_ref — or the C oracle if it is absent — on the host's
 cores, bounded sample), rollout (the fused T-step kernel, reported
-separately), clocks (nvidia-smi sampled during the timed region).
+separately), c4 (the 64-port battery station, config C4), ppo (C3), hetero
+(C5), clocks (nvidia-smi sampled during the timed region).
 
 Reference arm (--impl reference): the reference's compiled CPU kernel on all
 host cores, one step = one env-step of a bounded 2^16-env sample of the same
-workload over the same window of the day; rank 0 only.
+workload over the same window of the day; rank 0 only.  Its line also carries
+`api_level`: the reference's own throughput_probe (baseline/_ref) at B = 16 /
+4096 x workers 1 / all cores, and config C1 literally.
 """
 
 from __future__ import annotations
@@ -49,14 +54,27 @@ METRIC = "env-steps/sec (whole box)"
 UNIT = "env-steps/s"
 
 
-def algorithmic_bytes(t) -> dict:
-    """Bytes one env-step of the fused step kernel must move.
+def survey_bytes(t, T: int = 1) -> dict:
+    """SURVEY.md §8(d) algorithmic bytes per env-step (the canonical roofline
+    figure): minimal lossless SoA state S = 15 B/port + 44 B/env, read and
+    written; uint8 actions N+1; float32 obs 4*obs_len; reward + done 5 B.
+    N = 16: 2*284 + 17 + 420 + 5 = 1010 B (C2); C4: 3650 B.  The fused T-step
+    rollout streams obs/reward/done every step and the state once:
+    O + R + 2S/T (427 B at T = 288)."""
+    S = 15 * t.n_ports + 44
+    A = t.n_ports + 1
+    O = 4 * t.obs_len
+    return {"per_env_step": 2 * S + A + O + 5, "state": S, "actions": A, "obs": O, "reward_done": 5,
+            "rollout_per_env_step": O + 5 + 2 * S / T}
 
-    State contract: float64 i_drawn/soc/de + int16 dwell + uint8 meta per port;
-    per env int32 step/day, uint64 arrival key (read), float64 x4 + int32 x3
-    episode accumulators (read+write); actions uint8; obs float32; reward f32;
-    done u8.  The battery adds 2 x float64 read+write when enabled.
-    """
+
+def contract_bytes(t) -> dict:
+    """Bytes one env-step of the fused step kernel moves under its own state
+    layout: float64 i_drawn/soc/de + int16 dwell + uint8 meta
+    per port (24 B of floats where §8(d)'s fp32 layout has 12: the price of
+    bit-exact float64 state); per env int32 step/day, uint64 arrival key
+    (read), float64 x4 + int32 x3 episode accumulators (read+write); actions
+    uint8; obs float32; reward f32; done u8."""
     port = t.n_ports * (8 + 8 + 8 + 2 + 1)
     env_r = 4 + 4 + 8 + 4 * 8 + 3 * 4
     env_w = 4 + 4 * 8 + 3 * 4
@@ -66,6 +84,18 @@ def algorithmic_bytes(t) -> dict:
     total = 2 * port + env_r + env_w + batt + acts + obs + 4 + 1
     return {"per_env_step": total, "state_rw": 2 * port + env_r + env_w + batt, "actions": acts, "obs": obs,
             "reward_done": 5}
+
+
+def window_traffic(steps: list[int], name: str = "r2_k_step_day_dram.json") -> tuple[float | None, str | None]:
+    """Measured DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum, one
+    ncu pass over every launch of a whole 288-step day of this workload,
+    scripts/day_dram.sh) averaged over the day steps of the timed window."""
+    path = os.path.join(ROOT, "profiles", name)
+    if not os.path.exists(path):
+        return None, None
+    with open(path) as fh:
+        per = json.load(fh)["bytes_per_launch_by_step"]
+    return sum(per[s % len(per)] for s in steps) / len(steps), f"profiles/{name}"
 
 
 class ClockSampler:
@@ -148,7 +178,49 @@ def cpu_reference_rate(rc, B: int, advance: int, steps: int, threads: int, prefe
             "seconds": dt}
 
 
+def reference_api_rates(threads: int, budget_s: float = 4.0) -> dict | None:
+    """The reference's own public API, unmodified, from baseline/_ref (pip
+    install of /root/reference/pkg): throughput_probe (engine.py:515-556) with
+    backend="compiled" at B = 16 and 4096, workers 1 and all host threads, and
+    config C1 literally (16 envs x 288 steps, workers 1).  Each probe is sized
+    to about `budget_s` seconds from a short calibration run."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "voltyard")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import voltyard
+    from voltyard.config import default_setup as ref_setup
+    from voltyard.engine import throughput_probe
+
+    rc = ref_setup()
+    out = {"source": "baseline/_ref voltyard.engine.throughput_probe(backend='compiled')", "cores": threads,
+           "hardware": voltyard.engine.hardware_fingerprint(), "probes": []}
+    for B, w in ((16, 1), (16, threads), (4096, 1), (4096, threads)):
+        cal = throughput_probe(rc.env, rc.station, rc.dataset, batch_size=B, total_steps=B * 20, backend="compiled",
+                               workers=w)
+        total = max(B * 20, int(cal.steps_per_second * budget_s))
+        rep = throughput_probe(rc.env, rc.station, rc.dataset, batch_size=B, total_steps=total, backend="compiled",
+                               workers=w)
+        out["probes"].append({"batch_size": B, "workers": w, "steps_per_s": rep.steps_per_second,
+                              "total_steps": rep.total_steps, "seconds": rep.wall_seconds})
+    # C1 literally: 16 envs x 288 steps (one whole episode), repeated
+    reps = []
+    for _ in range(3):
+        rep = throughput_probe(rc.env, rc.station, rc.dataset, batch_size=16, total_steps=16 * 288,
+                               backend="compiled", workers=1)
+        reps.append(rep.steps_per_second)
+    out["c1_literal"] = {"batch_size": 16, "steps": 288, "workers": 1, "steps_per_s": statistics.median(reps),
+                         "repeats": len(reps)}
+    return out
+
+
 def run_reference_arm(args) -> None:
+    """The reference's CPU implementation of the path on the box's host cores:
+    its compiled kernel (oracle/_ref, built from the reference's own sources)
+    over all host threads on a bounded 2^16-env sample of C2 over the same day
+    window as our arm — the headline value; plus its public API
+    (throughput_probe, baseline/_ref) at the §8(d) probe points."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -157,19 +229,23 @@ def run_reference_arm(args) -> None:
     rc = default_setup()
     threads = len(os.sched_getaffinity(0))
     B = 1 << 16
-    res = cpu_reference_rate(rc, B, window_start(args.steps, args.warmup) + args.warmup, args.steps, threads)
+    w0 = window_start(args.steps, args.warmup) + args.warmup
+    res = cpu_reference_rate(rc, B, w0, args.steps, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "C2 default 16-port station, random actions (bounded CPU sample)",
                    "envs_per_step": B, "episode_steps": 288,
-                   "timed_window": f"steps {window_start(args.steps, args.warmup) + args.warmup}.."
-                                   f"{window_start(args.steps, args.warmup) + args.warmup + args.steps - 1} of the "
-                                   f"lockstep 288-step day (same window as the GPU arm)"},
+                   "timed_window": f"steps {w0}..{w0 + args.steps - 1} of the lockstep 288-step day "
+                                   f"(same window as the GPU arm)"},
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_extras:
+        api = reference_api_rates(threads)
+        if api is not None:
+            line["api_level"] = api
     print(json.dumps(line), flush=True)
 
 
@@ -181,9 +257,11 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--envs", type=int, default=B_PER_GPU)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-extras", action="store_true", help="skip e2e / rollout / PPO legs (profiling runs)")
+    ap.add_argument("--no-extras", action="store_true", help="skip e2e / rollout / PPO / C4 / C5 legs (profiling runs)")
     ap.add_argument("--ppo-iters", type=int, default=3, help="timed PPO iterations for the C3 leg (0 = skip)")
     args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
     if args.impl == "reference":
         run_reference_arm(args)
         return
@@ -193,6 +271,7 @@ def main() -> None:
 
     from paper_2507_01522_b200 import default_setup
     from paper_2507_01522_b200.batch import BatchEnv, DeviceRandomPolicy
+    from paper_2507_01522_b200.workloads import c4_setup
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -201,17 +280,11 @@ def main() -> None:
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-
-    rc = default_setup()
-    B = args.envs
-    env = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=B, master_seed=0, global_offset=rank * B)
-    pol = DeviceRandomPolicy(seed=0, n_ports=env.n_ports, k=rc.env.discretization_k)
-    pol.bind(range(rank * B, rank * B + B))
-    env.reset(as_numpy=False)
-    stream = torch.cuda.current_stream()
-    advance = window_start(args.steps, args.warmup, rc.env.episode_steps)
-    for _ in range(advance):
-        env.step(pol.actions(env), collect_infos=False)
+        # one tiny collective so every rank's NCCL communicator is up (and logged) before timing
+        t = torch.ones(1, device=dev)
+        dist.all_reduce(t)
+        if rank == 0:
+            print(f"[bench] NCCL communicator: nranks={int(t.item())} world={world}", file=sys.stderr, flush=True)
 
     def barrier():
         torch.cuda.synchronize()
@@ -226,71 +299,79 @@ def main() -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    for _ in range(args.warmup):
-        env.step(pol.actions(env), collect_infos=False)
-    barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = env.launch_count()
-    with ClockSampler(local) as clocks:
-        t_start.record(stream)
-        for i in range(args.steps):
-            a = pol.actions(env)
-            ev[i][0].record(stream)
-            env.step(a, collect_infos=False)
-            ev[i][1].record(stream)
-        t_end.record(stream)
-        barrier()
-    launches = env.launch_count() - launches0
-    ms = t_start.elapsed_time(t_end)
-    ms_max = max_over_ranks(ms)
-    step_kernel_ms = statistics.mean(s.elapsed_time(e) for s, e in ev)
-    total_steps = args.steps * B * world
-    value = total_steps / (ms_max / 1e3)
-
-    # roofline of the dominant kernel (the fused step)
-    ab = algorithmic_bytes(env.tables)
+    stream = torch.cuda.current_stream()
     peaks = load_peaks()
-    achieved = ab["per_env_step"] * B / (step_kernel_ms / 1e3) / 1e9
-    traffic = dram = None
-    tpath = os.path.join(ROOT, "profiles", "step_kernel_dram_bytes.json")
-    if os.path.exists(tpath) and B == B_PER_GPU and args.steps == 288:
-        # dram__bytes_read.sum + dram__bytes_write.sum per k_step launch, averaged over
-        # the 288 launches of this same day window (ncu, scripts/day_dram.sh).  The
-        # kernel neither reads nor rewrites ports that are empty in a whole 32-env
-        # tile, so its real traffic is below the step contract's 1414 B/env-step;
-        # dram_frac is that real traffic over the measured time.
-        with open(tpath) as fh:
-            traffic = json.load(fh).get("bytes_per_launch")
-        dram = {"bytes_per_env_step": traffic / B, "achieved": traffic / (step_kernel_ms / 1e3) / 1e9,
-                "frac": traffic / (step_kernel_ms / 1e3) / 1e9 / peaks.get("hbm_gbs"),
-                "source": "profiles/step_kernel_dram_bytes.json"}
+    hbm = peaks.get("hbm_gbs")
 
+    def timed_day_window(env, pol, K, W):
+        """Advance to the window centred mid-day, W warm-up steps, then time
+        exactly K fused steps (vy_step_random: RandomPolicy + step in one
+        kernel) bracketed by barrier + synchronize; per-step CUDA events on the
+        launching stream give the kernel's own average launch time."""
+        advance = window_start(K, W, env.tables.episode_steps)
+        for _ in range(advance + W):
+            env.step_random(pol)
+        barrier()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = env.launch_count()
+        t0.record(stream)
+        for i in range(K):
+            ev[i][0].record(stream)
+            env.step_random(pol)
+            ev[i][1].record(stream)
+        t1.record(stream)
+        barrier()
+        steps = list(range(advance + W, advance + W + K))
+        return (max_over_ranks(t0.elapsed_time(t1)), statistics.mean(s.elapsed_time(e) for s, e in ev),
+                env.launch_count() - l0, steps)
+
+    rc = default_setup()
+    B = args.envs
+    env = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=B, master_seed=0, global_offset=rank * B)
+    pol = DeviceRandomPolicy(seed=0, n_ports=env.n_ports, k=rc.env.discretization_k)
+    pol.bind(range(rank * B, rank * B + B))
+    env.reset(as_numpy=False)
+    with ClockSampler(local) as clocks:
+        ms, step_kernel_ms, launches, wsteps = timed_day_window(env, pol, args.steps, args.warmup)
+    value = args.steps * B * world / (ms / 1e3)
+
+    # roofline of the dominant (only) kernel: the fused step, on SURVEY §8(d) bytes
+    sb = survey_bytes(env.tables)
+    cb = contract_bytes(env.tables)
+    achieved = sb["per_env_step"] * B / (step_kernel_ms / 1e3) / 1e9
+    traffic, tsrc = window_traffic(wsteps) if B == B_PER_GPU else (None, None)
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference synthetic generators: shopping/medium/eu, seed 0, 365 days)",
-        "config": {"workload": "C2: default 16-port station (6 AC + 10 DC, multi_type), random actions, "
+        "config": {"workload": "C2: default 16-port station (6 AC + 10 DC, multi_type), RandomPolicy actions, "
                                "288-step episodes with in-kernel auto-reset",
                    "envs_per_gpu": B, "global_envs": B * world, "episode_steps": rc.env.episode_steps,
                    "parallelism": f"env-sharded x{world}", "l2": "inputs ~1.5 GB/GPU >> 126 MB L2 (no flush)",
-                   "obs_dtype": "f32", "actions": "u8 from device RandomPolicy",
-                   "timed_window": f"steps {advance + args.warmup}..{advance + args.warmup + args.steps - 1} "
-                                   f"of the lockstep {rc.env.episode_steps}-step day (centred mid-day)"},
+                   "obs_dtype": "f32", "state_dtype": "f64 (bit-exact with the reference)",
+                   "step": "vy_step_random: RandomPolicy rows drawn inside the step kernel (one launch per step)",
+                   "timed_window": f"steps {wsteps[0]}..{wsteps[-1]} of the lockstep {rc.env.episode_steps}-step "
+                                   f"day (centred mid-day)"},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-                     "frac": achieved / peaks.get("hbm_gbs"), "traffic": traffic,
-                     "kernel": "vy::k_step", "kernel_ms": step_kernel_ms,
-                     "bytes_per_env_step": ab["per_env_step"],
-                     "bytes_note": "step contract: full f64 port state read + written, u8 actions, f32 obs",
-                     "dram": dram,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic,
+                     "kernel": "vy::k_step<1> (fused RandomPolicy)", "kernel_ms": step_kernel_ms,
+                     "bytes_per_env_step": sb["per_env_step"],
+                     "bytes_note": "SURVEY §8(d): 2 x 284 B fp32 SoA state + 17 B u8 actions + 420 B f32 obs + 5 B",
+                     "traffic_source": tsrc,
+                     "traffic_per_env_step": traffic / B if traffic else None,
+                     "traffic_frac": traffic / (step_kernel_ms / 1e3) / 1e9 / hbm if traffic else None,
+                     "contract_f64": {"bytes_per_env_step": cb["per_env_step"],
+                                      "frac": cb["per_env_step"] * B / (step_kernel_ms / 1e3) / 1e9 / hbm,
+                                      "note": "the kernel's own float64-state contract (24 B of floats per port)"},
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not peaks.get("_fallback") else "fallback"},
         "clocks": clocks.summary(),
     }
 
     if not args.no_extras:
-        # fused T-step rollout (state in registers), reported separately
+        # fused T-step rollout (state resident across T steps), reported separately
         T = rc.env.episode_steps
         obs_b = torch.empty(1, B, env.obs_length, device=dev)
         rew_b = torch.empty(1, B, device=dev)
@@ -303,11 +384,13 @@ def main() -> None:
         s1.record(stream)
         barrier()
         rms = max_over_ranks(s0.elapsed_time(s1))
-        rb = ab["obs"] + ab["reward_done"] + 2 * ab["state_rw"] / T
+        rb = survey_bytes(env.tables, T)["rollout_per_env_step"]
         result["rollout"] = {"value": T * B * world / (rms / 1e3), "unit": UNIT, "T": T,
                              "ms": rms, "bytes_per_env_step": rb,
                              "achieved_gbs": rb * T * B / (rms / 1e3) / 1e9,
-                             "note": "fused T-step kernel, in-kernel RandomPolicy, obs/reward/done every step"}
+                             "frac": rb * T * B / (rms / 1e3) / 1e9 / hbm,
+                             "note": "fused T-step kernel, in-kernel RandomPolicy, obs/reward/done every step; "
+                                     "bytes = SURVEY §8(d) O + R + 2S/T"}
 
         # e2e through the public API with host buffers: every step copies its
         # actions H2D from pinned memory and its obs / reward / done D2H to pinned
@@ -327,7 +410,7 @@ def main() -> None:
         copy_stream = torch.cuda.Stream(device=dev)
         e_steps = max(3, min(args.steps, 20))
         while env._t != window_start(e_steps, 2, rc.env.episode_steps):  # centre this window mid-day too
-            env.step(pol.actions(env), collect_infos=False)
+            env.step_random(pol)
 
         def e2e_run(pipelined: bool) -> float:
             written = [torch.cuda.Event() for _ in range(2)]
@@ -368,6 +451,26 @@ def main() -> None:
                          "serial_value": e_steps * B * world / (ems_serial / 1e3),
                          "path": "BatchEnv.step with pinned host actions -> obs/reward/done to pinned host "
                                  "(two output sets, D2H on a copy stream overlapping the next step)"}
+    env.close()
+
+    if not args.no_extras:
+        # config C4: 64 DC ports, 3-level splitter tree, battery, profit + satisfaction reward
+        rc4 = c4_setup()
+        B4 = 1 << 18
+        env4 = BatchEnv(rc4.env, rc4.station, rc4.dataset, batch_size=B4, master_seed=0, global_offset=rank * B4)
+        pol4 = DeviceRandomPolicy(seed=0, n_ports=env4.n_ports, k=rc4.env.discretization_k)
+        pol4.bind(range(rank * B4, rank * B4 + B4))
+        env4.reset(as_numpy=False)
+        ms4, k4, _, w4 = timed_day_window(env4, pol4, args.steps, args.warmup)
+        sb4 = survey_bytes(env4.tables)["per_env_step"]
+        result["c4"] = {"metric": METRIC, "value": args.steps * B4 * world / (ms4 / 1e3), "unit": UNIT,
+                        "envs_per_gpu": B4, "ms_per_step": ms4 / args.steps, "kernel_ms": k4,
+                        "bytes_per_env_step": sb4, "frac": sb4 * B4 / (k4 / 1e3) / 1e9 / hbm,
+                        "kernel_mode": env4.last_step_mode(),
+                        "timed_window": f"steps {w4[0]}..{w4[-1]}",
+                        "workload": "C4: 64 DC ports, nested_splitters 34-node tree, battery, highway/high/eu, "
+                                    "sat0/sat1 penalties"}
+        env4.close()
 
     if not args.no_extras and args.ppo_iters > 0:
         # config C3: PPO with 4096 envs per GPU, Table 4 hyperparameters,
@@ -382,12 +485,15 @@ def main() -> None:
                          "env_steps_per_s": res["env_steps_per_s"], "envs_per_gpu": 4096,
                          "rollout_steps": cfg.rollout_steps, "epochs": cfg.update_epochs,
                          "minibatches": cfg.n_minibatches, "hidden": cfg.hidden, "timed_iterations": args.ppo_iters,
-                         "rollout": "CUDA graph (policy fwd bf16: 3 GEMMs with block-diagonal layer 2 and merged heads + vy_ppo_sample_rng Gumbel-max kernel with in-kernel uniforms + k_step) x 300",
-                         "update": ("one CUDA graph per update on 1 GPU (eager with the all-reduce): vy_gae, "
-                                    "vy_gather_rows minibatch gather, bf16 GEMMs at 8-aligned widths with column-sum bias "
-                                    "gradients (vy_colsum), vy_ppo_head_fwd/_bwd fused log-prob/entropy head, fused Adam"),
-                         "grad_allreduce": "NCCL all_reduce(AVG) per minibatch" if world > 1 else "none (1 GPU)",
-                         "paper_reference": "Chargax PPO(16) 0.65 s / 100k on RTX 4000 Ada (PAPER.md:239)"}
+                         "optimizer_steps_per_100k_env_steps": 1e5 * cfg.update_epochs * cfg.n_minibatches
+                                                               / (4096 * world * cfg.rollout_steps),
+                         "rollout": tr.describe_rollout() if hasattr(tr, "describe_rollout") else None,
+                         "update": ("one CUDA graph per update: vy_gae, vy_gather_rows minibatch gather, bf16 GEMMs "
+                                    "with column-sum bias gradients (vy_colsum), vy_ppo_head_fwd/_bwd fused "
+                                    "log-prob/entropy head, fused Adam"),
+                         "grad_allreduce": "NCCL all_reduce per minibatch" if world > 1 else "none (1 GPU)",
+                         "paper_reference": "Chargax PPO(16) 0.65 s / 100k on RTX 4000 Ada (PAPER.md:239); a "
+                                            "different workload (16 envs, 900-sample minibatches)"}
         penv.close()
 
     if not args.no_extras:
@@ -398,11 +504,10 @@ def main() -> None:
         hb = HeteroBatch(sweep_groups(B), master_seed=0, global_offset=rank * B, policy_seed=0)
         hb.reset()
         hsteps = args.steps  # the same day window as the main leg (K = 288: one whole day)
-        for _ in range(3 + window_start(hsteps, 3, rc.env.episode_steps)):  # window centred mid-day
+        for _ in range(args.warmup + window_start(hsteps, args.warmup, rc.env.episode_steps)):  # centred mid-day
             hb.graph_random_step()
         barrier()
         h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        l0 = sum(e.launch_count() for e in hb.envs)
         h0.record(stream)
         for _ in range(hsteps):
             hb.graph_random_step()  # one CUDA-graph launch per heterogeneous step
@@ -411,15 +516,14 @@ def main() -> None:
         hms = max_over_ranks(h0.elapsed_time(h1))
         result["hetero"] = {"metric": METRIC, "value": hsteps * hb.total * world / (hms / 1e3), "unit": UNIT,
                             "groups": len(hb.groups), "envs_per_gpu": hb.total, "global_envs": hb.total * world,
-                            "kernels_per_step": 2 * len(hb.groups), "graph_launches_per_step": 1,
+                            "kernels_per_step": hb.kernels_per_step(), "graph_launches_per_step": 1,
                             "workload": "C5: regions x scenarios x traffic, single/multi/nested stations"}
         hb.close()
 
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
         result["cpu_baseline"] = {k: v for k, v in cpu_reference_rate(
-            rc, 1 << 16, advance + args.warmup, args.steps, threads).items() if k != "seconds"}
-    env.close()
+            rc, 1 << 16, wsteps[0], args.steps, threads).items() if k != "seconds"}
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -204,6 +204,18 @@ int vy_random_actions(vy_handle *h, uint64_t seed, int64_t index0, int64_t call,
 int vy_random_actions_dev(vy_handle *h, uint64_t seed, int64_t index0, int64_t *call_counter, uint8_t *out,
                           void *stream);
 
+/* One step of every env with RandomPolicy actions generated inside the step
+ * kernel: the fused form of the throughput_probe loop body
+ * `env.step(policy.actions(obs))` (engine.py:541-545, policies.py:51-73).
+ * The actions equal vy_random_actions(seed, index0, call) bit for bit; the
+ * call index is `call`, plus *call_counter when call_counter is non-NULL (two
+ * int64, as vy_random_actions_dev; the kernel advances word 0 by one, so a
+ * graph replay draws the next call).  actions_out (NULL = not written)
+ * receives the uint8 [B][n_ports+1] actions.  flags as vy_step (no
+ * VY_F_INJECT). */
+int vy_step_random(vy_handle *h, uint64_t seed, int64_t index0, int64_t call, int64_t *call_counter,
+                   uint8_t *actions_out, uint32_t flags, void *stream);
+
 /* Fused multi-step rollout: T steps with in-kernel RandomPolicy actions and
  * auto-reset, state held in registers across steps.  Step t writes obs to
  * obs + t*obs_step_stride (elements; 0 = overwrite one buffer), reward to

@@ -57,6 +57,7 @@ _SIGS = {
     "vy_step": (C.c_int, [_P, _P, C.c_int32, C.c_int64, C.c_int64, C.c_uint32, C.POINTER(VyDraws), _P]),
     "vy_random_actions": (C.c_int, [_P, C.c_uint64, C.c_int64, C.c_int64, _P, _P]),
     "vy_random_actions_dev": (C.c_int, [_P, C.c_uint64, C.c_int64, _P, _P, _P]),
+    "vy_step_random": (C.c_int, [_P, C.c_uint64, C.c_int64, C.c_int64, _P, _P, C.c_uint32, _P]),
     "vy_rollout": (C.c_int, [_P, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, _P, C.c_int64, _P, _P, C.c_int64,
                              C.c_uint32, _P]),
     "vy_poll_error": (C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_uint32)]),

@@ -349,6 +349,36 @@ class BatchEnv:
             return obs, rew, done, infos
         return self.outs.obs, self.outs.reward, self.outs.done, infos
 
+    def step_random(self, policy: "DeviceRandomPolicy", collect_infos: bool = False, keep_actions: bool = False,
+                    device_counter: bool = False):
+        """``step(policy.actions(obs))`` as ONE kernel: the RandomPolicy rows
+        (policies.py:51-73) are drawn inside the step kernel (vy_step_random),
+        bit-identical to ``policy.actions(env)`` followed by ``step``.  The
+        throughput_probe loop body (engine.py:541-545).  With keep_actions the
+        actions are also written to ``policy.last_actions`` (uint8 [B, n+1]);
+        with device_counter the call index lives in device memory (graph
+        replay; ``policy.calls`` is then advanced by the caller)."""
+        if self._needs_reset:
+            raise EpisodeDone("call reset() before step()")
+        if policy.rows is not None and policy.rows != self.batch_size:
+            raise ValueError("policy bound to a different batch size")
+        if not self.auto_reset and self._episode_over():
+            raise EpisodeDone("an episode is done and auto_reset is off")
+        if collect_infos and self.outs.info is None:
+            self.outs.ensure_info()
+            self._bind()
+        out = policy._buffer(self) if keep_actions else None
+        counter = policy._device_counter(self) if device_counter else None
+        rc = self._lib.vy_step_random(self._h, policy.seed & ((1 << 64) - 1), policy.index0,
+                                      0 if device_counter else policy.calls, _ptr(counter), _ptr(out),
+                                      self._flags(collect_infos), self._stream)
+        nat.check(rc, "vy_step_random")
+        if not device_counter:
+            policy.calls += 1
+        self._advance_clock()
+        infos = self._build_infos() if collect_infos else None
+        return self.outs.obs, self.outs.reward, self.outs.done, infos
+
     def step_injected(self, actions, draws, collect_infos: bool = False):
         """Step with arrival draws taken from ``draws`` (VY_F_INJECT).
 
@@ -570,20 +600,35 @@ class DeviceRandomPolicy:
         self.rows = len(idx)
         self.calls = 0
 
+    def _buffer(self, env: BatchEnv) -> torch.Tensor:
+        B = env.batch_size
+        if self._out is None or self._out.shape[0] != B:
+            self._out = torch.empty(B, self.n_ports + 1, dtype=torch.uint8, device=env.device)
+        return self._out
+
+    def _device_counter(self, env: BatchEnv) -> torch.Tensor:
+        if getattr(self, "_counter", None) is None:
+            # {call index, scratch}: see vy_random_actions_dev
+            self._counter = torch.tensor([self.calls, 0], dtype=torch.int64, device=env.device)
+        return self._counter
+
+    @property
+    def last_actions(self) -> torch.Tensor | None:
+        """The uint8 [B, n+1] actions of the last actions() call (or
+        BatchEnv.step_random(keep_actions=True))."""
+        return self._out
+
     def actions(self, env: BatchEnv, device_counter: bool = False) -> torch.Tensor:
         """Next call's actions.  With device_counter the call index lives in
         device memory (graph-replayable); `calls` is then advanced by the caller."""
         B = env.batch_size
         if self.rows is not None and self.rows != B:
             raise ValueError("policy bound to a different batch size")
-        if self._out is None or self._out.shape[0] != B:
-            self._out = torch.empty(B, self.n_ports + 1, dtype=torch.uint8, device=env.device)
+        self._buffer(env)
         if device_counter:
-            if getattr(self, "_counter", None) is None:
-                # {call index, scratch}: see vy_random_actions_dev
-                self._counter = torch.tensor([self.calls, 0], dtype=torch.int64, device=env.device)
             rc = env._lib.vy_random_actions_dev(env._h, self.seed & ((1 << 64) - 1), self.index0,
-                                                self._counter.data_ptr(), self._out.data_ptr(), env._stream)
+                                                self._device_counter(env).data_ptr(), self._out.data_ptr(),
+                                                env._stream)
             nat.check(rc, "vy_random_actions_dev")
             return self._out
         rc = env._lib.vy_random_actions(env._h, self.seed & ((1 << 64) - 1), self.index0, self.calls,
@@ -627,7 +672,7 @@ def throughput_probe(config: EnvConfig, station: StationTree, dataset: Dataset, 
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(calls):
-        env.step(pol.actions(env), collect_infos=False)
+        env.step_random(pol)  # env.step(pol.actions(obs)) fused into one launch
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     env.close()

@@ -628,6 +628,40 @@ int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride
   return VY_OK;
 }
 
+int vy_step_random(vy_handle* h, uint64_t seed, int64_t index0, int64_t call, int64_t* call_counter,
+                   uint8_t* actions_out, uint32_t flags, void* stream) {
+  if (!h || !h->bound) return fail(VY_ERR_STATE, "handle not bound");
+  if ((flags & VY_F_INFOS) && !infos_bound(h->out)) return fail(VY_ERR_ARG, "info buffers not bound");
+  if (flags & VY_F_INJECT) return fail(VY_ERR_UNSUPPORTED, "vy_step_random draws its own arrivals (no VY_F_INJECT)");
+  if (2 * h->t.k + 1 > 256) return fail(VY_ERR_UNSUPPORTED, "RandomPolicy actions need 2k+1 <= 256");
+  Params P;
+  fill(h, P, false, true);  // the generated rows live in the tile's staged-action area
+  P.flags = flags;
+  P.actions = nullptr;
+  P.act_dtype = VY_ACT_U8;
+  P.policy = 1;
+  P.pol_seed = seed;
+  P.pol_index0 = index0;
+  P.pol_call = call;
+  P.pol_counter = call_counter;
+  P.pol_out = actions_out;
+  Geometry g;
+  const int mode = step_mode(h, flags, true);
+  h->last_mode = mode;
+  auto* kern = mode == 1 ? k_step<1> : mode == 2 ? k_step<2> : mode == 3 ? k_step<3> : k_step<0>;
+  if (int rc = geometry(h, kern, P.L, P.n_profiles, g)) return rc;
+  const unsigned resident = (unsigned)h->num_sms * (unsigned)(h->smem_per_sm / (g.smem + 1024));
+  unsigned grid = g.grid < resident ? g.grid : resident;
+  if (h->tiles_per_warp > 1) {
+    const unsigned k = (unsigned)h->tiles_per_warp, want = (g.grid + k - 1) / k;
+    grid = want < grid ? want : grid;
+  }
+  kern<<<grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P);
+  VY_CUDA(cudaGetLastError());
+  ++h->launches;
+  return VY_OK;
+}
+
 int vy_random_actions(vy_handle* h, uint64_t seed, int64_t index0, int64_t call, uint8_t* out, void* stream) {
   if (!h || !out) return fail(VY_ERR_ARG, "null argument");
   const int ns = h->t.n_ports + 1, hi = 2 * h->t.k + 1;

@@ -141,6 +141,12 @@ struct Params {
   int act_dtype;
   int64_t act_row, act_col;
   vy_draws inj;
+  // fused RandomPolicy (vy_step_random): actions generated in the step kernel
+  int policy;                 // 1: actions are RandomPolicy draws, not read from `actions`
+  uint64_t pol_seed;
+  int64_t pol_index0, pol_call;
+  int64_t* pol_counter;       // {call index, finished warps}: device call counter (graph replay), or null
+  uint8_t* pol_out;           // optional uint8 [B][n+1] copy of the generated actions
   uint32_t* err;
   unsigned long long* tile_ctr;  // [2] work-stealing tile counter, finished-warp counter (k_step)
   TileLayout L;

@@ -53,13 +53,40 @@ __device__ __forceinline__ void stage_tables(const Params& P, Prof& prof, const 
   dtab = nd <= 256 ? sd : nullptr;
 }
 
+// Fused RandomPolicy (policies.py:51-73, rng.py:154-170): this lane's n+1
+// actions of call `call` into its staged action row, computed while the
+// tile's state copies are in flight.  Row b draws from stream_key(seed,
+// index0 + b, 2); draw j = call*(n+1) + s + 1 is mix64(key + j*GOLDEN).
+// With P.pol_out the warp also writes its [32][n+1] block to global memory.
+__device__ __forceinline__ void policy_row(const Params& P, uint32_t tile, int64_t b0, int lane, int64_t call) {
+  const int ns = P.n_ports + 1, hi = 2 * P.k + 1;
+  const int64_t b = b0 + lane;
+  const uint64_t key = fold(fold(fold(kKey0, P.pol_seed), (uint64_t)(P.pol_index0 + b)), 2);
+  uint64_t kj = key + ((uint64_t)call * (uint64_t)ns + 1) * kGolden;
+  const uint32_t row = smem_base() + tile + P.L.acts + lane * ns;
+  for (int s = 0; s < ns; ++s, kj += kGolden) sts_u8(row + s, (uint32_t)policy_action(kj, 0, hi));
+  if (P.pol_out) {
+    __syncwarp();
+    const int64_t left = P.B - b0;
+    const int bytes = (left >= 32 ? 32 : (int)left) * ns;
+    const unsigned char* src = vy_smem + tile + P.L.acts;
+    uint8_t* g = P.pol_out + b0 * ns;
+    if ((bytes & 15) == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+      for (int o = lane * 16; o < bytes; o += 512)
+        *reinterpret_cast<uint4*>(g + o) = *reinterpret_cast<const uint4*>(src + o);
+    } else {
+      for (int o = lane; o < bytes; o += 32) g[o] = src[o];
+    }
+  }
+}
+
 // One step of the 32 envs of the tile starting at env b0.  Every lane runs
 // the transition (padding lanes on their harmless padding columns, side
 // effects masked) because the fused port loop synchronises the warp.
 template <int M>
 __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const double* dtab, PortC pc, TreeC tc,
                                           uint32_t tile, int64_t b0, int lane,
-                                          unsigned long long* claim = nullptr) {
+                                          unsigned long long* claim = nullptr, int64_t pol_call = 0) {
   using C = Spec<M>;
   const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
@@ -71,12 +98,13 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
   // occupies.  At night most ports are empty in every lane and are neither
   // read nor written (-12% step time); at the afternoon peak every port is
   // occupied somewhere and the extra round trip costs ~3% (day average -1.5%).
-  tile_issue_meta(P, tile, b0, lane, C::staged(P));
+  tile_issue_meta(P, tile, b0, lane, C::staged(P) && !P.policy);
   // exogenous inputs for this step and the obs globals of the next one, in
   // flight together with the tile copies
   const Frame F = load_frame<M>(P, E.step, E.day);
   const ObsGlobals G = load_obs_globals(P, E.step + 1, E.day);
   const uint64_t occ_ports = tile_issue_ports(P, tile, b0, lane);
+  if (P.policy) policy_row(P, tile, b0, lane, pol_call);  // ALU work under the copies' latency
   tile_wait();
   const ObsSink S = make_sink<M>(P, T, b, P.out.obs, /*in_place=*/true);
   const int dt = P.act_dtype;
@@ -137,12 +165,16 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t toff = tables_bytes(P.n_profiles, P.k, P.n_ports, P.n_nodes) + warp * P.L.bytes;
   const unsigned long long ntiles = (unsigned long long)((P.B + 31) >> 5);
+  // fused RandomPolicy: the call index, from the device counter when the
+  // launch is graph-replayed (advanced below by the last warp to finish, after
+  // every warp has read it)
+  const int64_t pol_call = P.policy ? P.pol_call + (P.pol_counter ? *(volatile int64_t*)P.pol_counter : 0) : 0;
   unsigned long long nxt = 0;  // lane 0: this warp's next tile (claimed inside step_tile)
   if (lane == 0) nxt = atomicAdd(P.tile_ctr, 1ull);
   for (;;) {
     const unsigned long long t = __shfl_sync(0xffffffffu, nxt, 0);
     if (t >= ntiles) break;
-    step_tile<M>(P, prof, dtab, pc, tc, toff, (int64_t)t * 32, lane, &nxt);
+    step_tile<M>(P, prof, dtab, pc, tc, toff, (int64_t)t * 32, lane, &nxt, pol_call);
     __syncwarp();
   }
   if (lane == 0) {
@@ -151,6 +183,7 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
     if (atomicAdd(P.tile_ctr + 1, 1ull) == warps - 1) {
       P.tile_ctr[0] = 0;
       P.tile_ctr[1] = 0;
+      if (P.policy && P.pol_counter) P.pol_counter[0] += 1;
     }
   }
 }

@@ -112,9 +112,10 @@ class HeteroBatch:
         return self._fan_out(one)
 
     def random_step(self):
-        """One step of every group with its device RandomPolicy actions."""
+        """One step of every group with its device RandomPolicy actions (drawn
+        inside each group's step kernel, vy_step_random)."""
         def one(i):
-            o, r, d, _ = self.envs[i].step(self.policies[i].actions(self.envs[i]), collect_infos=False)
+            o, r, d, _ = self.envs[i].step_random(self.policies[i])
             return o, r, d
 
         return self._fan_out(one)
@@ -124,11 +125,11 @@ class HeteroBatch:
         and their stream fork/join cost one graph launch.  Actions come from the
         device-counter RandomPolicy (vy_random_actions_dev), so every replay
         draws the next call; the host-side lockstep clocks and call counters are
-        advanced here because a replay runs no host code."""
+        advanced here because a replay runs no host code.  One fused
+        policy+step kernel per group."""
         if getattr(self, "_graph", None) is None:
             def one(i):
-                e = self.envs[i]
-                o, r, d, _ = e.step(self.policies[i].actions(e, device_counter=True), collect_infos=False)
+                o, r, d, _ = self.envs[i].step_random(self.policies[i], device_counter=True)
                 return o, r, d
 
             clocks = [e._t for e in self.envs]
@@ -149,6 +150,9 @@ class HeteroBatch:
         for e in self.envs:
             if e._t is not None:
                 e._t = (e._t + 1) % e.tables.episode_steps
+
+    def kernels_per_step(self) -> int:
+        return len(self.envs)
 
     def launch_count(self) -> int:
         return sum(e.launch_count() for e in self.envs)

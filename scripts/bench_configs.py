@@ -16,7 +16,7 @@ sys.path.insert(0, ".")
 from paper_2507_01522_b200 import (DEFAULT_BATTERY, EnvConfig, default_setup, generate_synthetic_defaults,  # noqa: E402
                                    preset_station)
 from paper_2507_01522_b200.batch import BatchEnv, DeviceRandomPolicy  # noqa: E402
-from bench import algorithmic_bytes, load_peaks  # noqa: E402
+from bench import contract_bytes as algorithmic_bytes, load_peaks  # noqa: E402
 
 
 def measure(name, cfg, station, ds, B, steps=288):

@@ -34,3 +34,6 @@ print(f"total warp inst {ti}  samples {ts}")
 print("== by stall samples")
 for x in sorted(rows, key=lambda x: -x[4])[:top]:
     print(f"{x[4] / ts * 100:5.1f}% samp {x[3] / ti * 100:5.1f}% inst  {x[0]}:{x[1]}  {x[2]}")
+print("== by instructions executed")
+for x in sorted(rows, key=lambda x: -x[3])[:top]:
+    print(f"{x[3] / ti * 100:5.1f}% inst {x[4] / ts * 100:5.1f}% samp  {x[0]}:{x[1]}  {x[2]}")
