@@ -281,6 +281,24 @@ int vy_ppo_head_bwd(const void *logits, int32_t dtype, int64_t ld, const uint8_t
                     void *grad, void *stream);
 /* PPO minibatch gather: dst row i = src row idx[i] for i < n, rows of
  * row_bytes bytes (a multiple of 16; src and dst 16-byte aligned). */
+/* PPO rollout policy forward on the tensor cores (tcgen05.mma, TMEM
+ * accumulators, bulk-async obs tiles): one launch per rollout step.
+ * obs: float32 [N][obs_ld] (first obs_dim columns used); the actor-critic of
+ * ppo.py (hidden 64: W1 [128 x obs_dim], Wa2/Wc2 [64 x 64], head [S*A x 64],
+ * value [1 x 64]) pre-packed by the host in the UMMA K-major layout:
+ * wpack bf16 blob of out[0] bytes, fpack out[1] floats (vy_policy_geometry
+ * gives the sizes; ppo.pack_policy the layout).  Writes the sampled uint8
+ * actions [N][S] (inverse-CDF categorical sampling, one uniform per (row,
+ * slot) from the counter-based stream keyed by seed and counter[0], which the
+ * kernel advances: counter = {call, scratch}), the log-probability [N] and
+ * the value [N]; logits_out (NULL = not written) receives the bf16-rounded
+ * logits [N][S*A] as float32.  Not part of the reference (trainer-free,
+ * SPEC.md:14); the paper's PPO network. */
+int vy_policy_geometry(int32_t obs_dim, int32_t obs_ld, int32_t S, int32_t A, int32_t out[4]);
+int vy_policy_step(const float *obs, int64_t obs_ld, int64_t N, int32_t obs_dim, int32_t S, int32_t A,
+                   const void *wpack, const float *fpack, uint64_t seed, int64_t *counter, uint8_t *actions,
+                   float *logp, float *value, float *logits_out, void *stream);
+
 int vy_gather_rows(const void *src, int64_t row_bytes, const int64_t *idx, int64_t n, void *dst, void *stream);
 /* Column sums (a linear layer's bias gradient): out[c] = sum over m < M of
  * g[m*ld + c], c < N; g float32 (dtype 0) or bfloat16 (1); out float32.

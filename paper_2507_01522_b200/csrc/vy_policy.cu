@@ -1,0 +1,492 @@
+// vy_policy.cu — the PPO rollout's policy forward on the 5th-generation
+// tensor cores: one persistent sm_100a kernel per rollout step that reads the
+// float32 observations the env step just wrote and writes the sampled
+// multi-discrete actions, their log-probability and the value estimate.
+//
+// Network (ppo.py ActorCritic, PureJaxRL's default actor-critic, PAPER.md
+// 465-490): h1 = tanh(W1 x + b1) for actor and critic at once ([2H x K1],
+// rows 0..H-1 actor, H..2H-1 critic), h2a = tanh(Wa2 h1a + b2a),
+// h2c = tanh(Wc2 h1c + b2c), logits = Wh h2a + bh (S slots x A actions),
+// value = wv . h2c + bv.  Numerics follow the bf16 autocast forward the
+// unfused path runs (cuBLAS bf16 GEMMs with fp32 accumulation, bf16 outputs,
+// bf16 tanh): every layer output is rounded to bf16 before the next use.
+//
+// Per 32-row sub-tile (one CTA per SM, 17 warps, persistent over sub-tiles;
+// the rows are replicated 4x into the M = 128 MMA tile, see k_policy_step):
+//   obs rows (32 x obs_ld float32, one contiguous block) -> shared
+//     memory with one bulk async copy (TMA engine, mbarrier completion), the
+//     next tile's copy in flight while this tile computes;
+//   convert to bf16 in the UMMA K-major no-swizzle layout ([k/8][row][8]);
+//   layer 1: 7 x tcgen05.mma (M=128, N=2H=128, K=16) into TMEM columns 0..127;
+//   epilogue 1: tcgen05.ld -> bias, tanh (SFU), bf16 -> shared A operand;
+//   layer 2: actor and critic halves, 2 x 4 tcgen05.mma (N=64) -> TMEM 128..255;
+//   epilogue 2: actor -> shared A operand, critic -> value dot product;
+//   layer 3: head, 2 tcgen05.mma chains (N=256 + N=160; slot s in columns
+//     24s..24s+A-1) -> TMEM 0..415;
+//   epilogue 3: per (row, slot): bf16 logits, max / exp / sum, one uniform
+//     from the in-kernel counter-based stream, inverse-CDF categorical sample,
+//     log-probability; per-row sums through shared memory.
+// Weights (~94 KB bf16, pre-laid-out by the host in the UMMA layout) are
+// bulk-copied into shared memory once per CTA.  One thread issues every MMA
+// and commits to an mbarrier the epilogue warps wait on.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/voltyard_b200.h"
+
+namespace vyp {
+
+constexpr int kWarps = 17;     // warp w: A chunk w of epilogues 1/2 (w < 16), action slot w of the head
+constexpr int kThreads = 32 * kWarps;
+constexpr int kRows = 32;      // unique rows per MMA tile (replicated 4x into M = 128)
+constexpr int kM = 128;        // rows per tile (UMMA M)
+constexpr int kH = 64;         // hidden width per branch
+constexpr int kSlotCols = 24;  // TMEM / head-row columns per action slot
+constexpr int kMaxK1 = 128;    // padded observation width
+constexpr int kMaxA = 21;      // actions per slot (2K+1 of the default K = 10)
+
+__host__ __device__ constexpr int ceil16(int x) { return (x + 15) / 16 * 16; }
+
+struct Geo {
+  int K1, C1;        // padded obs width (multiple of 16), its 8-column chunks
+  int N3, n3a, n3b;  // head width (S * kSlotCols padded to 16) and its two MMA widths
+  int obs_ld, obs_dim, S, A;
+  uint32_t off_w1, off_wa2, off_wc2, off_wh, w_bytes;  // weight blob (bf16, UMMA layout)
+  uint32_t off_f;      // float params: b1[2H] b2a[H] b2c[H] bh[N3] wv[H] bv
+  uint32_t f_floats;
+  uint32_t off_a;      // A operand [16][128][8] bf16
+  uint32_t off_obs;    // obs staging 128 x obs_ld float32
+  uint32_t off_part;   // vpart[32][8], lpart[32][S] float32
+  uint32_t off_bar;    // mbarriers: weights, obs, mma; TMEM base address
+  uint32_t smem;
+};
+
+__host__ __device__ inline Geo make_geo(int obs_dim, int obs_ld, int S, int A) {
+  Geo g{};
+  g.obs_dim = obs_dim;
+  g.obs_ld = obs_ld;
+  g.S = S;
+  g.A = A;
+  g.K1 = ceil16(obs_dim);
+  g.C1 = g.K1 / 8;
+  g.N3 = ceil16(S * kSlotCols);
+  g.n3a = g.N3 > 256 ? 256 : g.N3;
+  g.n3b = g.N3 - g.n3a;
+  g.off_w1 = 0;
+  g.off_wa2 = g.off_w1 + g.C1 * 2 * kH * 16;
+  g.off_wc2 = g.off_wa2 + 8 * kH * 16;
+  g.off_wh = g.off_wc2 + 8 * kH * 16;
+  g.w_bytes = g.off_wh + 8 * g.N3 * 16;
+  g.off_f = g.w_bytes;
+  g.f_floats = 2 * kH + kH + kH + g.N3 + kH + 4;  // a multiple of 4: one 16-byte-sized bulk copy
+  g.off_a = (g.off_f + g.f_floats * 4 + 127) & ~127u;
+  g.off_obs = g.off_a + 16 * kM * 16;
+  g.off_part = (g.off_obs + kRows * obs_ld * 4 + 15) & ~15u;
+  g.off_bar = (g.off_part + kRows * (8 + S) * 4 + 15) & ~15u;
+  g.smem = g.off_bar + 64;
+  return g;
+}
+
+// ---- PTX wrappers ----------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// bulk async copy global -> shared (TMA engine), completion counted in bytes on `bar`
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor, K-major, no swizzle: 8-row x 16-byte core
+// matrices; LBO = byte stride between the two 8-element K chunks of one MMA,
+// SBO = byte stride between 8-row groups (here 128: rows are 16 bytes apart).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+// instruction descriptor kind::f16: bf16 A/B, f32 accumulate, K-major A and B
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+// D = sum over k-steps of A[:, 16k:16k+16] B[:, 16k:16k+16]^T
+__device__ __forceinline__ void mma_chain(uint32_t d_tmem, uint32_t a, uint32_t a_lbo, uint32_t b, uint32_t b_lbo,
+                                          int ksteps, uint32_t idesc) {
+  for (int k = 0; k < ksteps; ++k)
+    mma_bf16(d_tmem, sdesc(a + 2 * k * a_lbo, a_lbo, 128), sdesc(b + 2 * k * b_lbo, b_lbo, 128), idesc, k > 0);
+}
+
+#define VYP_LD32(taddr, v)                                                                                          \
+  asm volatile(                                                                                                     \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                               \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),           \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),     \
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),   \
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])    \
+      : "r"(taddr))
+#define VYP_LD16(taddr, v)                                                                                   \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),    \
+                 "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),          \
+                 "=r"(v[15])                                                                                      \
+               : "r"(taddr))
+#define VYP_LD8(taddr, v, o)                                                                                 \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                     \
+               : "=r"(v[o + 0]), "=r"(v[o + 1]), "=r"(v[o + 2]), "=r"(v[o + 3]), "=r"(v[o + 4]), "=r"(v[o + 5]), \
+                 "=r"(v[o + 6]), "=r"(v[o + 7])                                                              \
+               : "r"(taddr))
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+// hardware tanh (MUFU.TANH, rel. error ~2^-11): its result is rounded to bf16 next
+__device__ __forceinline__ float tanh_sfu(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float exp2_sfu(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&p);
+}
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// 8 accumulator columns of this thread's row -> bf16(tanh(bf16(acc + bias)))
+// (cuBLAS bf16 output, then the bf16 tanh) -> one 16-byte A-operand chunk,
+// stored into all four row replicas
+__device__ __forceinline__ void act_to_a(const uint32_t* v, const float* bias, uint8_t* a_base, int c, int r) {
+  uint32_t w[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float x0 = tanh_sfu(bf16r(__uint_as_float(v[2 * j]) + bias[2 * j]));
+    const float x1 = tanh_sfu(bf16r(__uint_as_float(v[2 * j + 1]) + bias[2 * j + 1]));
+    w[j] = pack_bf16(x0, x1);
+  }
+  const uint4 val = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+  for (int rep = 0; rep < 4; ++rep)
+    *reinterpret_cast<uint4*>(a_base + (size_t)c * (kM * 16) + (r + kRows * rep) * 16) = val;
+}
+
+// Rows are processed 32 at a time (a sub-tile), each replicated into the four
+// 32-row quarters of the M = 128 MMA tile: every TMEM lane quadrant then holds
+// all 32 rows, so warp w (which may only read lane quadrant w % 4) can take
+// any column range of any row.  Epilogues 1 and 2: warp w < 16 owns 8-column
+// chunk w; the head: warp w owns slot w (S <= 17 warps).  The MMAs compute 4x
+// the rows they need — the tensor cores are idle here anyway — and a 4096-row
+// rollout step spreads over 128 CTAs instead of 32.
+__global__ void __launch_bounds__(kThreads, 1)
+    k_policy_step(const float* __restrict__ obs, int64_t N, Geo G, const uint8_t* __restrict__ wpack,
+                  const float* __restrict__ fpack, uint64_t seed, unsigned long long* counter,
+                  uint8_t* __restrict__ actions, float* __restrict__ logp, float* __restrict__ value,
+                  float* __restrict__ logits_out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t tq = (uint32_t)(32 * (warp & 3)) << 16;  // this warp's TMEM lane quadrant
+  const uint32_t s_base = smem_u32(sm);
+  const uint32_t bar_w = s_base + G.off_bar, bar_obs = bar_w + 8, bar_mma = bar_w + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + G.off_bar + 24);
+  float* fp = reinterpret_cast<float*>(sm + G.off_f);
+  const float *b1 = fp, *b2a = fp + 2 * kH, *b2c = fp + 3 * kH, *bh = fp + 4 * kH, *wv = fp + 4 * kH + G.N3;
+  const float bv = fpack[5 * kH + G.N3];
+  float* vpart = reinterpret_cast<float*>(sm + G.off_part);  // [32][8]
+  float* lpart = vpart + kRows * 8;                           // [32][S]
+  uint8_t* a_smem = sm + G.off_a;
+  const float* stage = reinterpret_cast<const float*>(sm + G.off_obs);
+  const int64_t ntiles = (N + kRows - 1) / kRows;
+  const bool elect = tid == 0;
+
+  // the sub-tile's obs rows: one bulk copy when 16-byte sized and aligned, else plain loads
+  auto issue_obs = [&](int64_t tile) {
+    const int64_t r0 = tile * kRows;
+    const int rows = (int)((N - r0) < kRows ? (N - r0) : kRows);
+    const uint32_t bytes = (uint32_t)rows * G.obs_ld * 4;
+    if ((bytes & 15u) == 0 && (reinterpret_cast<uintptr_t>(obs + r0 * G.obs_ld) & 15u) == 0) {
+      if (elect) {
+        mbar_expect_tx(bar_obs, bytes);
+        bulk_g2s(s_base + G.off_obs, obs + r0 * G.obs_ld, bytes, bar_obs);
+      }
+      return true;
+    }
+    return false;
+  };
+
+  if (elect) {
+    mbar_init(bar_w, 1);
+    mbar_init(bar_obs, 1);
+    mbar_init(bar_mma, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {  // TMEM: 512 columns (layer 1/2 at 0..255, the head at 0..N3-1 once they are consumed)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  int64_t tile = blockIdx.x;
+  bool bulk = tile < ntiles ? issue_obs(tile) : false;
+  if (elect) {  // weights and float parameters: two bulk copies completing on one barrier
+    mbar_expect_tx(bar_w, G.w_bytes + G.f_floats * 4);
+    bulk_g2s(s_base, wpack, G.w_bytes, bar_w);
+    bulk_g2s(s_base + G.off_f, fpack, G.f_floats * 4, bar_w);
+  }
+  const uint64_t key = mix64(seed ^ mix64(counter[0] + 0x9E3779B97F4A7C15ULL));
+  uint32_t ph_obs = 0, ph_mma = 0;
+  bool weights = false;
+
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * kRows;
+    const int rows = (int)((N - r0) < kRows ? (N - r0) : kRows);
+    if (bulk) {
+      mbar_wait(bar_obs, ph_obs);
+      ph_obs ^= 1;
+    } else {
+      float* st = reinterpret_cast<float*>(sm + G.off_obs);
+      for (int i = tid; i < rows * G.obs_ld; i += kThreads) st[i] = obs[r0 * G.obs_ld + i];
+      __syncthreads();
+    }
+    // obs (float32, row stride obs_ld) -> bf16 A operand [k/8][row][8], zero
+    // past obs_dim and past the last row, written into all four replicas
+    for (int it = tid; it < kRows * G.C1; it += kThreads) {
+      const int c = it / kRows, r = it - c * kRows;
+      const float* src = stage + r * G.obs_ld + 8 * c;
+      float x[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = (8 * c + j < G.obs_dim && r < rows) ? src[j] : 0.f;
+      const uint4 val =
+          make_uint4(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
+#pragma unroll
+      for (int rep = 0; rep < 4; ++rep)
+        *reinterpret_cast<uint4*>(a_smem + (size_t)c * (kM * 16) + (r + kRows * rep) * 16) = val;
+    }
+    fence_proxy_async();
+    __syncthreads();
+    // the staging area is free: the next sub-tile's obs copy overlaps this one's layers
+    const int64_t nxt = tile + gridDim.x;
+    if (nxt < ntiles) bulk = issue_obs(nxt);
+    if (!weights) {
+      mbar_wait(bar_w, 0);
+      weights = true;
+    }
+
+    // layer 1: D[0:128) = A[128 x K1] W1^T
+    if (elect) {
+      tc_fence_after();
+      mma_chain(tmem, s_base + G.off_a, kM * 16, s_base + G.off_w1, 2 * kH * 16, G.K1 / 16, idesc_bf16(kM, 2 * kH));
+      mma_commit(bar_mma);
+    }
+    mbar_wait(bar_mma, ph_mma);
+    ph_mma ^= 1;
+    tc_fence_after();
+    if (warp < 16) {  // h1 chunk `warp` (columns 8w..8w+7) of row `lane`
+      uint32_t v[8];
+      VYP_LD8(tmem + tq + 8 * warp, v, 0);
+      tmem_wait_ld();
+      act_to_a(v, b1 + 8 * warp, a_smem, warp, lane);
+    }
+    tc_fence_before();
+    fence_proxy_async();
+    __syncthreads();
+
+    // layer 2: actor D[128:192) = h1a Wa2^T, critic D[192:256) = h1c Wc2^T
+    if (elect) {
+      tc_fence_after();
+      mma_chain(tmem + 128, s_base + G.off_a, kM * 16, s_base + G.off_wa2, kH * 16, kH / 16, idesc_bf16(kM, kH));
+      mma_chain(tmem + 192, s_base + G.off_a + 8 * kM * 16, kM * 16, s_base + G.off_wc2, kH * 16, kH / 16,
+                idesc_bf16(kM, kH));
+      mma_commit(bar_mma);
+    }
+    mbar_wait(bar_mma, ph_mma);
+    ph_mma ^= 1;
+    tc_fence_after();
+    if (warp < 16) {
+      uint32_t v[8];
+      VYP_LD8(tmem + tq + 128 + 8 * warp, v, 0);
+      tmem_wait_ld();
+      if (warp < 8) {
+        act_to_a(v, b2a + 8 * warp, a_smem, warp, lane);  // h2a -> A chunks 0..7
+      } else {
+        // value head: bf16 h2c times the bf16 value weights, fp32 partial sums
+        const float* b = b2c + 8 * (warp - 8);
+        const float* w = wv + 8 * (warp - 8);
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc += bf16r(tanh_sfu(bf16r(__uint_as_float(v[j]) + b[j]))) * w[j];
+        vpart[lane * 8 + (warp - 8)] = acc;
+      }
+    }
+    tc_fence_before();
+    fence_proxy_async();
+    __syncthreads();
+
+    // layer 3: head D[0:N3) = h2a Wh^T (two chains: N = n3a, n3b)
+    if (elect) {
+      tc_fence_after();
+      mma_chain(tmem, s_base + G.off_a, kM * 16, s_base + G.off_wh, G.N3 * 16, kH / 16, idesc_bf16(kM, G.n3a));
+      if (G.n3b > 0)
+        mma_chain(tmem + G.n3a, s_base + G.off_a, kM * 16, s_base + G.off_wh + G.n3a * 16, G.N3 * 16, kH / 16,
+                  idesc_bf16(kM, G.n3b));
+      mma_commit(bar_mma);
+    }
+    const int64_t grow = r0 + lane;
+    const bool live = lane < rows;
+    if (warp == 16 && live) {  // idle during the head otherwise
+      const float* vp = vpart + lane * 8;
+      value[grow] = bf16r((((vp[0] + vp[1]) + (vp[2] + vp[3])) + ((vp[4] + vp[5]) + (vp[6] + vp[7]))) + bv);
+    }
+    mbar_wait(bar_mma, ph_mma);
+    ph_mma ^= 1;
+    tc_fence_after();
+    constexpr float kLog2e = 1.4426950408889634f;
+    for (int s = warp; s < G.S; s += kWarps) {
+      uint32_t v[24];
+      const uint32_t ta = tmem + tq + kSlotCols * s;
+      VYP_LD16(ta, v);
+      VYP_LD8(ta + 16, v, 16);
+      tmem_wait_ld();
+      float z[kMaxA];
+      float m = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < kMaxA; ++k) {
+        z[k] = k < G.A ? bf16r(__uint_as_float(v[k]) + bh[kSlotCols * s + k]) : -INFINITY;  // bf16 logits
+        m = fmaxf(m, z[k]);
+      }
+      const float mb = m * kLog2e;
+      float sum = 0.f;
+#pragma unroll
+      for (int k = 0; k < kMaxA; ++k) sum += exp2_sfu(fmaf(z[k], kLog2e, -mb));  // exp(z - m); 0 past A
+      // one uniform per (row, slot): element (row * S + s) of this call's stream
+      const uint64_t x = mix64(key + (uint64_t)(grow * G.S + s) * 0x9E3779B97F4A7C15ULL);
+      const float target = ((float)(x >> 41) + 0.5f) * (1.f / 8388608.f) * sum;
+      // inverse CDF: the first k whose running sum passes u * sum (the last
+      // valid action if rounding leaves target at or above the total)
+      float c = 0.f, za = z[0];
+      int a = -1;
+#pragma unroll
+      for (int k = 0; k < kMaxA; ++k) {
+        c += exp2_sfu(fmaf(z[k], kLog2e, -mb));
+        const bool take = a < 0 && k < G.A && (target < c || k == G.A - 1);
+        a = take ? k : a;
+        za = take ? z[k] : za;
+      }
+      lpart[lane * G.S + s] = (za - m) - __logf(sum);
+      if (live) {
+        actions[grow * G.S + s] = (uint8_t)a;
+        if (logits_out)
+#pragma unroll
+          for (int k = 0; k < kMaxA; ++k)
+            if (k < G.A) logits_out[grow * (G.S * G.A) + s * G.A + k] = z[k];
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0 && live) {  // log-probability: slot terms summed in slot order
+      float acc = 0.f;
+      for (int s = 0; s < G.S; ++s) acc += lpart[lane * G.S + s];
+      logp[grow] = acc;
+    }
+  }
+
+  // teardown: release TMEM; the last CTA out advances the call counter
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+  if (elect) {
+    __threadfence();
+    if (atomicAdd(counter + 1, 1ull) == gridDim.x - 1) {
+      counter[1] = 0;
+      counter[0] += 1;
+      __threadfence();
+    }
+  }
+}
+
+thread_local std::string g_err;
+
+}  // namespace vyp
+
+extern "C" {
+
+int vy_policy_geometry(int32_t obs_dim, int32_t obs_ld, int32_t S, int32_t A, int32_t out[4]) {
+  if (obs_dim < 1 || obs_ld < obs_dim || vyp::ceil16(obs_dim) > vyp::kMaxK1 || obs_ld > vyp::kMaxK1 || S < 1 ||
+      A < 2 || A > vyp::kMaxA || vyp::ceil16(S * vyp::kSlotCols) > 512 || S > 64)
+    return VY_ERR_UNSUPPORTED;
+  const vyp::Geo g = vyp::make_geo(obs_dim, obs_ld, S, A);
+  out[0] = (int32_t)g.w_bytes;   // bf16 weight blob bytes
+  out[1] = (int32_t)g.f_floats;  // float parameter count
+  out[2] = g.N3;                 // head rows (slot s at rows 24s..24s+A-1)
+  out[3] = (int32_t)g.smem;      // dynamic shared memory per CTA
+  return VY_OK;
+}
+
+int vy_policy_step(const float* obs, int64_t obs_ld, int64_t N, int32_t obs_dim, int32_t S, int32_t A,
+                   const void* wpack, const float* fpack, uint64_t seed, int64_t* counter, uint8_t* actions,
+                   float* logp, float* value, float* logits_out, void* stream) {
+  if (!obs || !wpack || !fpack || !counter || !actions || !logp || !value || N < 1) return VY_ERR_ARG;
+  int32_t geo[4];
+  if (vy_policy_geometry(obs_dim, (int32_t)obs_ld, S, A, geo) != VY_OK) return VY_ERR_UNSUPPORTED;
+  if (((reinterpret_cast<uintptr_t>(wpack) | reinterpret_cast<uintptr_t>(fpack)) & 15u) != 0) return VY_ERR_ARG;
+  const vyp::Geo g = vyp::make_geo(obs_dim, (int)obs_ld, S, A);
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(vyp::k_policy_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  }
+  const int64_t tiles = (N + vyp::kRows - 1) / vyp::kRows;
+  const unsigned grid = (unsigned)(tiles < num_sms ? tiles : num_sms);
+  vyp::k_policy_step<<<grid, vyp::kThreads, g.smem, (cudaStream_t)stream>>>(
+      obs, N, g, static_cast<const uint8_t*>(wpack), fpack, seed, reinterpret_cast<unsigned long long*>(counter),
+      actions, logp, value, logits_out);
+  return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
+}
+
+}  // extern "C"

@@ -4,11 +4,13 @@ The reference ships no trainer; the paper trains a PureJaxRL PPO
 agent (hyperparameters PAPER.md:465-490).  This module is that
 loop B200-first:
 
-* rollout: policy forward (bf16 autocast on the tensor cores via cuBLAS),
-  categorical sampling over the 17 x 21 multi-discrete head, and the fused
-  env step kernel, for T steps, captured once as a CUDA graph and replayed
-  every iteration (the rollout is ~5 kernels per step; replay removes the
-  per-launch host overhead);
+* rollout: per step ONE policy kernel (csrc/vy_policy.cu: the three MLP
+  layers as tcgen05.mma on the 5th-generation tensor cores with TMEM
+  accumulators, observation tiles bulk-copied by the TMA engine, tanh /
+  bias epilogues and the categorical sampling of the 17 x 21 multi-discrete
+  head fused) and the fused env step kernel, for T steps, captured once as a
+  CUDA graph and replayed every iteration (fused_policy=False keeps the
+  earlier cuBLAS + sampler-kernel path for comparison);
 * advantages: the vy_gae reverse-scan kernel (csrc/vy_ppo.cu);
 * update: clipped PPO objective with value clipping, entropy bonus, Adam,
   global-norm gradient clipping; under torch.distributed the flattened
@@ -58,6 +60,7 @@ class PPOConfig:
     use_graph: bool = True
     fused_head: bool = True  # vy_ppo_sample / vy_ppo_head_* kernels instead of the torch op chain
     graph_update: bool = True  # the whole update (GAE + epochs x minibatches + Adam) as one CUDA graph (1 GPU)
+    fused_policy: bool = True  # rollout forward + sampling in the tcgen05 kernel (vy_policy_step)
 
 
 def _ortho(layer: nn.Linear, gain: float) -> nn.Linear:
@@ -226,6 +229,64 @@ class ActorCritic(nn.Module):
         return out, out[:, self.out_dim]
 
 
+def policy_geometry(net: "ActorCritic", obs_ld: int | None = None) -> tuple[int, int, int, int]:
+    """(weight blob bytes, float params, head rows, shared memory) of the
+    tcgen05 policy kernel for this network (vy_policy_geometry)."""
+    out = (C.c_int32 * 4)()
+    rc = nat.lib().vy_policy_geometry(net.obs_dim, obs_ld or net.obs_dim, net.n_slots, net.n_actions, out)
+    if rc != nat.VY_OK or net.hidden != 64:
+        raise NotImplementedError("the tcgen05 policy kernel covers hidden=64, obs width <= 128, A <= 21")
+    return tuple(out)
+
+
+def _umma_k_major(w: torch.Tensor) -> torch.Tensor:
+    """[N][K] -> the UMMA K-major no-swizzle layout [K/8][N][8] (bf16, flat)."""
+    n, k = w.shape
+    return w.to(torch.bfloat16).reshape(n, k // 8, 8).permute(1, 0, 2).reshape(-1)
+
+
+def pack_policy(net: "ActorCritic", geo: tuple | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """The network's weights in the tcgen05 policy kernel's layout
+    (csrc/vy_policy.cu): a bf16 blob [W1 | Wa2 | Wc2 | Wh] with every matrix
+    in the UMMA K-major layout (W1 zero-padded to 16-column K steps; head row
+    24s + k = logit k of slot s, the rest zero) and the float parameters
+    b1, b2a, b2c, bh (same row map), wv, bv, each rounded through bf16 like
+    the autocast forward's weights.  Differentiable ops on the live weights:
+    call it inside a captured rollout so every replay uses the current ones."""
+    geo = geo or policy_geometry(net)
+    H, S, A = net.hidden, net.n_slots, net.n_actions
+    dev = net.inp.weight.device
+    k1 = (net.obs_dim + 15) // 16 * 16
+    w1 = nn.functional.pad(net.inp.weight, (0, k1 - net.inp.weight.shape[1]))
+    rows = (torch.arange(S, device=dev)[:, None] * 24 + torch.arange(A, device=dev)[None, :]).reshape(-1)
+    wh = torch.zeros(geo[2], H, device=dev, dtype=net.inp.weight.dtype).index_copy(0, rows, net.actor[2].weight[: S * A])
+    bh = torch.zeros(geo[2], device=dev, dtype=net.inp.weight.dtype).index_copy(0, rows, net.actor[2].bias[: S * A])
+    blob = torch.cat([_umma_k_major(w1), _umma_k_major(net.actor[0].weight), _umma_k_major(net.critic[0].weight),
+                      _umma_k_major(wh)])
+    fp = torch.cat([net.inp.bias, net.actor[0].bias, net.critic[0].bias, bh, net.critic[2].weight[0],
+                    net.critic[2].bias, torch.zeros(3, device=dev)])
+    fp = fp.to(torch.bfloat16).float()
+    assert blob.numel() * 2 == geo[0] and fp.numel() == geo[1]
+    return blob, fp
+
+
+def policy_step(obs: torch.Tensor, obs_dim: int, S: int, A: int, packed: tuple, seed: int, counter: torch.Tensor,
+                actions: torch.Tensor, logp: torch.Tensor, value: torch.Tensor,
+                logits_out: torch.Tensor | None = None) -> None:
+    """One rollout step of the policy on the tensor cores (vy_policy_step):
+    float32 obs rows [N, >= obs_dim] -> uint8 actions [N, S], log-probability
+    and value [N] (float32), sampled with the device counter `counter`."""
+    N = obs.shape[0]
+    if obs.stride(1) != 1:
+        raise ValueError("obs rows must be contiguous")
+    blob, fp = packed
+    rc = nat.lib().vy_policy_step(obs.data_ptr(), obs.stride(0), N, obs_dim, S, A, blob.data_ptr(), fp.data_ptr(),
+                                  seed & ((1 << 64) - 1), counter.data_ptr(), actions.data_ptr(), logp.data_ptr(),
+                                  value.data_ptr(), logits_out.data_ptr() if logits_out is not None else None,
+                                  torch.cuda.current_stream().cuda_stream)
+    nat.check(rc, "vy_policy_step")
+
+
 def _dtype_code(t: torch.Tensor) -> int:
     if t.dtype == torch.float32:
         return 0
@@ -353,12 +414,24 @@ class PPOTrainer:
         self.iterations = 0
         self.n_iters = max(1, cfg.total_timesteps // (T * B * self.world))
         self._graph = None
+        self._fused_policy = cfg.fused_policy
+        if self._fused_policy:
+            self._geo = policy_geometry(self.net)
+            self._scratch_a = torch.zeros(B, A, dtype=torch.uint8, device=dev)
+            self._scratch_lp = torch.zeros(B, device=dev)
         env.reset(as_numpy=False)
         self.obs[0].copy_(env.outs.obs)
 
     # -- rollout -----------------------------------------------------------------
 
     def _policy_step(self, t: int) -> None:
+        if self._fused_policy:
+            # obs -> 3 tcgen05 GEMM layers -> sampled actions / log-prob / value, one kernel
+            policy_step(self.obs[t], self.env.obs_length, self.net.n_slots, self.net.n_actions, self._packed,
+                        self._sample_seed, self._sample_ctr, self.actions[t], self.logp[t], self.values[t])
+            self.env.set_outputs(obs=self.obs[t + 1], reward=self.rewards[t], done=self.dones[t])
+            self.env.step(self.actions[t], collect_infos=False)
+            return
         fused = self.cfg.fused_head
         # the padded bf16 network input in one copy (the zero padding columns of
         # the persistent buffer are never written): no pad + cast pair per step
@@ -392,6 +465,15 @@ class PPOTrainer:
         # one autocast region for the whole rollout: the bf16 copies of the
         # weights are made once per rollout (autocast's weight cache), not once
         # per policy step
+        if self._fused_policy:
+            self._packed = pack_policy(self.net, self._geo)  # inside the graph: from the live weights each replay
+            for t in range(self.cfg.rollout_steps):
+                self._policy_step(t)
+            # bootstrap value of the last obs (its actions / log-prob land in scratch rows)
+            T = self.cfg.rollout_steps
+            policy_step(self.obs[T], self.env.obs_length, self.net.n_slots, self.net.n_actions, self._packed,
+                        self._sample_seed, self._sample_ctr, self._scratch_a, self._scratch_lp, self.values[T])
+            return
         with torch.autocast("cuda", dtype=torch.bfloat16):
             if self.cfg.fused_head:
                 self._iw = self.net.inference_weights()  # inside the graph: rebuilt from the live weights each replay
@@ -508,6 +590,13 @@ class PPOTrainer:
                 stats = {"loss": loss.detach(), "pg": pg.detach(), "vf": vl.detach(), "ent": ent.detach()}
         self.obs[0].copy_(self.obs[T])
         return stats
+
+    def describe_rollout(self) -> str:
+        if self._fused_policy:
+            return ("CUDA graph x T: vy_policy_step (tcgen05 3-layer MLP, TMEM accumulators, bulk-async obs tiles, "
+                    "fused tanh/bias epilogues + inverse-CDF sampling, log-prob, value) + k_step")
+        return ("CUDA graph x T: cuBLAS bf16 GEMMs (block-diagonal layer 2, merged heads) + vy_ppo_sample_rng "
+                "Gumbel-max kernel + k_step")
 
     def iterate(self) -> dict:
         self.rollout()

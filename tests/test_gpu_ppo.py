@@ -361,7 +361,7 @@ def test_trainer_non_default_modes_run(fused, graph):
 
     rc = default_setup()
     env = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=256, master_seed=1)
-    tr = PPOTrainer(env, PPOConfig(rollout_steps=20, fused_head=fused, use_graph=graph))
+    tr = PPOTrainer(env, PPOConfig(rollout_steps=20, fused_head=fused, fused_policy=fused, use_graph=graph))
     for _ in range(2):
         st = tr.iterate()
     assert all(torch.isfinite(v).all() for v in st.values())
