@@ -61,6 +61,7 @@ class PPOConfig:
     fused_head: bool = True  # vy_ppo_sample / vy_ppo_head_* kernels instead of the torch op chain
     graph_update: bool = True  # the whole update (GAE + epochs x minibatches + Adam) as one CUDA graph (1 GPU)
     fused_policy: bool = True  # rollout forward + sampling in the tcgen05 kernel (vy_policy_step)
+    allreduce: str = "auto"  # gradient all-reduce: "auto" (world > 1), "always" (also at world 1: tests)
 
 
 def _ortho(layer: nn.Linear, gain: float) -> nn.Linear:
@@ -350,6 +351,26 @@ def head_reference(logits: torch.Tensor, actions: torch.Tensor):
     return lp, ent
 
 
+def allreduce_mean_(tensors: list, world: int, flat: torch.Tensor | None = None, group=None) -> None:
+    """Average `tensors` over the ranks, in place: one flattened all-reduce
+    (SUM, then / world — gloo has no AVG) instead of one per tensor.  `flat`
+    (optional) is a preallocated buffer of the total size (graph capture:
+    the same address every replay)."""
+    n = sum(t.numel() for t in tensors)
+    if flat is None:
+        flat = torch.empty(n, dtype=tensors[0].dtype, device=tensors[0].device)
+    off = 0
+    for t in tensors:
+        flat[off:off + t.numel()].copy_(t.reshape(-1))
+        off += t.numel()
+    dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    flat.div_(world)
+    off = 0
+    for t in tensors:
+        t.copy_(flat[off:off + t.numel()].view_as(t))
+        off += t.numel()
+
+
 def gae(values, rewards, dones, last_value, gamma, lam):
     """Advantages and returns via the vy_gae kernel; [T, B] float32 / uint8 inputs."""
     T, B = values.shape
@@ -389,10 +410,12 @@ class PPOTrainer:
         if self.world > 1:  # identical initial weights on every rank
             for p in self.net.parameters():
                 dist.broadcast(p.data, 0)
-        # one graph replay per update on a single GPU (the update is launch-bound
-        # otherwise: ~300 kernels per minibatch); with a gradient all-reduce
-        # the update stays eager
-        self._graph_update = cfg.graph_update and cfg.use_graph and self.world == 1
+        # one graph replay per update (the update is launch-bound otherwise:
+        # ~300 kernels per minibatch); under NCCL the per-minibatch gradient
+        # all-reduce is captured in the same graph
+        self._allreduce = self.world > 1 or cfg.allreduce == "always"
+        nccl = dist.is_initialized() and dist.get_backend() == "nccl"
+        self._graph_update = cfg.graph_update and cfg.use_graph and (not self._allreduce or nccl)
         if self._graph_update:
             self._lr = torch.tensor(cfg.lr, device=dev)
             self.opt = torch.optim.Adam(self.net.parameters(), lr=self._lr, eps=1e-5, fused=True, capturable=True)
@@ -510,16 +533,14 @@ class PPOTrainer:
     # -- update -------------------------------------------------------------------
 
     def _allreduce_grads(self) -> None:
-        if self.world == 1:
+        """Mean of the minibatch gradients over the ranks (NCCL over NVLink):
+        the only data-path collective of the system, once per minibatch."""
+        if not self._allreduce:
             return
-        grads = [p.grad for p in self.net.parameters() if p.grad is not None]
-        flat = torch.cat([g.reshape(-1) for g in grads])
-        dist.all_reduce(flat, op=dist.ReduceOp.AVG)
-        off = 0
-        for g in grads:
-            n = g.numel()
-            g.copy_(flat[off:off + n].view_as(g))
-            off += n
+        grads = [p.grad for p in self.net.parameters()]
+        if getattr(self, "_flat_grad", None) is None:
+            self._flat_grad = torch.empty(sum(g.numel() for g in grads), device=grads[0].device)
+        allreduce_mean_(grads, self.world, self._flat_grad)
 
     def update(self) -> dict:
         cfg = self.cfg

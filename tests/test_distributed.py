@@ -83,3 +83,44 @@ def test_sweep_groups_cover_c5_grid():
     assert len(gs) == 36 and sum(g.batch_size for g in gs) == 1 << 16
     assert len({g.name.split("/")[0] for g in gs}) == 3 and len({g.name.split("/")[1] for g in gs}) == 4
     assert {g.station.n_ports for g in gs} == {8, 16}
+
+
+def _grad_worker(rank, world, port, out):
+    """PPO's gradient all-reduce (ppo.allreduce_mean_) on gloo: different
+    per-rank gradients become their mean on every rank, and the Adam step that
+    follows leaves identical weights everywhere."""
+    from paper_2507_01522_b200.ppo import ActorCritic, allreduce_mean_
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.manual_seed(rank)  # different initial weights: the broadcast must fix them
+    net = ActorCritic(105, 17, 21, 64)
+    for p in net.parameters():
+        dist.broadcast(p.data, 0)
+    opt = torch.optim.Adam(net.parameters(), lr=1e-3)
+    g = torch.Generator().manual_seed(100 + rank)  # rank-specific data
+    x = torch.randn(64, 105, generator=g)
+    logits, v = net(x)
+    (logits.square().mean() + v.square().mean()).backward()
+    local = [p.grad.clone() for p in net.parameters()]
+    allreduce_mean_([p.grad for p in net.parameters()], world)
+    opt.step()
+    out[rank] = ([t.numpy() for t in local], [p.grad.numpy().copy() for p in net.parameters()],
+                 [p.data.numpy().copy() for p in net.parameters()])
+    dist.destroy_process_group()
+
+
+def test_two_rank_ppo_gradient_mean_and_identical_weights():
+    world = 2
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_grad_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+        res = dict(out)
+    local0, mean0, w0 = res[0]
+    local1, mean1, w1 = res[1]
+    for a, b, m0, m1 in zip(local0, local1, mean0, mean1):
+        assert not np.array_equal(a, b)
+        np.testing.assert_allclose(m0, (a + b) / 2, rtol=1e-6, atol=1e-7)
+        np.testing.assert_array_equal(m0, m1)
+    for a, b in zip(w0, w1):
+        np.testing.assert_array_equal(a, b)

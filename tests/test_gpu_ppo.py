@@ -366,3 +366,40 @@ def test_trainer_non_default_modes_run(fused, graph):
         st = tr.iterate()
     assert all(torch.isfinite(v).all() for v in st.values())
     env.close()
+
+
+def test_update_graph_with_captured_nccl_allreduce():
+    """The multi-GPU update path on one GPU: a 1-rank NCCL group with the
+    per-minibatch gradient all-reduce forced on, captured inside the update
+    CUDA graph.  SUM / 1 is exact, so the weights after two iterations equal
+    the all-reduce-free trainer's bit for bit."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2507_01522_b200 import default_setup
+    from paper_2507_01522_b200.batch import BatchEnv
+    from paper_2507_01522_b200.ppo import PPOConfig, PPOTrainer
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rc = default_setup()
+        weights = []
+        for mode in ("always", "auto"):
+            env = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=512, master_seed=2)
+            tr = PPOTrainer(env, PPOConfig(rollout_steps=32, allreduce=mode))
+            assert tr._graph_update and tr._allreduce == (mode == "always")
+            for _ in range(3):
+                st = tr.iterate()
+            assert all(torch.isfinite(v).all() for v in st.values())
+            weights.append([p.detach().clone() for p in tr.net.parameters()])
+            env.close()
+        for a, b in zip(*weights):
+            assert torch.equal(a, b)
+    finally:
+        dist.destroy_process_group()
