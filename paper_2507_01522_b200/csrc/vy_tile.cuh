@@ -575,14 +575,14 @@ __device__ __forceinline__ void stage_zero_obs(const ObsSink& S, int lane, bool 
 }
 
 __device__ __forceinline__ void store_port(const Params& P, int64_t b, int i, uint32_t mt, double idr, double soc,
-                                           double de, int dt) {
+                                           double de, int dt, bool meta = true) {
   const vy_state& s = P.st;
   const int64_t e = (int64_t)i * P.ld + b;
   s.port_i[e] = idr;
   s.port_soc[e] = soc;
   s.port_de[e] = de;
   s.port_dtrem[e] = (int16_t)dt;
-  s.port_meta[e] = (uint8_t)mt;
+  if (meta) s.port_meta[e] = (uint8_t)mt;  // callers skip it when unchanged
 }
 
 // One transition of one env (_kernel.pyx:283-571).  `act(slot)` returns the
@@ -751,26 +751,32 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
       dt -= occ ? 1 : 0;
       const int p = (mt >> 1) & 1u;
       dep = occ & ((p == 0 & dt <= 0) | (p == 1 & de == 0.0));  // bitwise: no short-circuit branches
-      const int over = dt < 0 ? -dt : 0, early = dt > 0 ? dt : 0;
-      if (info && dep) {
-        const int64_t at = (int64_t)nd * ld + b;
-        O.dep_port[at] = i;
-        O.dep_missing[at] = de;
-        O.dep_overtime[at] = over;
-        O.dep_early[at] = early;
-        O.dep_pref[at] = p;
-        O.dep_cap[at] = prof.cap(pf);
-        O.dep_soc[at] = soc;
+      // Departure bookkeeping (_kernel.pyx:426-458) behind a warp vote: about
+      // 1.3% of occupied port-steps depart, so most warps skip it; lanes of a
+      // voting warp without a departure add +0 (sums that start at +0 never
+      // become -0, so that equals the reference's skipped add).
+      if (__any_sync(0xffffffffu, dep)) {
+        const int over = dt < 0 ? -dt : 0, early = dt > 0 ? dt : 0;
+        if (info && dep) {
+          const int64_t at = (int64_t)nd * ld + b;
+          O.dep_port[at] = i;
+          O.dep_missing[at] = de;
+          O.dep_overtime[at] = over;
+          O.dep_early[at] = early;
+          O.dep_pref[at] = p;
+          O.dep_cap[at] = prof.cap(pf);
+          O.dep_soc[at] = soc;
+        }
+        sat0 += dep & (p == 0) ? de : 0.0;
+        const double s1 = (double)over - P.beta * (double)early;
+        sat1 += dep & (p == 1) ? s1 : 0.0;
+        E.ep_missing += dep ? de : 0.0;
+        E.ep_overtime += dep ? over : 0;
+        E.ep_departures += dep ? 1 : 0;
+        nd += dep ? 1 : 0;
       }
-      sat0 += dep & (p == 0) ? de : 0.0;
-      const double s1 = (double)over - P.beta * (double)early;
-      sat1 += dep & (p == 1) ? s1 : 0.0;
-      E.ep_missing += dep ? de : 0.0;
-      E.ep_overtime += dep ? over : 0;
-      E.ep_departures += dep ? 1 : 0;
-      nd += dep ? 1 : 0;
-      // _kernel.pyx:559-561 (arrivals add dt > 0 only)
-      tover += !dep & last & (p == 1) & (dt < 0) ? -dt : 0;
+      // _kernel.pyx:559-561 (arrivals add dt > 0 only): the episode's last step only
+      if (last) tover += !dep & (p == 1) & (dt < 0) ? -dt : 0;
       occm |= (uint64_t)(occ && !dep) << i;
     }
     if (info) O.delivered[i * ld + b] = got;
@@ -781,8 +787,9 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
         dt = 0;
       }
       if (S.in_place) {
-        // padding lanes (b >= B) write their own padding columns of the [n][ld] state: harmless, no branch
-        store_port(P, b, i, mt, cur, soc, de, dt);
+        // padding lanes (b >= B) write their own padding columns of the [n][ld] state: harmless, no branch;
+        // the meta byte changes only on a departure
+        store_port(P, b, i, mt, cur, soc, de, dt, dep);
         __syncwarp();  // every lane has read port i before its slots take obs columns
       } else {
         T.meta(i) = (uint8_t)mt;
