@@ -345,11 +345,11 @@ int step_mode(const vy_handle* h, uint32_t flags, bool staged_actions) {
 
 Profile make_profile(double cap, double r_ac, double r_dc, double tau) {
   const double omt = 1.0 - tau;
-  return Profile{cap, r_ac, r_dc, tau, omt, 1.0 / cap, 1.0 / omt, 0.0};
+  return Profile{cap, r_ac, r_dc, tau, omt, 1.0 / cap, 1.0 / omt, 0.0, 0.0};
 }
 
 int upload_profiles(vy_handle* h) {
-  std::vector<Profile> all(kMaxProfiles, Profile{1.0, 0.0, 0.0, 0.5, 0.5, 1.0, 2.0, 0.0});
+  std::vector<Profile> all(kMaxProfiles, Profile{1.0, 0.0, 0.0, 0.5, 0.5, 1.0, 2.0, 0.0, 0.0});
   for (size_t i = 0; i < h->profiles.size(); ++i) all[i] = h->profiles[i];
   VY_CUDA(cudaMemcpy(h->d_prof, all.data(), sizeof(Profile) * kMaxProfiles, cudaMemcpyHostToDevice));
   return VY_OK;
@@ -371,6 +371,8 @@ int vy_create(const vy_tables* t, int64_t batch, int device, vy_handle** out) {
   if ((int64_t)t->episode_steps + t->stay_hi > 32000 || t->stay_hi > 32000)
     return fail(VY_ERR_UNSUPPORTED, "stay / episode lengths exceed the int16 dwell-time state");
   if (t->n_days < 1 || t->lam_len < 1 || t->steps_per_day < 1) return fail(VY_ERR_ARG, "empty series");
+  if (t->dt_min < 1 || t->dt_min > 1440 || t->episode_steps < 1)
+    return fail(VY_ERR_ARG, "dt_min must be in [1, 1440] and episode_steps >= 1");
   vy_handle* h = new vy_handle();
   h->device = device;
   h->B = batch;
@@ -411,8 +413,10 @@ int vy_create(const vy_tables* t, int64_t batch, int device, vy_handle** out) {
     h->node_eta.push_back(t->node_eta[m]);
     h->node_order.push_back(t->node_order[m]);
   }
-  for (int c = 0; c < t->n_cat; ++c)
+  for (int c = 0; c < t->n_cat; ++c) {
     h->profiles.push_back(make_profile(t->cat_cap[c], t->cat_rac[c], t->cat_rdc[c], t->cat_tau[c]));
+    h->profiles.back().cum = t->cat_cum[c];
+  }
   // Poisson: per (weekday flag, step-of-profile) the number of full 32-chunks and the
   // threshold of the last chunk, reproducing rng.py:94-115 / _kernel.pyx:55-73 on the host.
   const int L = t->lam_len;

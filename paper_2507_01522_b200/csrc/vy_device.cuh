@@ -79,7 +79,8 @@ __device__ __forceinline__ double div_rcp(double x, double d, double y) {
 struct Profile {  // car profile: catalogue entry (or injected car)
   double cap, r_ac, r_dc, tau, omt;  // omt = 1.0 - tau, same rounding as the reference's runtime expression
   double rcp_cap, rcp_omt;           // RN(1/cap), RN(1/omt)
-  double pad[2];  // 72-byte stride: profiles 0..4 start in distinct bank pairs (per-lane lookups of different cars)
+  double cum;     // catalogue entries: cumulative sampling weight (data.py:112-114), read by the arrivals' car draw
+  double pad;     // 72-byte stride: profiles 0..4 start in distinct bank pairs (per-lane lookups of different cars)
 };
 
 // Byte offsets inside one warp's shared-memory tile (32 envs, lane = env).

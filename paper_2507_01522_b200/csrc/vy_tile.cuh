@@ -86,6 +86,7 @@ struct Prof {
   __device__ __forceinline__ double omt(int c) const { return at(c, 4); }
   __device__ __forceinline__ double rcp_cap(int c) const { return at(c, 5); }
   __device__ __forceinline__ double rcp_omt(int c) const { return at(c, 6); }
+  __device__ __forceinline__ double cum(int c) const { return at(c, 7); }
 };
 
 // Per-port constants staged in shared memory (one 96-byte record per port):
@@ -476,6 +477,16 @@ struct StepResult {
   bool done;
 };
 
+// eff_day = (day + t*dt_min // 1440) % n_days (_kernel.pyx:290) in 32-bit
+// integers (t*dt_min < 32000 * 1440: vy_create bounds the episode) with the
+// constant divisors strength-reduced; the runtime modulo only when the day
+// wraps (0 <= day < n_days)
+__device__ __forceinline__ int effective_day(const Params& P, int t, int day) {
+  int eff = day + t * P.dt_min / 1440;
+  if (eff >= P.n_days) eff %= P.n_days;
+  return eff;
+}
+
 // Exogenous inputs of the step at (step, day) (_kernel.pyx:289-295), loaded
 // before the tile's cp.async copies are awaited so their latency overlaps.
 struct Frame {
@@ -485,14 +496,13 @@ struct Frame {
 template <int M>
 __device__ __forceinline__ Frame load_frame(const Params& P, int t, int day) {
   Frame F;
-  const int64_t minutes = (int64_t)t * P.dt_min;
-  const int eff_day = (int)(((int64_t)day + minutes / 1440) % P.n_days);
-  F.hidx = eff_day * 24 + (int)((minutes / 60) % 24);
+  const int eff_day = effective_day(P, t, day);
+  F.hidx = eff_day * 24 + (t * P.dt_min / 60) % 24;
   F.p_buy = ldg_nc_f64(P.buy + F.hidx);
   F.p_sg = ldg_nc_f64(P.sellg + F.hidx);
   F.moer = Spec<M>::moer(P) ? ldg_nc_f64(P.moer + F.hidx) : 0.0;
   F.dgrid = Spec<M>::dgrid(P) ? ldg_nc_f64(P.dgrid + F.hidx) : 0.0;
-  F.lam_idx = (ldg_nc_s8(P.weekday + eff_day) ? 0 : P.lam_len) + t % P.lam_len;
+  F.lam_idx = (ldg_nc_s8(P.weekday + eff_day) ? 0 : P.lam_len) + (t < P.lam_len ? t : t % P.lam_len);
   F.pfull = ldg_nc_s32(P.pois_full + F.lam_idx);
   F.pthr = ldg_nc_f64(P.pois_thr + F.lam_idx);
   return F;
@@ -506,10 +516,9 @@ struct ObsGlobals {
 };
 __device__ __forceinline__ ObsGlobals load_obs_globals(const Params& P, int step, int day) {
   ObsGlobals G;
-  const int64_t minutes = (int64_t)step * P.dt_min;
-  const int eff_day = (int)(((int64_t)day + minutes / 1440) % P.n_days);
-  const int hidx = eff_day * 24 + (int)((minutes / 60) % 24);
-  const int sod = step % P.steps_per_day;
+  const int eff_day = effective_day(P, step, day);
+  const int hidx = eff_day * 24 + (step * P.dt_min / 60) % 24;
+  const int sod = step < P.steps_per_day ? step : step % P.steps_per_day;
   G.buy = ldg_nc_f64(P.buy + hidx);
   G.sellg = ldg_nc_f64(P.sellg + hidx);
   G.sinv = ldg_nc_f64(P.sin_t + sod);
@@ -868,7 +877,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
       const double u = unit(st);
       car = P.n_cat - 1;
       for (int e = 0; e < P.n_cat - 1; ++e)
-        if (u < __ldg(P.cat_cum + e)) {
+        if (u < prof.cum(e)) {
           car = e;
           break;
         }
