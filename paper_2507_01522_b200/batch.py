@@ -24,6 +24,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import platform
+import sys
 import time
 from dataclasses import dataclass
 
@@ -189,6 +190,7 @@ class BatchEnv:
         self._act_buf = None
         self._host_act = None
         self._pins: dict = {}
+        self._rings: dict = {}
         if env_seeds is None:
             self._seed_from_master(master_seed)
         else:
@@ -340,6 +342,13 @@ class BatchEnv:
         self._advance_clock()
         infos = self._build_infos() if collect_infos else None
         if host:
+            if self.obs_dtype == torch.float64:
+                # exact drop-in: D2H straight into pinned arrays handed to the caller
+                obs = self._ring_out("obs", self.outs.obs)
+                rew = self._ring_out("rew", self.outs.reward)
+                done = self._ring_out("done", self.outs.done, np.bool_)
+                self.check_errors()  # syncs the stream: the copies are complete
+                return obs, rew, done, infos
             pins = [self._pinned(n, t) for n, t in (("obs", self.outs.obs), ("rew", self.outs.reward),
                                                      ("done", self.outs.done))]
             self.check_errors()  # syncs the stream: the copies into the pinned buffers are complete
@@ -445,6 +454,30 @@ class BatchEnv:
         nat.check(rc, "vy_rollout")
         if self._t is not None:
             self._t = (self._t + T) % self.tables.episode_steps
+
+    def _ring_out(self, name: str, t: torch.Tensor, view=None, depth: int = 4) -> np.ndarray:
+        """Enqueue a D2H copy of `t` into a pinned host buffer and return it as
+        a numpy array the caller owns.  The reference returns fresh copies
+        (engine.py:463-464) so callers may keep them; buffers are drawn from a
+        small ring and one is reused only once nothing but the ring refers to
+        its array (a caller still holding the previous step's arrays keeps
+        them intact), so the steady state allocates nothing and the copy lands
+        at full DMA bandwidth with no second host pass."""
+        ring = self._rings.setdefault(name, [])
+        slot = None
+        for cand in ring:
+            # referents: the ring's list entry and getrefcount's argument
+            if sys.getrefcount(cand[1]) <= 2:
+                slot = cand
+                break
+        if slot is None:
+            pin = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            arr = pin.numpy() if view is None else pin.numpy().view(view)
+            slot = [pin, arr]
+            if len(ring) < depth:
+                ring.append(slot)
+        slot[0].copy_(t, non_blocking=True)
+        return slot[1]
 
     def _pinned(self, name: str, t: torch.Tensor) -> torch.Tensor:
         """Enqueue a D2H copy of `t` into a persistent pinned buffer (full DMA

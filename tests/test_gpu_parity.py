@@ -446,3 +446,28 @@ def test_injected_car_known_answers():
     assert infos[0].flows.e_net == pytest.approx(5.0 / 3.0, rel=1e-12)
     assert infos[0].flows.e_grid_in == pytest.approx((5.0 / 3.0) / 0.9, rel=1e-12)
     env.close()
+
+
+def test_numpy_outputs_are_owned_by_the_caller():
+    """The exact numpy path hands out pinned ring buffers: arrays a caller
+    keeps are never overwritten by later steps (reference semantics: fresh
+    copies, engine.py:463-464), and the steady state reuses the ring."""
+    fx = Fixture("c1_default")
+    env = make_env(fx, obs_dtype=torch.float64)
+    env.reset()
+    kept = []
+    for t in range(12):
+        obs, r, d, _ = env.step(fx["actions"][t], collect_infos=False)
+        kept.append((t, obs, r, d))
+    for t, obs, r, d in kept:
+        np.testing.assert_array_equal(obs, fx["obs"][t], err_msg=f"kept obs t={t}")
+        np.testing.assert_array_equal(r, fx["reward"][t])
+        np.testing.assert_array_equal(d.astype(np.int8), fx["done"][t])
+    kept.clear()
+    ids = set()
+    for t in range(12, 30):
+        obs, r, d, _ = env.step(fx["actions"][t], collect_infos=False)
+        np.testing.assert_array_equal(obs, fx["obs"][t], err_msg=f"t={t}")
+        ids.add(obs.ctypes.data)
+    assert len(ids) <= 4  # ring buffers, not a fresh allocation per step
+    env.close()
