@@ -8,6 +8,7 @@
 // _kernel.pyx:305), size the per-warp shared-memory tiles, and launch.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <cmath>
@@ -173,11 +174,16 @@ TileLayout tile_layout(const vy_tables& t, bool rollout, bool acts) {
   const int staging = 132 * t.obs_len;
   L.obs = 0;
   if (rollout) {
+    // f32 obs leave through the per-port chunk ring (ObsSink::chunk): two
+    // 6-column buffers, also holding the 9 + horizon tail columns
+    const int ring = std::max(2 * kChunkBuf, (9 + t.horizon) * kChunkCol * 4);
     L.obs = (off + 15) & ~15;
-    off = L.obs + staging;
+    off = L.obs + ring;
   } else if (off < staging) {
     off = staging;  // in-place staging may run past the state into the dwell/meta/action area
   }
+  L.bar = (off + 15) & ~15;
+  off = L.bar + 16;
   L.bytes = (off + 127) & ~127;
   return L;
 }

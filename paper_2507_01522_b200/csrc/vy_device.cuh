@@ -98,6 +98,7 @@ struct TileLayout {
   int ports;  // byte offset of port 0's float64 slots (port i at ports + i*768)
   int dtrem, meta, acts;
   int obs;    // byte offset of obs column 0 (0 in-place; `extra` area for rollouts)
+  int bar;    // byte offset of the warp's mbarrier (8 B) completing the tile's bulk copies
   int bytes;
 };
 

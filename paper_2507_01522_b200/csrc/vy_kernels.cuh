@@ -85,7 +85,7 @@ __device__ __forceinline__ void policy_row(const Params& P, uint32_t tile, int64
 // effects masked) because the fused port loop synchronises the warp.
 template <int M>
 __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const double* dtab, PortC pc, TreeC tc,
-                                          uint32_t tile, int64_t b0, int lane,
+                                          uint32_t tile, int64_t b0, int lane, WarpBar& wb,
                                           unsigned long long* claim = nullptr, int64_t pol_call = 0) {
   using C = Spec<M>;
   const Lane T = make_lane(P, tile, lane);
@@ -98,14 +98,14 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
   // occupies.  At night most ports are empty in every lane and are neither
   // read nor written (-12% step time); at the afternoon peak every port is
   // occupied somewhere and the extra round trip costs ~3% (day average -1.5%).
-  tile_issue_meta(P, tile, b0, lane, C::staged(P) && !P.policy);
+  tile_issue_meta(P, tile, b0, lane, C::staged(P) && !P.policy, wb);
   // exogenous inputs for this step and the obs globals of the next one, in
   // flight together with the tile copies
   const Frame F = load_frame<M>(P, E.step, E.day);
   const ObsGlobals G = load_obs_globals(P, E.step + 1, E.day);
-  const uint64_t occ_ports = tile_issue_ports(P, tile, b0, lane);
+  const uint64_t occ_ports = tile_issue_ports(P, tile, b0, lane, wb);
   if (P.policy) policy_row(P, tile, b0, lane, pol_call);  // ALU work under the copies' latency
-  tile_wait();
+  tile_wait(wb);
   const ObsSink S = make_sink<M>(P, T, b, P.out.obs, /*in_place=*/true);
   const int dt = P.act_dtype;
   const int64_t rs = P.act_row, cs = P.act_col;
@@ -169,12 +169,13 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
   // launch is graph-replayed (advanced below by the last warp to finish, after
   // every warp has read it)
   const int64_t pol_call = P.policy ? P.pol_call + (P.pol_counter ? *(volatile int64_t*)P.pol_counter : 0) : 0;
+  WarpBar wb = warp_bar_init(P, toff, lane);
   unsigned long long nxt = 0;  // lane 0: this warp's next tile (claimed inside step_tile)
   if (lane == 0) nxt = atomicAdd(P.tile_ctr, 1ull);
   for (;;) {
     const unsigned long long t = __shfl_sync(0xffffffffu, nxt, 0);
     if (t >= ntiles) break;
-    step_tile<M>(P, prof, dtab, pc, tc, toff, (int64_t)t * 32, lane, &nxt, pol_call);
+    step_tile<M>(P, prof, dtab, pc, tc, toff, (int64_t)t * 32, lane, wb, &nxt, pol_call);
     __syncwarp();
   }
   if (lane == 0) {
@@ -205,8 +206,9 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
   const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
-  tile_issue(P, tile, b0, lane, false);
-  tile_wait();
+  WarpBar wb = warp_bar_init(P, tile, lane);
+  tile_issue(P, tile, b0, lane, false, wb);
+  tile_wait(wb);
   EnvRegs E{};  // zero for padding lanes so the obs path stays in bounds
   uint64_t pkey = 0, seed = 0;
   int episode = 0;
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
   for (int t = 0; t < T_steps; ++t) {
     void* obs_t = f64 ? (void*)(reinterpret_cast<double*>(P.out.obs) + t * obs_stride)
                       : (void*)(reinterpret_cast<float*>(P.out.obs) + t * obs_stride);
-    const ObsSink S = make_sink<M>(P, T, b, obs_t, /*in_place=*/false);
+    const ObsSink S = make_chunk_sink<M>(P, T, b0, obs_t);
     const uint64_t j0 = (uint64_t)(call0 + t) * (uint64_t)ns;
     auto act = [&](int slot) -> int { return policy_action(pkey, j0 + slot + 1, hi); };
     const Frame F = load_frame<M>(P, E.step, E.day);
@@ -230,7 +232,16 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
       ++episode;
       reset_scalars(P, E, seed, episode, 0, false);
       clear_tile_ports(P, T);
-      for (int i = 0; i < P.n_ports; ++i) stage_port_obs(P, prof, S, lane, active, i, 0u, 0.0, 0.0, 0.0, 0, 1.0, 1.0);
+      if (!S.chunk)
+        for (int i = 0; i < P.n_ports; ++i) stage_port_obs(P, prof, S, lane, active, i, 0u, 0.0, 0.0, 0.0, 0, 1.0, 1.0);
+    }
+    if (S.chunk) {
+      // the reset obs of every env that just finished: all port columns +0
+      const uint32_t dm = __ballot_sync(0xffffffffu, r.done);
+      if (dm) {
+        __syncwarp();  // after this step's port read-outs and arrival rows
+        for (int i = 0; i < P.n_ports; ++i) chunk_zero6(P, S, lane, 6 * i, dm);
+      }
     }
     if (active) {
       if (f64)
@@ -264,8 +275,9 @@ __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P,
   const int64_t b = b0 + lane;
   const bool active = b < P.B;
   // masked-out envs keep their state: stage the tile so the write-back is a no-op for them
-  tile_issue(P, tile, b0, lane, false);
-  tile_wait();
+  WarpBar wb = warp_bar_init(P, tile, lane);
+  tile_issue(P, tile, b0, lane, false, wb);
+  tile_wait(wb);
   const bool mine = active && (!mask || mask[b]);
   EnvRegs E{};  // zero for padding lanes so the obs path stays in bounds
   if (active) load_env<0>(P, b, E);

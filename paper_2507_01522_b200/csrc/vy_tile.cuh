@@ -197,45 +197,111 @@ __device__ __forceinline__ Lane make_lane(const Params& P, uint32_t tile, int la
               reinterpret_cast<int16_t*>(b + P.L.dtrem + lane * 2), b + P.L.meta + lane, lane, &P.L};
 }
 
-__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
+// ---- tile stage-in: bulk copies (TMA engine) completing on a per-warp mbarrier ----
+//
+// Each (field, port) column of a 32-env tile is one contiguous, aligned run
+// in the port-major global layout (256 B of float64, 64 B of int16 dwell, 32
+// B of meta), and the tile's uint8 action rows are one contiguous block.  A
+// lane issues whole columns as cp.async.bulk copies (one instruction per
+// column instead of one 16-byte cp.async per lane and chunk, no per-lane
+// address math); they complete on the warp's mbarrier with the expected byte
+// count armed by lane 0, and the warp waits on the barrier's phase.
+__device__ __forceinline__ void mbar_init(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "VY_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra VY_WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void* gsrc, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(sdst),
+               "l"(gsrc), "r"(bytes), "r"(bar)
+               : "memory");
+}
+// generic-proxy accesses of this thread to shared memory are ordered before
+// later async-proxy (bulk copy) accesses
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// The step kernel's two-stage load keeps 16-byte cp.async copies: issuing the
+// same columns as bulk copies measured slower on B200 (2^20 envs, mid-day
+// window: +5% step time for the meta stage as bulk copies, +8.5% for the
+// port slots — 32-256 byte copies, ~80 per tile; scripts/ab_roll.sh,
+// profiles/r2_bulk_ab.txt).  Rollout and reset kernels load their tile once
+// with bulk copies.  -DVY_BULK_META=1 / -DVY_BULK_SLOTS=1 select the bulk variants.
+#ifndef VY_BULK_META
+#define VY_BULK_META 0
+#endif
+#ifndef VY_BULK_SLOTS
+#define VY_BULK_SLOTS 0
+#endif
+__device__ __forceinline__ void cp_async16(uint32_t sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n" ::: "memory");
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
-// Warp-cooperative stage-in of a tile (HBM -> smem).  Each (field, port)
-// column of 32 envs is one contiguous run in the port-major global layout;
-// lanes copy 16 B each.  The uint8 action block of the 32 envs is contiguous
-// too (row-major [B][n+1]).
-__device__ __forceinline__ void tile_issue(const Params& P, uint32_t toff, int64_t b0, int lane, bool with_acts) {
-  unsigned char* t = vy_smem + toff;
+// The warp's barrier: shared address and the parity of its next phase.
+struct WarpBar {
+  uint32_t a;
+  uint32_t phase;
+  bool armed;  // a stage is in flight (tile_wait waits for it)
+};
+__device__ __forceinline__ WarpBar warp_bar_init(const Params& P, uint32_t toff, int lane) {
+  WarpBar wb{smem_base() + toff + (uint32_t)P.L.bar, 0u, false};
+  if (lane == 0) {
+    mbar_init(wb.a);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  return wb;
+}
+__device__ __forceinline__ void bar_wait(WarpBar& wb) {
+  if (wb.armed) {
+    mbar_wait(wb.a, wb.phase);
+    wb.phase ^= 1u;
+    wb.armed = false;
+  }
+}
+
+// the n port columns of every field plus the action rows (rollout / reset: one stage)
+__device__ __forceinline__ void tile_issue(const Params& P, uint32_t toff, int64_t b0, int lane, bool with_acts,
+                                           WarpBar& wb) {
+  const uint32_t t = smem_base() + toff;
   const int n = P.n_ports;
   const int64_t ld = P.ld;
   const TileLayout& L = P.L;
-  const int q16 = (lane & 15) * 16;
-  for (int i = lane >> 4; i < n; i += 2) {
-    const int64_t g = ((int64_t)i * ld + b0) * 8 + q16;
-    unsigned char* d = t + L.ports + i * 768 + q16;
-    cp_async16(d, reinterpret_cast<const char*>(P.st.port_i) + g);
-    cp_async16(d + 256, reinterpret_cast<const char*>(P.st.port_soc) + g);
-    cp_async16(d + 512, reinterpret_cast<const char*>(P.st.port_de) + g);
+  fence_async_smem();
+  __syncwarp();
+  const uint32_t abytes = with_acts ? 32u * (uint32_t)(n + 1) : 0u;
+  if (lane == 0) mbar_expect_tx(wb.a, (uint32_t)n * (768u + 64u + 32u) + abytes);
+  for (int i = lane >> 1; i < n; i += 16) {
+    const int64_t e = (int64_t)i * ld + b0;
+    const uint32_t s = t + L.ports + i * 768;
+    if (lane & 1) {
+      bulk_g2s(s, P.st.port_i + e, 256, wb.a);
+      bulk_g2s(s + 256, P.st.port_soc + e, 256, wb.a);
+    } else {
+      bulk_g2s(s + 512, P.st.port_de + e, 256, wb.a);
+      bulk_g2s(t + L.dtrem + i * 64, P.st.port_dtrem + e, 64, wb.a);
+      bulk_g2s(t + L.meta + i * 32, P.st.port_meta + e, 32, wb.a);
+    }
   }
-  const char* dsrc = reinterpret_cast<const char*>(P.st.port_dtrem);
-  for (int c = lane >> 2; c < n; c += 8)
-    cp_async16(t + L.dtrem + c * 64 + (lane & 3) * 16, dsrc + ((int64_t)c * ld + b0) * 2 + (lane & 3) * 16);
-  const char* msrc = reinterpret_cast<const char*>(P.st.port_meta);
-  for (int c = lane >> 1; c < n; c += 16)
-    cp_async16(t + L.meta + c * 32 + (lane & 1) * 16, msrc + ((int64_t)c * ld + b0) + (lane & 1) * 16);
-  if (with_acts) {
-    // 32 rows x (n+1) bytes; the host guarantees a 16-byte aligned block and
-    // that reading whole 16-byte chunks past B stays inside the allocation
-    const int bytes = 32 * (n + 1);
-    const char* asrc = reinterpret_cast<const char*>(P.actions) + b0 * (n + 1);
-    for (int o = lane * 16; o < bytes; o += 512) cp_async16(t + L.acts + o, asrc + o);
-  }
+  // 32 rows x (n+1) bytes; the host guarantees a 16-byte aligned block and
+  // that reading the whole block of a ragged last tile stays inside the allocation
+  if (with_acts && lane == 31)
+    bulk_g2s(t + L.acts, reinterpret_cast<const uint8_t*>(P.actions) + b0 * (n + 1), abytes, wb.a);
+  wb.armed = true;
 }
 
 // Two-stage tile load (step kernel): the meta bytes (and action rows) first;
@@ -244,20 +310,30 @@ __device__ __forceinline__ void tile_issue(const Params& P, uint32_t toff, int64
 // in every lane is never read (its slots are not used: phase 1 zeroes its
 // current slot, phase 2 stages +0 obs and does not store it).
 __device__ __forceinline__ void tile_issue_meta(const Params& P, uint32_t toff, int64_t b0, int lane,
-                                                bool with_acts) {
-  unsigned char* t = vy_smem + toff;
+                                                bool with_acts, WarpBar& wb) {
+  const uint32_t t = smem_base() + toff;
   const int n = P.n_ports;
   const int64_t ld = P.ld;
   const TileLayout& L = P.L;
+  fence_async_smem();
+  __syncwarp();
+  const uint32_t abytes = with_acts ? 32u * (uint32_t)(n + 1) : 0u;
+#if VY_BULK_META
+  if (lane == 0) mbar_expect_tx(wb.a, 32u * (uint32_t)n + abytes);
+  for (int c = lane; c < n; c += 32) bulk_g2s(t + L.meta + c * 32, P.st.port_meta + (int64_t)c * ld + b0, 32, wb.a);
+  if (with_acts && lane == 31)
+    bulk_g2s(t + L.acts, reinterpret_cast<const uint8_t*>(P.actions) + b0 * (n + 1), abytes, wb.a);
+  wb.armed = true;
+#else
   const char* msrc = reinterpret_cast<const char*>(P.st.port_meta);
   for (int c = lane >> 1; c < n; c += 16)
     cp_async16(t + L.meta + c * 32 + (lane & 1) * 16, msrc + ((int64_t)c * ld + b0) + (lane & 1) * 16);
   if (with_acts) {
-    const int bytes = 32 * (n + 1);
     const char* asrc = reinterpret_cast<const char*>(P.actions) + b0 * (n + 1);
-    for (int o = lane * 16; o < bytes; o += 512) cp_async16(t + L.acts + o, asrc + o);
+    for (int o = lane * 16; o < (int)abytes; o += 512) cp_async16(t + L.acts + o, asrc + o);
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
+#endif
 }
 
 // warp-uniform mask of the ports any env of the tile occupies (meta staged):
@@ -280,19 +356,25 @@ __device__ __forceinline__ uint64_t occupied_ports(const Params& P, uint32_t tof
 
 // after tile_issue_meta: wait for the meta bytes, vote the occupied ports and
 // issue their slot copies; returns the warp-uniform port mask
-__device__ __forceinline__ uint64_t tile_issue_ports(const Params& P, uint32_t toff, int64_t b0, int lane) {
+__device__ __forceinline__ uint64_t tile_issue_ports(const Params& P, uint32_t toff, int64_t b0, int lane,
+                                                     WarpBar& wb) {
+#if VY_BULK_META
+  bar_wait(wb);
+#else
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncwarp();
-  unsigned char* t = vy_smem + toff;
+#endif
+  const uint32_t t = smem_base() + toff;
   const int n = P.n_ports;
   const int64_t ld = P.ld;
   const TileLayout& L = P.L;
   const uint64_t mask = occupied_ports(P, toff, lane);
+#if !VY_BULK_SLOTS
   const int q16 = (lane & 15) * 16;
   for (int i = lane >> 4; i < n; i += 2) {
     if (!((mask >> i) & 1ull)) continue;
     const int64_t g = ((int64_t)i * ld + b0) * 8 + q16;
-    unsigned char* d = t + L.ports + i * 768 + q16;
+    const uint32_t d = t + L.ports + i * 768 + q16;
     cp_async16(d, reinterpret_cast<const char*>(P.st.port_i) + g);
     cp_async16(d + 256, reinterpret_cast<const char*>(P.st.port_soc) + g);
     cp_async16(d + 512, reinterpret_cast<const char*>(P.st.port_de) + g);
@@ -301,12 +383,34 @@ __device__ __forceinline__ uint64_t tile_issue_ports(const Params& P, uint32_t t
   for (int c = lane >> 2; c < n; c += 8)
     if ((mask >> c) & 1ull)
       cp_async16(t + L.dtrem + c * 64 + (lane & 3) * 16, dsrc + ((int64_t)c * ld + b0) * 2 + (lane & 3) * 16);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  return mask;
+#endif
+  if (mask) {
+    if (lane == 0) mbar_expect_tx(wb.a, (uint32_t)__popcll(mask) * (768u + 64u));
+    for (int i = lane >> 1; i < n; i += 16) {
+      if (!((mask >> i) & 1ull)) continue;
+      const int64_t e = (int64_t)i * ld + b0;
+      const uint32_t s = t + L.ports + i * 768;
+      if (lane & 1) {
+        bulk_g2s(s, P.st.port_i + e, 256, wb.a);
+        bulk_g2s(s + 256, P.st.port_soc + e, 256, wb.a);
+      } else {
+        bulk_g2s(s + 512, P.st.port_de + e, 256, wb.a);
+        bulk_g2s(t + L.dtrem + i * 64, P.st.port_dtrem + e, 64, wb.a);
+      }
+    }
+    wb.armed = true;
+  }
   return mask;
 }
 
-__device__ __forceinline__ void tile_wait() {
+__device__ __forceinline__ void tile_wait(WarpBar& wb) {
+  bar_wait(wb);
+#if !VY_BULK_SLOTS || !VY_BULK_META
   cp_async_wait_all();
   __syncwarp();
+#endif
 }
 
 template <int M>
@@ -541,11 +645,54 @@ struct ObsSink {
   uint32_t cells;
   double* row64;
   bool in_place;
+  // Rollout ("chunk") mode: no whole-tile staging area.  Each port's six
+  // columns go through a two-port ring of 6-column buffers (column stride
+  // kChunkCol words) and leave right away: lane l stores column l % 6 of rows
+  // l / 6 + 5k (k = 0..6), 24-byte row segments the L2 merges into whole
+  // sectors.  The smem a tile needs drops from 132 * obs_len bytes to
+  // 2 * 6 * 4 * kChunkCol, so more warps fit per SM.
+  bool chunk;
+  float* gtile;  // chunk: f32 obs row 0 of the tile
+  int rows;      // chunk: live rows of the tile
+  int rf, rr;    // chunk: this lane's read-out column (l % 6) and first row (l / 6)
 };
+// column stride of the chunk buffers in 4-byte words: 37 = 5 mod 32, so the
+// read-out's (column f, row r) words 37f + r hit distinct banks for f < 6, r < 5
+constexpr int kChunkCol = 37;
+constexpr int kChunkBuf = 6 * kChunkCol * 4;  // bytes per 6-column buffer
+
+// chunk mode: coalesced read-out of 6 staged columns (buffer `buf`) into
+// global obs columns [c0, c0 + 6) of the tile's rows; `rowmask` selects rows
+__device__ __forceinline__ void chunk_out6(const Params& P, const ObsSink& S, int lane, uint32_t buf, int c0,
+                                           uint32_t rowmask = 0xffffffffu) {
+  if (lane < 30) {
+    const int OL = P.obs_len;
+    float* g = S.gtile + (int64_t)S.rr * OL + c0 + S.rf;
+    const uint32_t a = buf + S.rf * (kChunkCol * 4) + S.rr * 4;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+      const int r = S.rr + 5 * k;
+      if (r < S.rows && ((rowmask >> r) & 1u)) __stcs(g + 5 * k * OL, lds_f32(a + 20 * k));
+    }
+  }
+}
+// chunk mode: +0 into obs columns [c0, c0 + 6) of the rows in `rowmask`
+__device__ __forceinline__ void chunk_zero6(const Params& P, const ObsSink& S, int lane, int c0,
+                                            uint32_t rowmask = 0xffffffffu) {
+  if (lane < 30) {
+    const int OL = P.obs_len;
+    float* g = S.gtile + (int64_t)S.rr * OL + c0 + S.rf;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+      const int r = S.rr + 5 * k;
+      if (r < S.rows && ((rowmask >> r) & 1u)) __stcs(g + 5 * k * OL, 0.0f);
+    }
+  }
+}
 
 __device__ __forceinline__ void stage_port_obs(const Params& P, Prof prof, const ObsSink& S, int lane,
                                                bool active, int i, uint32_t mt, double idr, double soc, double de,
-                                               int dt, double i_denom, double rcp_i_denom) {
+                                               int dt, double i_denom, double rcp_i_denom, bool own_row = false) {
   const bool occ = mt & 1u;
   double v[6];
   v[0] = occ ? 1.0 : 0.0;
@@ -559,6 +706,18 @@ __device__ __forceinline__ void stage_port_obs(const Params& P, Prof prof, const
     if (active)
 #pragma unroll
       for (int f = 0; f < 6; ++f) S.row64[6 * i + f] = v[f];
+  } else if (S.chunk) {
+    if (own_row) {  // a single lane's port (arrivals): its own row, directly
+      if (active)
+#pragma unroll
+        for (int f = 0; f < 6; ++f) S.gtile[(int64_t)lane * P.obs_len + 6 * i + f] = (float)v[f];
+    } else {
+      const uint32_t buf = S.cells + (i & 1) * kChunkBuf;
+#pragma unroll
+      for (int f = 0; f < 6; ++f) sts_f32(buf + f * (kChunkCol * 4) + lane * 4, (float)v[f]);
+      __syncwarp();  // also orders the read-out of port i - 1 (other buffer) before port i + 1 reuses it
+      chunk_out6(P, S, lane, buf, 6 * i);
+    }
   } else {
     const uint32_t col = S.cells + 6 * i * 132 + lane * 4;
 #pragma unroll
@@ -571,11 +730,13 @@ __device__ __forceinline__ void stage_port_obs(const Params& P, Prof prof, const
 }
 
 // the six obs columns of a port that is empty (all-zero state): +0
-__device__ __forceinline__ void stage_zero_obs(const ObsSink& S, int lane, bool active, int i) {
+__device__ __forceinline__ void stage_zero_obs(const Params& P, const ObsSink& S, int lane, bool active, int i) {
   if (S.row64) {
     if (active)
 #pragma unroll
       for (int f = 0; f < 6; ++f) S.row64[6 * i + f] = 0.0;
+  } else if (S.chunk) {
+    chunk_zero6(P, S, lane, 6 * i);
   } else {
     const uint32_t col = S.cells + 6 * i * 132 + lane * 4;
 #pragma unroll
@@ -816,9 +977,10 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
       // HBM copy already holds this state, so it is not rewritten, and its
       // six obs columns are +0.  Arrivals below store the ports they fill.
       if (S.in_place) __syncwarp();  // every lane has read port i before its slots take obs columns
-      stage_zero_obs(S, T.lane, active, i);
+      stage_zero_obs(P, S, T.lane, active, i);
     }
   }
+  if (S.chunk) __syncwarp();  // the ports' read-outs land before arrivals rewrite their own rows
   double e_b = 0.0, bgot = 0.0;
   if (battery) {
     bgot = div_rcp(P.b_dtv * E.b_i, 1000.0, P.rcp_1000);
@@ -910,7 +1072,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
       T.dtrem(port) = (int16_t)stay;
     }
     // a new car draws no current yet: I / i_denom = 0 for any denominator
-    stage_port_obs(P, prof, S, T.lane, active, port, mt, 0.0, soc0, de0, stay, 1.0, 1.0);
+    stage_port_obs(P, prof, S, T.lane, active, port, mt, 0.0, soc0, de0, stay, 1.0, 1.0, /*own_row=*/true);
   }
   E.ep_declined += declined;
   if (info) {
@@ -975,7 +1137,6 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
 
 // ---- observation (_kernel.pyx:575-607; layout config.py:99-130) ----------------
 
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_s2g(void* gdst, uint32_t soff, uint32_t bytes) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(vy_smem + soff);
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(s), "r"(bytes)
@@ -1018,6 +1179,26 @@ __device__ __forceinline__ ObsSink make_sink(const Params& P, const Lane& T, int
   S.cells = smem_base() + T.t + P.L.obs;
   S.row64 = Spec<M>::f64(P) ? reinterpret_cast<double*>(obs_base) + b * P.obs_len : nullptr;
   S.in_place = in_place;
+  S.chunk = false;
+  S.gtile = nullptr;
+  S.rows = 0;
+  S.rf = S.rr = 0;
+  return S;
+}
+
+// rollout sink: f32 obs through the per-port chunk ring (ObsSink::chunk), or
+// f64 rows directly
+template <int M>
+__device__ __forceinline__ ObsSink make_chunk_sink(const Params& P, const Lane& T, int64_t b0, void* obs_base) {
+  ObsSink S = make_sink<M>(P, T, b0 + T.lane, obs_base, /*in_place=*/false);
+  if (!S.row64) {
+    S.chunk = true;
+    S.gtile = reinterpret_cast<float*>(obs_base) + b0 * P.obs_len;
+    const int64_t left = P.B - b0;
+    S.rows = left >= 32 ? 32 : (int)left;
+    S.rf = T.lane % 6;
+    S.rr = T.lane / 6;
+  }
   return S;
 }
 
@@ -1041,25 +1222,50 @@ __device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const 
   gv[7] = G.wk;
   gv[8] = G.dayf;
   const int c0 = 6 * n;
+  // chunk mode: the tail columns are staged from column 0 of the chunk ring
+  // (stride kChunkCol words) once every lane's earlier read-outs are done
+  if (S.chunk) __syncwarp();
+  const uint32_t tcell = S.chunk ? S.cells + lane * 4 : S.cells + c0 * 132 + lane * 4;
+  const uint32_t tstride = S.chunk ? kChunkCol * 4 : 132;
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
     if (S.row64) {
       if (active) S.row64[c0 + k] = gv[k];
     } else {
-      sts_f32(S.cells + (c0 + k) * 132 + lane * 4, (float)gv[k]);
+      sts_f32(tcell + k * tstride, (float)gv[k]);
     }
   }
-  for (int h = 0; h < Spec<M>::horizon(P); ++h) {
+  const int H = Spec<M>::horizon(P);
+  for (int h = 0; h < H; ++h) {
     const int64_t fmin = (int64_t)(E.step + 1 + h) * P.dt_min;
     const int64_t fday = ((int64_t)E.day + fmin / 1440) % P.n_days;
     const double v = __ldg(P.buy + fday * 24 + (fmin / 60) % 24);
     if (S.row64) {
       if (active) S.row64[c0 + 9 + h] = v;
     } else {
-      sts_f32(S.cells + (c0 + 9 + h) * 132 + lane * 4, (float)v);
+      sts_f32(tcell + (9 + h) * tstride, (float)v);
     }
   }
   if (S.row64) return;
+  if (S.chunk) {
+    // columns [c0, OL) of every row: lane l takes column l % C of rows l / C + k * (32 / C)
+    __syncwarp();
+    const int C = 9 + H;
+    const uint32_t base = S.cells;
+    if (C <= 32) {
+      const int per = 32 / C;
+      if (lane < per * C) {
+        const int f = lane % C;
+        for (int r = lane / C; r < S.rows; r += per)
+          __stcs(S.gtile + (int64_t)r * OL + c0 + f, lds_f32(base + f * (kChunkCol * 4) + r * 4));
+      }
+    } else {
+      for (int f = 0; f < C; ++f)
+        if (lane < S.rows) __stcs(S.gtile + (int64_t)lane * OL + c0 + f, lds_f32(base + f * (kChunkCol * 4) + lane * 4));
+    }
+    __syncwarp();  // read-out done before the next step stages into the ring
+    return;
+  }
   __syncwarp();
   if (Spec<M>::probe(P, 0x400u)) return;  // probe: no obs stores
   // Row-major read-out: row r, column c = lane + 32 j lives at

@@ -212,6 +212,45 @@ def test_rollout_kernel_equals_stepwise():
     b.close()
 
 
+@pytest.mark.parametrize("horizon,obs_dtype", [(6, "f32"), (30, "f32"), (4, "f64")])
+def test_rollout_generic_horizon_equals_stepwise(horizon, obs_dtype):
+    """The generic rollout kernel (price horizon: obs tail of 9 + H columns,
+    wider than the per-port chunk ring for H > 3, and beyond one warp for
+    H > 23; f64 obs written per lane) equals single steps over an episode
+    boundary, ragged last tile included."""
+    from paper_2507_01522_b200 import EnvConfig, default_setup
+    from paper_2507_01522_b200.batch import BatchEnv, DeviceRandomPolicy
+
+    rc = default_setup()
+    cfg = EnvConfig(observe_price_horizon=horizon)
+    dt = torch.float64 if obs_dtype == "f64" else torch.float32
+    B, T = 1000, 300
+    a = BatchEnv(cfg, rc.station, rc.dataset, batch_size=B, master_seed=2, obs_dtype=dt)
+    b = BatchEnv(cfg, rc.station, rc.dataset, batch_size=B, master_seed=2, obs_dtype=dt)
+    a.reset(as_numpy=False)
+    b.reset(as_numpy=False)
+    pol = DeviceRandomPolicy(3, a.n_ports, cfg.discretization_k)
+    pol.bind(range(B))
+    obs_s, rew_s, done_s = [], [], []
+    for _ in range(T):
+        o, r, d, _ = a.step(pol.actions(a), collect_infos=False)
+        obs_s.append(o.clone())
+        rew_s.append(r.clone())
+        done_s.append(d.clone())
+    obs_r = torch.empty(T, B, b.obs_length, device="cuda", dtype=dt)
+    rew_r = torch.empty(T, B, device="cuda", dtype=dt)
+    done_r = torch.empty(T, B, dtype=torch.uint8, device="cuda")
+    b.rollout(T, 3, 0, obs_r, rew_r, done_r)
+    torch.testing.assert_close(obs_r, torch.stack(obs_s), rtol=0, atol=0)
+    torch.testing.assert_close(rew_r, torch.stack(rew_s), rtol=0, atol=0)
+    torch.testing.assert_close(done_r, torch.stack(done_s), rtol=0, atol=0)
+    sa, sb = a.reference_state(), b.reference_state()
+    for k in STATE_KEYS:
+        np.testing.assert_array_equal(sa[k], sb[k], err_msg=k)
+    a.close()
+    b.close()
+
+
 def test_rollout_equals_stepwise_large_tree_lean():
     """Lean instantiations for a large capacity tree (mode 2, nested splitters):
     the fused rollout equals single steps, and a scattered subset of the
