@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
       const uint32_t dm = __ballot_sync(0xffffffffu, r.done);
       if (dm) {
         __syncwarp();  // after this step's port read-outs and arrival rows
-        for (int i = 0; i < P.n_ports; ++i) chunk_zero6(P, S, lane, 6 * i, dm);
+        for (int i = 0; i < P.n_ports; ++i) chunk_zero6(S, lane, i, dm);
       }
     }
     if (active) {

@@ -653,40 +653,49 @@ struct ObsSink {
   // 2 * 6 * 4 * kChunkCol, so more warps fit per SM.
   bool chunk;
   float* gtile;  // chunk: f32 obs row 0 of the tile
+  float* glane;  // chunk: this lane's read-out cell of port 0: row l / 6, column l % 6
+  uint32_t soff; // chunk: byte offset of that cell in a ring buffer
+  int s5;        // chunk: 5 * obs_len (5 rows per read-out pass)
   int rows;      // chunk: live rows of the tile
-  int rf, rr;    // chunk: this lane's read-out column (l % 6) and first row (l / 6)
 };
 // column stride of the chunk buffers in 4-byte words: 37 = 5 mod 32, so the
 // read-out's (column f, row r) words 37f + r hit distinct banks for f < 6, r < 5
 constexpr int kChunkCol = 37;
 constexpr int kChunkBuf = 6 * kChunkCol * 4;  // bytes per 6-column buffer
 
-// chunk mode: coalesced read-out of 6 staged columns (buffer `buf`) into
-// global obs columns [c0, c0 + 6) of the tile's rows; `rowmask` selects rows
-__device__ __forceinline__ void chunk_out6(const Params& P, const ObsSink& S, int lane, uint32_t buf, int c0,
-                                           uint32_t rowmask = 0xffffffffu) {
-  if (lane < 30) {
-    const int OL = P.obs_len;
-    float* g = S.gtile + (int64_t)S.rr * OL + c0 + S.rf;
-    const uint32_t a = buf + S.rf * (kChunkCol * 4) + S.rr * 4;
+// chunk mode: coalesced read-out of port i's 6 staged columns (ring buffer
+// `buf`) into global obs columns [6i, 6i + 6): lanes 0..29 store rows l / 6 +
+// 5k, column l % 6 (k = 0..6; rows 30, 31 by lanes 0..11)
+__device__ __forceinline__ void chunk_out6(const ObsSink& S, int lane, uint32_t buf, int i) {
+  if (lane >= 30) return;
+  float* g = S.glane + 6 * i;
+  const uint32_t a = buf + S.soff;
+  if (S.rows == 32) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      __stcs(g, lds_f32(a + 20 * k));
+      g += S.s5;
+    }
+    if (lane < 12) __stcs(g, lds_f32(a + 120));
+  } else {
+    const int r0 = lane / 6;
 #pragma unroll
     for (int k = 0; k < 7; ++k) {
-      const int r = S.rr + 5 * k;
-      if (r < S.rows && ((rowmask >> r) & 1u)) __stcs(g + 5 * k * OL, lds_f32(a + 20 * k));
+      if (r0 + 5 * k < S.rows) __stcs(g, lds_f32(a + 20 * k));
+      g += S.s5;
     }
   }
 }
-// chunk mode: +0 into obs columns [c0, c0 + 6) of the rows in `rowmask`
-__device__ __forceinline__ void chunk_zero6(const Params& P, const ObsSink& S, int lane, int c0,
-                                            uint32_t rowmask = 0xffffffffu) {
-  if (lane < 30) {
-    const int OL = P.obs_len;
-    float* g = S.gtile + (int64_t)S.rr * OL + c0 + S.rf;
+// chunk mode: +0 into port i's obs columns of the rows in `rowmask`
+__device__ __forceinline__ void chunk_zero6(const ObsSink& S, int lane, int i, uint32_t rowmask) {
+  if (lane >= 30) return;
+  float* g = S.glane + 6 * i;
+  const int r0 = lane / 6;
 #pragma unroll
-    for (int k = 0; k < 7; ++k) {
-      const int r = S.rr + 5 * k;
-      if (r < S.rows && ((rowmask >> r) & 1u)) __stcs(g + 5 * k * OL, 0.0f);
-    }
+  for (int k = 0; k < 7; ++k) {
+    const int r = r0 + 5 * k;
+    if (r < S.rows && ((rowmask >> r) & 1u)) __stcs(g, 0.0f);
+    g += S.s5;
   }
 }
 
@@ -716,7 +725,7 @@ __device__ __forceinline__ void stage_port_obs(const Params& P, Prof prof, const
 #pragma unroll
       for (int f = 0; f < 6; ++f) sts_f32(buf + f * (kChunkCol * 4) + lane * 4, (float)v[f]);
       __syncwarp();  // also orders the read-out of port i - 1 (other buffer) before port i + 1 reuses it
-      chunk_out6(P, S, lane, buf, 6 * i);
+      chunk_out6(S, lane, buf, i);
     }
   } else {
     const uint32_t col = S.cells + 6 * i * 132 + lane * 4;
@@ -736,7 +745,7 @@ __device__ __forceinline__ void stage_zero_obs(const Params& P, const ObsSink& S
 #pragma unroll
       for (int f = 0; f < 6; ++f) S.row64[6 * i + f] = 0.0;
   } else if (S.chunk) {
-    chunk_zero6(P, S, lane, 6 * i);
+    chunk_zero6(S, lane, i, 0xffffffffu);
   } else {
     const uint32_t col = S.cells + 6 * i * 132 + lane * 4;
 #pragma unroll
@@ -1181,8 +1190,10 @@ __device__ __forceinline__ ObsSink make_sink(const Params& P, const Lane& T, int
   S.in_place = in_place;
   S.chunk = false;
   S.gtile = nullptr;
+  S.glane = nullptr;
+  S.soff = 0;
+  S.s5 = 0;
   S.rows = 0;
-  S.rf = S.rr = 0;
   return S;
 }
 
@@ -1196,8 +1207,10 @@ __device__ __forceinline__ ObsSink make_chunk_sink(const Params& P, const Lane& 
     S.gtile = reinterpret_cast<float*>(obs_base) + b0 * P.obs_len;
     const int64_t left = P.B - b0;
     S.rows = left >= 32 ? 32 : (int)left;
-    S.rf = T.lane % 6;
-    S.rr = T.lane / 6;
+    const int rf = T.lane % 6, rr = T.lane / 6;
+    S.glane = S.gtile + rr * P.obs_len + rf;
+    S.soff = (uint32_t)(rf * (kChunkCol * 4) + rr * 4);
+    S.s5 = 5 * P.obs_len;
   }
   return S;
 }
