@@ -245,6 +245,27 @@ int32_t vy_last_step_mode(vy_handle *h);
  * tiles.  Default 1 (as many CTAs as fit).  Results never depend on it. */
 int vy_set_tiles_per_warp(vy_handle *h, int32_t k);
 
+/* Heterogeneous batch in one launch (config C5).  The
+ * reference steps one (config, station, dataset) per BatchEnv (engine.py:370,
+ * SPEC.md:482); a multi handle stacks n bound group handles (each keeps its
+ * own tables, state and outputs) and steps all of them with ONE persistent
+ * kernel: global tile t -> group g by the per-tile config index tile0[],
+ * the group's Params stacked in device memory, every distinct table set
+ * staged once per CTA.  Actions are each group's device RandomPolicy rows
+ * (policy_seeds[g], env index0[g]; policies.py:51-73), drawn in the kernel
+ * as in vy_step_random; call_counter (device, may be NULL) as there.  Distinct
+ * car-profile tables and station tables (<= 8 each) are staged once per CTA.  Every
+ * group's outputs equal a vy_step_random of that group alone.  Create after
+ * the group handles are bound (the Params snapshot their buffers). */
+typedef struct vy_multi vy_multi;
+int vy_multi_create(vy_handle *const *handles, int32_t n, const uint64_t *policy_seeds, const int64_t *index0,
+                    vy_multi **out);
+int vy_multi_step_random(vy_multi *m, int64_t call, int64_t *call_counter, void *stream);
+/* out4 = {Spec mode, 16 * car-profile sets + station sets, warps per CTA, grid} */
+int32_t vy_multi_info(vy_multi *m, int32_t *out4);
+int64_t vy_multi_launch_count(vy_multi *m);
+int vy_multi_destroy(vy_multi *m);
+
 /* PPO support (config C3): generalised advantage estimation as a reverse
  * scan over a [T][B] rollout (float32 values/rewards, uint8 dones, last_value
  * [B]); writes advantages and returns [T][B].  Not part of the reference

@@ -77,6 +77,12 @@ _SIGS = {
     "vy_policy_step": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _P, _P, C.c_uint64, _P,
                                  _P, _P, _P, _P, _P]),
     "vy_selftest_div": (C.c_int, [C.POINTER(C.c_double), C.c_int32, C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),
+    "vy_multi_create": (C.c_int, [C.POINTER(_P), C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_int64),
+                                  C.POINTER(_P)]),
+    "vy_multi_step_random": (C.c_int, [_P, C.c_int64, _P, _P]),
+    "vy_multi_info": (C.c_int32, [_P, C.POINTER(C.c_int32)]),
+    "vy_multi_launch_count": (C.c_int64, [_P]),
+    "vy_multi_destroy": (C.c_int, [_P]),
 }
 
 

@@ -13,6 +13,8 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -142,6 +144,7 @@ struct vy_handle {
   std::vector<Profile> profiles;
   double *d_buy = nullptr, *d_sellg = nullptr, *d_moer = nullptr, *d_dgrid = nullptr, *d_sin = nullptr,
          *d_cos = nullptr, *d_catcum = nullptr, *d_pthr = nullptr, *d_dtab = nullptr, *d_portc = nullptr, *d_treec = nullptr;
+  int* d_order = nullptr;
   int8_t* d_wk = nullptr;
   int* d_pfull = nullptr;
   Profile* d_prof = nullptr;
@@ -245,36 +248,16 @@ void fill(vy_handle* h, Params& P, bool rollout, bool acts) {
   P.rcp_1000 = rcp(1000.0);
   P.rcp_ep = rcp((double)t.episode_steps);
   P.rcp_365 = rcp(365.0);
-  for (int i = 0; i < t.n_ports; ++i) {
-    P.volt[i] = h->volt[i];
-    P.imax_c[i] = h->imax_c[i];
-    P.imax_d[i] = h->imax_d[i];
-    P.eta_c[i] = h->eta_c[i];
-    P.eta_d[i] = h->eta_d[i];
-    P.i_denom[i] = h->i_denom[i];
-    P.dtv[i] = t.dt_h * h->volt[i];  // (dt_h * V) * I / 1000 evaluates left to right (_kernel.pyx:366)
-    P.kind[i] = h->kind[i];
-    P.order[i] = h->order[i];
-    P.rcp_volt[i] = rcp(h->volt[i]);
-    P.rcp_eta_c[i] = rcp(h->eta_c[i]);
-    P.rcp_i_denom[i] = rcp(h->i_denom[i]);
-    uint32_t mask = 0;
-    for (int m = 0; m < t.n_nodes && m < kFastNodes; ++m)
-      if (h->node_lo[m] <= i && i < h->node_hi[m]) mask |= 1u << m;
-    P.port_nodes[i] = t.n_nodes <= kFastNodes ? mask : 0u;
-  }
   P.battery_node_mask = 0;
   if (t.battery_enabled && t.n_nodes <= kFastNodes)
     for (int m = 0; m < t.n_nodes; ++m)
       if (h->node_lo[m] <= t.n_ports && t.n_ports < h->node_hi[m]) P.battery_node_mask |= 1 << m;
-  for (int m = 0; m < t.n_nodes; ++m) {
+  for (int m = 0; m < t.n_nodes && m < kFastNodes; ++m) {
     P.node_cap[m] = h->node_cap[m];
     P.node_eta[m] = h->node_eta[m];
-    P.node_lo[m] = h->node_lo[m];
-    P.node_hi[m] = h->node_hi[m];
-    P.node_order[m] = h->node_order[m];
     P.node_rcp_eta[m] = rcp(h->node_eta[m]);
   }
+  P.order = h->d_order;
   P.buy = h->d_buy;
   P.sellg = h->d_sellg;
   P.moer = h->d_moer;
@@ -487,6 +470,7 @@ int vy_create(const vy_tables* t, int64_t batch, int device, vy_handle** out) {
     }
     if (!rc) rc = upload(&h->d_treec, tcv.data(), tcv.size());
   }
+  if (!rc) rc = upload(&h->d_order, h->order.data(), h->order.size());
   if (!rc) rc = upload<Profile>(&h->d_prof, nullptr, kMaxProfiles);
   if (!rc) rc = upload<uint32_t>(&h->d_err, nullptr, 1);
   if (!rc && cudaMemset(h->d_err, 0, 4) != cudaSuccess) rc = fail(VY_ERR_CUDA, "memset");
@@ -504,7 +488,8 @@ int vy_create(const vy_tables* t, int64_t batch, int device, vy_handle** out) {
 int vy_destroy(vy_handle* h) {
   if (!h) return VY_OK;
   void* ptrs[] = {h->d_buy, h->d_sellg, h->d_moer, h->d_dgrid, h->d_sin, h->d_cos, h->d_catcum,
-                  h->d_pthr, h->d_dtab, h->d_portc, h->d_treec, h->d_wk, h->d_pfull, h->d_prof, h->d_err, h->d_tile_ctr};
+                  h->d_pthr, h->d_dtab, h->d_portc, h->d_treec, h->d_wk, h->d_pfull, h->d_prof, h->d_err, h->d_tile_ctr,
+                  h->d_order};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete h;
@@ -762,6 +747,222 @@ int vy_selftest_div(const double* divisors, int32_t nd, int64_t samples_per_divi
   cudaFree(dy);
   cudaFree(dbad);
   return rc;
+}
+
+}  // extern "C"
+
+// ---- heterogeneous batch in one launch (k_step_multi) ---------------------
+
+struct vy_multi {
+  std::vector<vy_handle*> hs;
+  int mode = 1;
+  vy::MultiArgs A{};
+  unsigned long long* d_ctr = nullptr;
+  int smem = 0, warps = 1;
+  unsigned grid = 0;
+  int64_t launches = 0;
+};
+
+namespace {
+// c_groups slots in use (constant memory is per module: live multi handles share it)
+std::mutex g_slot_mu;
+std::vector<bool> g_slot_used(kConstGroups, false);
+int alloc_slots(int n) {
+  std::lock_guard<std::mutex> lk(g_slot_mu);
+  for (int s0 = 0; s0 + n <= kConstGroups; ++s0) {
+    bool ok = true;
+    for (int j = 0; j < n && ok; ++j) ok = !g_slot_used[(size_t)(s0 + j)];
+    if (ok) {
+      for (int j = 0; j < n; ++j) g_slot_used[(size_t)(s0 + j)] = true;
+      return s0;
+    }
+  }
+  return -1;
+}
+void free_slots(int s0, int n) {
+  std::lock_guard<std::mutex> lk(g_slot_mu);
+  for (int j = 0; j < n; ++j) g_slot_used[(size_t)(s0 + j)] = false;
+}
+// the bytes of a group's car-profile table / station tables (action grid,
+// per-port constants, capacity tree): groups with equal bytes share one
+// staged copy per CTA
+int profile_bytes_of(const Params& P, std::vector<unsigned char>& out) {
+  const size_t np = (size_t)P.n_profiles * sizeof(Profile);
+  out.assign(4 + np, 0);
+  std::memcpy(out.data(), &P.n_profiles, 4);
+  VY_CUDA(cudaMemcpy(out.data() + 4, P.profiles, np, cudaMemcpyDeviceToHost));
+  return VY_OK;
+}
+int station_bytes_of(const Params& P, std::vector<unsigned char>& out) {
+  const size_t nd = (size_t)(2 * P.k + 1) * 8, npc = (size_t)P.n_ports * 8 * kPortWords, nt = (size_t)P.n_nodes * 32;
+  out.assign(12 + nd + npc + nt, 0);
+  const int32_t dims[3] = {P.k, P.n_ports, P.n_nodes};
+  std::memcpy(out.data(), dims, 12);
+  unsigned char* o = out.data() + 12;
+  VY_CUDA(cudaMemcpy(o, P.delta_tab, nd, cudaMemcpyDeviceToHost));
+  VY_CUDA(cudaMemcpy(o + nd, P.portc, npc, cudaMemcpyDeviceToHost));
+  VY_CUDA(cudaMemcpy(o + nd + npc, P.treec, nt, cudaMemcpyDeviceToHost));
+  return VY_OK;
+}
+// index of `key` in `sets` (appended if new; -1 when full)
+int intern_set(std::vector<std::vector<unsigned char>>& sets, const std::vector<unsigned char>& key) {
+  for (size_t s = 0; s < sets.size(); ++s)
+    if (sets[s] == key) return (int)s;
+  if ((int)sets.size() == kMaxSets) return -1;
+  sets.push_back(key);
+  return (int)sets.size() - 1;
+}
+}  // namespace
+
+extern "C" {
+
+int vy_multi_create(vy_handle* const* hs, int32_t n, const uint64_t* policy_seeds, const int64_t* index0,
+                    vy_multi** out) {
+  if (!hs || !out || !policy_seeds || !index0 || n < 1) return fail(VY_ERR_ARG, "bad arguments");
+  if (n > kConstGroups) return fail(VY_ERR_UNSUPPORTED, "at most 48 groups per multi batch");
+  auto m = std::make_unique<vy_multi>();
+  std::vector<Params> ps((size_t)n);
+  std::vector<std::vector<unsigned char>> psets, ssets;
+  int mode = 1;
+  int device = -1;
+  bool battery = false, generic = false, big_tree = false;
+  int64_t tiles = 0;
+  int tile_bytes = 0;
+  for (int g = 0; g < n; ++g) {
+    vy_handle* h = hs[g];
+    if (!h || !h->bound) return fail(VY_ERR_STATE, "every group handle must be bound");
+    if (device < 0) device = h->device;
+    if (h->device != device) return fail(VY_ERR_ARG, "groups on different devices");
+    if (2 * h->t.k + 1 > 256) return fail(VY_ERR_UNSUPPORTED, "RandomPolicy actions need 2k+1 <= 256");
+    const int md = step_mode(h, VY_F_AUTO_RESET, true);
+    generic |= md == 0;
+    battery |= md == 3;
+    big_tree |= md == 2;
+    Params& P = ps[(size_t)g];
+    fill(h, P, false, true);
+    P.flags = VY_F_AUTO_RESET;
+    P.actions = nullptr;
+    P.act_dtype = VY_ACT_U8;
+    P.policy = 1;
+    P.pol_seed = policy_seeds[g];
+    P.pol_index0 = index0[g];
+    P.pol_call = 0;
+    P.pol_counter = nullptr;
+    P.pol_out = nullptr;
+    m->A.tile0[g] = tiles;
+    tiles += (h->B + 31) / 32;
+    tile_bytes = std::max(tile_bytes, P.L.bytes);
+    std::vector<unsigned char> key;
+    const size_t np0 = psets.size(), ns0 = ssets.size();
+    if (int rc = profile_bytes_of(P, key)) return rc;
+    const int ps_ = intern_set(psets, key);
+    if (int rc = station_bytes_of(P, key)) return rc;
+    const int ss_ = intern_set(ssets, key);
+    if (ps_ < 0 || ss_ < 0) return fail(VY_ERR_UNSUPPORTED, "at most 8 distinct car-profile / station table sets");
+    if (psets.size() > np0) m->A.pset_group[ps_] = g;  // a new set: this group's tables define it
+    if (ssets.size() > ns0) m->A.sset_group[ss_] = g;
+    m->A.group_pset[g] = (int8_t)ps_;
+    m->A.group_sset[g] = (int8_t)ss_;
+    m->hs.push_back(h);
+  }
+  // one Spec<M> for all groups: M = 2 runs any tree (node sums from the tile),
+  // M = 3 adds the battery, M = 0 everything else
+  mode = generic ? 0 : battery ? 3 : big_tree ? 2 : 1;
+  if (battery && big_tree) mode = 3;
+  m->mode = mode;
+  m->A.n_groups = n;
+  m->A.n_psets = (int)psets.size();
+  m->A.n_ssets = (int)ssets.size();
+  m->A.tile0[n] = tiles;
+  int off = 0;
+  for (int s = 0; s < m->A.n_psets; ++s) {
+    m->A.pset_off[s] = off;
+    off += pset_bytes(ps[(size_t)m->A.pset_group[s]].n_profiles);
+  }
+  for (int s = 0; s < m->A.n_ssets; ++s) {
+    const Params& P = ps[(size_t)m->A.sset_group[s]];
+    m->A.sset_off[s] = off;
+    off += sset_bytes(P.k, P.n_ports, P.n_nodes);
+  }
+  off = (off + 127) & ~127;
+  m->A.tiles_off = off;
+  m->A.tile_bytes = (tile_bytes + 16 + 127) & ~127;  // + the warp's mbarrier at the end
+  VY_CUDA(cudaSetDevice(device));
+  const int slot0 = alloc_slots(n);
+  if (slot0 < 0) return fail(VY_ERR_UNSUPPORTED, "constant-memory group slots exhausted (48 across live multi batches)");
+  m->A.slot0 = slot0;
+  int rc = VY_OK;
+  if (cudaMemcpyToSymbol(c_groups, ps.data(), sizeof(Params) * (size_t)n, sizeof(Params) * (size_t)slot0) !=
+      cudaSuccess)
+    rc = fail(VY_ERR_CUDA, "cudaMemcpyToSymbol(c_groups)");
+  if (!rc) rc = upload<unsigned long long>(&m->d_ctr, nullptr, 2);
+  if (!rc && cudaMemset(m->d_ctr, 0, 16) != cudaSuccess) rc = fail(VY_ERR_CUDA, "memset");
+  if (rc) {
+    free_slots(slot0, n);
+    cudaFree(m->d_ctr);
+    return rc;
+  }
+  m->A.ctr = m->d_ctr;
+  // geometry: as many warps per SM as shared memory allows (all sets staged per CTA)
+  const vy_handle* h0 = hs[0];
+  const int per_sm = h0->smem_per_sm;
+  int best_w = 1, best_total = 0;
+  for (int w = 1; w <= kMultiThreads / 32; ++w) {
+    const int bytes = off + w * m->A.tile_bytes;
+    if (bytes + 1024 > per_sm) break;
+    const int total = (per_sm / (bytes + 1024)) * w;
+    if (total >= best_total) {
+      best_total = total;
+      best_w = w;
+    }
+  }
+  if (const char* ov = std::getenv("VY_WARPS_PER_CTA")) {
+    const int w = std::atoi(ov);
+    if (w >= 1 && w <= kMultiThreads / 32 && off + w * m->A.tile_bytes + 1024 <= per_sm) best_w = w;
+  }
+  m->warps = best_w;
+  m->smem = off + best_w * m->A.tile_bytes;
+  if (m->smem + 1024 > per_sm) return fail(VY_ERR_UNSUPPORTED, "groups too large for one shared-memory tile");
+  auto* kern = mode == 1 ? k_step_multi<1> : mode == 2 ? k_step_multi<2> : mode == 3 ? k_step_multi<3> : k_step_multi<0>;
+  VY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, m->smem));
+  const unsigned resident = (unsigned)h0->num_sms * (unsigned)(per_sm / (m->smem + 1024));
+  const unsigned want = (unsigned)((tiles + best_w - 1) / best_w);
+  m->grid = want < resident ? want : resident;
+  *out = m.release();
+  return VY_OK;
+}
+
+int vy_multi_step_random(vy_multi* m, int64_t call, int64_t* call_counter, void* stream) {
+  if (!m) return fail(VY_ERR_ARG, "null multi handle");
+  vy::MultiArgs A = m->A;
+  A.pol_call = call;
+  A.pol_counter = call_counter;
+  auto* kern = m->mode == 1 ? k_step_multi<1> : m->mode == 2 ? k_step_multi<2> : m->mode == 3 ? k_step_multi<3>
+                                                                                                 : k_step_multi<0>;
+  kern<<<m->grid, m->warps * 32, m->smem, (cudaStream_t)stream>>>(A);
+  VY_CUDA(cudaGetLastError());
+  ++m->launches;
+  for (vy_handle* h : m->hs) h->last_mode = m->mode;
+  return VY_OK;
+}
+
+int32_t vy_multi_info(vy_multi* m, int32_t* out4) {
+  if (!m || !out4) return fail(VY_ERR_ARG, "null argument");
+  out4[0] = m->mode;
+  out4[1] = m->A.n_psets * 16 + m->A.n_ssets;
+  out4[2] = m->warps;
+  out4[3] = (int32_t)m->grid;
+  return VY_OK;
+}
+
+int64_t vy_multi_launch_count(vy_multi* m) { return m ? m->launches : -1; }
+
+int vy_multi_destroy(vy_multi* m) {
+  if (!m) return VY_OK;
+  free_slots(m->A.slot0, m->A.n_groups);
+  cudaFree(m->d_ctr);
+  delete m;
+  return VY_OK;
 }
 
 }  // extern "C"

@@ -118,15 +118,11 @@ struct Params {
   int battery_node_mask;  // bit m: battery slot in node m's range (m < kFastNodes)
   int act_tile;           // actions are row-major uint8 [B][n+1], staged per tile
   int n_profiles;         // live entries of the car-profile table
-  // ports
-  double volt[kMaxPorts], imax_c[kMaxPorts], imax_d[kMaxPorts], eta_c[kMaxPorts], eta_d[kMaxPorts];
-  double i_denom[kMaxPorts], dtv[kMaxPorts];
-  double rcp_volt[kMaxPorts], rcp_eta_c[kMaxPorts], rcp_i_denom[kMaxPorts];
-  int kind[kMaxPorts], order[kMaxPorts];
-  uint32_t port_nodes[kMaxPorts];  // bit m: port in node m's range (m < kFastNodes)
-  // capacity tree: node m sums slots [lo, hi) in order (battery slot = n_ports, last)
-  double node_cap[kMaxNodes], node_eta[kMaxNodes], node_rcp_eta[kMaxNodes];
-  int node_lo[kMaxNodes], node_hi[kMaxNodes], node_order[kMaxNodes];
+  // ports: per-port constants live in `portc` (staged per CTA); the parking
+  // order (generic path only) in device memory
+  const int* order;  // [n_ports]
+  // capacity tree: the fast (register) path's nodes m < kFastNodes; every node in `treec`
+  double node_cap[kFastNodes], node_eta[kFastNodes], node_rcp_eta[kFastNodes];
   // series (device)
   const double *buy, *sellg, *moer, *dgrid, *sin_t, *cos_t, *cat_cum;
   const int8_t* weekday;

@@ -86,7 +86,8 @@ __device__ __forceinline__ void policy_row(const Params& P, uint32_t tile, int64
 template <int M>
 __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const double* dtab, PortC pc, TreeC tc,
                                           uint32_t tile, int64_t b0, int lane, WarpBar& wb,
-                                          unsigned long long* claim = nullptr, int64_t pol_call = 0) {
+                                          unsigned long long* claim = nullptr, int64_t pol_call = 0,
+                                          unsigned long long* claim_ctr = nullptr) {
   using C = Spec<M>;
   const Lane T = make_lane(P, tile, lane);
   const int64_t b = b0 + lane;
@@ -146,7 +147,7 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
   // the next tile is claimed before the obs read-out so the atomic's round
   // trip overlaps it (and not earlier: a claim held across a whole step
   // lengthens the tail of the launch)
-  if (claim && lane == 0) *claim = atomicAdd(P.tile_ctr, 1ull);
+  if (claim && lane == 0) *claim = atomicAdd(claim_ctr ? claim_ctr : P.tile_ctr, 1ull);
   emit_tail<M>(P, T, E, G, S, b0, active, P.out.obs);
 }
 
@@ -185,6 +186,117 @@ __global__ void __launch_bounds__(256) k_step(const __grid_constant__ Params P) 
       P.tile_ctr[0] = 0;
       P.tile_ctr[1] = 0;
       if (P.policy && P.pol_counter) P.pol_counter[0] += 1;
+    }
+  }
+}
+
+// ---- heterogeneous batch in one launch (config C5) -------------------------
+//
+// Many station/market configurations ("groups", each a regular handle with
+// its own tables, state and outputs) stepped by ONE persistent launch.  Global
+// tile t belongs to group g with tile0[g] <= t < tile0[g+1] (the per-tile
+// config index); a warp claims global tiles from one counter and steps each
+// with its group's Params (stacked in global memory, read through the
+// read-only path) and its group's table set (car profiles, action grid,
+// per-port constants, capacity tree), every distinct set staged once per CTA
+// in shared memory.  Every group's trajectory is bit-identical to stepping it
+// alone: the same step_tile code runs on the same tables and state.
+constexpr int kMaxGroups = 64;
+// 7 warps x 2 CTAs per SM fill shared memory; the bound lets ptxas use up to 144 registers
+constexpr int kMultiThreads = 224;
+constexpr int kMaxSets = 8;
+// Group Params live in constant memory (slot-allocated per multi handle): a
+// warp-uniform group index reads them through the constant cache into
+// uniform registers, like a single launch's __grid_constant__ Params (a
+// global-memory copy measured 10-20% slower: loads in the dependency chains
+// and per-thread registers for every hoisted field).
+constexpr int kConstGroups = 48;  // 48 x 1136 B of the 64 KB constant bank
+__constant__ Params c_groups[kConstGroups];
+
+struct MultiArgs {
+  int slot0;                // first c_groups slot of this batch
+  int n_groups, n_psets, n_ssets;
+  int64_t tile0[kMaxGroups + 1];  // first global tile of each group; tile0[n_groups] = total
+  int8_t group_pset[kMaxGroups];  // car-profile set of each group
+  int8_t group_sset[kMaxGroups];  // station set (action grid, per-port constants, tree) of each group
+  int pset_group[kMaxSets], sset_group[kMaxSets];  // a group whose tables define the set
+  int pset_off[kMaxSets], sset_off[kMaxSets];      // smem byte offsets of the staged sets
+  int tiles_off;                  // smem byte offset of warp tile 0
+  int tile_bytes;                 // bytes per warp tile (max over groups)
+  unsigned long long* ctr;        // [2] tile counter, finished warps
+  int64_t pol_call;               // RandomPolicy call index (+ *pol_counter when set)
+  int64_t* pol_counter;
+};
+// station set layout: action grid (2k+1 doubles, 16-aligned), per-port constants, tree
+__host__ __device__ inline int sset_portc_off(int k) { return ((2 * k + 1) * 8 + 15) & ~15; }
+__host__ __device__ inline int sset_treec_off(int k, int n_ports) { return sset_portc_off(k) + n_ports * 8 * kPortWords; }
+__host__ __device__ inline int sset_bytes(int k, int n_ports, int n_nodes) {
+  return (sset_treec_off(k, n_ports) + n_nodes * 32 + 15) & ~15;
+}
+__host__ __device__ inline int pset_bytes(int n_profiles) { return (n_profiles * (int)sizeof(Profile) + 15) & ~15; }
+
+__device__ __forceinline__ void stage_multi_sets(const MultiArgs& A) {
+  for (int s = 0; s < A.n_psets; ++s) {
+    const Params& P = c_groups[A.slot0 + A.pset_group[s]];
+    double* d = reinterpret_cast<double*>(vy_smem + A.pset_off[s]);
+    const double* gp = reinterpret_cast<const double*>(P.profiles);
+    for (int i = threadIdx.x; i < P.n_profiles * kProfileWords; i += blockDim.x) d[i] = __ldg(gp + i);
+  }
+  for (int s = 0; s < A.n_ssets; ++s) {
+    const Params& P = c_groups[A.slot0 + A.sset_group[s]];
+    unsigned char* base = vy_smem + A.sset_off[s];
+    double* sd = reinterpret_cast<double*>(base);
+    for (int i = threadIdx.x; i < 2 * P.k + 1; i += blockDim.x) sd[i] = __ldg(P.delta_tab + i);
+    double* sp = reinterpret_cast<double*>(base + sset_portc_off(P.k));
+    for (int i = threadIdx.x; i < P.n_ports * kPortWords; i += blockDim.x) sp[i] = __ldg(P.portc + i);
+    double* st = reinterpret_cast<double*>(base + sset_treec_off(P.k, P.n_ports));
+    for (int i = threadIdx.x; i < P.n_nodes * 4; i += blockDim.x) st[i] = __ldg(P.treec + i);
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(kMultiThreads) k_step_multi(const __grid_constant__ MultiArgs A) {
+  stage_multi_sets(A);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t toff = (uint32_t)(A.tiles_off + warp * A.tile_bytes);
+  WarpBar wb{smem_base() + toff + (uint32_t)A.tile_bytes - 16u, 0u, false};
+  if (lane == 0) {
+    mbar_init(wb.a);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  const unsigned long long ntiles = (unsigned long long)A.tile0[A.n_groups];
+  const int64_t pol_call = A.pol_call + (A.pol_counter ? *(volatile int64_t*)A.pol_counter : 0);
+  unsigned long long nxt = 0;
+  if (lane == 0) nxt = atomicAdd(A.ctr, 1ull);
+  for (;;) {
+    const unsigned long long t = __shfl_sync(0xffffffffu, nxt, 0);
+    if (t >= ntiles) break;
+    // group: last g with tile0[g] <= t, from two warp votes over the tile
+    // offsets (a vote result is warp-uniform, so the group's Params below are
+    // read with uniform constant loads into uniform registers)
+    const unsigned v0 = __ballot_sync(0xffffffffu, lane < A.n_groups && (unsigned long long)A.tile0[lane] <= t);
+    const unsigned v1 =
+        __ballot_sync(0xffffffffu, lane + 32 < A.n_groups && (unsigned long long)A.tile0[lane + 32] <= t);
+    const int g = __popc(v0) + __popc(v1) - 1;
+    const Params& P = c_groups[A.slot0 + g];
+    const uint32_t so = (uint32_t)A.sset_off[A.group_sset[g]];
+    const int kk = P.k;
+    const Prof prof{smem_base() + (uint32_t)A.pset_off[A.group_pset[g]]};
+    const PortC pc{smem_base() + so + (uint32_t)sset_portc_off(kk)};
+    const TreeC tc{smem_base() + so + (uint32_t)sset_treec_off(kk, P.n_ports)};
+    const double* dtab = reinterpret_cast<const double*>(vy_smem + so);
+    step_tile<M>(P, prof, dtab, pc, tc, toff, ((int64_t)t - A.tile0[g]) * 32, lane, wb, &nxt, pol_call, A.ctr);
+    __syncwarp();
+  }
+  if (lane == 0) {
+    __threadfence();
+    const unsigned long long warps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(A.ctr + 1, 1ull) == warps - 1) {
+      A.ctr[0] = 0;
+      A.ctr[1] = 0;
+      if (A.pol_counter) A.pol_counter[0] += 1;
     }
   }
 }
@@ -289,7 +401,7 @@ __global__ void __launch_bounds__(256) k_reset(const __grid_constant__ Params P,
     store_env<0>(P, b, E, true);
   }
   // masked-out rows still get their (unchanged) obs rewritten, which is idempotent
-  emit_obs(P, prof, T, E, load_obs_globals(P, E.step, E.day), b0, active, P.out.obs, /*store_state=*/true);
+  emit_obs(P, prof, pc, T, E, load_obs_globals(P, E.step, E.day), b0, active, P.out.obs, /*store_state=*/true);
 }
 
 }  // namespace vy

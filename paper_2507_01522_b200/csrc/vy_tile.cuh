@@ -733,10 +733,6 @@ __device__ __forceinline__ void stage_port_obs(const Params& P, Prof prof, const
     for (int f = 0; f < 6; ++f) sts_f32(col + f * 132, (float)v[f]);
   }
 }
-__device__ __forceinline__ void stage_port_obs(const Params& P, Prof prof, const ObsSink& S, int lane, bool active,
-                                               int i, uint32_t mt, double idr, double soc, double de, int dt) {
-  stage_port_obs(P, prof, S, lane, active, i, mt, idr, soc, de, dt, P.i_denom[i], P.rcp_i_denom[i]);
-}
 
 // the six obs columns of a port that is empty (all-zero state): +0
 __device__ __forceinline__ void stage_zero_obs(const Params& P, const ObsSink& S, int lane, bool active, int i) {
@@ -1332,7 +1328,7 @@ __device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const 
 
 // Obs of the tile's current state (reset kernel): write the state back to HBM
 // (bulk copies) if asked, then stage every port and finish.
-__device__ __forceinline__ void emit_obs(const Params& P, Prof prof, const Lane& T, const EnvRegs& E,
+__device__ __forceinline__ void emit_obs(const Params& P, Prof prof, PortC pc, const Lane& T, const EnvRegs& E,
                                          ObsGlobals G, int64_t b0, bool active, void* obs_base, bool store_state) {
   const int64_t b = b0 + T.lane;
   const ObsSink S = make_sink<0>(P, T, b, obs_base, P.L.obs == 0);
@@ -1343,7 +1339,9 @@ __device__ __forceinline__ void emit_obs(const Params& P, Prof prof, const Lane&
     const double idr = T.idr(i), soc = T.soc(i), de = T.de(i);
     const int dt = T.dtrem(i);
     if (S.in_place) __syncwarp();  // every lane has read port i before its slots are reused
-    stage_port_obs(P, prof, S, T.lane, active, i, mt, idr, soc, de, dt);
+    double i_denom, rcp_i_denom;
+    pc.pair(i, 5, i_denom, rcp_i_denom);
+    stage_port_obs(P, prof, S, T.lane, active, i, mt, idr, soc, de, dt, i_denom, rcp_i_denom);
   }
   emit_tail<0>(P, T, E, G, S, b0, active, obs_base);
 }

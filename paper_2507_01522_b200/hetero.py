@@ -14,6 +14,13 @@ are global indices offset_g .. offset_g + B_g - 1), so a group's trajectory is
 bit-identical to a standalone BatchEnv with that global_offset — which is
 what the tests check.
 
+``MultiStep`` (``HeteroBatch.multi_random_step``) is the one-launch form: a
+multi handle (vy_multi_create) stacks the groups' Params in device memory and
+one persistent kernel (k_step_multi) steps every group, global tile t mapped
+to its group by the per-tile config index and each
+distinct table set staged once per CTA; the outputs equal the per-group
+launches bit for bit.
+
 ``sweep_groups`` builds the C5 sweep: regions {eu, us, world} x scenarios
 {highway, residential, work, shopping} x traffic {low, medium, high}, station
 presets rotating over single / multi / nested layouts.
@@ -21,11 +28,13 @@ presets rotating over single / multi / nested layouts.
 
 from __future__ import annotations
 
+import ctypes as C
 import itertools
 from dataclasses import dataclass
 
 import torch
 
+from . import _native as nat
 from .batch import BatchEnv, DeviceRandomPolicy
 from .envconfig import EnvConfig
 from .exogenous import REGIONS, SCENARIOS, TRAFFIC_FACTORS, Dataset, generate_synthetic_defaults
@@ -151,6 +160,73 @@ class HeteroBatch:
             if e._t is not None:
                 e._t = (e._t + 1) % e.tables.episode_steps
 
+    # ---- one launch per step over all groups (k_step_multi) -------------
+    def _multi_handle(self):
+        if getattr(self, "_multi", None) is None:
+            if len(self.policies) != len(self.envs):
+                raise ValueError("multi_random_step needs a policy_seed (device RandomPolicy per group)")
+            n = len(self.envs)
+            hs = (C.c_void_p * n)(*[e._h for e in self.envs])
+            seeds = (C.c_uint64 * n)(*[p.seed & ((1 << 64) - 1) for p in self.policies])
+            idx = (C.c_int64 * n)(*[p.index0 for p in self.policies])
+            out = C.c_void_p()
+            lib = self.envs[0]._lib
+            nat.check(lib.vy_multi_create(hs, n, seeds, idx, C.byref(out)), "vy_multi_create")
+            self._multi = out
+        return self._multi
+
+    def multi_info(self) -> dict:
+        """Spec mode, distinct table sets, warps per CTA and grid of the one-launch step."""
+        v = (C.c_int32 * 4)()
+        nat.check(self.envs[0]._lib.vy_multi_info(self._multi_handle(), v), "vy_multi_info")
+        return {"mode": v[0], "profile_sets": v[1] // 16, "station_sets": v[1] % 16, "warps_per_cta": v[2],
+                "grid": v[3]}
+
+    def multi_random_step(self, device_counter: torch.Tensor | None = None) -> None:
+        """One step of every group with its device RandomPolicy rows as ONE
+        kernel launch (k_step_multi); outputs land in each group's buffers
+        (``self.envs[g].outs``), bit-identical to ``random_step``.  With
+        ``device_counter`` (int64 [2] on the device, zeroed) the policy call
+        index is read from device memory and advanced by the kernel (CUDA
+        graph replay); the host clocks and call counters advance here."""
+        for e in self.envs:
+            if e._needs_reset:
+                raise nat.EpisodeDone("call reset() before step()")
+        m = self._multi_handle()
+        lib = self.envs[0]._lib
+        call = 0 if device_counter is not None else self.policies[0].calls
+        if device_counter is None and any(p.calls != call for p in self.policies):
+            raise ValueError("group policies are at different call indices")
+        ptr = device_counter.data_ptr() if device_counter is not None else None
+        nat.check(lib.vy_multi_step_random(m, call, ptr, torch.cuda.current_stream().cuda_stream), "vy_multi_step")
+        for p in self.policies:
+            p.calls += 1
+        for e in self.envs:
+            e._advance_clock()
+
+    def graph_multi_step(self) -> None:
+        """multi_random_step replayed from a captured CUDA graph (one kernel
+        node); the device counter carries the RandomPolicy call index."""
+        if getattr(self, "_mgraph", None) is None:
+            self._mcounter = torch.zeros(2, dtype=torch.int64, device=self.envs[0].outs.obs.device)
+            self._mcounter[0] = self.policies[0].calls
+            self.multi_random_step(self._mcounter)  # warm-up: this call's step
+            clocks = [e._t for e in self.envs]
+            calls = [p.calls for p in self.policies]
+            self._mgraph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self._mgraph):
+                self.multi_random_step(self._mcounter)
+            for e, c in zip(self.envs, clocks):
+                e._t = c  # capture did not execute
+            for p, c in zip(self.policies, calls):
+                p.calls = c
+            return
+        self._mgraph.replay()
+        for p in self.policies:
+            p.calls += 1
+        for e in self.envs:
+            e._advance_clock()
+
     def kernels_per_step(self) -> int:
         return len(self.envs)
 
@@ -158,5 +234,8 @@ class HeteroBatch:
         return sum(e.launch_count() for e in self.envs)
 
     def close(self) -> None:
+        if getattr(self, "_multi", None) is not None:
+            self.envs[0]._lib.vy_multi_destroy(self._multi)
+            self._multi = None
         for e in self.envs:
             e.close()
