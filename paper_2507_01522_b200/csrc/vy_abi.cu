@@ -163,9 +163,27 @@ struct vy_handle {
 namespace {
 
 // per-warp tile layout (see TileLayout); rollouts get a separate obs area
-TileLayout tile_layout(const vy_tables& t, bool rollout, bool acts) {
+TileLayout tile_layout(const vy_tables& t, bool rollout, bool acts, bool stream = false) {
   TileLayout L{};
   const int n = t.n_ports;
+  if (stream) {
+    // streamed tile (Spec<4>): i_drawn slots, meta, actions, the obs chunk ring
+    L.ps = 256;
+    L.ports = 0;
+    int off = n * 256;
+    L.dtrem = 0;  // dwell times are read from HBM in the port loop
+    L.meta = off;
+    off += ((n * 32) + 15) & ~15;
+    L.acts = off;
+    if (acts) off += ((32 * (n + 1)) + 15) & ~15;
+    L.obs = (off + 15) & ~15;
+    off = L.obs + std::max(2 * kChunkBuf, (9 + t.horizon) * kChunkCol * 4);
+    L.bar = (off + 15) & ~15;
+    off = L.bar + 16;
+    L.bytes = (off + 127) & ~127;
+    return L;
+  }
+  L.ps = 768;
   L.ports = (24 * n + 15) & ~15;
   int off = L.ports + n * 768;
   L.dtrem = off;
@@ -193,7 +211,7 @@ TileLayout tile_layout(const vy_tables& t, bool rollout, bool acts) {
 
 double rcp(double d) { return 1.0 / d; }
 
-void fill(vy_handle* h, Params& P, bool rollout, bool acts) {
+void fill(vy_handle* h, Params& P, bool rollout, bool acts, bool stream = false) {
   const vy_tables& t = h->t;
   std::memset(&P, 0, sizeof(P));
   P.n_ports = t.n_ports;
@@ -278,7 +296,7 @@ void fill(vy_handle* h, Params& P, bool rollout, bool acts) {
   P.tile_ctr = h->d_tile_ctr;
   P.act_tile = acts;
   P.n_profiles = (int)h->profiles.size();
-  P.L = tile_layout(t, rollout, acts);
+  P.L = tile_layout(t, rollout, acts, stream);
 }
 
 // Warps per CTA: fill the SM's shared memory with as many tiles as possible
@@ -328,7 +346,9 @@ int step_mode(const vy_handle* h, uint32_t flags, bool staged_actions) {
   const bool lean = (flags & ~VY_F_AUTO_RESET) == 0 && staged_actions && !t.has_moer && !t.has_dgrid &&
                     t.horizon == 0 && h->order_identity && 2 * t.k < 32;
   if (!lean) return 0;
-  if (t.battery_enabled) return 3;
+  // battery stations: large ones (config C4, 64 ports: a 62 KB resident tile,
+  // 3 warps per SM) stream their tile (4), small ones keep it resident (3)
+  if (t.battery_enabled) return t.n_ports > 16 ? 4 : 3;
   return t.n_nodes <= kFastNodes ? 1 : 2;
 }
 
@@ -597,8 +617,9 @@ int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride
   const bool acts = dtype == VY_ACT_U8 && col_stride == 1 && row_stride == na &&
                     (reinterpret_cast<uintptr_t>(actions) % 16) == 0 && (32 * na) % 16 == 0 &&
                     (h->B % 32) == 0;
+  const int mode = step_mode(h, flags, acts);
   Params P;
-  fill(h, P, false, acts);
+  fill(h, P, false, acts, mode == 4);
   P.flags = flags;
   P.actions = actions;
   P.act_dtype = dtype;
@@ -606,9 +627,8 @@ int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride
   P.act_col = col_stride;
   if (inj) P.inj = *inj;
   Geometry g;
-  const int mode = step_mode(h, flags, acts);
   h->last_mode = mode;
-  auto* kern = mode == 1 ? k_step<1> : mode == 2 ? k_step<2> : mode == 3 ? k_step<3> : k_step<0>;
+  auto* kern = mode == 1 ? k_step<1> : mode == 2 ? k_step<2> : mode == 3 ? k_step<3> : mode == 4 ? k_step<4> : k_step<0>;
   if (int rc = geometry(h, kern, P.L, P.n_profiles, g)) return rc;
   // persistent grid: every resident CTA slot, never more CTAs than tiles need
   const unsigned resident = (unsigned)h->num_sms * (unsigned)(h->smem_per_sm / (g.smem + 1024));
@@ -629,8 +649,9 @@ int vy_step_random(vy_handle* h, uint64_t seed, int64_t index0, int64_t call, in
   if ((flags & VY_F_INFOS) && !infos_bound(h->out)) return fail(VY_ERR_ARG, "info buffers not bound");
   if (flags & VY_F_INJECT) return fail(VY_ERR_UNSUPPORTED, "vy_step_random draws its own arrivals (no VY_F_INJECT)");
   if (2 * h->t.k + 1 > 256) return fail(VY_ERR_UNSUPPORTED, "RandomPolicy actions need 2k+1 <= 256");
+  const int mode = step_mode(h, flags, true);
   Params P;
-  fill(h, P, false, true);  // the generated rows live in the tile's staged-action area
+  fill(h, P, false, true, mode == 4);  // the generated rows live in the tile's staged-action area
   P.flags = flags;
   P.actions = nullptr;
   P.act_dtype = VY_ACT_U8;
@@ -641,9 +662,8 @@ int vy_step_random(vy_handle* h, uint64_t seed, int64_t index0, int64_t call, in
   P.pol_counter = call_counter;
   P.pol_out = actions_out;
   Geometry g;
-  const int mode = step_mode(h, flags, true);
   h->last_mode = mode;
-  auto* kern = mode == 1 ? k_step<1> : mode == 2 ? k_step<2> : mode == 3 ? k_step<3> : k_step<0>;
+  auto* kern = mode == 1 ? k_step<1> : mode == 2 ? k_step<2> : mode == 3 ? k_step<3> : mode == 4 ? k_step<4> : k_step<0>;
   if (int rc = geometry(h, kern, P.L, P.n_profiles, g)) return rc;
   const unsigned resident = (unsigned)h->num_sms * (unsigned)(h->smem_per_sm / (g.smem + 1024));
   unsigned grid = g.grid < resident ? g.grid : resident;
@@ -696,7 +716,8 @@ int vy_rollout(vy_handle* h, int32_t T, uint64_t policy_seed, int64_t index0, in
   P.out.reward = reward;
   P.out.done = done;
   Geometry g;
-  const int mode = step_mode(h, flags, true);
+  int mode = step_mode(h, flags, true);
+  if (mode == 4) mode = 3;  // a rollout keeps the whole tile resident for its T steps
   auto* kern = mode == 1 ? k_rollout<1> : mode == 2 ? k_rollout<2> : mode == 3 ? k_rollout<3> : k_rollout<0>;
   if (int rc = geometry(h, kern, P.L, P.n_profiles, g)) return rc;
   kern<<<g.grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P, T, policy_seed, index0, call0, obs_step_stride,
@@ -836,7 +857,7 @@ int vy_multi_create(vy_handle* const* hs, int32_t n, const uint64_t* policy_seed
     if (2 * h->t.k + 1 > 256) return fail(VY_ERR_UNSUPPORTED, "RandomPolicy actions need 2k+1 <= 256");
     const int md = step_mode(h, VY_F_AUTO_RESET, true);
     generic |= md == 0;
-    battery |= md == 3;
+    battery |= md == 3 || md == 4;  // the multi launch keeps tiles resident (Spec<3>)
     big_tree |= md == 2;
     Params& P = ps[(size_t)g];
     fill(h, P, false, true);

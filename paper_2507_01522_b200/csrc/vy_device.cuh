@@ -99,6 +99,7 @@ struct TileLayout {
   int dtrem, meta, acts;
   int obs;    // byte offset of obs column 0 (0 in-place; `extra` area for rollouts)
   int bar;    // byte offset of the warp's mbarrier (8 B) completing the tile's bulk copies
+  int ps;     // bytes between consecutive ports' slots: 768 (i_drawn, soc, de) or 256 (streamed tile: i_drawn)
   int bytes;
 };
 
@@ -167,12 +168,17 @@ struct Spec {
   __device__ __forceinline__ static bool info(const Params& P) { return !lean && (P.flags & VY_F_INFOS); }
   __device__ __forceinline__ static bool inject(const Params& P) { return !lean && (P.flags & VY_F_INJECT); }
   __device__ __forceinline__ static bool f64(const Params& P) { return !lean && (P.flags & VY_F_OUT_F64); }
-  __device__ __forceinline__ static bool battery(const Params& P) { return (M == 0 || M == 3) && P.battery; }
+  // M = 4: M = 3 with a streamed tile (large battery stations, e.g. config C4):
+  // only the port currents stay in shared memory; soc / energy / dwell are
+  // read from HBM a few ports ahead in the port loops, obs leave through the
+  // per-port chunk ring, so a 64-port tile needs ~22 KB instead of ~62 KB
+  static constexpr bool stream = M == 4;
+  __device__ __forceinline__ static bool battery(const Params& P) { return (M == 0 || M == 3 || M == 4) && P.battery; }
   __device__ __forceinline__ static bool moer(const Params& P) { return !lean && P.has_moer; }
   __device__ __forceinline__ static bool dgrid(const Params& P) { return !lean && P.has_dgrid; }
   __device__ __forceinline__ static int horizon(const Params& P) { return lean ? 0 : P.horizon; }
   __device__ __forceinline__ static bool fast_tree(const Params& P) {
-    return M == 1 || ((M == 0 || M == 3) && P.n_nodes <= kFastNodes);
+    return M == 1 || ((M == 0 || M == 3 || M == 4) && P.n_nodes <= kFastNodes);
   }
   __device__ __forceinline__ static bool identity(const Params& P) { return lean || P.order_identity; }
   __device__ __forceinline__ static bool staged(const Params& P) { return lean || P.act_tile; }

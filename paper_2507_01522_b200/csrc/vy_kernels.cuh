@@ -104,10 +104,13 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
   // flight together with the tile copies
   const Frame F = load_frame<M>(P, E.step, E.day);
   const ObsGlobals G = load_obs_globals(P, E.step + 1, E.day);
-  const uint64_t occ_ports = tile_issue_ports(P, tile, b0, lane, wb);
+  const uint64_t occ_ports = tile_issue_ports(P, tile, b0, lane, wb, C::stream);
   if (P.policy) policy_row(P, tile, b0, lane, pol_call);  // ALU work under the copies' latency
   tile_wait(wb);
-  const ObsSink S = make_sink<M>(P, T, b, P.out.obs, /*in_place=*/true);
+  // state goes back to HBM port by port; obs staged in the consumed port slots,
+  // or (streamed tile) through the per-port chunk ring
+  const ObsSink S = C::stream ? make_chunk_sink<M>(P, T, b0, P.out.obs, /*state_to_hbm=*/true)
+                              : make_sink<M>(P, T, b, P.out.obs, /*in_place=*/true);
   const int dt = P.act_dtype;
   const int64_t rs = P.act_row, cs = P.act_col;
   const uint8_t* arow = vy_smem + tile + P.L.acts + lane * (P.n_ports + 1);
@@ -131,10 +134,18 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
     reset_scalars(P, E, active ? P.st.env_seed[b] : 0ull, ep, 0, false);
     for (int i = 0; i < P.n_ports; ++i) {
       if (active) store_port(P, b, i, 0u, 0.0, 0.0, 0.0, 0);
-      stage_port_obs(P, prof, S, lane, active, i, 0u, 0.0, 0.0, 0.0, 0, 1.0, 1.0);  // I = 0: any denominator
+      if (!S.chunk) stage_port_obs(P, prof, S, lane, active, i, 0u, 0.0, 0.0, 0.0, 0, 1.0, 1.0);  // I = 0: any denominator
     }
     if (active) P.st.episode[b] = ep;
     reset = true;
+  }
+  if (S.chunk && (P.flags & VY_F_AUTO_RESET)) {
+    // the reset obs of every env that just finished: all port columns +0
+    const uint32_t dm = __ballot_sync(0xffffffffu, r.done);
+    if (dm) {
+      __syncwarp();  // after this step's port read-outs and arrival rows
+      for (int i = 0; i < P.n_ports; ++i) chunk_zero6(S, lane, i, dm);
+    }
   }
   if (active) {
     if (!C::probe(P, 0x800u)) store_env<M>(P, b, E, reset);

@@ -149,6 +149,19 @@ __device__ __forceinline__ int ldg_nc_s8(const int8_t* p) {
   return v;
 }
 
+// streamed-tile loads (Spec<4>): per-lane coalesced reads of a port's state,
+// issued a few ports ahead of their use (volatile: kept where written)
+__device__ __forceinline__ double ldg_st_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ldg_st_s16(const int16_t* p) {
+  int16_t v;
+  asm volatile("ld.global.s16 %0, [%1];" : "=h"(v) : "l"(p));
+  return v;
+}
+
 struct EnvRegs {
   int step, day;
   uint64_t akey;
@@ -184,9 +197,10 @@ struct Lane {
   uint8_t* m;  // this lane's meta entry of port 0 (ports 32 apart)
   int lane;
   const TileLayout* L;
-  __device__ __forceinline__ double& idr(int i) const { return p[i * 96]; }
-  __device__ __forceinline__ double& soc(int i) const { return p[i * 96 + 32]; }
-  __device__ __forceinline__ double& de(int i) const { return p[i * 96 + 64]; }
+  int ps;      // doubles between ports' slots (96; 32 in a streamed tile, which holds i_drawn only)
+  __device__ __forceinline__ double& idr(int i) const { return p[i * ps]; }
+  __device__ __forceinline__ double& soc(int i) const { return p[i * ps + 32]; }
+  __device__ __forceinline__ double& de(int i) const { return p[i * ps + 64]; }
   __device__ __forceinline__ int16_t& dtrem(int i) const { return d[i * 32]; }
   __device__ __forceinline__ uint8_t& meta(int i) const { return m[i * 32]; }
 };
@@ -194,7 +208,7 @@ struct Lane {
 __device__ __forceinline__ Lane make_lane(const Params& P, uint32_t tile, int lane) {
   unsigned char* b = vy_smem + tile;
   return Lane{tile, reinterpret_cast<double*>(b + P.L.ports + lane * 8),
-              reinterpret_cast<int16_t*>(b + P.L.dtrem + lane * 2), b + P.L.meta + lane, lane, &P.L};
+              reinterpret_cast<int16_t*>(b + P.L.dtrem + lane * 2), b + P.L.meta + lane, lane, &P.L, P.L.ps / 8};
 }
 
 // ---- tile stage-in: bulk copies (TMA engine) completing on a per-warp mbarrier ----
@@ -357,7 +371,7 @@ __device__ __forceinline__ uint64_t occupied_ports(const Params& P, uint32_t tof
 // after tile_issue_meta: wait for the meta bytes, vote the occupied ports and
 // issue their slot copies; returns the warp-uniform port mask
 __device__ __forceinline__ uint64_t tile_issue_ports(const Params& P, uint32_t toff, int64_t b0, int lane,
-                                                     WarpBar& wb) {
+                                                     WarpBar& wb, bool stream = false) {
 #if VY_BULK_META
   bar_wait(wb);
 #else
@@ -371,6 +385,14 @@ __device__ __forceinline__ uint64_t tile_issue_ports(const Params& P, uint32_t t
   const uint64_t mask = occupied_ports(P, toff, lane);
 #if !VY_BULK_SLOTS
   const int q16 = (lane & 15) * 16;
+  if (stream) {  // streamed tile: the i_drawn slots only (soc / de / dwell are read in the port loops)
+    for (int i = lane >> 4; i < n; i += 2) {
+      if (!((mask >> i) & 1ull)) continue;
+      cp_async16(t + L.ports + i * 256 + q16, reinterpret_cast<const char*>(P.st.port_i) + ((int64_t)i * ld + b0) * 8 + q16);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    return mask;
+  }
   for (int i = lane >> 4; i < n; i += 2) {
     if (!((mask >> i) & 1ull)) continue;
     const int64_t g = ((int64_t)i * ld + b0) * 8 + q16;
@@ -799,11 +821,29 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
   double nsum[kFastNodes];
 #pragma unroll
   for (int m = 0; m < kFastNodes; ++m) nsum[m] = 0.0;
+  // streamed tile: soc of port i + 2 is requested while port i is worked on (3 ahead measured 4% slower: registers)
+  const uint64_t occ_mask = occ_ports ? *occ_ports : ~0ull;
+  auto soc_at = [&](int i) -> double {
+    return i < n && ((occ_mask >> i) & 1ull) ? ldg_st_f64(P.st.port_soc + (int64_t)i * ld + b) : 0.0;
+  };
+  double soc_q0 = 0.0, soc_q1 = 0.0;
+  if (C::stream) {
+    soc_q0 = soc_at(0);
+    soc_q1 = soc_at(1);
+  }
 #pragma unroll 1  // rolled: smaller hot loop measured faster than unroll 2 or 4
   for (int i = 0; i < n; ++i) {
     const double d = delta_of(act(i));
     const uint32_t mt = T.meta(i);
-    const double idr_i = T.idr(i), soc_i = T.soc(i);
+    const double idr_i = T.idr(i);
+    double soc_i;
+    if (C::stream) {
+      soc_i = soc_q0;
+      soc_q0 = soc_q1;
+      soc_q1 = soc_at(i + 2);
+    } else {
+      soc_i = T.soc(i);
+    }
     // A port no lane of the warp occupies is skipped (a bit of the tile's
     // warp-uniform port mask, one uniform branch); otherwise branch-free: an
     // empty port (meta 0 -> profile 0, zero slots) runs the same arithmetic
@@ -884,11 +924,35 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
   int nd = 0, tover = 0;
   uint64_t occm = 0;
   const bool last = t + 1 == P.episode_steps;
+  // streamed tile: soc / de / dwell of port i + 2 requested while port i is worked on
+  struct PortQ {
+    double soc, de;
+    int dt;
+  };
+  auto q_at = [&](int i) -> PortQ {
+    if (i < n && ((occ_mask >> i) & 1ull)) {
+      const int64_t e = (int64_t)i * ld + b;
+      return {ldg_st_f64(P.st.port_soc + e), ldg_st_f64(P.st.port_de + e), ldg_st_s16(P.st.port_dtrem + e)};
+    }
+    return {0.0, 0.0, 0};
+  };
+  PortQ q0{0.0, 0.0, 0}, q1{0.0, 0.0, 0};
+  if (C::stream) {
+    q0 = q_at(0);
+    q1 = q_at(1);
+  }
 #pragma unroll 1  // rolled: smaller hot loop measured faster than unroll 2 or 4
   for (int i = 0; i < n; ++i) {
     uint32_t mt = T.meta(i);
-    double cur = T.idr(i), soc = T.soc(i), de = T.de(i);
-    int dt = T.dtrem(i);
+    double cur = T.idr(i), soc, de;
+    int dt;
+    if (C::stream) {
+      soc = q0.soc, de = q0.de, dt = q0.dt;
+      q0 = q1;
+      q1 = q_at(i + 2);
+    } else {
+      soc = T.soc(i), de = T.de(i), dt = T.dtrem(i);
+    }
     // Ports no lane of the warp occupies are skipped (port mask, uniform
     // branch).  Otherwise branch-free: an empty port holds meta 0 and zero
     // slots, its current is 0 (phase 1), so the arithmetic below yields
@@ -1196,8 +1260,9 @@ __device__ __forceinline__ ObsSink make_sink(const Params& P, const Lane& T, int
 // rollout sink: f32 obs through the per-port chunk ring (ObsSink::chunk), or
 // f64 rows directly
 template <int M>
-__device__ __forceinline__ ObsSink make_chunk_sink(const Params& P, const Lane& T, int64_t b0, void* obs_base) {
-  ObsSink S = make_sink<M>(P, T, b0 + T.lane, obs_base, /*in_place=*/false);
+__device__ __forceinline__ ObsSink make_chunk_sink(const Params& P, const Lane& T, int64_t b0, void* obs_base,
+                                                   bool state_to_hbm = false) {
+  ObsSink S = make_sink<M>(P, T, b0 + T.lane, obs_base, /*in_place=*/state_to_hbm);
   if (!S.row64) {
     S.chunk = true;
     S.gtile = reinterpret_cast<float*>(obs_base) + b0 * P.obs_len;

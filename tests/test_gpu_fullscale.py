@@ -107,7 +107,7 @@ def test_c4_full_scale_every_row():
 
     rc = c4_setup()
     env, pol, hb, hp = _paired(rc, 1 << 18, master=3, pseed=5)
-    _run_full(env, pol, hb, hp, steps=300, slab=1024, mode=3)
+    _run_full(env, pol, hb, hp, steps=300, slab=1024, mode=4)  # streamed tile (Spec<4>)
     env.close()
 
 

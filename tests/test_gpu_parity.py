@@ -76,7 +76,7 @@ def test_golden_trajectory_f32_device_path(name):
 
 
 LEAN = {"bp_coarse_dt": 1, "bp_default": 1, "bp_no_discharge": 1, "c1_default": 1, "default_maxcharge": 1,
-        "bp_random_tree": 2, "c4_highway64": 3, "c5_nested_residential_us": 2, "c5_single_highway_world": 1,
+        "bp_random_tree": 2, "c4_highway64": 4, "c5_nested_residential_us": 2, "c5_single_highway_world": 1,
         "c2_default_tile": 1}
 
 

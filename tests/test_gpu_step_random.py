@@ -18,11 +18,11 @@ from scenarios import Fixture  # noqa: E402
 STATE = ("occ", "soc", "de", "i_drawn", "dtrem", "step", "day", "episode", "ep_reward", "ep_profit")
 
 
-def _pair(B, obs_dtype, steps, device_counter=False, seed=7, index0=0, master=3):
+def _pair(B, obs_dtype, steps, device_counter=False, seed=7, index0=0, master=3, rc=None):
     from paper_2507_01522_b200 import EnvConfig, default_setup
     from paper_2507_01522_b200.batch import BatchEnv, DeviceRandomPolicy
 
-    rc = default_setup(EnvConfig(episode_steps=40), days=20)
+    rc = rc or default_setup(EnvConfig(episode_steps=40), days=20)
     envs = [BatchEnv(rc.env, rc.station, rc.dataset, batch_size=B, master_seed=master, obs_dtype=obs_dtype)
             for _ in range(2)]
     pols = [DeviceRandomPolicy(seed, envs[0].n_ports, rc.env.discretization_k) for _ in range(2)]
@@ -134,3 +134,21 @@ def test_fused_policy_step_equals_reference_actions_and_oracle():
         np.testing.assert_array_equal(r.cpu().numpy(), r_h.astype(np.float32))
         np.testing.assert_array_equal(d.cpu().numpy().astype(bool), d_h)
     env.close()
+
+
+@pytest.mark.parametrize("B", [1000, 4096])
+def test_fused_policy_step_streamed_c4_tile(B):
+    """Config C4's 64-port battery station runs the streamed tile (Spec<4>:
+    currents resident, soc / energy / dwell read a few ports ahead, obs
+    through the per-port chunk ring).  It equals the two-launch form — the
+    generic kernel for the ragged B = 1000, the same streamed kernel fed
+    staged actions for B = 4096 — over an episode boundary (auto-reset obs)."""
+    from paper_2507_01522_b200 import EnvConfig, RunConfig
+    from paper_2507_01522_b200.workloads import c4_setup
+
+    c4 = c4_setup(days=20)
+    env = EnvConfig(battery_enabled=True, alpha=c4.env.alpha, beta=c4.env.beta, episode_steps=30)
+    rc = RunConfig(env=env, station=c4.station, dataset=c4.dataset)
+    modes = _pair(B, torch.float32, 70, rc=rc)
+    assert modes[1] == 4 and modes[0] == (0 if B % 32 else 4), modes
+
