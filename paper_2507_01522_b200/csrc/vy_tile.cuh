@@ -692,7 +692,12 @@ __device__ __forceinline__ void chunk_out6(const ObsSink& S, int lane, uint32_t 
   if (lane >= 30) return;
   float* g = S.glane + 6 * i;
   const uint32_t a = buf + S.soff;
-  if (S.rows == 32) {
+  if (S.rows == 32 && S.s5 == 5 * 105) {
+    // the 16-port station (obs_len 105): row offsets are immediates of the stores
+#pragma unroll
+    for (int k = 0; k < 6; ++k) __stcs(g + 525 * k, lds_f32(a + 20 * k));
+    if (lane < 12) __stcs(g + 3150, lds_f32(a + 120));
+  } else if (S.rows == 32) {
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
       __stcs(g, lds_f32(a + 20 * k));
