@@ -453,6 +453,17 @@ def main() -> None:
                                  "(two output sets, D2H on a copy stream overlapping the next step)"}
     env.close()
 
+    if not args.no_extras and world == 1:
+        # the public API call a reference user makes: throughput_probe (engine.py:515-556), wall clock,
+        # one whole 288-step day of 2^20 envs from reset (device RandomPolicy fused into the step)
+        from paper_2507_01522_b200.batch import throughput_probe
+
+        rep = throughput_probe(rc.env, rc.station, rc.dataset, batch_size=B, total_steps=B * rc.env.episode_steps)
+        result["api_probe"] = {"value": rep.steps_per_second, "unit": UNIT, "wall_seconds": rep.wall_seconds,
+                               "total_steps": rep.total_steps, "batch_size": rep.batch_size,
+                               "call": "throughput_probe(default_setup, batch_size=2^20, total_steps=288 * 2^20)",
+                               "note": "wall clock incl. per-step host launch; the whole day from reset"}
+
     if not args.no_extras:
         # config C4: 64 DC ports, 3-level splitter tree, battery, profit + satisfaction reward
         rc4 = c4_setup()
@@ -493,8 +504,24 @@ def main() -> None:
                                     "log-prob/entropy head, fused Adam"),
                          "grad_allreduce": "NCCL all_reduce per minibatch" if world > 1 else "none (1 GPU)",
                          "paper_reference": "Chargax PPO(16) 0.65 s / 100k on RTX 4000 Ada (PAPER.md:239); a "
-                                            "different workload (16 envs, 900-sample minibatches)"}
+                                            "different workload (16 envs, 900-sample minibatches): see ppo_paper"}
         penv.close()
+        if world == 1:
+            # the paper's own PPO workload: Table 4 -- 12 vectorised envs, rollout 300
+            # (batch 3600), 4 minibatches of 900, 4 epochs -- and the PPO(16) row's 16 envs
+            legs = {}
+            for n_envs in (12, 16):
+                qenv = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=n_envs, master_seed=1)
+                qtr = PPOTrainer(qenv, PPOConfig(rollout_steps=300))
+                qres = seconds_per_100k(qtr, 6, warmup=1)
+                legs[f"envs_{n_envs}"] = {"value": qres["s_per_100k_steps"], "env_steps_per_s": qres["env_steps_per_s"],
+                                          "minibatch": n_envs * 300 // 4, "timed_iterations": 6}
+                qenv.close()
+            result["ppo_paper"] = {"metric": "s per 100k PPO steps", "unit": "s", "higher_is_better": False,
+                                   "legs": legs, "paper": {"PPO(16)": 0.65, "PPO(1)": 9.79, "hardware":
+                                                           "RTX 4000 Ada (PAPER.md:239)"},
+                                   "note": "same trainer and kernels as the ppo leg; at 12-16 envs a step is "
+                                           "launch/latency bound (CUDA graphs: one replay per rollout, one per update)"}
 
     if not args.no_extras:
         # config C5: 36 heterogeneous (region, scenario, traffic, station layout) groups sharing the GPU,
@@ -526,7 +553,7 @@ def main() -> None:
                             "groups": len(hb.groups), "envs_per_gpu": hb.total, "global_envs": hb.total * world,
                             "kernels_per_step": 1, "graph_launches_per_step": 1,
                             "step": "k_step_multi: one persistent launch over all groups, per-tile config index, "
-                                    "per-group Params stacked in device memory, distinct table sets staged per CTA",
+                                    "group Params in a constant-memory table, distinct table sets staged per CTA",
                             "multi": hb.multi_info(),
                             "per_group_streams": {"value": streams_value, "kernels_per_step": kernels_streams,
                                                   "note": "one fused step kernel per group on 12 streams, "
