@@ -177,14 +177,15 @@ TileLayout tile_layout(const vy_tables& t, bool rollout, bool acts, bool stream 
     L.acts = off;
     if (acts) off += ((32 * (n + 1)) + 15) & ~15;
     L.obs = (off + 15) & ~15;
-    off = L.obs + std::max(2 * kChunkBuf, (9 + t.horizon) * kChunkCol * 4);
+    off = L.obs + (kRingBufs == 1 ? kChunkBuf : std::max(2 * kChunkBuf, (9 + t.horizon) * kChunkCol * 4));
     L.bar = (off + 15) & ~15;
     off = L.bar + 16;
     L.bytes = (off + 127) & ~127;
     return L;
   }
   L.ps = 768;
-  L.ports = (24 * n + 15) & ~15;
+  // the 24n-byte pad lets in-place obs staging (k_step) run ahead of the slots; rollouts stage elsewhere
+  L.ports = rollout && kRingBufs == 1 ? 0 : (24 * n + 15) & ~15;
   int off = L.ports + n * 768;
   L.dtrem = off;
   off += n * 64;
@@ -197,7 +198,7 @@ TileLayout tile_layout(const vy_tables& t, bool rollout, bool acts, bool stream 
   if (rollout) {
     // f32 obs leave through the per-port chunk ring (ObsSink::chunk): two
     // 6-column buffers, also holding the 9 + horizon tail columns
-    const int ring = std::max(2 * kChunkBuf, (9 + t.horizon) * kChunkCol * 4);
+    const int ring = kRingBufs == 1 ? kChunkBuf : std::max(2 * kChunkBuf, (9 + t.horizon) * kChunkCol * 4);
     L.obs = (off + 15) & ~15;
     off = L.obs + ring;
   } else if (off < staging) {
@@ -205,7 +206,7 @@ TileLayout tile_layout(const vy_tables& t, bool rollout, bool acts, bool stream 
   }
   L.bar = (off + 15) & ~15;
   off = L.bar + 16;
-  L.bytes = (off + 127) & ~127;
+  L.bytes = rollout && kRingBufs == 1 ? (off + 15) & ~15 : (off + 127) & ~127;
   return L;
 }
 

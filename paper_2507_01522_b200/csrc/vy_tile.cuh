@@ -684,6 +684,14 @@ struct ObsSink {
 // read-out's (column f, row r) words 37f + r hit distinct banks for f < 6, r < 5
 constexpr int kChunkCol = 37;
 constexpr int kChunkBuf = 6 * kChunkCol * 4;  // bytes per 6-column buffer
+// VY_RING1 (default): one 6-column buffer (a second __syncwarp per port) and
+// the tail columns stored from registers by each lane, so a rollout tile
+// fits 15 warps per SM instead of 14 (rollout -2.8%, streamed C4 -4.8% step
+// time against the two-buffer ring, profiles/r2_ring_ab.txt)
+#ifndef VY_RING1
+#define VY_RING1 1
+#endif
+constexpr int kRingBufs = VY_RING1 ? 1 : 2;
 
 // chunk mode: coalesced read-out of port i's 6 staged columns (ring buffer
 // `buf`) into global obs columns [6i, 6i + 6): lanes 0..29 store rows l / 6 +
@@ -748,11 +756,12 @@ __device__ __forceinline__ void stage_port_obs(const Params& P, Prof prof, const
 #pragma unroll
         for (int f = 0; f < 6; ++f) S.gtile[(int64_t)lane * P.obs_len + 6 * i + f] = (float)v[f];
     } else {
-      const uint32_t buf = S.cells + (i & 1) * kChunkBuf;
+      const uint32_t buf = S.cells + (kRingBufs == 2 ? (i & 1) * kChunkBuf : 0);
 #pragma unroll
       for (int f = 0; f < 6; ++f) sts_f32(buf + f * (kChunkCol * 4) + lane * 4, (float)v[f]);
       __syncwarp();  // also orders the read-out of port i - 1 (other buffer) before port i + 1 reuses it
       chunk_out6(S, lane, buf, i);
+      if (kRingBufs == 1) __syncwarp();  // one buffer: read out before the next port stages
     }
   } else {
     const uint32_t col = S.cells + 6 * i * 132 + lane * 4;
@@ -1304,6 +1313,21 @@ __device__ __forceinline__ void emit_tail(const Params& P, const Lane& T, const 
   // chunk mode: the tail columns are staged from column 0 of the chunk ring
   // (stride kChunkCol words) once every lane's earlier read-outs are done
   if (S.chunk) __syncwarp();
+  if (S.chunk && kRingBufs == 1) {
+    // single-buffer ring: each lane stores its own row's tail columns
+    if (active) {
+      float* row = S.gtile + (int64_t)lane * OL + c0;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) __stcs(row + k, (float)gv[k]);
+      for (int h = 0; h < Spec<M>::horizon(P); ++h) {
+        const int64_t fmin = (int64_t)(E.step + 1 + h) * P.dt_min;
+        const int64_t fday = ((int64_t)E.day + fmin / 1440) % P.n_days;
+        __stcs(row + 9 + h, (float)__ldg(P.buy + fday * 24 + (fmin / 60) % 24));
+      }
+    }
+    __syncwarp();
+    return;
+  }
   const uint32_t tcell = S.chunk ? S.cells + lane * 4 : S.cells + c0 * 132 + lane * 4;
   const uint32_t tstride = S.chunk ? kChunkCol * 4 : 132;
 #pragma unroll
