@@ -464,6 +464,29 @@ def main() -> None:
                                "call": "throughput_probe(default_setup, batch_size=2^20, total_steps=288 * 2^20)",
                                "note": "wall clock incl. per-step host launch; the whole day from reset"}
 
+    if not args.no_extras and world == 1:
+        # config C1 (the reference's own CPU-runnable case: 16 envs x 288-step episodes) on the GPU: the fused
+        # rollout on the small-batch kernel (one warp per env, one lane per port), one launch per episode
+        c1 = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=16, master_seed=0)
+        c1.reset(as_numpy=False)
+        T1 = rc.env.episode_steps
+        o1 = torch.empty(T1, 16, c1.obs_length, device=dev)
+        r1 = torch.empty(T1, 16, device=dev)
+        d1 = torch.empty(T1, 16, dtype=torch.uint8, device=dev)
+        c1.rollout(T1, 0, 0, o1, r1, d1)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record(stream)
+        for rep in range(5):
+            c1.rollout(T1, 0, (rep + 1) * T1, o1, r1, d1)
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        c1ms = ev[0].elapsed_time(ev[1]) / 5
+        result["c1"] = {"metric": METRIC, "value": 16 * T1 / (c1ms / 1e3), "unit": UNIT, "envs": 16, "T": T1,
+                        "ms_per_episode": c1ms, "kernel": f"k_rollout_wide (mode {c1.last_step_mode()})",
+                        "note": "config C1 on one B200: latency-bound (3 us per step of 16 envs); the reference "
+                                "arm's api_level.c1_literal is the same workload on the host"}
+        c1.close()
+
     if not args.no_extras:
         # config C4: 64 DC ports, 3-level splitter tree, battery, profit + satisfaction reward
         rc4 = c4_setup()

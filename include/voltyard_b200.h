@@ -244,6 +244,14 @@ int32_t vy_last_step_mode(vy_handle *h);
  * ceil(tiles / (warps per CTA * k)) CTAs, so each warp steps about k 32-env
  * tiles.  Default 1 (as many CTAs as fit).  Results never depend on it. */
 int vy_set_tiles_per_warp(vy_handle *h, int32_t k);
+/* Small-batch kernel choice: 1 = one warp per env / one lane per port
+ * (k_rollout_wide: low latency at small batches, e.g. config C1's 16 envs) for
+ * vy_rollout and for vy_step with staged uint8 actions and auto-reset, 0 = one
+ * thread per env, -1 = by batch size (default: vy_rollout goes wide at <= 4096
+ * envs, vy_step stays on the tile kernel).  Wide needs a lean station without
+ * a battery, <= 32 ports, float32 obs; otherwise the tile kernels run.
+ * Outputs are identical. */
+int vy_set_wide(vy_handle *h, int32_t mode);
 
 /* Heterogeneous batch in one launch (config C5).  The
  * reference steps one (config, station, dataset) per BatchEnv (engine.py:370,

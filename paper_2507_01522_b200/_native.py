@@ -64,6 +64,7 @@ _SIGS = {
     "vy_launch_count": (C.c_int64, [_P]),
     "vy_last_step_mode": (C.c_int32, [_P]),
     "vy_set_tiles_per_warp": (C.c_int, [_P, C.c_int32]),
+    "vy_set_wide": (C.c_int, [_P, C.c_int32]),
     "vy_gae": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_int64, C.c_float, C.c_float, _P, _P, _P]),
     "vy_ppo_sample": (C.c_int, [_P, C.c_int32, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]),
     "vy_ppo_sample_rng": (C.c_int, [_P, C.c_int32, C.c_int64, C.c_uint64, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P,

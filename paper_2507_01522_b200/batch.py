@@ -503,6 +503,14 @@ class BatchEnv:
         other batches (HeteroBatch): about k 32-env tiles per warp."""
         nat.check(self._lib.vy_set_tiles_per_warp(self._h, int(k)), "vy_set_tiles_per_warp")
 
+    def set_wide(self, mode: int) -> None:
+        """Small-batch kernel: 1 = one warp per env / one lane per port (low
+        latency at small batches) for rollouts and for steps with uint8
+        actions, 0 = one thread per env, -1 = by batch size (default: rollouts
+        of <= 4096 envs go wide, steps stay on the tile kernel).  Outputs are
+        identical either way (vy_set_wide)."""
+        nat.check(self._lib.vy_set_wide(self._h, int(mode)), "vy_set_wide")
+
     def last_step_mode(self) -> int:
         """Step-kernel instantiation of the last step (1/2 lean, 0 generic; diagnostics)."""
         return int(self._lib.vy_last_step_mode(self._h))

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "vy_kernels.cuh"
+#include "vy_wide.cuh"
 
 using namespace vy;
 
@@ -158,6 +159,7 @@ struct vy_handle {
   int smem_per_sm = 0, num_sms = 0;
   int last_mode = -1;  // Spec<M> of the last vy_step launch (diagnostics)
   int tiles_per_warp = 1;  // persistent k_step grid: at most ceil(tiles / (warps per CTA * this)) CTAs
+  int wide = -1;           // rollout kernel: 1 warp-per-env (k_rollout_wide), 0 tiles, -1 by batch size
 };
 
 namespace {
@@ -619,6 +621,23 @@ int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride
                     (reinterpret_cast<uintptr_t>(actions) % 16) == 0 && (32 * na) % 16 == 0 &&
                     (h->B % 32) == 0;
   const int mode = step_mode(h, flags, acts);
+  // small batches: the one-warp-per-env kernel for a single step (auto-reset on, staged uint8 rows),
+  // when the handle asks for it (vy_set_wide(h, 1); the PPO trainer does at its batch sizes)
+  if ((mode == 1 || mode == 2) && flags == VY_F_AUTO_RESET && h->t.n_ports <= 32 && h->wide == 1) {
+    Params P;
+    fill(h, P, true, false);
+    P.flags = flags;
+    const int smem = tables_bytes(P.n_profiles, P.k, P.n_ports, P.n_nodes) + kWideWarps * 32 * 8;
+    auto* kern = mode == 1 ? k_rollout_wide<1> : k_rollout_wide<2>;
+    if (smem > 48 * 1024) VY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const unsigned grid = (unsigned)((h->B + kWideWarps - 1) / kWideWarps);
+    kern<<<grid, 32 * kWideWarps, smem, (cudaStream_t)stream>>>(P, 1, 0, 0, 0, 0, 0,
+                                                                  static_cast<const uint8_t*>(actions));
+    VY_CUDA(cudaGetLastError());
+    ++h->launches;
+    h->last_mode = 10 + mode;
+    return VY_OK;
+  }
   Params P;
   fill(h, P, false, acts, mode == 4);
   P.flags = flags;
@@ -718,6 +737,29 @@ int vy_rollout(vy_handle* h, int32_t T, uint64_t policy_seed, int64_t index0, in
   P.out.done = done;
   Geometry g;
   int mode = step_mode(h, flags, true);
+  // small batches: one warp per env, one lane per port (vy_wide.cuh) — lean
+  // stations without a battery, <= 32 ports; by default up to 4096 envs, where
+  // the tile kernel is latency-bound (16 envs: 3.2 vs 10 us per step; 4096:
+  // 8.3 vs 12.2 us, scripts/probe_c1.py)
+  const bool wide_ok = (mode == 1 || mode == 2) && h->t.n_ports <= 32 && !(flags & VY_F_OUT_F64);
+  if (wide_ok && (h->wide == 1 || (h->wide < 0 && h->B <= 4096))) {
+    Params P;
+    fill(h, P, true, false);
+    P.flags = flags;
+    P.out.obs = obs;
+    P.out.reward = reward;
+    P.out.done = done;
+    const int smem = tables_bytes(P.n_profiles, P.k, P.n_ports, P.n_nodes) + kWideWarps * 32 * 8;
+    auto* kern = mode == 1 ? k_rollout_wide<1> : k_rollout_wide<2>;
+    if (smem > 48 * 1024) VY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const unsigned grid = (unsigned)((h->B + kWideWarps - 1) / kWideWarps);
+    kern<<<grid, 32 * kWideWarps, smem, (cudaStream_t)stream>>>(P, T, policy_seed, index0, call0, obs_step_stride,
+                                                                  rew_step_stride, nullptr);
+    VY_CUDA(cudaGetLastError());
+    ++h->launches;
+    h->last_mode = 10 + mode;  // diagnostics: 11 / 12 = wide rollout
+    return VY_OK;
+  }
   if (mode == 4) mode = 3;  // a rollout keeps the whole tile resident for its T steps
   auto* kern = mode == 1 ? k_rollout<1> : mode == 2 ? k_rollout<2> : mode == 3 ? k_rollout<3> : k_rollout<0>;
   if (int rc = geometry(h, kern, P.L, P.n_profiles, g)) return rc;
@@ -738,6 +780,12 @@ int vy_poll_error(vy_handle* h, int clear, void* stream, uint32_t* out) {
 
 int64_t vy_launch_count(vy_handle* h) { return h ? h->launches : -1; }
 int32_t vy_last_step_mode(vy_handle* h) { return h ? h->last_mode : -1; }
+
+int vy_set_wide(vy_handle* h, int32_t mode) {
+  if (!h || mode < -1 || mode > 1) return fail(VY_ERR_ARG, "wide mode must be -1 (auto), 0 or 1");
+  h->wide = mode;
+  return VY_OK;
+}
 
 int vy_set_tiles_per_warp(vy_handle* h, int32_t k) {
   if (!h || k < 1) return fail(VY_ERR_ARG, "tiles per warp must be >= 1");

@@ -62,6 +62,7 @@ class PPOConfig:
     graph_update: bool = True  # the whole update (GAE + epochs x minibatches + Adam) as one CUDA graph (1 GPU)
     fused_policy: bool = True  # rollout forward + sampling in the tcgen05 kernel (vy_policy_step)
     allreduce: str = "auto"  # gradient all-reduce: "auto" (world > 1), "always" (also at world 1: tests)
+    wide_env: bool = True  # env step on the one-warp-per-env kernel at <= 2048 envs (vy_set_wide)
 
 
 def _ortho(layer: nn.Linear, gain: float) -> nn.Linear:
@@ -404,6 +405,12 @@ class PPOTrainer:
     def __init__(self, env: BatchEnv, cfg: PPOConfig):
         self.env, self.cfg = env, cfg
         dev = env.device
+        if cfg.wide_env and env.batch_size <= 2048:
+            # small batches: the tile step is latency-bound (a few warps on the
+            # whole GPU); one warp per env, one lane per port steps in ~8 us
+            # instead of ~14 (scripts/probe_step_small.py; at 4096 envs the
+            # tile step is as fast and the wide one stops paying)
+            env.set_wide(1)
         torch.manual_seed(cfg.seed + env.global_offset)
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         self.net = ActorCritic(env.obs_length, env.action_size, env.actions_per_slot, cfg.hidden).to(dev)
