@@ -31,13 +31,26 @@ for B, dt in ((256, torch.float32), (100, torch.float64)):
     torch.cuda.synchronize()
     env.check_errors()
     env.close()
-# rollout with a ragged last tile
-env = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=77, master_seed=4)
+# rollouts with a ragged last tile: the tile kernel and the one-warp-per-env kernel; wide single steps
+for wide in (0, 1):
+    env = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=77, master_seed=4)
+    env.set_wide(wide)
+    env.reset(as_numpy=False)
+    obs = torch.empty(30, 77, env.obs_length, device="cuda")
+    rew = torch.empty(30, 77, device="cuda")
+    done = torch.empty(30, 77, dtype=torch.uint8, device="cuda")
+    env.rollout(30, 2, 0, obs, rew, done)
+    print("rollout mode", env.last_step_mode())
+    torch.cuda.synchronize()
+    env.close()
+env = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=64, master_seed=4)
+env.set_wide(1)
+pol = DeviceRandomPolicy(seed=1, n_ports=env.n_ports, k=rc.env.discretization_k)
+pol.bind(range(64))
 env.reset(as_numpy=False)
-obs = torch.empty(30, 77, env.obs_length, device="cuda")
-rew = torch.empty(30, 77, device="cuda")
-done = torch.empty(30, 77, dtype=torch.uint8, device="cuda")
-env.rollout(30, 2, 0, obs, rew, done)
+for _ in range(30):
+    env.step(pol.actions(env), collect_infos=False)
+print("step mode", env.last_step_mode())
 torch.cuda.synchronize()
 env.close()
 # streamed C4 tile (ragged), episode boundary
