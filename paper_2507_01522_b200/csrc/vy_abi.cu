@@ -627,7 +627,7 @@ int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride
     Params P;
     fill(h, P, true, false);
     P.flags = flags;
-    const int smem = tables_bytes(P.n_profiles, P.k, P.n_ports, P.n_nodes) + kWideWarps * 32 * 8;
+    const int smem = tables_bytes(P.n_profiles, P.k, P.n_ports, P.n_nodes) + kWideWarps * kWideScratch * 8;
     auto* kern = mode == 1 ? k_rollout_wide<1> : k_rollout_wide<2>;
     if (smem > 48 * 1024) VY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const unsigned grid = (unsigned)((h->B + kWideWarps - 1) / kWideWarps);
@@ -749,7 +749,7 @@ int vy_rollout(vy_handle* h, int32_t T, uint64_t policy_seed, int64_t index0, in
     P.out.obs = obs;
     P.out.reward = reward;
     P.out.done = done;
-    const int smem = tables_bytes(P.n_profiles, P.k, P.n_ports, P.n_nodes) + kWideWarps * 32 * 8;
+    const int smem = tables_bytes(P.n_profiles, P.k, P.n_ports, P.n_nodes) + kWideWarps * kWideScratch * 8;
     auto* kern = mode == 1 ? k_rollout_wide<1> : k_rollout_wide<2>;
     if (smem > 48 * 1024) VY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const unsigned grid = (unsigned)((h->B + kWideWarps - 1) / kWideWarps);

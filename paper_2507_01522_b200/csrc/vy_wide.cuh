@@ -15,10 +15,10 @@
 // operation order are tile_step's (vy_tile.cuh), so the outputs are
 // bit-identical to k_rollout and to the reference.
 //
-// Lean configurations without a battery (Spec<1>: trees of at most
-// kFastNodes nodes, node loads summed on the fly; Spec<2>: any tree, node
-// loads summed from a per-warp shared copy of the currents), at most 32
-// ports, float32 obs.  With `acts` the kernel is also the small-batch single
+// Lean configurations without a battery (Spec<1> / Spec<2>: any tree; node
+// loads are summed from a per-warp shared copy of the currents, the energy
+// flows from a shared copy of the per-port terms, broadcast reads in port
+// order), at most 32 ports, float32 obs.  With `acts` the kernel is also the small-batch single
 // step (T = 1) for caller-supplied uint8 actions (vy_step; the PPO rollout).
 #pragma once
 
@@ -27,6 +27,7 @@
 namespace vy {
 
 constexpr int kWideWarps = 8;  // warps (= envs) per CTA
+constexpr int kWideScratch = 32 + 4 * 32;  // doubles of per-warp shared scratch
 
 // _kernel.pyx:626-649 on a flat array of currents (lane 0 only; rare: a tree
 // node over capacity).  Same values and pass structure as fit_tree.
@@ -78,7 +79,6 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_rollout_wide(const __grid_c
                                                                   uint64_t policy_seed, int64_t index0, int64_t call0,
                                                                   int64_t obs_stride, int64_t rew_stride,
                                                                   const uint8_t* __restrict__ acts) {
-  using C = Spec<M>;
   static_assert(M == 1 || M == 2, "lean stations without a battery");
   Prof prof;
   PortC pc;
@@ -92,7 +92,11 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_rollout_wide(const __grid_c
   const int n = P.n_ports, OL = P.obs_len;
   const bool isport = lane < n;
   const int64_t ld = P.ld;
-  double* cur_s = reinterpret_cast<double*>(vy_smem + tables_bytes(P.n_profiles, P.k, P.n_ports, P.n_nodes)) + warp * 32;
+  // per-warp scratch: the ports' currents (node loads, rescale) and their
+  // energy-flow terms {got, in, out, -} (the sequential flow sums)
+  double* cur_s = reinterpret_cast<double*>(vy_smem + tables_bytes(P.n_profiles, P.k, P.n_ports, P.n_nodes)) +
+                  warp * kWideScratch;
+  double* flow_s = cur_s + 32;
 
   // this lane's port: constants for all T steps, state in registers
   double imax_c = 0.0, imax_d = 0.0, volt = 1.0, rcp_volt = 1.0, kindv = 0.0, nodesv = 0.0;
@@ -128,6 +132,9 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_rollout_wide(const __grid_c
     float* orow = reinterpret_cast<float*>(P.out.obs) + t * obs_stride + b * OL;
     const int tt = E.step;
     const Frame F = load_frame<M>(P, tt, E.day);
+    // the obs globals of the state after this step, in flight during it (lanes 0..8 write them)
+    ObsGlobals G{};
+    if (lane < 9) G = load_obs_globals(P, tt + 1, E.day);
     // slot j's action on lane j: RandomPolicy (policies.py:51-73), or the
     // caller's uint8 rows [B][n+1] (vy_step: one step, acts != null)
     int a = P.k;
@@ -158,40 +165,23 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_rollout_wide(const __grid_c
     // tree: excess on the requested currents (_kernel.pyx:611-624), node loads in leaf order
     double excess = 0.0;
     uint64_t clean = 0;
-    if (C::fast_tree(P)) {
-      double nsum[kFastNodes];
-#pragma unroll
-      for (int m = 0; m < kFastNodes; ++m) nsum[m] = 0.0;
-      for (int j = 0; j < n; ++j) {
-        const double cj = __shfl_sync(FULL, c, j);
-        const uint32_t pj = __shfl_sync(FULL, pm, j);
-#pragma unroll
-        for (int m = 0; m < kFastNodes; ++m)
-          if (pj & (1u << m)) nsum[m] += cj;
-      }
-#pragma unroll
-      for (int m = 0; m < kFastNodes; ++m) {
-        if (m < P.n_nodes) {
-          const double over = fabs(node_load(nsum[m], P.node_eta[m], P.node_rcp_eta[m])) - P.node_cap[m];
-          if (over > excess) excess = over;
-        }
-      }
-    } else {
-      if (isport) cur_s[lane] = c;
-      __syncwarp();
-      for (int q = 0; q < P.n_nodes; ++q) {
-        double cap, eta, rcp_eta;
-        int lo, hq;
-        tc.rec(q, cap, eta, rcp_eta, lo, hq);
-        const int hp = hq < n ? hq : n;
-        double s = 0.0;
-        for (int j = lo; j < hp; ++j) s += cur_s[j];
-        const double over = fabs(node_load(s, eta, rcp_eta)) - cap;
-        if (over > excess) excess = over;
-        if (!(over > 0.0)) clean |= 1ull << (q & 63);
-      }
-      __syncwarp();
+    // node loads from a shared copy of the currents, each node's range summed
+    // in leaf order (a per-port shuffle + masked adds for up to kFastNodes
+    // nodes measured 18% of the kernel's instructions)
+    if (isport) cur_s[lane] = c;
+    __syncwarp();
+    for (int q = 0; q < P.n_nodes; ++q) {
+      double cap, eta, rcp_eta;
+      int lo, hq;
+      tc.rec(q, cap, eta, rcp_eta, lo, hq);
+      const int hp = hq < n ? hq : n;
+      double s = 0.0;
+      for (int j = lo; j < hp; ++j) s += cur_s[j];
+      const double over = fabs(node_load(s, eta, rcp_eta)) - cap;
+      if (over > excess) excess = over;
+      if (!(over > 0.0)) clean |= 1ull << (q & 63);
     }
+    __syncwarp();
     if (excess > 0.0) {  // warp-uniform: every lane summed the same values
       if (isport) cur_s[lane] = c;
       __syncwarp();
@@ -236,11 +226,19 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_rollout_wide(const __grid_c
     }
     // the reference's sequential sums over the ports, in port order, on every lane
     double e_net = 0.0, e_in = 0.0, e_out = 0.0;
-    for (int j = 0; j < n; ++j) {
-      e_net += __shfl_sync(FULL, got, j);
-      e_in += __shfl_sync(FULL, t_in, j);
-      e_out += __shfl_sync(FULL, t_out, j);
+    if (isport) {
+      flow_s[4 * lane] = got;
+      flow_s[4 * lane + 1] = t_in;
+      flow_s[4 * lane + 2] = t_out;
     }
+    __syncwarp();
+    for (int j = 0; j < n; ++j) {  // broadcast reads: one 16-byte and one 8-byte load per port
+      const double2 gi = *reinterpret_cast<const double2*>(flow_s + 4 * j);
+      e_net += gi.x;
+      e_in += gi.y;
+      e_out += flow_s[4 * j + 2];
+    }
+    __syncwarp();
     double sat0 = 0.0, sat1 = 0.0;
     const unsigned depm = __ballot_sync(FULL, dep);
     if (depm) {
@@ -355,7 +353,7 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_rollout_wide(const __grid_c
       __stcs(pr + 5, (float)((mt >> 1) & 1u));
     }
     if (lane < 9) {
-      const ObsGlobals G = load_obs_globals(P, E.step, E.day);
+      if (done) G = load_obs_globals(P, E.step, E.day);  // reset: the new episode's day
       const double v = lane == 0 ? E.b_soc
                        : lane == 1 ? div_rcp(E.b_i, P.b_idenom, P.b_rcp_idenom)
                        : lane == 2 ? G.buy
