@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_wide.py tests/test_gpu_parity.py -m gpu -q -x -k "wide or rollout" > gpurun_out/t_wide.log 2>&1; echo rc=$? >> gpurun_out/t_wide.log
-for v in ab/wide_base.so ab/wide_v2.so ab/wide_base.so ab/wide_v2.so; do cp $v paper_2507_01522_b200/libvoltyard_b200.so; echo "== $v"; timeout 200 python scripts/probe_c1.py 2>&1 | grep wide; timeout 200 python scripts/probe_c1.py --B 4096 2>&1 | grep wide; done > gpurun_out/ab.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_step_random.py tests/test_gpu_fullscale.py -m gpu -q -x -k "golden or fused or every_row or rollout or c2" > gpurun_out/t_nw.log 2>&1; echo rc=$? >> gpurun_out/t_nw.log
+bash scripts/ab_roll.sh ab/base3.so ab/nw.so > gpurun_out/ab.log 2>&1
