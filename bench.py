@@ -445,10 +445,30 @@ def main() -> None:
         ems_serial = e2e_run(False)
         ems = e2e_run(True)
         env.restore_outputs()
+
+        def pcie_ms() -> float:
+            """The bus alone: the same D2H bytes with the H2D bytes concurrently, no kernel."""
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(e_steps):
+                for h, d in zip(h_out[0], d_out[0]):
+                    h.copy_(d, non_blocking=True)
+                with torch.cuda.stream(copy_stream):
+                    d_act.copy_(h_act, non_blocking=True)
+            stream.wait_stream(copy_stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / e_steps
+
+        bus_ms = pcie_ms()
         result["e2e"] = {"value": e_steps * B * world / (ems / 1e3), "unit": UNIT,
                          "h2d_bytes_per_step": h_act.numel(),
                          "d2h_bytes_per_step": sum(t.numel() * t.element_size() for t in h_out[0]),
                          "serial_value": e_steps * B * world / (ems_serial / 1e3),
+                         "pcie_bound": B * world / (bus_ms / 1e3),
+                         "pcie_frac": (e_steps * B / (ems / 1e3)) / (B / (bus_ms / 1e3)),
+                         "pcie_note": "pcie_bound: the same bytes copied alone (pinned D2H with the H2D concurrent), "
+                                      "measured in this run",
                          "path": "BatchEnv.step with pinned host actions -> obs/reward/done to pinned host "
                                  "(two output sets, D2H on a copy stream overlapping the next step)"}
     env.close()
