@@ -543,8 +543,9 @@ def main() -> None:
                                                                / (4096 * world * cfg.rollout_steps),
                          "rollout": tr.describe_rollout() if hasattr(tr, "describe_rollout") else None,
                          "update": ("one CUDA graph per update: vy_gae, vy_gather_rows minibatch gather, bf16 GEMMs "
-                                    "with column-sum bias gradients (vy_colsum), vy_ppo_head_fwd/_bwd fused "
-                                    "log-prob/entropy head, fused Adam"),
+                                    "with column-sum bias gradients (vy_colsum), vy_ppo_loss (log-prob, entropy, "
+                                    "value, clipped surrogate / value losses and d loss / d head rows in one pass), "
+                                    "fused Adam"),
                          "grad_allreduce": "NCCL all_reduce per minibatch" if world > 1 else "none (1 GPU)",
                          "paper_reference": "Chargax PPO(16) 0.65 s / 100k on RTX 4000 Ada (PAPER.md:239); a "
                                             "different workload (16 envs, 900-sample minibatches): see ppo_paper"}

@@ -253,6 +253,19 @@ int vy_set_tiles_per_warp(vy_handle *h, int32_t k);
  * Outputs are identical. */
 int vy_set_wide(vy_handle *h, int32_t mode);
 
+/* PPO minibatch loss head in one pass (vy_ppo.cu): from bf16 head rows
+ * (S slots x A logits, the value in padding column value_col, row stride ld)
+ * and the stored actions, the per-sample {old log-prob, old value, advantage,
+ * return} rows (float32 x 4, 16-byte aligned) and the advantage mean / std
+ * (device, 2 floats): the log-probabilities, entropies, values, the clipped
+ * surrogate + clipped value loss + entropy bonus of PAPER.md:465-490, and
+ * their gradient with respect to the head rows (bf16, same layout) for the
+ * mean loss.  stats (device, 4 floats, zeroed by the caller) receives the
+ * sums of {loss, pg, vf, ent} over the N samples. */
+int vy_ppo_loss(const void *logits, int64_t ld, const uint8_t *actions, int64_t N, int32_t S, int32_t A,
+                const float *scal4, const float *adv_stats, float clip_eps, float vf_clip, float vf_coef,
+                float ent_coef, int32_t value_col, void *grad, float *stats, void *stream);
+
 /* Heterogeneous batch in one launch (config C5).  The
  * reference steps one (config, station, dataset) per BatchEnv (engine.py:370,
  * SPEC.md:482); a multi handle stacks n bound group handles (each keeps its

@@ -272,6 +272,139 @@ __global__ void __launch_bounds__(kHeadThreads) k_ppo_head_bwd(const T* __restri
   cp_async_wait<0>();
 }
 
+// The whole PPO minibatch loss head in one pass over the logits: per
+// sample the log-probability of the stored actions and the entropy (as
+// k_ppo_head_fwd), the value from its padding column, the clipped surrogate,
+// clipped value loss and entropy bonus (PPO; torch's
+// min / max / clamp subgradients: ties split evenly, clamp bounds inclusive),
+// and the gradient of
+//   loss = mean(-min(r a, clip(r) a)) + vf_coef * mean(0.5 max((v-R)^2, (v_c-R)^2)) - ent_coef * mean(H)
+// with respect to the logits rows (as k_ppo_head_bwd with the per-sample
+// upstream gradients computed in place).  a = normalised advantage, from the
+// minibatch mean / std in `adv_stats` (device).  Per-block partial sums of
+// {loss, pg, vf, ent} (x N) go to `stats` with one atomic each per block.
+struct LossCfg {
+  float clip_eps, vf_clip, vf_coef, ent_coef;
+};
+
+template <class T, int AC>
+__global__ void __launch_bounds__(kHeadThreads) k_ppo_loss(const T* __restrict__ logits,
+                                                           const uint8_t* __restrict__ actions, int64_t N, int S,
+                                                           int A, int64_t ld, int G, const float4* __restrict__ scal,
+                                                           const float* __restrict__ adv_stats, LossCfg cfg,
+                                                           int value_col, T* __restrict__ grad,
+                                                           float* __restrict__ stats) {
+  extern __shared__ __align__(16) unsigned char ppo_raw[];
+  const size_t rb = raw_rows_bytes<T>(G, ld);
+  T* buf0 = reinterpret_cast<T*>(ppo_raw);
+  T* buf1 = reinterpret_cast<T*>(ppo_raw + rb);
+  float* out = reinterpret_cast<float*>(ppo_raw + 2 * rb);  // [G][ld]
+  float* part = out + (size_t)G * ld;                       // [2][G*S] slot partials
+  float* gs = part + 2 * (size_t)G * S;                     // [3][G] per-sample g_lp, g_ent, g_v
+  const int SA = S * A, pad = (int)(ld - SA);
+  const int64_t nch = (N + G - 1) / G;
+  const int t = threadIdx.x;
+  const float inv_n = 1.f / (float)N;
+  const float amean = adv_stats[0], astd = adv_stats[1];
+  float acc_loss = 0.f, acc_pg = 0.f, acc_vf = 0.f, acc_ent = 0.f;  // samples of thread t (t < G)
+  int64_t c = blockIdx.x;
+  if (c < nch) issue_rows(logits + c * G * ld, (int64_t)min((int64_t)G, N - c * G) * ld, buf0);
+  cp_async_commit();
+  for (int i = 0; c < nch; c += gridDim.x, ++i) {
+    const int64_t cn = c + gridDim.x;
+    T* cur = (i & 1) ? buf1 : buf0;
+    if (cn < nch) issue_rows(logits + cn * G * ld, (int64_t)min((int64_t)G, N - cn * G) * ld, (i & 1) ? buf0 : buf1);
+    cp_async_commit();
+    const int64_t n0 = c * G;
+    const int gh = (int)min((int64_t)G, N - n0);
+    const bool live = t < gh * S;
+    const int r = live ? t / S : 0, s = t - r * S;
+    const int a = live ? actions[n0 * S + t] : 0;
+    float4 sc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t < gh) sc = scal[n0 + t];
+    cp_async_wait<1>();
+    __syncthreads();  // chunk c landed; the previous chunk's gradient rows have left `out`
+    // per (sample, slot): softmax statistics, log-probability of the action, entropy
+    float m = 0.f, logsum = 0.f, inv = 0.f, h = 0.f;
+    const T* zs = cur + (size_t)r * ld + s * A;
+    if (live) {
+      const Slot<AC, T> z(zs, A);
+      slot_stats(z, m, logsum, inv, h);
+      part[t] = (to_f(zs[a]) - m) - logsum;
+      part[G * S + t] = h;
+    }
+    __syncthreads();
+    // per sample: the loss terms and their gradients with respect to lp, H, v
+    if (t < gh) {
+      float lp = 0.f, ent = 0.f;
+      for (int q = 0; q < S; ++q) {
+        lp += part[t * S + q];
+        ent += part[G * S + t * S + q];
+      }
+      const float v = to_f(cur[(size_t)t * ld + value_col]);
+      const float old_lp = sc.x, old_v = sc.y, an = (sc.z - amean) / (astd + 1e-8f), ret = sc.w;
+      const float ratio = expf(lp - old_lp);
+      const float u = ratio * an;
+      const float rc = fminf(fmaxf(ratio, 1.f - cfg.clip_eps), 1.f + cfg.clip_eps);
+      const float cc = rc * an;
+      const float pg = -fminf(u, cc);
+      const bool inside = ratio >= 1.f - cfg.clip_eps && ratio <= 1.f + cfg.clip_eps;
+      const float du = u < cc ? 1.f : (u > cc ? 0.f : 0.5f), dc = 1.f - du;
+      const float g_lp = -(du + dc * (inside ? 1.f : 0.f)) * an * ratio * inv_n;
+      const float dv = v - old_v;
+      const float dvc = fminf(fmaxf(dv, -cfg.vf_clip), cfg.vf_clip);
+      const float vc = old_v + dvc;
+      const float e1 = (v - ret) * (v - ret), e2 = (vc - ret) * (vc - ret);
+      const float vl = 0.5f * fmaxf(e1, e2);
+      const float d1 = e1 > e2 ? 1.f : (e1 < e2 ? 0.f : 0.5f), d2 = 1.f - d1;
+      const bool vin = dv >= -cfg.vf_clip && dv <= cfg.vf_clip;
+      const float g_v = cfg.vf_coef * inv_n * (d1 * (v - ret) + d2 * (vc - ret) * (vin ? 1.f : 0.f));
+      gs[t] = g_lp;
+      gs[G + t] = -cfg.ent_coef * inv_n;
+      gs[2 * G + t] = g_v;
+      acc_pg += pg;
+      acc_vf += vl;
+      acc_ent += ent;
+      acc_loss += pg + cfg.vf_coef * vl - cfg.ent_coef * ent;
+    }
+    __syncthreads();
+    // per (sample, slot): d loss / d logits (k_ppo_head_bwd's formula)
+    if (live) {
+      const float gl = gs[r], ge = gs[G + r];
+      float* os = out + (size_t)r * ld + s * A;
+      const Slot<AC, T> z(zs, A);
+#pragma unroll
+      for (int k = 0; k < z.size(); ++k) {
+        const float d = z[k] - m, p = __expf(d) * inv, l = d - logsum;
+        os[k] = gl * ((k == a ? 1.f : 0.f) - p) - ge * p * (l + h);
+      }
+    }
+    for (int j = t; j < gh * pad; j += blockDim.x) {  // padding columns: 0, or the value head's gradient
+      const int rr = j / pad, col = SA + (j - rr * pad);
+      out[(size_t)rr * ld + col] = col == value_col ? gs[2 * G + rr] : 0.f;
+    }
+    __syncthreads();
+    store_rows(out, (int64_t)gh * ld, grad + n0 * ld);
+  }
+  cp_async_wait<0>();
+  // the block's partial sums: threads 0..G-1 hold them (warp 0 when G <= 32)
+  if (t < 32) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc_loss += __shfl_down_sync(0xffffffffu, acc_loss, o);
+      acc_pg += __shfl_down_sync(0xffffffffu, acc_pg, o);
+      acc_vf += __shfl_down_sync(0xffffffffu, acc_vf, o);
+      acc_ent += __shfl_down_sync(0xffffffffu, acc_ent, o);
+    }
+    if (t == 0) {
+      atomicAdd(stats, acc_loss);
+      atomicAdd(stats + 1, acc_pg);
+      atomicAdd(stats + 2, acc_vf);
+      atomicAdd(stats + 3, acc_ent);
+    }
+  }
+}
+
 // Row gather with 16-byte vectors: a row's vectors go to consecutive threads
 // (coalesced reads of each random row, fully coalesced writes).
 // I = 32-bit element indices when the gathered block fits (cheap division).
@@ -622,5 +755,29 @@ extern "C" int vy_gae(const float* values, const float* rewards, const uint8_t* 
   if (!values || !rewards || !dones || !last_value || !adv || !ret || T < 1 || B < 1) return VY_ERR_ARG;
   const unsigned grid = (unsigned)((B + 255) / 256);
   k_gae<<<grid, 256, 0, (cudaStream_t)stream>>>(values, rewards, dones, last_value, T, B, gamma, lam, adv, ret);
+  return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
+}
+
+extern "C" int vy_ppo_loss(const void* logits, int64_t ld, const uint8_t* actions, int64_t N, int32_t S, int32_t A,
+                           const float* scal4, const float* adv_stats, float clip_eps, float vf_clip, float vf_coef,
+                           float ent_coef, int32_t value_col, void* grad, float* stats, void* stream) {
+  if (!logits || !actions || !scal4 || !adv_stats || !grad || !stats || N < 1 || S < 1 || A < 1 ||
+      head_rows(S) < 1 || head_rows(S) > 32 || ld < (int64_t)S * A || value_col < S * A || value_col >= ld ||
+      (reinterpret_cast<uintptr_t>(scal4) & 15u))
+    return VY_ERR_ARG;
+  auto st = (cudaStream_t)stream;
+  const int G = head_rows(S);
+  const size_t smem = 2 * raw_rows_bytes<__nv_bfloat16>(G, ld) + (size_t)G * ld * sizeof(float) +
+                      (2 * (size_t)G * S + 3 * (size_t)G) * sizeof(float);
+  if (smem > 200 * 1024) return VY_ERR_ARG;
+  const int64_t nch = (N + G - 1) / G;
+  const unsigned grid = (unsigned)std::min<int64_t>(nch, 148 * 8);
+  auto k = A == 21 ? k_ppo_loss<__nv_bfloat16, 21> : k_ppo_loss<__nv_bfloat16, 0>;
+  if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return VY_ERR_CUDA;
+  const LossCfg cfg{clip_eps, vf_clip, vf_coef, ent_coef};
+  k<<<grid, kHeadThreads, smem, st>>>(static_cast<const __nv_bfloat16*>(logits), actions, N, S, A, ld, G,
+                                      reinterpret_cast<const float4*>(scal4), adv_stats, cfg, value_col,
+                                      static_cast<__nv_bfloat16*>(grad), stats);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }

@@ -61,6 +61,7 @@ class PPOConfig:
     fused_head: bool = True  # vy_ppo_sample / vy_ppo_head_* kernels instead of the torch op chain
     graph_update: bool = True  # the whole update (GAE + epochs x minibatches + Adam) as one CUDA graph (1 GPU)
     fused_policy: bool = True  # rollout forward + sampling in the tcgen05 kernel (vy_policy_step)
+    fused_loss: bool = True  # the update's loss head (log-prob, entropy, value, clipped losses, gradient) as one pass
     allreduce: str = "auto"  # gradient all-reduce: "auto" (world > 1), "always" (also at world 1: tests)
     wide_env: bool = True  # env step on the one-warp-per-env kernel at <= 2048 envs (vy_set_wide)
 
@@ -344,6 +345,44 @@ class PolicyHead(torch.autograd.Function):
         return grad, None, None, None, None
 
 
+class PPOLoss(torch.autograd.Function):
+    """The whole minibatch loss head as one pass (vy_ppo_loss): log-prob of
+    the stored actions, entropy and value from the bf16 head rows, the
+    clipped surrogate, clipped value loss and entropy bonus, and their
+    gradient with respect to the head rows, all in the forward pass.  Returns
+    the mean loss (differentiable) and the detached means (pg, vf, ent).  The
+    gradient is exact for the loss as the root of the backward pass
+    (`loss.backward()`: a unit upstream gradient), which is how the trainer
+    uses it; other upstream gradients scale it."""
+
+    @staticmethod
+    def forward(ctx, logits, actions, scal, adv_stats, S: int, A: int, value_col: int, clip_eps: float,
+                vf_clip: float, vf_coef: float, ent_coef: float, unit_root: bool = True):
+        if logits.dtype != torch.bfloat16 or logits.stride(-1) != 1 or logits.dim() != 2:
+            raise ValueError("PPOLoss needs bf16 2-D head rows")
+        N = logits.shape[0]
+        grad = torch.empty_like(logits)
+        stats = torch.zeros(4, device=logits.device)
+        scal = scal.contiguous()
+        nat.check(nat.lib().vy_ppo_loss(logits.data_ptr(), logits.stride(0), actions.data_ptr(), N, S, A,
+                                        scal.data_ptr(), adv_stats.data_ptr(), clip_eps, vf_clip, vf_coef, ent_coef,
+                                        value_col, grad.data_ptr(), stats.data_ptr(),
+                                        torch.cuda.current_stream().cuda_stream), "vy_ppo_loss")
+        ctx.save_for_backward(grad)
+        ctx.unit_root = unit_root
+        loss = stats[0] / N
+        means = stats[1:] / N
+        ctx.mark_non_differentiable(means)
+        return loss, means
+
+    @staticmethod
+    def backward(ctx, g_loss, g_rest):
+        (grad,) = ctx.saved_tensors
+        if not ctx.unit_root:
+            grad = grad * g_loss.to(grad.dtype)
+        return (grad,) + (None,) * 11
+
+
 def head_reference(logits: torch.Tensor, actions: torch.Tensor):
     """Plain torch restatement of PolicyHead (tests only)."""
     lsm = torch.log_softmax(logits, dim=-1)
@@ -597,6 +636,21 @@ class PPOTrainer:
                     else:
                         logits, v = self.net(gather_rows(obs, idx), logits_fp32=True)
                         v = v.float()
+                if cfg.fused_head and cfg.fused_loss and logits.dtype == torch.bfloat16:
+                    # one pass: log-prob, entropy, value, clipped losses and d loss / d head rows
+                    sc = gather_rows(scal, idx)
+                    a = sc[:, 2]
+                    adv_stats = torch.stack([a.mean(), a.std()])
+                    loss, means = PPOLoss.apply(logits, act[idx], sc, adv_stats, self.net.n_slots, self.net.n_actions,
+                                                self.net.out_dim, cfg.clip_eps, cfg.vf_clip, cfg.vf_coef,
+                                                cfg.ent_coef, True)
+                    self.opt.zero_grad(set_to_none=False)
+                    loss.backward()
+                    self._allreduce_grads()
+                    nn.utils.clip_grad_norm_(self.net.parameters(), cfg.max_grad_norm)
+                    self.opt.step()
+                    stats = {"loss": loss.detach(), "pg": means[0], "vf": means[1], "ent": means[2]}
+                    continue
                 if cfg.fused_head:  # the value column rides through the head kernels too
                     lp, ent, v = PolicyHead.apply(logits, act[idx], self.net.n_slots, self.net.n_actions,
                                                   self.net.out_dim)

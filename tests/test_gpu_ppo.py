@@ -403,3 +403,52 @@ def test_update_graph_with_captured_nccl_allreduce():
             assert torch.equal(a, b)
     finally:
         dist.destroy_process_group()
+
+
+def test_fused_ppo_loss_matches_torch():
+    """vy_ppo_loss (PPOLoss): the minibatch loss, its parts and d loss / d head
+    rows equal the torch restatement (log-softmax head, clipped surrogate,
+    clipped value loss, entropy bonus; advantages normalised per minibatch)
+    within bf16 / fast-math tolerances, ratios on both sides of the clip."""
+    from paper_2507_01522_b200.ppo import PPOLoss, head_reference
+
+    torch.manual_seed(3)
+    S, A, N = 17, 21, 3001
+    vcol, ld = S * A, S * A + 11  # value in a padding column, padded row stride
+    dev = "cuda"
+    raw = (torch.randn(N, ld, device=dev) * 1.5).to(torch.bfloat16)
+    act = torch.randint(0, A, (N, S), device=dev, dtype=torch.uint8)
+    with torch.no_grad():
+        lp0, _ = head_reference(raw[:, :S * A].float().view(N, S, A), act)
+    old_lp = lp0 + 0.3 * torch.randn(N, device=dev)  # ratios around 1, many beyond 1 +- 0.2
+    old_v = raw[:, vcol].float() + 4.0 * torch.randn(N, device=dev)  # some value updates clipped at 10
+    adv = torch.randn(N, device=dev) * 2 + 0.3
+    ret = torch.randn(N, device=dev) * 5
+    scal = torch.stack([old_lp, old_v, adv, ret], 1).contiguous()
+    adv_stats = torch.stack([adv.mean(), adv.std()])
+    cfg = dict(clip_eps=0.2, vf_clip=10.0, vf_coef=0.25, ent_coef=0.01)
+
+    logits = raw.clone().requires_grad_()
+    loss, means = PPOLoss.apply(logits, act, scal, adv_stats, S, A, vcol, cfg["clip_eps"], cfg["vf_clip"],
+                                cfg["vf_coef"], cfg["ent_coef"], True)
+    loss.backward()
+
+    lg = raw.float().requires_grad_()
+    lp, ent = head_reference(lg[:, :S * A].reshape(N, S, A), act)
+    v = lg[:, vcol]
+    a = (adv - adv.mean()) / (adv.std() + 1e-8)
+    ratio = torch.exp(lp - old_lp)
+    pg = -torch.min(ratio * a, torch.clamp(ratio, 1 - cfg["clip_eps"], 1 + cfg["clip_eps"]) * a).mean()
+    v_clip = old_v + (v - old_v).clamp(-cfg["vf_clip"], cfg["vf_clip"])
+    vl = 0.5 * torch.max((v - ret) ** 2, (v_clip - ret) ** 2).mean()
+    ent_m = ent.mean()
+    ref = pg + cfg["vf_coef"] * vl - cfg["ent_coef"] * ent_m
+    ref.backward()
+
+    torch.testing.assert_close(loss, ref.detach(), rtol=2e-4, atol=1e-5)
+    torch.testing.assert_close(means, torch.stack([pg, vl, ent_m]).detach(), rtol=2e-4, atol=1e-5)
+    g = logits.grad.float()
+    want = lg.grad.to(torch.bfloat16).float()
+    torch.testing.assert_close(g[:, :S * A], want[:, :S * A], rtol=2e-2, atol=2e-7)
+    torch.testing.assert_close(g[:, vcol], want[:, vcol], rtol=2e-2, atol=2e-7)
+    assert torch.all(g[:, S * A:vcol] == 0) and torch.all(g[:, vcol + 1:] == 0)
