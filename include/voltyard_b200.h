@@ -266,6 +266,10 @@ int vy_ppo_loss(const void *logits, int64_t ld, const uint8_t *actions, int64_t 
                 const float *scal4, const float *adv_stats, float clip_eps, float vf_clip, float vf_coef,
                 float ent_coef, int32_t value_col, void *grad, float *stats, void *stream);
 
+/* x[i] *= *g for n bf16 values unless *g == 1 (device scalar; PPOLoss's
+ * backward: the upstream gradient without a host sync). */
+int vy_scale_bf16(void *x, int64_t n, const float *g, void *stream);
+
 /* Heterogeneous batch in one launch (config C5).  The
  * reference steps one (config, station, dataset) per BatchEnv (engine.py:370,
  * SPEC.md:482); a multi handle stacks n bound group handles (each keeps its

@@ -80,6 +80,7 @@ _SIGS = {
     "vy_selftest_div": (C.c_int, [C.POINTER(C.c_double), C.c_int32, C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),
     "vy_ppo_loss": (C.c_int, [_P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P, C.c_float, C.c_float,
                               C.c_float, C.c_float, C.c_int32, _P, _P, _P]),
+    "vy_scale_bf16": (C.c_int, [_P, C.c_int64, _P, _P]),
     "vy_multi_create": (C.c_int, [C.POINTER(_P), C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_int64),
                                   C.POINTER(_P)]),
     "vy_multi_step_random": (C.c_int, [_P, C.c_int64, _P, _P]),

@@ -781,3 +781,23 @@ extern "C" int vy_ppo_loss(const void* logits, int64_t ld, const uint8_t* action
                                       static_cast<__nv_bfloat16*>(grad), stats);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
+
+namespace {
+// x *= *g for bf16 x, unless *g == 1 (read on the device: no host sync; the
+// unit upstream gradient of a loss that is the root of backward() costs one
+// tiny launch)
+__global__ void k_scale_bf16_unless_one(__nv_bfloat16* __restrict__ x, int64_t n, const float* __restrict__ g) {
+  const float s = *g;
+  if (s == 1.f) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = __float2bfloat16_rn(__bfloat162float(x[i]) * s);
+}
+}  // namespace
+
+extern "C" int vy_scale_bf16(void* x, int64_t n, const float* g, void* stream) {
+  if (!x || !g || n < 0) return VY_ERR_ARG;
+  if (n == 0) return VY_OK;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_scale_bf16_unless_one<<<grid, 256, 0, (cudaStream_t)stream>>>(static_cast<__nv_bfloat16*>(x), n, g);
+  return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
+}

@@ -351,13 +351,14 @@ class PPOLoss(torch.autograd.Function):
     clipped surrogate, clipped value loss and entropy bonus, and their
     gradient with respect to the head rows, all in the forward pass.  Returns
     the mean loss (differentiable) and the detached means (pg, vf, ent).  The
-    gradient is exact for the loss as the root of the backward pass
-    (`loss.backward()`: a unit upstream gradient), which is how the trainer
-    uses it; other upstream gradients scale it."""
+    backward scales the stored gradient by the upstream gradient on the
+    device, in place (vy_scale_bf16: an early exit when it is 1, the loss
+    being the root of ``backward()``, as in the trainer), so the graph is
+    differentiated once (no ``retain_graph`` reuse)."""
 
     @staticmethod
     def forward(ctx, logits, actions, scal, adv_stats, S: int, A: int, value_col: int, clip_eps: float,
-                vf_clip: float, vf_coef: float, ent_coef: float, unit_root: bool = True):
+                vf_clip: float, vf_coef: float, ent_coef: float):
         if logits.dtype != torch.bfloat16 or logits.stride(-1) != 1 or logits.dim() != 2:
             raise ValueError("PPOLoss needs bf16 2-D head rows")
         N = logits.shape[0]
@@ -369,7 +370,6 @@ class PPOLoss(torch.autograd.Function):
                                         value_col, grad.data_ptr(), stats.data_ptr(),
                                         torch.cuda.current_stream().cuda_stream), "vy_ppo_loss")
         ctx.save_for_backward(grad)
-        ctx.unit_root = unit_root
         loss = stats[0] / N
         means = stats[1:] / N
         ctx.mark_non_differentiable(means)
@@ -378,9 +378,10 @@ class PPOLoss(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g_loss, g_rest):
         (grad,) = ctx.saved_tensors
-        if not ctx.unit_root:
-            grad = grad * g_loss.to(grad.dtype)
-        return (grad,) + (None,) * 11
+        g = g_loss.float().contiguous()
+        nat.check(nat.lib().vy_scale_bf16(grad.data_ptr(), grad.numel(), g.data_ptr(),
+                                          torch.cuda.current_stream().cuda_stream), "vy_scale_bf16")
+        return (grad,) + (None,) * 10
 
 
 def head_reference(logits: torch.Tensor, actions: torch.Tensor):
@@ -643,7 +644,7 @@ class PPOTrainer:
                     adv_stats = torch.stack([a.mean(), a.std()])
                     loss, means = PPOLoss.apply(logits, act[idx], sc, adv_stats, self.net.n_slots, self.net.n_actions,
                                                 self.net.out_dim, cfg.clip_eps, cfg.vf_clip, cfg.vf_coef,
-                                                cfg.ent_coef, True)
+                                                cfg.ent_coef)
                     self.opt.zero_grad(set_to_none=False)
                     loss.backward()
                     self._allreduce_grads()

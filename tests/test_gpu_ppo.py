@@ -430,8 +430,8 @@ def test_fused_ppo_loss_matches_torch():
 
     logits = raw.clone().requires_grad_()
     loss, means = PPOLoss.apply(logits, act, scal, adv_stats, S, A, vcol, cfg["clip_eps"], cfg["vf_clip"],
-                                cfg["vf_coef"], cfg["ent_coef"], True)
-    loss.backward()
+                                cfg["vf_coef"], cfg["ent_coef"])
+    (3.0 * loss).backward()  # a non-unit upstream gradient scales the stored one
 
     lg = raw.float().requires_grad_()
     lp, ent = head_reference(lg[:, :S * A].reshape(N, S, A), act)
@@ -443,7 +443,7 @@ def test_fused_ppo_loss_matches_torch():
     vl = 0.5 * torch.max((v - ret) ** 2, (v_clip - ret) ** 2).mean()
     ent_m = ent.mean()
     ref = pg + cfg["vf_coef"] * vl - cfg["ent_coef"] * ent_m
-    ref.backward()
+    (3.0 * ref).backward()
 
     torch.testing.assert_close(loss, ref.detach(), rtol=2e-4, atol=1e-5)
     torch.testing.assert_close(means, torch.stack([pg, vl, ent_m]).detach(), rtol=2e-4, atol=1e-5)
