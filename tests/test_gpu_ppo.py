@@ -405,7 +405,8 @@ def test_update_graph_with_captured_nccl_allreduce():
         dist.destroy_process_group()
 
 
-def test_fused_ppo_loss_matches_torch():
+@pytest.mark.parametrize("S,A,N", [(17, 21, 3001), (9, 21, 2500), (17, 7, 700)])
+def test_fused_ppo_loss_matches_torch(S, A, N):
     """vy_ppo_loss (PPOLoss): the minibatch loss, its parts and d loss / d head
     rows equal the torch restatement (log-softmax head, clipped surrogate,
     clipped value loss, entropy bonus; advantages normalised per minibatch)
@@ -413,7 +414,6 @@ def test_fused_ppo_loss_matches_torch():
     from paper_2507_01522_b200.ppo import PPOLoss, head_reference
 
     torch.manual_seed(3)
-    S, A, N = 17, 21, 3001
     vcol, ld = S * A, S * A + 11  # value in a padding column, padded row stride
     dev = "cuda"
     raw = (torch.randn(N, ld, device=dev) * 1.5).to(torch.bfloat16)
