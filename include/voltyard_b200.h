@@ -345,6 +345,22 @@ int vy_policy_step(const float *obs, int64_t obs_ld, int64_t N, int32_t obs_dim,
                    const void *wpack, const float *fpack, uint64_t seed, int64_t *counter, uint8_t *actions,
                    float *logp, float *value, float *logits_out, void *stream);
 
+/* The whole PPO rollout as ONE kernel launch (small batches: 16 envs per
+ * CTA, one CTA per SM): T x {policy forward + sampling on the tensor cores
+ * (the same arithmetic and sampling stream as vy_policy_step), env step (the
+ * one-warp-per-env step, auto-reset)} and a last policy pass for the
+ * bootstrap value.  Equivalent, bit for bit, to T + 1 vy_policy_step calls
+ * interleaved with T vy_step calls on the sampled actions.  obs: float32
+ * [T+1][B][obs_len] (row 0 = the current obs, read; rows 1..T written);
+ * actions uint8 [T][B][S]; logp / reward float32 [T][B]; value float32
+ * [T+1][B]; done uint8 [T][B]; S = n_ports + 1, A = 2k + 1; counter as for
+ * vy_policy_step, advanced by T + 1.  VY_ERR_UNSUPPORTED unless the station
+ * is lean without a battery and has <= 32 ports (callers then run the
+ * per-step pair).  Not part of the reference (trainer-free). */
+int vy_ppo_rollout(vy_handle *h, int32_t T, const void *wpack, const float *fpack, int32_t S, int32_t A,
+                   uint64_t seed, int64_t *counter, float *obs, uint8_t *actions, float *logp, float *value,
+                   float *reward, uint8_t *done, void *stream);
+
 int vy_gather_rows(const void *src, int64_t row_bytes, const int64_t *idx, int64_t n, void *dst, void *stream);
 /* Column sums (a linear layer's bias gradient): out[c] = sum over m < M of
  * g[m*ld + c], c < N; g float32 (dtype 0) or bfloat16 (1); out float32.

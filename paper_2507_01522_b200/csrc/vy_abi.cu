@@ -20,6 +20,7 @@
 
 #include "vy_kernels.cuh"
 #include "vy_wide.cuh"
+#include "vy_ppo_rollout.cuh"
 
 using namespace vy;
 
@@ -780,6 +781,43 @@ int vy_poll_error(vy_handle* h, int clear, void* stream, uint32_t* out) {
 
 int64_t vy_launch_count(vy_handle* h) { return h ? h->launches : -1; }
 int32_t vy_last_step_mode(vy_handle* h) { return h ? h->last_mode : -1; }
+
+int vy_ppo_rollout(vy_handle* h, int32_t T, const void* wpack, const float* fpack, int32_t S, int32_t A,
+                   uint64_t seed, int64_t* counter, float* obs, uint8_t* actions, float* logp, float* value,
+                   float* reward, uint8_t* done, void* stream) {
+  if (!h || !h->bound) return fail(VY_ERR_STATE, "handle not bound");
+  if (T < 1 || !wpack || !fpack || !counter || !obs || !actions || !logp || !value || !reward || !done)
+    return fail(VY_ERR_ARG, "bad PPO rollout arguments");
+  if (((reinterpret_cast<uintptr_t>(wpack) | reinterpret_cast<uintptr_t>(fpack)) & 15u) != 0)
+    return fail(VY_ERR_ARG, "weight packs must be 16-byte aligned");
+  // the env side is the one-warp-per-env step: lean stations without a battery, <= 32 ports
+  const int mode = step_mode(h, VY_F_AUTO_RESET, true);
+  if (!(mode == 1 || mode == 2) || h->t.n_ports > 32 || S != h->t.n_ports + 1)
+    return fail(VY_ERR_UNSUPPORTED, "fused PPO rollout needs a lean station without a battery, <= 32 ports");
+  const int OL = h->t.obs_len;
+  int32_t geo[4];
+  if (vy_policy_geometry(OL, OL, S, A, geo) != VY_OK) return fail(VY_ERR_UNSUPPORTED, "policy geometry");
+  if (A != 2 * h->t.k + 1) return fail(VY_ERR_ARG, "actions per slot must be 2k+1");
+  const vyp::Geo g = vyp::make_geo(OL, OL, S, A);
+  Params P;
+  fill(h, P, true, false);
+  P.flags = VY_F_AUTO_RESET;
+  P.out.reward = reward;
+  P.out.done = done;
+  const uint32_t pol = ppo_policy_off(ppo_scratch_off(P.n_profiles, P.k, P.n_ports, P.n_nodes));
+  const int smem = (int)(pol + g.smem);
+  if (smem > 227 * 1024) return fail(VY_ERR_UNSUPPORTED, "fused PPO rollout: shared memory");
+  auto* kern = mode == 1 ? k_ppo_rollout<1> : k_ppo_rollout<2>;
+  VY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  PpoBufs R{static_cast<const uint8_t*>(wpack), fpack, seed, reinterpret_cast<unsigned long long*>(counter),
+            obs, actions, logp, value};
+  const unsigned grid = (unsigned)((h->B + kPpoEnvs - 1) / kPpoEnvs);
+  kern<<<grid, kPpoThreads, smem, (cudaStream_t)stream>>>(P, T, g, R);
+  VY_CUDA(cudaGetLastError());
+  ++h->launches;
+  h->last_mode = 20 + mode;  // diagnostics: 21 / 22 = fused PPO rollout
+  return VY_OK;
+}
 
 int vy_set_wide(vy_handle* h, int32_t mode) {
   if (!h || mode < -1 || mode > 1) return fail(VY_ERR_ARG, "wide mode must be -1 (auto), 0 or 1");

@@ -74,82 +74,80 @@ __device__ __noinline__ void fit_tree_flat(const Params& P, TreeC tc, double* cu
   }
 }
 
+// One environment on one warp: lane j holds port j's constants and state in
+// registers for as many steps as the caller runs; every lane also carries the
+// env's scalars.  Shared by the rollout below and the fused PPO rollout
+// (vy_ppo_rollout.cuh), which runs it on its env warps between policy passes.
 template <int M>
-__global__ void __launch_bounds__(32 * kWideWarps) k_rollout_wide(const __grid_constant__ Params P, int T_steps,
-                                                                  uint64_t policy_seed, int64_t index0, int64_t call0,
-                                                                  int64_t obs_stride, int64_t rew_stride,
-                                                                  const uint8_t* __restrict__ acts) {
+struct WideEnv {
   static_assert(M == 1 || M == 2, "lean stations without a battery");
-  Prof prof;
-  PortC pc;
-  TreeC tc;
-  const double* dtab;
-  stage_tables(P, prof, dtab, pc, tc);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t b = (int64_t)blockIdx.x * kWideWarps + warp;
-  if (b >= P.B) return;
-  const unsigned FULL = 0xffffffffu;
-  const int n = P.n_ports, OL = P.obs_len;
-  const bool isport = lane < n;
-  const int64_t ld = P.ld;
-  // per-warp scratch: the ports' currents (node loads, rescale) and their
-  // energy-flow terms {got, in, out, -} (the sequential flow sums)
-  double* cur_s = reinterpret_cast<double*>(vy_smem + tables_bytes(P.n_profiles, P.k, P.n_ports, P.n_nodes)) +
-                  warp * kWideScratch;
-  double* flow_s = cur_s + 32;
-
-  // this lane's port: constants for all T steps, state in registers
-  double imax_c = 0.0, imax_d = 0.0, volt = 1.0, rcp_volt = 1.0, kindv = 0.0, nodesv = 0.0;
+  double imax_c = 0.0, imax_d = 0.0, volt = 1.0, rcp_volt = 1.0, kindv = 0.0;
   double dtv = 0.0, eta_d = 1.0, eta_c = 1.0, rcp_eta_c = 1.0, i_denom = 1.0, rcp_i_denom = 1.0;
   double idr = 0.0, soc = 0.0, de = 0.0;
   int dt = 0;
   uint32_t mt = 0;
-  if (isport) {
-    pc.pair(lane, 0, imax_c, imax_d);
-    pc.pair(lane, 1, volt, rcp_volt);
-    pc.pair(lane, 2, kindv, nodesv);
-    pc.pair(lane, 3, dtv, eta_d);
-    pc.pair(lane, 4, eta_c, rcp_eta_c);
-    pc.pair(lane, 5, i_denom, rcp_i_denom);
-    const int64_t e = (int64_t)lane * ld + b;
-    idr = P.st.port_i[e];
-    soc = P.st.port_soc[e];
-    de = P.st.port_de[e];
-    dt = P.st.port_dtrem[e];
-    mt = P.st.port_meta[e];
-  }
-  const uint32_t pm = (uint32_t)nodesv;
-  const uint64_t nmask = n == 64 ? ~0ull : ((1ull << n) - 1);
   EnvRegs E;
-  load_env<M>(P, b, E);  // every lane: the env's scalars (broadcast loads)
-  const uint64_t pkey = fold(fold(fold(kKey0, policy_seed), (uint64_t)(index0 + b)), 2);
-  int episode = P.st.episode[b];
-  const uint64_t seed = P.st.env_seed[b];
-  const int ns = n + 1, hi = 2 * P.k + 1, hi_a = 2 * P.k;
-  const double grid_lane = dtab[lane <= hi_a ? lane : 0];  // (a-k)/k, one entry per lane (2k+1 <= 32)
+  int episode;
+  uint64_t seed, nmask;
+  double grid_lane;
+  int64_t b;
 
-  for (int t = 0; t < T_steps; ++t) {
-    float* orow = reinterpret_cast<float*>(P.out.obs) + t * obs_stride + b * OL;
+  __device__ __forceinline__ void load(const Params& P, const PortC& pc, const double* dtab, int64_t b_, int lane) {
+    b = b_;
+    const int n = P.n_ports;
+    if (lane < n) {
+      double nodesv;
+      pc.pair(lane, 0, imax_c, imax_d);
+      pc.pair(lane, 1, volt, rcp_volt);
+      pc.pair(lane, 2, kindv, nodesv);
+      pc.pair(lane, 3, dtv, eta_d);
+      pc.pair(lane, 4, eta_c, rcp_eta_c);
+      pc.pair(lane, 5, i_denom, rcp_i_denom);
+      const int64_t e = (int64_t)lane * P.ld + b;
+      idr = P.st.port_i[e];
+      soc = P.st.port_soc[e];
+      de = P.st.port_de[e];
+      dt = P.st.port_dtrem[e];
+      mt = P.st.port_meta[e];
+    }
+    nmask = n == 64 ? ~0ull : ((1ull << n) - 1);
+    load_env<M>(P, b, E);  // every lane: the env's scalars (broadcast loads)
+    episode = P.st.episode[b];
+    seed = P.st.env_seed[b];
+    grid_lane = dtab[lane <= 2 * P.k ? lane : 0];  // (a-k)/k, one entry per lane (2k+1 <= 32)
+  }
+
+  __device__ __forceinline__ void store(const Params& P, int lane) const {
+    if (lane < P.n_ports) {
+      const int64_t e = (int64_t)lane * P.ld + b;
+      P.st.port_i[e] = idr;
+      P.st.port_soc[e] = soc;
+      P.st.port_de[e] = de;
+      P.st.port_dtrem[e] = (int16_t)dt;
+      P.st.port_meta[e] = (uint8_t)mt;
+    }
+    if (lane == 0) {
+      store_env<M>(P, b, E, true);
+      P.st.episode[b] = episode;
+    }
+  }
+
+  // One step with action `a` on this lane's port (P.k on lanes past the
+  // ports): obs row -> orow (and, with kStage, a float copy -> srow), reward
+  // and done -> element `rix` of P.out.reward / P.out.done.  cur_s / flow_s:
+  // this warp's shared scratch (32 + 4 x 32 doubles).
+  template <bool kStage>
+  __device__ __forceinline__ void step(const Params& P, const Prof& prof, const TreeC& tc, int lane, int a,
+                                       float* orow, float* srow, int64_t rix, double* cur_s, double* flow_s) {
+    const unsigned FULL = 0xffffffffu;
+    const int n = P.n_ports;
+    const bool isport = lane < n;
+    const int64_t ld = P.ld;
     const int tt = E.step;
     const Frame F = load_frame<M>(P, tt, E.day);
     // the obs globals of the state after this step, in flight during it (lanes 0..8 write them)
     ObsGlobals G{};
     if (lane < 9) G = load_obs_globals(P, tt + 1, E.day);
-    // slot j's action on lane j: RandomPolicy (policies.py:51-73), or the
-    // caller's uint8 rows [B][n+1] (vy_step: one step, acts != null)
-    int a = P.k;
-    if (isport) {
-      if (acts) {
-        a = acts[b * ns + lane];
-        if (a > hi_a) {  // out of range: clamped and flagged (the lazy error word, engine.py:440-442)
-          atomicOr(P.err, 1u);
-          a = hi_a;
-        }
-      } else {
-        a = policy_action(pkey, (uint64_t)(call0 + t) * (uint64_t)ns + lane + 1, hi);
-      }
-    }
-    if (acts && lane == 0 && acts[b * ns + n] > hi_a) atomicOr(P.err, 1u);  // the battery slot is validated too
     const double d = __shfl_sync(FULL, grid_lane, a);
 
     // phase 1: apply actions (_kernel.pyx:297-356)
@@ -329,8 +327,8 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_rollout_wide(const __grid_c
         es[7 * ld + b] = (double)tover;
         P.out.term_overtime[b] = tover;
       }
-      reinterpret_cast<float*>(P.out.reward)[t * rew_stride + b] = (float)reward;
-      P.out.done[t * rew_stride + b] = done;
+      reinterpret_cast<float*>(P.out.reward)[rix] = (float)reward;
+      P.out.done[rix] = done;
     }
     if (done) {  // in-kernel auto-reset: the obs row becomes the reset obs of episode + 1
       ++episode;
@@ -344,13 +342,15 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_rollout_wide(const __grid_c
     if (isport) {
       const bool o = mt & 1u;
       const double dec = div_rcp(de, prof.cap(mt >> 2), prof.rcp_cap(mt >> 2));
+      const float v[6] = {o ? 1.0f : 0.0f, (float)div_rcp(idr, i_denom, rcp_i_denom), (float)soc,
+                          o ? (float)dec : 0.0f, (float)div_rcp((double)dt, (double)P.episode_steps, P.rcp_ep),
+                          (float)((mt >> 1) & 1u)};
       float* pr = orow + 6 * lane;
-      __stcs(pr, o ? 1.0f : 0.0f);
-      __stcs(pr + 1, (float)div_rcp(idr, i_denom, rcp_i_denom));
-      __stcs(pr + 2, (float)soc);
-      __stcs(pr + 3, o ? (float)dec : 0.0f);
-      __stcs(pr + 4, (float)div_rcp((double)dt, (double)P.episode_steps, P.rcp_ep));
-      __stcs(pr + 5, (float)((mt >> 1) & 1u));
+#pragma unroll
+      for (int q = 0; q < 6; ++q) __stcs(pr + q, v[q]);
+      if (kStage)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) srow[6 * lane + q] = v[q];
     }
     if (lane < 9) {
       if (done) G = load_obs_globals(P, E.step, E.day);  // reset: the new episode's day
@@ -364,20 +364,55 @@ __global__ void __launch_bounds__(32 * kWideWarps) k_rollout_wide(const __grid_c
                        : lane == 7 ? G.wk
                                    : G.dayf;
       __stcs(orow + 6 * n + lane, (float)v);
+      if (kStage) srow[6 * n + lane] = (float)v;
     }
   }
-  if (isport) {
-    const int64_t e = (int64_t)lane * ld + b;
-    P.st.port_i[e] = idr;
-    P.st.port_soc[e] = soc;
-    P.st.port_de[e] = de;
-    P.st.port_dtrem[e] = (int16_t)dt;
-    P.st.port_meta[e] = (uint8_t)mt;
+};
+
+template <int M>
+__global__ void __launch_bounds__(32 * kWideWarps) k_rollout_wide(const __grid_constant__ Params P, int T_steps,
+                                                                  uint64_t policy_seed, int64_t index0, int64_t call0,
+                                                                  int64_t obs_stride, int64_t rew_stride,
+                                                                  const uint8_t* __restrict__ acts) {
+  Prof prof;
+  PortC pc;
+  TreeC tc;
+  const double* dtab;
+  stage_tables(P, prof, dtab, pc, tc);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b = (int64_t)blockIdx.x * kWideWarps + warp;
+  if (b >= P.B) return;
+  const int n = P.n_ports, OL = P.obs_len;
+  // per-warp scratch: the ports' currents (node loads, rescale) and their
+  // energy-flow terms {got, in, out, -} (the sequential flow sums)
+  double* cur_s = reinterpret_cast<double*>(vy_smem + tables_bytes(P.n_profiles, P.k, P.n_ports, P.n_nodes)) +
+                  warp * kWideScratch;
+  double* flow_s = cur_s + 32;
+  WideEnv<M> env;
+  env.load(P, pc, dtab, b, lane);
+  const uint64_t pkey = fold(fold(fold(kKey0, policy_seed), (uint64_t)(index0 + b)), 2);
+  const int ns = n + 1, hi = 2 * P.k + 1, hi_a = 2 * P.k;
+
+  for (int t = 0; t < T_steps; ++t) {
+    // slot j's action on lane j: RandomPolicy (policies.py:51-73), or the
+    // caller's uint8 rows [B][n+1] (vy_step: one step, acts != null)
+    int a = P.k;
+    if (lane < n) {
+      if (acts) {
+        a = acts[b * ns + lane];
+        if (a > hi_a) {  // out of range: clamped and flagged (the lazy error word, engine.py:440-442)
+          atomicOr(P.err, 1u);
+          a = hi_a;
+        }
+      } else {
+        a = policy_action(pkey, (uint64_t)(call0 + t) * (uint64_t)ns + lane + 1, hi);
+      }
+    }
+    if (acts && lane == 0 && acts[b * ns + n] > hi_a) atomicOr(P.err, 1u);  // the battery slot is validated too
+    float* orow = reinterpret_cast<float*>(P.out.obs) + t * obs_stride + b * OL;
+    env.template step<false>(P, prof, tc, lane, a, orow, nullptr, t * rew_stride + b, cur_s, flow_s);
   }
-  if (lane == 0) {
-    store_env<M>(P, b, E, true);
-    P.st.episode[b] = episode;
-  }
+  env.store(P, lane);
 }
 
 }  // namespace vy

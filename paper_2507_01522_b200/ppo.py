@@ -10,7 +10,10 @@ loop B200-first:
   bias epilogues and the categorical sampling of the 17 x 21 multi-discrete
   head fused) and the fused env step kernel, for T steps, captured once as a
   CUDA graph and replayed every iteration (fused_policy=False keeps the
-  earlier cuBLAS + sampler-kernel path for comparison);
+  earlier cuBLAS + sampler-kernel path for comparison); at up to 2368 envs
+  on lean stations the whole rollout is ONE kernel instead
+  (csrc/vy_ppo_rollout.cuh: 16 envs per CTA, the same policy arithmetic and
+  env step, weights and TMEM set up once for all T steps);
 * advantages: the vy_gae reverse-scan kernel (csrc/vy_ppo.cu);
 * update: clipped PPO objective with value clipping, entropy bonus, Adam,
   global-norm gradient clipping; under torch.distributed the flattened
@@ -61,6 +64,10 @@ class PPOConfig:
     fused_head: bool = True  # vy_ppo_sample / vy_ppo_head_* kernels instead of the torch op chain
     graph_update: bool = True  # the whole update (GAE + epochs x minibatches + Adam) as one CUDA graph (1 GPU)
     fused_policy: bool = True  # rollout forward + sampling in the tcgen05 kernel (vy_policy_step)
+    # the whole rollout (policy passes + env steps) as one kernel at <= 2368 envs
+    # (vy_ppo_rollout: 16 envs per CTA, one wave on 148 SMs); lean stations
+    # without a battery, else the per-step pair
+    fused_rollout: bool = True
     fused_loss: bool = True  # the update's loss head (log-prob, entropy, value, clipped losses, gradient) as one pass
     allreduce: str = "auto"  # gradient all-reduce: "auto" (world > 1), "always" (also at world 1: tests)
     wide_env: bool = True  # env step on the one-warp-per-env kernel at <= 2048 envs (vy_set_wide)
@@ -290,6 +297,26 @@ def policy_step(obs: torch.Tensor, obs_dim: int, S: int, A: int, packed: tuple, 
     nat.check(rc, "vy_policy_step")
 
 
+def ppo_rollout(env: BatchEnv, T: int, S: int, A: int, packed: tuple, seed: int, counter: torch.Tensor,
+                obs: torch.Tensor, actions: torch.Tensor, logp: torch.Tensor, values: torch.Tensor,
+                rewards: torch.Tensor, dones: torch.Tensor) -> None:
+    """The whole rollout in one launch (vy_ppo_rollout): T x {tcgen05 policy
+    pass + sampling, env step} and the bootstrap value, bit-identical to T + 1
+    policy_step calls interleaved with T env.step calls.  obs [T+1, B, L]
+    (row 0 read), actions [T, B, S], logp / rewards [T, B], values [T+1, B],
+    dones [T, B]; all contiguous.  Raises NotImplementedError for stations the
+    kernel does not cover (battery, > 32 ports)."""
+    for t in (obs, actions, logp, values, rewards, dones):
+        if not t.is_contiguous():
+            raise ValueError("rollout buffers must be contiguous")
+    blob, fp = packed
+    rc = nat.lib().vy_ppo_rollout(env._h, int(T), blob.data_ptr(), fp.data_ptr(), S, A, seed & ((1 << 64) - 1),
+                                  counter.data_ptr(), obs.data_ptr(), actions.data_ptr(), logp.data_ptr(),
+                                  values.data_ptr(), rewards.data_ptr(), dones.data_ptr(),
+                                  torch.cuda.current_stream().cuda_stream)
+    nat.check(rc, "vy_ppo_rollout")
+
+
 def _dtype_code(t: torch.Tensor) -> int:
     if t.dtype == torch.float32:
         return 0
@@ -485,6 +512,7 @@ class PPOTrainer:
         self.n_iters = max(1, cfg.total_timesteps // (T * B * self.world))
         self._graph = None
         self._fused_policy = cfg.fused_policy
+        self._fused_rollout = cfg.fused_rollout and self._fused_policy and B <= 148 * 16
         if self._fused_policy:
             self._geo = policy_geometry(self.net)
             self._scratch_a = torch.zeros(B, A, dtype=torch.uint8, device=dev)
@@ -537,6 +565,14 @@ class PPOTrainer:
         # per policy step
         if self._fused_policy:
             self._packed = pack_policy(self.net, self._geo)  # inside the graph: from the live weights each replay
+            if self._fused_rollout:
+                try:
+                    ppo_rollout(self.env, self.cfg.rollout_steps, self.net.n_slots, self.net.n_actions, self._packed,
+                                self._sample_seed, self._sample_ctr, self.obs, self.actions, self.logp, self.values,
+                                self.rewards, self.dones)
+                    return
+                except NotImplementedError:  # decided on the first (uncaptured) rollout
+                    self._fused_rollout = False
             for t in range(self.cfg.rollout_steps):
                 self._policy_step(t)
             # bootstrap value of the last obs (its actions / log-prob land in scratch rows)
@@ -675,6 +711,10 @@ class PPOTrainer:
         return stats
 
     def describe_rollout(self) -> str:
+        if self._fused_rollout:
+            return ("one kernel per rollout: vy_ppo_rollout (per CTA 16 envs x T steps: tcgen05 3-layer MLP, TMEM "
+                    "accumulators, fused epilogues + inverse-CDF sampling, then the one-warp-per-env step; weights, "
+                    "TMEM and station tables set up once) + pack_policy")
         if self._fused_policy:
             return ("CUDA graph x T: vy_policy_step (tcgen05 3-layer MLP, TMEM accumulators, bulk-async obs tiles, "
                     "fused tanh/bias epilogues + inverse-CDF sampling, log-prob, value) + k_step")

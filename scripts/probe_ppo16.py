@@ -12,10 +12,11 @@ from paper_2507_01522_b200.ppo import PPOConfig, PPOTrainer  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--envs", type=int, default=16)
+ap.add_argument("--per-step", action="store_true", help="the per-step policy + env pair, not vy_ppo_rollout")
 args = ap.parse_args()
 rc = default_setup()
 env = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=args.envs, master_seed=1)
-tr = PPOTrainer(env, PPOConfig(rollout_steps=300))
+tr = PPOTrainer(env, PPOConfig(rollout_steps=300, fused_rollout=not args.per_step))
 for _ in range(2):
     tr.iterate()
 torch.cuda.synchronize()
@@ -30,5 +31,5 @@ for _ in range(5):
     torch.cuda.synchronize()
     ro.append(ev[0].elapsed_time(ev[1]))
     up.append(ev[1].elapsed_time(ev[2]))
-print(f"envs {args.envs}: rollout {min(ro):.2f} ms ({min(ro) / 300 * 1e3:.1f} us/step), update {min(up):.2f} ms; "
+print(f"{tr.describe_rollout()[:40]}... envs {args.envs}: rollout {min(ro):.2f} ms ({min(ro) / 300 * 1e3:.1f} us/step), update {min(up):.2f} ms; "
       f"{(min(ro) + min(up)) / (300 * args.envs) * 1e5 / 1e3:.3f} s per 100k")
