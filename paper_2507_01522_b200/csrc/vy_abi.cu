@@ -811,13 +811,26 @@ int vy_ppo_rollout(vy_handle* h, int32_t T, const void* wpack, const float* fpac
   VY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   PpoBufs R{static_cast<const uint8_t*>(wpack), fpack, seed, reinterpret_cast<unsigned long long*>(counter),
             obs, actions, logp, value};
-  const unsigned grid = (unsigned)((h->B + kPpoEnvs - 1) / kPpoEnvs);
-  kern<<<grid, kPpoThreads, smem, (cudaStream_t)stream>>>(P, T, g, R);
+  // envs per CTA: as few as one wave of CTAs allows (fewer env warps per SM
+  // step faster; the policy pass costs the same for 1 or 16 rows), at least 2
+  // (16 envs: 8.9 us per step at 2-4 per CTA, 10.0 at 16; scripts/gpu_r2_ppo_epc.sh)
+  const int64_t per = (h->B + h->num_sms - 1) / h->num_sms;
+  int epc = per < 2 ? 2 : (per > kPpoEnvs ? kPpoEnvs : (int)per);
+  if (const char* e = getenv("VY_PPO_EPC")) epc = atoi(e) < 1 ? 1 : (atoi(e) > kPpoEnvs ? kPpoEnvs : atoi(e));
+  const unsigned grid = (unsigned)((h->B + epc - 1) / epc);
+  kern<<<grid, kPpoThreads, smem, (cudaStream_t)stream>>>(P, T, epc, g, R);
   VY_CUDA(cudaGetLastError());
   ++h->launches;
   h->last_mode = 20 + mode;  // diagnostics: 21 / 22 = fused PPO rollout
   return VY_OK;
 }
+
+#ifdef VY_PPO_PROF
+int vy_ppo_prof_read(unsigned long long* out) {
+  VY_CUDA(cudaMemcpyFromSymbol(out, g_ppo_prof, sizeof(g_ppo_prof)));
+  return VY_OK;
+}
+#endif
 
 int vy_set_wide(vy_handle* h, int32_t mode) {
   if (!h || mode < -1 || mode > 1) return fail(VY_ERR_ARG, "wide mode must be -1 (auto), 0 or 1");

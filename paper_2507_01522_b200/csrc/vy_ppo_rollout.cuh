@@ -59,9 +59,21 @@ __host__ __device__ inline uint32_t ppo_policy_off(uint32_t scratch) {
   return (ppo_acts_off(scratch) + kPpoEnvs * kPpoActRow + 1023) & ~1023u;
 }
 
+#ifdef VY_PPO_PROF  // phase timing build (scripts/probe_ppo_phases.py): clock64 deltas of CTA 0 thread 0
+__device__ unsigned long long g_ppo_prof[16];
+#define PPO_MARK(i)                                   \
+  if (blockIdx.x == 0 && threadIdx.x == 0) {          \
+    const unsigned long long now_ = clock64();        \
+    g_ppo_prof[i] += now_ - prof_last;                \
+    prof_last = now_;                                 \
+  }
+#else
+#define PPO_MARK(i)
+#endif
+
 template <int M>
 __global__ void __launch_bounds__(kPpoThreads, 1)
-    k_ppo_rollout(const __grid_constant__ Params P, int T, const vyp::Geo G, const PpoBufs R) {
+    k_ppo_rollout(const __grid_constant__ Params P, int T, int epc, const vyp::Geo G, const PpoBufs R) {
   using vyp::kH;
   using vyp::kM;
   using vyp::kRows;
@@ -84,8 +96,8 @@ __global__ void __launch_bounds__(kPpoThreads, 1)
   uint8_t* a_smem = sm + G.off_a;
   float* stage = reinterpret_cast<float*>(sm + G.off_obs);  // obs rows, float32, stride obs_ld
   const bool elect = tid == 0;
-  const int64_t B = P.B, b0 = (int64_t)blockIdx.x * kPpoEnvs;
-  const int rows = (int)((B - b0) < kPpoEnvs ? (B - b0) : kPpoEnvs);
+  const int64_t B = P.B, b0 = (int64_t)blockIdx.x * epc;
+  const int rows = (int)((B - b0) < epc ? (B - b0) : epc);  // this CTA's envs (epc <= 16)
   const int n = P.n_ports, OL = P.obs_len;
 
   if (elect) {
@@ -123,7 +135,11 @@ __global__ void __launch_bounds__(kPpoThreads, 1)
   uint32_t ph_mma = 0;
   constexpr float kLog2e = 1.4426950408889634f;
 
+#ifdef VY_PPO_PROF
+  unsigned long long prof_last = clock64();
+#endif
   for (int t = 0;; ++t) {
+    PPO_MARK(0);
     // the sampler key of policy pass t (k_policy_step's key of call call0 + t)
     const uint64_t key = vyp::mix64(R.seed ^ vyp::mix64(call0 + (unsigned long long)t + 0x9E3779B97F4A7C15ULL));
     // obs rows -> bf16 A operand [k/8][row][8], zero past obs_dim and past the last row, 4 replicas
@@ -142,6 +158,7 @@ __global__ void __launch_bounds__(kPpoThreads, 1)
     vyp::fence_proxy_async();
     __syncthreads();
     if (t == 0) vyp::mbar_wait(bar_w, 0);
+    PPO_MARK(1);
 
     // layer 1: D[0:128) = A[128 x K1] W1^T
     if (elect) {
@@ -151,6 +168,7 @@ __global__ void __launch_bounds__(kPpoThreads, 1)
     }
     vyp::mbar_wait(bar_mma, ph_mma);
     ph_mma ^= 1;
+    PPO_MARK(2);
     vyp::tc_fence_after();
     {  // h1 chunk `warp` (columns 8w..8w+7) of row `lane`
       uint32_t v[8];
@@ -161,6 +179,7 @@ __global__ void __launch_bounds__(kPpoThreads, 1)
     vyp::tc_fence_before();
     vyp::fence_proxy_async();
     __syncthreads();
+    PPO_MARK(3);
 
     // layer 2: actor D[128:192) = h1a Wa2^T, critic D[192:256) = h1c Wc2^T
     if (elect) {
@@ -172,6 +191,7 @@ __global__ void __launch_bounds__(kPpoThreads, 1)
     }
     vyp::mbar_wait(bar_mma, ph_mma);
     ph_mma ^= 1;
+    PPO_MARK(4);
     vyp::tc_fence_after();
     {
       uint32_t v[8];
@@ -192,6 +212,7 @@ __global__ void __launch_bounds__(kPpoThreads, 1)
     vyp::tc_fence_before();
     vyp::fence_proxy_async();
     __syncthreads();
+    PPO_MARK(5);
 
     // layer 3: head D[0:N3) = h2a Wh^T (two chains: N = n3a, n3b)
     if (elect) {
@@ -210,57 +231,93 @@ __global__ void __launch_bounds__(kPpoThreads, 1)
     }
     vyp::mbar_wait(bar_mma, ph_mma);
     ph_mma ^= 1;
+    PPO_MARK(6);
     vyp::tc_fence_after();
     const bool sample = t < T;  // pass T is the bootstrap value only
-    for (int s = warp; sample && s < G.S; s += kPpoWarps) {
+    // the head, slot by slot: rows 0..15 are this CTA's envs (TMEM lanes 0..15
+    // of every quadrant); a warp with a second slot s0 + 16 reads it into its
+    // upper half-warp with the .16x32bx2 shape, so 17 slots take one round
+    const int hrow = lane & 15;
+    const int64_t hgrow = b0 + hrow;
+    for (int s0 = warp; sample && s0 < G.S; s0 += 2 * kPpoWarps) {
+      const bool pair = s0 + kPpoWarps < G.S;  // warp-uniform
       uint32_t v[24];
-      const uint32_t ta = tmem + tq + kSlotCols * s;
-      VYP_LD16(ta, v);
-      VYP_LD8(ta + 16, v, 16);
+      const uint32_t ta = tmem + tq + kSlotCols * s0;
+      if (pair) {
+        VYP_LD16X2(ta, v, 384);  // 384 = kPpoWarps * kSlotCols columns: slot s0 + 16
+        VYP_LD8X2(ta + 16, v, 16, 384);
+      } else {
+        VYP_LD16(ta, v);
+        VYP_LD8(ta + 16, v, 16);
+      }
       vyp::tmem_wait_ld();
-      float z[kMaxA];
+      const int s = (pair && lane >= 16) ? s0 + kPpoWarps : s0;
+      const bool mine = lane < 16 || pair;  // an unpaired warp's upper lanes hold unused rows
+      // the slot's 24 head biases as six 16-byte loads, all issued before use
+      // (a slot owns kSlotCols bias entries, so the reads stay inside bh)
+      float bq[kSlotCols];
+#pragma unroll
+      for (int q = 0; q < kSlotCols / 4; ++q) {
+        const float4 f = reinterpret_cast<const float4*>(bh + kSlotCols * s)[q];
+        bq[4 * q] = f.x;
+        bq[4 * q + 1] = f.y;
+        bq[4 * q + 2] = f.z;
+        bq[4 * q + 3] = f.w;
+      }
+      float z[kMaxA], e[kMaxA];
       float m = -INFINITY;
 #pragma unroll
       for (int k = 0; k < kMaxA; ++k) {
-        z[k] = k < G.A ? vyp::bf16r(__uint_as_float(v[k]) + bh[kSlotCols * s + k]) : -INFINITY;  // bf16 logits
+        const float zk = vyp::bf16r(__uint_as_float(v[k]) + bq[k]);  // bf16 logits
+        z[k] = k < G.A ? zk : -INFINITY;
         m = fmaxf(m, z[k]);
       }
       const float mb = m * kLog2e;
       float sum = 0.f;
 #pragma unroll
-      for (int k = 0; k < kMaxA; ++k) sum += vyp::exp2_sfu(fmaf(z[k], kLog2e, -mb));  // exp(z - m); 0 past A
+      for (int k = 0; k < kMaxA; ++k) {
+        e[k] = vyp::exp2_sfu(fmaf(z[k], kLog2e, -mb));  // exp(z - m); 0 past A
+        sum += e[k];
+      }
       // one uniform per (row, slot): element (row * S + s) of this pass's stream
-      const uint64_t x = vyp::mix64(key + (uint64_t)(grow * G.S + s) * 0x9E3779B97F4A7C15ULL);
+      const uint64_t x = vyp::mix64(key + (uint64_t)(hgrow * G.S + s) * 0x9E3779B97F4A7C15ULL);
       const float target = ((float)(x >> 41) + 0.5f) * (1.f / 8388608.f) * sum;
+      // inverse CDF: the first k whose running sum passes u * sum (the last
+      // valid action if rounding leaves target at or above the total)
       float c = 0.f, za = z[0];
       int a = -1;
 #pragma unroll
       for (int k = 0; k < kMaxA; ++k) {
-        c += vyp::exp2_sfu(fmaf(z[k], kLog2e, -mb));
+        c += e[k];
         const bool take = a < 0 && k < G.A && (target < c || k == G.A - 1);
         a = take ? k : a;
         za = take ? z[k] : za;
       }
-      lpart[lane * G.S + s] = (za - m) - __logf(sum);
-      if (live) {
-        R.actions[(t * B + grow) * G.S + s] = (uint8_t)a;
-        act_s[lane * kPpoActRow + s] = (uint8_t)a;
+      if (mine) {
+        lpart[hrow * G.S + s] = (za - m) - __logf(sum);
+        if (hrow < rows) {
+          R.actions[(t * B + hgrow) * G.S + s] = (uint8_t)a;
+          act_s[hrow * kPpoActRow + s] = (uint8_t)a;
+        }
       }
     }
     vyp::tc_fence_before();
     __syncthreads();
+    PPO_MARK(7);
     if (!sample) break;
-    if (warp == 0 && live) {  // log-probability: slot terms summed in slot order
-      float acc = 0.f;
+    if (warp == kPpoWarps - 1 && live) {  // log-probability: slot terms summed in slot order (off the env warps
+      float acc = 0.f;                      // unless the CTA has 16 envs)
       for (int s = 0; s < G.S; ++s) acc += lpart[lane * G.S + s];
       R.logp[t * B + grow] = acc;
     }
+    PPO_MARK(8);
     // env step t on the env warps: next obs -> rollout row t + 1 and the staging row
     if (env_warp) {
       const int a = lane < n ? act_s[warp * kPpoActRow + lane] : P.k;
       env.template step<true>(P, prof, tc, lane, a, R.obs + ((int64_t)(t + 1) * B + b0 + warp) * OL,
                               stage + warp * G.obs_ld, (int64_t)t * B + b0 + warp, scratch, scratch + 32);
     }
+    PPO_MARK(9);
     __syncthreads();
   }
   if (env_warp) env.store(P, lane);

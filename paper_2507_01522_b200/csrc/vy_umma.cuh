@@ -141,6 +141,21 @@ __device__ __forceinline__ void mma_chain(uint32_t d_tmem, uint32_t a, uint32_t 
                : "=r"(v[o + 0]), "=r"(v[o + 1]), "=r"(v[o + 2]), "=r"(v[o + 3]), "=r"(v[o + 4]), "=r"(v[o + 5]), \
                  "=r"(v[o + 6]), "=r"(v[o + 7])                                                              \
                : "r"(taddr))
+// 16 TMEM lanes, two column ranges: threads 0..15 read lanes 0..15 of the
+// warp's quadrant at columns [c, c+n), threads 16..31 the same lanes at
+// [c + off, c + off + n) (the .16x32bx2 shape; `off` an immediate)
+#define VYP_LD16X2(taddr, v, off)                                                                             \
+  asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, " \
+               "[%16], " #off ";"                                                                             \
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),    \
+                 "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),          \
+                 "=r"(v[15])                                                                                      \
+               : "r"(taddr))
+#define VYP_LD8X2(taddr, v, o, off)                                                                           \
+  asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], " #off ";"             \
+               : "=r"(v[o + 0]), "=r"(v[o + 1]), "=r"(v[o + 2]), "=r"(v[o + 3]), "=r"(v[o + 4]), "=r"(v[o + 5]), \
+                 "=r"(v[o + 6]), "=r"(v[o + 7])                                                              \
+               : "r"(taddr))
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }

@@ -163,22 +163,37 @@ struct WideEnv {
     // tree: excess on the requested currents (_kernel.pyx:611-624), node loads in leaf order
     double excess = 0.0;
     uint64_t clean = 0;
-    // node loads from a shared copy of the currents, each node's range summed
-    // in leaf order (a per-port shuffle + masked adds for up to kFastNodes
-    // nodes measured 18% of the kernel's instructions)
+    // node loads from a shared copy of the currents: lane q sums node q's
+    // range in leaf order (the reference's order and roundings), so the
+    // dependent chain is the largest range, not the sum of all ranges; the
+    // excess is the max over the nodes' overloads (exact in any order) and
+    // the within-capacity nodes a ballot
     if (isport) cur_s[lane] = c;
     __syncwarp();
-    for (int q = 0; q < P.n_nodes; ++q) {
-      double cap, eta, rcp_eta;
-      int lo, hq;
-      tc.rec(q, cap, eta, rcp_eta, lo, hq);
-      const int hp = hq < n ? hq : n;
-      double s = 0.0;
-      for (int j = lo; j < hp; ++j) s += cur_s[j];
-      const double over = fabs(node_load(s, eta, rcp_eta)) - cap;
+    for (int q0 = 0; q0 < P.n_nodes; q0 += 32) {
+      const int q = q0 + lane;
+      double over = 0.0;
+      bool ok = false;
+      if (q < P.n_nodes) {
+        double cap, eta, rcp_eta;
+        int lo, hq;
+        tc.rec(q, cap, eta, rcp_eta, lo, hq);
+        const int hp = hq < n ? hq : n;
+        double s = 0.0;
+        for (int j = lo; j < hp; ++j) s += cur_s[j];
+        over = fabs(node_load(s, eta, rcp_eta)) - cap;
+        ok = !(over > 0.0);
+      }
       if (over > excess) excess = over;
-      if (!(over > 0.0)) clean |= 1ull << (q & 63);
+      const uint64_t bits = __ballot_sync(FULL, ok);
+      if (q0 < 64) clean |= bits << q0;
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {  // warp max of the overloads (NaN never wins, as in the serial scan)
+      const double x = __shfl_xor_sync(FULL, excess, o);
+      if (x > excess) excess = x;
+    }
+    if (P.n_nodes > 64) clean = 0;  // fit_tree_flat tracks clean nodes only up to 64
     __syncwarp();
     if (excess > 0.0) {  // warp-uniform: every lane summed the same values
       if (isport) cur_s[lane] = c;

@@ -1,0 +1,55 @@
+"""Phase timing of the fused PPO rollout (k_ppo_rollout): builds a variant of
+the extension with -DVY_PPO_PROF (clock64 marks of CTA 0 thread 0) into
+/tmp/vyprof, runs one rollout and prints the cycles per step of each phase.
+python scripts/probe_ppo_phases.py [--envs 16] [--epc 4]"""
+import argparse
+import ctypes as C
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+sys.path.insert(0, ".")
+ap = argparse.ArgumentParser()
+ap.add_argument("--envs", type=int, default=16)
+ap.add_argument("--epc", type=int, default=0)
+args = ap.parse_args()
+if args.epc:
+    os.environ["VY_PPO_EPC"] = str(args.epc)
+from paper_2507_01522_b200 import _build, _native  # noqa: E402
+
+out = Path("/tmp/vyprof")
+out.mkdir(exist_ok=True)
+objs = []
+for src in _build._sources():
+    o = out / (src.stem + ".o")
+    subprocess.run([_build.nvcc(), *_build.NVCC_FLAGS, "-DVY_PPO_PROF", "-c", str(src), "-o", str(o)], check=True,
+                   capture_output=True)
+    objs.append(str(o))
+lib = out / "libvoltyard_b200.so"
+subprocess.run([_build.nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(lib), *objs],
+               check=True)
+_native.LIB_PATH = lib
+
+import torch  # noqa: E402
+
+from paper_2507_01522_b200 import default_setup  # noqa: E402
+from paper_2507_01522_b200.batch import BatchEnv  # noqa: E402
+from paper_2507_01522_b200.ppo import PPOConfig, PPOTrainer  # noqa: E402
+
+rc = default_setup()
+env = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=args.envs, master_seed=1)
+T = 300
+tr = PPOTrainer(env, PPOConfig(rollout_steps=T, use_graph=False))
+tr.rollout()
+torch.cuda.synchronize()
+h = _native.lib()
+h.vy_ppo_prof_read.argtypes = [C.c_void_p]
+buf = (C.c_ulonglong * 16)()
+h.vy_ppo_prof_read(buf)
+names = ["env sync wait", "obs->A + sync", "L1 mma", "ep1 + sync", "L2 mma", "ep2 + sync", "L3 mma", "head + sync",
+         "logp", "env step (warp 0)"]
+tot = sum(buf[i] for i in range(10))
+for i, nm in enumerate(names):
+    print(f"{nm:20s} {buf[i] / T:8.0f} cyc/step  {100 * buf[i] / tot:5.1f}%")
+print(f"total {tot / T:.0f} cycles per step")
