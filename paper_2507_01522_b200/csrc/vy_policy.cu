@@ -213,45 +213,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(bar_mma, ph_mma);
     ph_mma ^= 1;
     tc_fence_after();
-    constexpr float kLog2e = 1.4426950408889634f;
     for (int s = warp; s < G.S; s += kWarps) {
       uint32_t v[24];
       const uint32_t ta = tmem + tq + kSlotCols * s;
       VYP_LD16(ta, v);
       VYP_LD8(ta + 16, v, 16);
       tmem_wait_ld();
-      float z[kMaxA];
-      float m = -INFINITY;
-#pragma unroll
-      for (int k = 0; k < kMaxA; ++k) {
-        z[k] = k < G.A ? bf16r(__uint_as_float(v[k]) + bh[kSlotCols * s + k]) : -INFINITY;  // bf16 logits
-        m = fmaxf(m, z[k]);
-      }
-      const float mb = m * kLog2e;
-      float sum = 0.f;
-#pragma unroll
-      for (int k = 0; k < kMaxA; ++k) sum += exp2_sfu(fmaf(z[k], kLog2e, -mb));  // exp(z - m); 0 past A
       // one uniform per (row, slot): element (row * S + s) of this call's stream
       const uint64_t x = mix64(key + (uint64_t)(grow * G.S + s) * 0x9E3779B97F4A7C15ULL);
-      const float target = ((float)(x >> 41) + 0.5f) * (1.f / 8388608.f) * sum;
-      // inverse CDF: the first k whose running sum passes u * sum (the last
-      // valid action if rounding leaves target at or above the total)
-      float c = 0.f, za = z[0];
-      int a = -1;
-#pragma unroll
-      for (int k = 0; k < kMaxA; ++k) {
-        c += exp2_sfu(fmaf(z[k], kLog2e, -mb));
-        const bool take = a < 0 && k < G.A && (target < c || k == G.A - 1);
-        a = take ? k : a;
-        za = take ? z[k] : za;
-      }
-      lpart[lane * G.S + s] = (za - m) - __logf(sum);
+      int a;
+      float lp;
+      if (G.A == kMaxA)
+        sample_slot<kMaxA>(v, bh + kSlotCols * s, G.A, x, a, lp);
+      else
+        sample_slot<0>(v, bh + kSlotCols * s, G.A, x, a, lp);
+      lpart[lane * G.S + s] = lp;
       if (live) {
         actions[grow * G.S + s] = (uint8_t)a;
         if (logits_out)
 #pragma unroll
           for (int k = 0; k < kMaxA; ++k)
-            if (k < G.A) logits_out[grow * (G.S * G.A) + s * G.A + k] = z[k];
+            if (k < G.A) logits_out[grow * (G.S * G.A) + s * G.A + k] = bf16r(__uint_as_float(v[k]) + bh[kSlotCols * s + k]);
       }
     }
     tc_fence_before();

@@ -133,7 +133,6 @@ __global__ void __launch_bounds__(kPpoThreads, 1)
   if (env_warp) env.load(P, pc, dtab, b0 + warp, lane);
   const unsigned long long call0 = R.counter[0];
   uint32_t ph_mma = 0;
-  constexpr float kLog2e = 1.4426950408889634f;
 
 #ifdef VY_PPO_PROF
   unsigned long long prof_last = clock64();
@@ -234,67 +233,37 @@ __global__ void __launch_bounds__(kPpoThreads, 1)
     PPO_MARK(6);
     vyp::tc_fence_after();
     const bool sample = t < T;  // pass T is the bootstrap value only
-    // the head, slot by slot: rows 0..15 are this CTA's envs (TMEM lanes 0..15
-    // of every quadrant); a warp with a second slot s0 + 16 reads it into its
-    // upper half-warp with the .16x32bx2 shape, so 17 slots take one round
+    // the head: rows 0..15 are this CTA's envs (TMEM lanes 0..15 of every
+    // quadrant), so a warp takes two slots at once — lanes 0..15 slot s0,
+    // lanes 16..31 slot s0 + 8 through the .16x32bx2 load — and 17 slots
+    // occupy 9 warps for one round (warp w < 8: slots w, w + 8; warp w >= 8:
+    // slot w + 8 and, for S > 24, w + 16)
     const int hrow = lane & 15;
     const int64_t hgrow = b0 + hrow;
-    for (int s0 = warp; sample && s0 < G.S; s0 += 2 * kPpoWarps) {
-      const bool pair = s0 + kPpoWarps < G.S;  // warp-uniform
+    for (int s0 = warp < 8 ? warp : warp + 8; sample && s0 < G.S; s0 += 32) {
+      const bool pair = s0 + 8 < G.S;  // warp-uniform
       uint32_t v[24];
       const uint32_t ta = tmem + tq + kSlotCols * s0;
       if (pair) {
-        VYP_LD16X2(ta, v, 384);  // 384 = kPpoWarps * kSlotCols columns: slot s0 + 16
-        VYP_LD8X2(ta + 16, v, 16, 384);
+        VYP_LD16X2(ta, v, 192);  // 192 = 8 * kSlotCols columns: slot s0 + 8
+        VYP_LD8X2(ta + 16, v, 16, 192);
       } else {
         VYP_LD16(ta, v);
         VYP_LD8(ta + 16, v, 16);
       }
       vyp::tmem_wait_ld();
-      const int s = (pair && lane >= 16) ? s0 + kPpoWarps : s0;
+      const int s = (pair && lane >= 16) ? s0 + 8 : s0;
       const bool mine = lane < 16 || pair;  // an unpaired warp's upper lanes hold unused rows
-      // the slot's 24 head biases as six 16-byte loads, all issued before use
-      // (a slot owns kSlotCols bias entries, so the reads stay inside bh)
-      float bq[kSlotCols];
-#pragma unroll
-      for (int q = 0; q < kSlotCols / 4; ++q) {
-        const float4 f = reinterpret_cast<const float4*>(bh + kSlotCols * s)[q];
-        bq[4 * q] = f.x;
-        bq[4 * q + 1] = f.y;
-        bq[4 * q + 2] = f.z;
-        bq[4 * q + 3] = f.w;
-      }
-      float z[kMaxA], e[kMaxA];
-      float m = -INFINITY;
-#pragma unroll
-      for (int k = 0; k < kMaxA; ++k) {
-        const float zk = vyp::bf16r(__uint_as_float(v[k]) + bq[k]);  // bf16 logits
-        z[k] = k < G.A ? zk : -INFINITY;
-        m = fmaxf(m, z[k]);
-      }
-      const float mb = m * kLog2e;
-      float sum = 0.f;
-#pragma unroll
-      for (int k = 0; k < kMaxA; ++k) {
-        e[k] = vyp::exp2_sfu(fmaf(z[k], kLog2e, -mb));  // exp(z - m); 0 past A
-        sum += e[k];
-      }
       // one uniform per (row, slot): element (row * S + s) of this pass's stream
       const uint64_t x = vyp::mix64(key + (uint64_t)(hgrow * G.S + s) * 0x9E3779B97F4A7C15ULL);
-      const float target = ((float)(x >> 41) + 0.5f) * (1.f / 8388608.f) * sum;
-      // inverse CDF: the first k whose running sum passes u * sum (the last
-      // valid action if rounding leaves target at or above the total)
-      float c = 0.f, za = z[0];
-      int a = -1;
-#pragma unroll
-      for (int k = 0; k < kMaxA; ++k) {
-        c += e[k];
-        const bool take = a < 0 && k < G.A && (target < c || k == G.A - 1);
-        a = take ? k : a;
-        za = take ? z[k] : za;
-      }
+      int a;
+      float lp;
+      if (G.A == kMaxA)
+        vyp::sample_slot<kMaxA>(v, bh + kSlotCols * s, G.A, x, a, lp);
+      else
+        vyp::sample_slot<0>(v, bh + kSlotCols * s, G.A, x, a, lp);
       if (mine) {
-        lpart[hrow * G.S + s] = (za - m) - __logf(sum);
+        lpart[hrow * G.S + s] = lp;
         if (hrow < rows) {
           R.actions[(t * B + hgrow) * G.S + s] = (uint8_t)a;
           act_s[hrow * kPpoActRow + s] = (uint8_t)a;

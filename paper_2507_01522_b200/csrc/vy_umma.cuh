@@ -158,7 +158,14 @@ __device__ __forceinline__ void mma_chain(uint32_t d_tmem, uint32_t a, uint32_t 
                : "r"(taddr))
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-__device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+// float -> bf16 (round to nearest even) -> float on the integer pipe: the
+// same value as __float2bfloat16_rn for every non-NaN input (overflow to
+// infinity included); NaN passes through unchanged
+__device__ __forceinline__ float bf16r(float x) {
+  const uint32_t u = __float_as_uint(x);
+  const uint32_t r = (u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u;
+  return x != x ? x : __uint_as_float(r);
+}
 // hardware tanh (MUFU.TANH, rel. error ~2^-11): its result is rounded to bf16 next
 __device__ __forceinline__ float tanh_sfu(float x) {
   float y;
@@ -195,6 +202,58 @@ __device__ __forceinline__ void act_to_a(const uint32_t* v, const float* bias, u
 #pragma unroll
   for (int rep = 0; rep < 4; ++rep)
     *reinterpret_cast<uint4*>(a_base + (size_t)c * (kM * 16) + (r + kRows * rep) * 16) = val;
+}
+
+// One (row, slot) of the multi-discrete head: bf16 logits z = bf16(acc +
+// bias) for the slot's A actions, max, exp(z - m) summed in action order, the
+// inverse-CDF sample of the uniform `x >> 41` (the first k whose running sum
+// passes u * sum; the last action if rounding leaves the target at or above
+// the total) and its log-probability (z_a - m) - log(sum).  v: the slot's 24
+// accumulator columns; bias: its 24 head biases (16-byte aligned).  AC: the
+// action count at compile time (0 = runtime A).  Shared by k_policy_step and
+// k_ppo_rollout so both sample identically.
+template <int AC>
+__device__ __forceinline__ void sample_slot(const uint32_t* v, const float* bias, int A_rt, uint64_t x, int& act,
+                                            float& lp) {
+  constexpr float kLog2e = 1.4426950408889634f;
+  const int A = AC ? AC : A_rt;
+  float bq[kSlotCols];
+#pragma unroll
+  for (int q = 0; q < kSlotCols / 4; ++q) {  // six 16-byte loads, all issued before use
+    const float4 f = reinterpret_cast<const float4*>(bias)[q];
+    bq[4 * q] = f.x;
+    bq[4 * q + 1] = f.y;
+    bq[4 * q + 2] = f.z;
+    bq[4 * q + 3] = f.w;
+  }
+  constexpr int KN = AC ? AC : kMaxA;
+  float z[KN], e[KN];
+  float m = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < KN; ++k) {
+    const float zk = bf16r(__uint_as_float(v[k]) + bq[k]);  // bf16 logits
+    z[k] = (AC || k < A) ? zk : -INFINITY;
+    m = fmaxf(m, z[k]);
+  }
+  const float mb = m * kLog2e;
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < KN; ++k) {
+    e[k] = exp2_sfu(fmaf(z[k], kLog2e, -mb));  // exp(z - m); 0 past A
+    sum += e[k];
+  }
+  const float target = ((float)(x >> 41) + 0.5f) * (1.f / 8388608.f) * sum;
+  float c = 0.f, za = z[0];
+  int a = -1;
+#pragma unroll
+  for (int k = 0; k < KN; ++k) {
+    c += e[k];
+    const bool take = a < 0 && (AC || k < A) && (target < c || k == A - 1);
+    a = take ? k : a;
+    za = take ? z[k] : za;
+  }
+  act = a;
+  lp = (za - m) - __logf(sum);
 }
 
 }  // namespace vyp
