@@ -830,6 +830,10 @@ int vy_ppo_prof_read(unsigned long long* out) {
   VY_CUDA(cudaMemcpyFromSymbol(out, g_ppo_prof, sizeof(g_ppo_prof)));
   return VY_OK;
 }
+int vy_env_stamps_read(unsigned long long* out) {
+  VY_CUDA(cudaMemcpyFromSymbol(out, g_env_stamp, sizeof(g_env_stamp)));
+  return VY_OK;
+}
 #endif
 
 int vy_set_wide(vy_handle* h, int32_t mode) {

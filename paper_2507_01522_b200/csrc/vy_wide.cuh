@@ -29,6 +29,18 @@ namespace vy {
 constexpr int kWideWarps = 8;  // warps (= envs) per CTA
 constexpr int kWideScratch = 32 + 4 * 32;  // doubles of per-warp shared scratch
 
+#ifdef VY_PPO_PROF  // phase stamps of the env step (scripts/probe_ppo_phases.py): CTA 0 thread 0, first 256 steps
+__device__ unsigned long long g_env_stamp[256 * 16];
+__device__ int g_env_t;
+#define ENV_MARK(i)                                                                           \
+  if (blockIdx.x == 0 && threadIdx.x == 0 && g_env_t < 256) g_env_stamp[g_env_t * 16 + (i)] = clock64();
+#define ENV_NEXT() \
+  if (blockIdx.x == 0 && threadIdx.x == 0) ++g_env_t;
+#else
+#define ENV_MARK(i)
+#define ENV_NEXT()
+#endif
+
 // _kernel.pyx:626-649 on a flat array of currents (lane 0 only; rare: a tree
 // node over capacity).  Same values and pass structure as fit_tree.
 __device__ __noinline__ void fit_tree_flat(const Params& P, TreeC tc, double* cur, int n, uint64_t clean) {
@@ -143,6 +155,7 @@ struct WideEnv {
     const int n = P.n_ports;
     const bool isport = lane < n;
     const int64_t ld = P.ld;
+    ENV_MARK(0);
     const int tt = E.step;
     const Frame F = load_frame<M>(P, tt, E.day);
     // the obs globals of the state after this step, in flight during it (lanes 0..8 write them)
@@ -160,6 +173,7 @@ struct WideEnv {
       c = clip_current(tgt, soc, prof.tau(pf), prof.omt(pf), prof.rcp_omt(pf),
                        kindv != 0.0 ? prof.r_dc(pf) : prof.r_ac(pf), volt, rcp_volt, imax_c, imax_d);
     }
+    ENV_MARK(1);
     // tree: excess on the requested currents (_kernel.pyx:611-624), node loads in leaf order
     double excess = 0.0;
     uint64_t clean = 0;
@@ -195,6 +209,7 @@ struct WideEnv {
     }
     if (P.n_nodes > 64) clean = 0;  // fit_tree_flat tracks clean nodes only up to 64
     __syncwarp();
+    ENV_MARK(9);
     if (excess > 0.0) {  // warp-uniform: every lane summed the same values
       if (isport) cur_s[lane] = c;
       __syncwarp();
@@ -204,6 +219,7 @@ struct WideEnv {
       __syncwarp();
     }
 
+    ENV_MARK(2);
     // phases 2+3: charge, dwell countdown, departures (_kernel.pyx:358-458)
     double got = 0.0, t_in = 0.0, t_out = 0.0, t_sat0 = 0.0, t_sat1 = 0.0, t_miss = 0.0;
     bool dep = false;
@@ -237,6 +253,7 @@ struct WideEnv {
       }
       if (!dep && p == 1 && dt < 0) t_over = -dt;
     }
+    ENV_MARK(3);
     // the reference's sequential sums over the ports, in port order, on every lane
     double e_net = 0.0, e_in = 0.0, e_out = 0.0;
     if (isport) {
@@ -252,6 +269,7 @@ struct WideEnv {
       e_out += flow_s[4 * j + 2];
     }
     __syncwarp();
+    ENV_MARK(4);
     double sat0 = 0.0, sat1 = 0.0;
     const unsigned depm = __ballot_sync(FULL, dep);
     if (depm) {
@@ -273,6 +291,7 @@ struct WideEnv {
     idr = c;
     uint64_t occm = (uint64_t)__ballot_sync(FULL, isport && (mt & 1u));
 
+    ENV_MARK(5);
     // phase 4: arrivals (_kernel.pyx:460-509), drawn identically on every lane
     uint64_t st = fold(E.akey, (uint64_t)(int64_t)tt);
     int marr = 0;
@@ -307,6 +326,7 @@ struct WideEnv {
     }
     E.ep_declined += declined;
 
+    ENV_MARK(6);
     // reward (_kernel.pyx:511-551), lean: no battery / carbon / demand terms
     const double e_b = 0.0;
     const double e_grid_net = e_in + e_out + e_b;
@@ -353,6 +373,7 @@ struct WideEnv {
       dt = 0;
     }
 
+    ENV_MARK(7);
     // observation (_kernel.pyx:575-607): port j's six columns from lane j, the globals from lanes 0..8
     if (isport) {
       const bool o = mt & 1u;
@@ -381,6 +402,8 @@ struct WideEnv {
       __stcs(orow + 6 * n + lane, (float)v);
       if (kStage) srow[6 * n + lane] = (float)v;
     }
+    ENV_MARK(8);
+    ENV_NEXT();
   }
 };
 

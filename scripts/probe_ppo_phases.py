@@ -53,3 +53,19 @@ tot = sum(buf[i] for i in range(10))
 for i, nm in enumerate(names):
     print(f"{nm:20s} {buf[i] / T:8.0f} cyc/step  {100 * buf[i] / tot:5.1f}%")
 print(f"total {tot / T:.0f} cycles per step")
+
+h.vy_env_stamps_read.argtypes = [C.c_void_p]
+st = (C.c_ulonglong * (256 * 16))()
+h.vy_env_stamps_read(st)
+import numpy as np  # noqa: E402
+
+a = np.frombuffer(st, dtype=np.uint64).reshape(256, 16)[:, :9].astype(np.int64)
+d = np.diff(a, axis=1)[1:]  # skip the first step (cold)
+enames = ["frame+act+clip", "node sums", "charge", "flow sums", "dep sums", "arrivals", "reward+out", "obs"]
+for i, nm in enumerate(enames):
+    print(f"  env {nm:12s} mean {d[:, i].mean():7.0f}  median {np.median(d[:, i]):7.0f}  p90 {np.percentile(d[:, i], 90):7.0f}")
+print(f"  env total mean {d.sum(1).mean():.0f}")
+full = np.frombuffer(st, dtype=np.uint64).reshape(256, 16).astype(np.int64)[1:]
+pre, fit = full[:, 9] - full[:, 1], full[:, 2] - full[:, 9]
+print(f"  node sums before the rescale: mean {pre.mean():.0f}; rescale: mean {fit.mean():.0f}, "
+      f"steps with a rescale {(fit > 200).mean() * 100:.0f}%")
