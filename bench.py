@@ -542,10 +542,7 @@ def main() -> None:
                          "optimizer_steps_per_100k_env_steps": 1e5 * cfg.update_epochs * cfg.n_minibatches
                                                                / (4096 * world * cfg.rollout_steps),
                          "rollout": tr.describe_rollout() if hasattr(tr, "describe_rollout") else None,
-                         "update": ("one CUDA graph per update: vy_gae, vy_gather_rows minibatch gather, bf16 GEMMs "
-                                    "with column-sum bias gradients (vy_colsum), vy_ppo_loss (log-prob, entropy, "
-                                    "value, clipped surrogate / value losses and d loss / d head rows in one pass), "
-                                    "fused Adam"),
+                         "update": tr.describe_update(),
                          "grad_allreduce": "NCCL all_reduce per minibatch" if world > 1 else "none (1 GPU)",
                          "paper_reference": "Chargax PPO(16) 0.65 s / 100k on RTX 4000 Ada (PAPER.md:239); a "
                                             "different workload (16 envs, 900-sample minibatches): see ppo_paper"}

@@ -361,6 +361,31 @@ int vy_ppo_rollout(vy_handle *h, int32_t T, const void *wpack, const float *fpac
                    uint64_t seed, int64_t *counter, float *obs, uint8_t *actions, float *logp, float *value,
                    float *reward, uint8_t *done, void *stream);
 
+/* One PPO minibatch update for small batches in three launches (fp32):
+ * vy_ppo_update_grad = forward of the ppo.py actor-critic from its live fp32
+ * weights (weights[10]: the module's parameters in order — W1 [2H][K1], b1,
+ * Wa2, ba2, Wh [NO][H], bh, Wc2, bc2, wv [1][H], bv; K1 = obs_dim rounded up
+ * to 8, NO = S*A rounded up to 8, H = hidden = 64), the clipped PPO loss of
+ * vy_ppo_loss with the advantages normalised over the minibatch, backward,
+ * per-CTA partial gradients summed in CTA order into grad_out[P] (the flat
+ * gradient, module order), the minibatch means {loss, pg, vf, ent} into
+ * stats[4], *step += 1.  Rows: idx[M] into obs [*][obs_ld] float32, actions
+ * [*][S] uint8, scal4 [*] float4 {old_lp, old_v, adv, ret}.
+ * vy_ppo_update_adam = torch's clip_grad_norm_(max_grad_norm) coefficient
+ * and Adam (betas, eps, lr read on the device, bias correction from *step)
+ * on params[10] in place; exp_avg / exp_avg_sq [P] zero-initialised by the
+ * caller.  A multi-GPU caller all-reduces grad_out between the two.
+ * vy_ppo_update_workspace: out = {P, work floats, grad CTAs, shared bytes}.
+ * Not part of the reference (trainer-free). */
+int vy_ppo_update_workspace(int32_t obs_dim, int32_t S, int32_t A, int32_t hidden, int64_t M, int64_t out[4]);
+int vy_ppo_update_grad(const float *const *weights, int32_t obs_dim, int32_t S, int32_t A, int32_t hidden,
+                       const float *obs, int64_t obs_ld, const uint8_t *actions, const float *scal4,
+                       const int64_t *idx, int64_t M, float clip_eps, float vf_clip, float vf_coef, float ent_coef,
+                       float *work, float *grad_out, float *stats, float *step, void *stream);
+int vy_ppo_update_adam(float *const *params, int32_t obs_dim, int32_t S, int32_t A, int32_t hidden, int64_t M,
+                       float *work, const float *grad, float *exp_avg, float *exp_avg_sq, const float *lr,
+                       const float *step, float beta1, float beta2, float eps, float max_grad_norm, void *stream);
+
 int vy_gather_rows(const void *src, int64_t row_bytes, const int64_t *idx, int64_t n, void *dst, void *stream);
 /* Column sums (a linear layer's bias gradient): out[c] = sum over m < M of
  * g[m*ld + c], c < N; g float32 (dtype 0) or bfloat16 (1); out float32.

@@ -68,6 +68,9 @@ class PPOConfig:
     # (vy_ppo_rollout: 16 envs per CTA, one wave on 148 SMs); lean stations
     # without a battery, else the per-step pair
     fused_rollout: bool = True
+    # minibatches of <= 8192 samples: forward + loss + backward + clip + Adam as
+    # three kernels per minibatch, fp32 (vy_ppo_update_*), instead of autograd
+    fused_update: bool = True
     fused_loss: bool = True  # the update's loss head (log-prob, entropy, value, clipped losses, gradient) as one pass
     allreduce: str = "auto"  # gradient all-reduce: "auto" (world > 1), "always" (also at world 1: tests)
     wide_env: bool = True  # env step on the one-warp-per-env kernel at <= 2048 envs (vy_set_wide)
@@ -517,6 +520,25 @@ class PPOTrainer:
             self._geo = policy_geometry(self.net)
             self._scratch_a = torch.zeros(B, A, dtype=torch.uint8, device=dev)
             self._scratch_lp = torch.zeros(B, device=dev)
+        self._fused_update = False
+        mb = T * B // cfg.n_minibatches
+        if cfg.fused_update and cfg.hidden == 64 and 2 <= mb <= 8192:
+            ws = (C.c_int64 * 4)()
+            if nat.lib().vy_ppo_update_workspace(self.net.obs_dim, self.net.n_slots, self.net.n_actions, cfg.hidden,
+                                                 mb, ws) == nat.VY_OK:
+                self._fused_update = True
+                P = ws[0]
+                self._uwork = torch.zeros(ws[1], device=dev)
+                self._ugrad = torch.zeros(P, device=dev)
+                self._adam_m = torch.zeros(P, device=dev)
+                self._adam_v = torch.zeros(P, device=dev)
+                self._adam_step = torch.zeros(1, device=dev)
+                self._ustats_buf = torch.zeros(4, device=dev)
+                if not hasattr(self, "_lr"):
+                    self._lr = torch.tensor(cfg.lr, device=dev)
+                prm = list(self.net.parameters())
+                assert sum(p.numel() for p in prm) == P
+                self._uparams = (C.c_void_p * len(prm))(*[p.data_ptr() for p in prm])
         env.reset(as_numpy=False)
         self.obs[0].copy_(env.outs.obs)
 
@@ -631,6 +653,8 @@ class PPOTrainer:
         if not self._graph_update:
             for g in self.opt.param_groups:
                 g["lr"] = lr
+            if self._fused_update:
+                self._lr.fill_(lr)
             stats = self._update_body()
         else:
             self._lr.fill_(lr)
@@ -663,6 +687,8 @@ class PPOTrainer:
         n = T * B
         mb = n // cfg.n_minibatches
         stats = {}
+        if self._fused_update:
+            return self._fused_update_body(adv, ret, scal, n, mb)
         for _ in range(cfg.update_epochs):
             perm = torch.argsort(torch.rand(n, device=obs.device))  # a uniform permutation, capture-safe
             for k in range(cfg.n_minibatches):
@@ -709,6 +735,45 @@ class PPOTrainer:
                 stats = {"loss": loss.detach(), "pg": pg.detach(), "vf": vl.detach(), "ent": ent.detach()}
         self.obs[0].copy_(self.obs[T])
         return stats
+
+    def _fused_update_body(self, adv, ret, scal, n: int, mb: int) -> dict:
+        """Epochs x minibatches of vy_ppo_update_grad (+ the gradient all-reduce
+        across ranks) + vy_ppo_update_adam; the rollout rows are read in place
+        through each minibatch's index slice."""
+        cfg, T = self.cfg, self.cfg.rollout_steps
+        lib, st = nat.lib(), torch.cuda.current_stream().cuda_stream
+        obs = self.obs[:T].reshape(n, -1)
+        act = self.actions.reshape(n, -1)
+        scal = scal.contiguous()
+        S, A, H, od = self.net.n_slots, self.net.n_actions, cfg.hidden, self.net.obs_dim
+        for _ in range(cfg.update_epochs):
+            perm = torch.argsort(torch.rand(n, device=obs.device))  # a uniform permutation, capture-safe
+            for k in range(cfg.n_minibatches):
+                idx = perm[k * mb:(k + 1) * mb]
+                nat.check(lib.vy_ppo_update_grad(self._uparams, od, S, A, H, obs.data_ptr(), obs.stride(0),
+                                                 act.data_ptr(), scal.data_ptr(), idx.data_ptr(), mb, cfg.clip_eps,
+                                                 cfg.vf_clip, cfg.vf_coef, cfg.ent_coef, self._uwork.data_ptr(),
+                                                 self._ugrad.data_ptr(), self._ustats_buf.data_ptr(),
+                                                 self._adam_step.data_ptr(), st), "vy_ppo_update_grad")
+                if self._allreduce:  # the flat gradient, SUM then / world (gloo has no AVG)
+                    dist.all_reduce(self._ugrad, op=dist.ReduceOp.SUM)
+                    self._ugrad.div_(self.world)
+                nat.check(lib.vy_ppo_update_adam(self._uparams, od, S, A, H, mb, self._uwork.data_ptr(),
+                                                 self._ugrad.data_ptr(), self._adam_m.data_ptr(),
+                                                 self._adam_v.data_ptr(), self._lr.data_ptr(),
+                                                 self._adam_step.data_ptr(), 0.9, 0.999, 1e-5, cfg.max_grad_norm, st),
+                          "vy_ppo_update_adam")
+        self.obs[0].copy_(self.obs[T])
+        s = self._ustats_buf
+        return {"loss": s[0].clone(), "pg": s[1].clone(), "vf": s[2].clone(), "ent": s[3].clone()}
+
+    def describe_update(self) -> str:
+        if self._fused_update:
+            return ("per minibatch: vy_ppo_update_grad (fp32 forward, clipped loss, backward, per-CTA partial "
+                    "gradients; 16 samples per CTA) + k_ppo_gsum (ordered sum, squares) + vy_ppo_update_adam "
+                    "(clip_grad_norm_ + Adam in place); epochs x minibatches in one CUDA graph")
+        return ("one CUDA graph per update: vy_gae, vy_gather_rows minibatch gather, bf16 GEMMs with column-sum "
+                "bias gradients (vy_colsum), vy_ppo_loss, fused Adam")
 
     def describe_rollout(self) -> str:
         if self._fused_rollout:
