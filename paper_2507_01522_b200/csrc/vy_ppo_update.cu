@@ -6,16 +6,17 @@
 // weight casts, three GEMM pairs, bias column sums, tanh forward/backward,
 // the loss kernel, the norm, Adam — each a few microseconds of latency on an
 // idle GPU at these sizes (~190 us per minibatch, CUDA graph replayed).  Here:
-//   k_ppo_grad  (ceil(M/16) CTAs x 256 threads): every CTA normalises the
+//   k_ppo_grad  (ceil(M/8) CTAs x 512 threads): every CTA normalises the
 //     minibatch's advantages (mean / unbiased std over all M rows, the same
-//     fixed-order reduction in every CTA), gathers its <= 16 rows, runs the
-//     actor-critic forward in fp32 from the live fp32 weights (L2-resident),
+//     fixed-order reduction in every CTA), gathers its <= 8 rows, runs the
+//     actor-critic forward in fp32 from transposed copies of the live fp32
+//     weight matrices (L2-resident; k_ppo_adam keeps them in step), 
 //     the loss head of k_ppo_loss (same formulas: log-softmax per slot,
 //     entropy, clipped surrogate, clipped value loss), the backward through
 //     the three layers, and writes its partial weight gradient (sum over its
 //     rows) and loss sums;
-//   k_ppo_gsum  (one thread per parameter): the partials summed over the CTAs
-//     in CTA order (deterministic) -> the flat gradient; per-block sums of
+//   k_ppo_gsum  (four threads per parameter): the partials summed over the
+//     CTAs in a fixed order (contiguous quarters, then the quarters in order) -> the flat gradient; per-block sums of
 //     squares; block 0 also sums the loss statistics and advances the Adam
 //     step counter;
 //   (the caller may all-reduce the flat gradient here: NCCL, multi-GPU)
@@ -33,13 +34,15 @@
 
 namespace vyu {
 
-constexpr int kRows = 16;      // rows per CTA
-constexpr int kThreads = 256;
+// rows per CTA: 8, or 16 when 8 would need more than one wave of CTAs
+__host__ __device__ inline int rows_per_cta(int64_t M, int num_sms) { return M <= 8LL * num_sms ? 8 : 16; }
+constexpr int kThreads = 512;
 constexpr int kH = 64;         // hidden width per branch
 constexpr int kNP = 10;        // parameter tensors (ActorCritic order)
 
 struct Net {
   const float* w[kNP];  // w1, b1, wa2, ba2, wh, bh, wc2, bc2, wv, bv
+  const float* wt;      // W1 transposed [K1][2H] (coalesced first-layer reads)
   int64_t off[kNP + 1];  // flat offsets (the module's parameter order)
   int K1, NO;            // padded input width (W1 columns), head rows (out_dim)
 };
@@ -84,23 +87,57 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return red[32];
 }
 
-// out[r][n] = act(b[n] + sum_k W[n][k] in[r][k]) for r < R, n < N; thread
-// item (n, g) takes rows g, g + G, ...  W row-major global (float4 rows).
-template <int G, bool kTanh>
-__device__ __forceinline__ void dense(const float* __restrict__ W, const float* __restrict__ b, int N, int K,
-                                      const float* in, int ldi, float* out, int ldo, int R) {
-  constexpr int RP = kRows / G;
+// out[r][n] = act(b[n] + sum_k WT[k][n] in[r][k]) for r < R, n < N; thread
+// item (n, g) takes rows g, g + G, ...  WT: the transposed weight [K][N] in
+// global memory (the threads of a warp read consecutive n: coalesced).
+template <int ROWS, int G, bool kTanh>
+__device__ __forceinline__ void dense_gt(const float* __restrict__ WT, const float* __restrict__ b, int N, int K,
+                                         const float* in, int ldi, float* out, int ldo, int R) {
+  constexpr int RP = ROWS / G;
   for (int it = threadIdx.x; it < N * G; it += kThreads) {
     const int n = it % N, g = it / N;
     float acc[RP];
 #pragma unroll
     for (int j = 0; j < RP; ++j) acc[j] = 0.f;
-    const float4* wr = reinterpret_cast<const float4*>(W + (int64_t)n * K);
-    for (int k4 = 0; k4 < K / 4; ++k4) {
-      const float4 w = __ldg(wr + k4);
+#pragma unroll 4
+    for (int k = 0; k < K; k += 4) {
+      const float w0 = __ldg(WT + (int64_t)k * N + n), w1 = __ldg(WT + (int64_t)(k + 1) * N + n);
+      const float w2 = __ldg(WT + (int64_t)(k + 2) * N + n), w3 = __ldg(WT + (int64_t)(k + 3) * N + n);
 #pragma unroll
       for (int j = 0; j < RP; ++j) {
-        const float4 x = *reinterpret_cast<const float4*>(in + (g + j * G) * ldi + 4 * k4);
+        const float4 x = *reinterpret_cast<const float4*>(in + (g + j * G) * ldi + k);
+        acc[j] = fmaf(w0, x.x, acc[j]);
+        acc[j] = fmaf(w1, x.y, acc[j]);
+        acc[j] = fmaf(w2, x.z, acc[j]);
+        acc[j] = fmaf(w3, x.w, acc[j]);
+      }
+    }
+    const float bn = __ldg(b + n);
+#pragma unroll
+    for (int j = 0; j < RP; ++j) {
+      const int r = g + j * G;
+      if (r < R) out[r * ldo + n] = kTanh ? tanhf(acc[j] + bn) : acc[j] + bn;
+    }
+  }
+}
+
+// the same from a row-major weight staged in shared memory, row stride ldw
+// (kH + 4: 16-byte row reads by consecutive n fall in distinct banks)
+template <int ROWS, int G, bool kTanh>
+__device__ __forceinline__ void dense_s(const float* W, int ldw, const float* __restrict__ b, int N, int K,
+                                        const float* in, int ldi, float* out, int ldo, int R) {
+  constexpr int RP = ROWS / G;
+  for (int it = threadIdx.x; it < N * G; it += kThreads) {
+    const int n = it % N, g = it / N;
+    float acc[RP];
+#pragma unroll
+    for (int j = 0; j < RP; ++j) acc[j] = 0.f;
+#pragma unroll 4
+    for (int k = 0; k < K; k += 4) {
+      const float4 w = *reinterpret_cast<const float4*>(W + n * ldw + k);
+#pragma unroll
+      for (int j = 0; j < RP; ++j) {
+        const float4 x = *reinterpret_cast<const float4*>(in + (g + j * G) * ldi + k);
         acc[j] = fmaf(w.x, x.x, acc[j]);
         acc[j] = fmaf(w.y, x.y, acc[j]);
         acc[j] = fmaf(w.z, x.z, acc[j]);
@@ -117,88 +154,141 @@ __device__ __forceinline__ void dense(const float* __restrict__ W, const float* 
 }
 
 // out[r][j] = (1 - h[r][j]^2) * sum_o d[r][o] W[o][j] (the gradient through
-// y = W x and the tanh that produced h), j < J, o < N; W row-major [N][J]
-template <int G>
-__device__ __forceinline__ void dense_t(const float* __restrict__ W, int N, int J, const float* d, int ldd,
-                                        const float* h, int ldh, float* out, int ldo, int R) {
-  constexpr int RP = kRows / G;
+// y = W x and the tanh that produced h), j < J, o < N; W row-major in shared
+// memory (row stride ldw; consecutive j: conflict-free), N a multiple of 4
+template <int ROWS, int G>
+__device__ __forceinline__ void dense_t(const float* W, int ldw, int N, int J, const float* d, int ldd,
+                                        const float* h, int ldh, float* out, int ldo) {
+  constexpr int RP = ROWS / G;
   for (int it = threadIdx.x; it < J * G; it += kThreads) {
     const int j = it % J, g = it / J;
     float acc[RP];
 #pragma unroll
     for (int q = 0; q < RP; ++q) acc[q] = 0.f;
-    for (int o = 0; o < N; ++o) {
-      const float w = __ldg(W + (int64_t)o * J + j);
+#pragma unroll 4
+    for (int o = 0; o < N; o += 4) {
+      const float w0 = W[o * ldw + j], w1 = W[(o + 1) * ldw + j], w2 = W[(o + 2) * ldw + j],
+                  w3 = W[(o + 3) * ldw + j];
 #pragma unroll
-      for (int q = 0; q < RP; ++q) acc[q] = fmaf(d[(g + q * G) * ldd + o], w, acc[q]);
+      for (int q = 0; q < RP; ++q) {
+        const float4 dq = *reinterpret_cast<const float4*>(d + (g + q * G) * ldd + o);
+        acc[q] = fmaf(dq.x, w0, acc[q]);
+        acc[q] = fmaf(dq.y, w1, acc[q]);
+        acc[q] = fmaf(dq.z, w2, acc[q]);
+        acc[q] = fmaf(dq.w, w3, acc[q]);
+      }
     }
 #pragma unroll
     for (int q = 0; q < RP; ++q) {
       const int r = g + q * G;
-      if (r < R) {
-        const float hv = h[r * ldh + j];
-        out[r * ldo + j] = acc[q] * (1.f - hv * hv);
-      }
+      const float hv = h[r * ldh + j];
+      out[r * ldo + j] = acc[q] * (1.f - hv * hv);
     }
   }
 }
 
 // partial gradients of y = W x + b over this CTA's rows: gW[n][k] = sum_r
-// d[r][n] in[r][k] -> dst[n*K + k], gb[n] = sum_r d[r][n] -> dstb[n]
-__device__ __forceinline__ void wgrad(const float* d, int ldd, const float* in, int ldi, int N, int K, int R,
+// d[r][n] in[r][k] -> dst[n*K + k], gb[n] = sum_r d[r][n] -> dstb[n].  All
+// ROWS rows (d is zero past the CTA's rows), four k per thread: 16-byte
+// loads, the whole row loop unrolled so its loads are in flight together.
+template <int ROWS>
+__device__ __forceinline__ void wgrad(const float* d, int ldd, const float* in, int ldi, int N, int K,
                                       float* __restrict__ dst, float* __restrict__ dstb) {
-  for (int e = threadIdx.x; e < N * K; e += kThreads) {
-    const int n = e / K, k = e - n * K;
-    float acc = 0.f;
-    for (int r = 0; r < R; ++r) acc = fmaf(d[r * ldd + n], in[r * ldi + k], acc);
-    dst[e] = acc;
+  const int K4 = K / 4;
+  for (int e = threadIdx.x; e < N * K4; e += kThreads) {
+    const int n = e / K4, k4 = e - n * K4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const float dn = d[r * ldd + n];
+      const float4 x = *reinterpret_cast<const float4*>(in + r * ldi + 4 * k4);
+      acc.x = fmaf(dn, x.x, acc.x);
+      acc.y = fmaf(dn, x.y, acc.y);
+      acc.z = fmaf(dn, x.z, acc.z);
+      acc.w = fmaf(dn, x.w, acc.w);
+    }
+    float* o = dst + (int64_t)n * K + 4 * k4;  // dst offsets are not 16-byte aligned in general
+    o[0] = acc.x;
+    o[1] = acc.y;
+    o[2] = acc.z;
+    o[3] = acc.w;
   }
   for (int n = threadIdx.x; n < N; n += kThreads) {
     float acc = 0.f;
-    for (int r = 0; r < R; ++r) acc += d[r * ldd + n];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) acc += d[r * ldd + n];
     dstb[n] = acc;
   }
 }
 
 __host__ __device__ inline int ld_pad(int x) { return (x + 3) / 4 * 4; }
+constexpr int kLdw = kH + 4;  // row stride of the staged [*][kH] weights
 
 struct Smem {
   int ldx, ldz;
+  int wa2, wc2, wh;                                    // staged weights (row stride kLdw)
   int x, h1, h2, z, dz2, dz1, rows, slot, red, bytes;  // float offsets
 };
-__host__ __device__ inline Smem smem_layout(int K1, int NO, int S) {
+__host__ __device__ inline Smem smem_layout(int rows, int K1, int NO, int S) {
   Smem s;
   s.ldx = K1;
   s.ldz = ld_pad(NO);
-  s.x = 0;
-  s.h1 = s.x + kRows * s.ldx;
-  s.h2 = s.h1 + kRows * 2 * kH;
-  s.z = s.h2 + kRows * 2 * kH;
-  s.dz2 = s.z + kRows * s.ldz;
-  s.dz1 = s.dz2 + kRows * 2 * kH;
-  s.rows = s.dz1 + kRows * 2 * kH;  // v, dv, g_lp, g_ent per row
-  s.slot = s.rows + 4 * kRows;      // [2][kRows * S]: log-prob and entropy terms
-  s.red = s.slot + 2 * kRows * ld_pad(S);
+  s.wa2 = 0;
+  s.wc2 = s.wa2 + kH * kLdw;
+  s.wh = s.wc2 + kH * kLdw;
+  s.x = s.wh + NO * kLdw;
+  s.h1 = s.x + rows * s.ldx;
+  s.h2 = s.h1 + rows * 2 * kH;
+  s.z = s.h2 + rows * 2 * kH;
+  s.dz2 = s.z + rows * s.ldz;
+  s.dz1 = s.dz2 + rows * 2 * kH;
+  s.rows = s.dz1 + rows * 2 * kH;  // v, dv, g_lp, g_ent per row
+  s.slot = s.rows + 4 * rows;      // [2][rows * S]: log-prob and entropy terms
+  s.red = s.slot + 2 * rows * ld_pad(S);
   s.bytes = (s.red + 40) * 4;
   return s;
 }
 
-__global__ void __launch_bounds__(kThreads) k_ppo_grad(const Net net, const Batch bt, const Work wk, int64_t P) {
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src) : "memory");
+}
+
+// [n][kH] row-major weight -> shared rows of stride kLdw, 16-byte async copies
+__device__ __forceinline__ void stage_weight(float* dst, const float* __restrict__ src, int n) {
+  for (int i = threadIdx.x; i < n * (kH / 4); i += kThreads) {
+    const int r = i / (kH / 4), c = i - r * (kH / 4);
+    cp_async16(dst + r * kLdw + 4 * c, src + (int64_t)r * kH + 4 * c);
+  }
+}
+
+template <int ROWS>
+__global__ void __launch_bounds__(kThreads, 1) k_ppo_grad(const Net net, const Batch bt, const Work wk, int64_t P) {
   extern __shared__ __align__(16) float su[];
-  const Smem L = smem_layout(net.K1, net.NO, bt.S);
+  const Smem L = smem_layout(ROWS, net.K1, net.NO, bt.S);
   float *x = su + L.x, *h1 = su + L.h1, *h2 = su + L.h2, *z = su + L.z, *dz2 = su + L.dz2, *dz1 = su + L.dz1;
-  float *v = su + L.rows, *dv = v + kRows, *glp = dv + kRows, *gent = glp + kRows;
-  float *slp = su + L.slot, *sent = slp + kRows * ld_pad(bt.S), *red = su + L.red;
+  float *v = su + L.rows, *dv = v + ROWS, *glp = dv + ROWS, *gent = glp + ROWS;
+  float *slp = su + L.slot, *sent = slp + ROWS * ld_pad(bt.S), *red = su + L.red;
+  float *swa2 = su + L.wa2, *swc2 = su + L.wc2, *swh = su + L.wh;
   const int t = threadIdx.x;
-  const int64_t r0 = (int64_t)blockIdx.x * kRows;
-  const int R = (int)((bt.M - r0) < kRows ? (bt.M - r0) : kRows);
+  const int64_t r0 = (int64_t)blockIdx.x * ROWS;
+  const int R = (int)((bt.M - r0) < ROWS ? (bt.M - r0) : ROWS);
   const int S = bt.S, A = bt.A, SA = S * A, K1 = net.K1, NO = net.NO;
+
+  // the second layers and the head into shared memory, in flight during the
+  // advantage statistics, the row gather and the first layer
+  stage_weight(swa2, net.w[2], kH);
+  stage_weight(swc2, net.w[6], kH);
+  stage_weight(swh, net.w[4], NO);
+  asm volatile("cp.async.commit_group;" ::: "memory");
 
   // advantage normalisation over the whole minibatch (torch: a.mean(), a.std() unbiased)
   float s = 0.f;
+#pragma unroll 4
   for (int64_t i = t; i < bt.M; i += kThreads) s += bt.scal[bt.idx[i]].z;
   const float amean = block_sum(s, red) / (float)bt.M;
   float q = 0.f;
+#pragma unroll 4
   for (int64_t i = t; i < bt.M; i += kThreads) {
     const float d = bt.scal[bt.idx[i]].z - amean;
     q = fmaf(d, d, q);
@@ -206,19 +296,20 @@ __global__ void __launch_bounds__(kThreads) k_ppo_grad(const Net net, const Batc
   const float astd = sqrtf(block_sum(q, red) / (float)(bt.M - 1));
 
   // this CTA's rows (zero-padded past obs_dim)
-  for (int e = t; e < R * K1; e += kThreads) {
+  for (int e = t; e < ROWS * K1; e += kThreads) {  // rows past R: zeros (finite activations, zero gradients)
     const int r = e / K1, k = e - r * K1;
-    x[r * L.ldx + k] = k < bt.obs_dim ? bt.obs[bt.idx[r0 + r] * bt.obs_ld + k] : 0.f;
+    x[r * L.ldx + k] = (r < R && k < bt.obs_dim) ? bt.obs[bt.idx[r0 + r] * bt.obs_ld + k] : 0.f;
   }
   __syncthreads();
 
   // forward: h1 = tanh(W1 x + b1) [actor | critic]; h2a, h2c; head z; value
-  dense<2, true>(net.w[0], net.w[1], 2 * kH, K1, x, L.ldx, h1, 2 * kH, R);
+  dense_gt<ROWS, 4, true>(net.wt, net.w[1], 2 * kH, K1, x, L.ldx, h1, 2 * kH, ROWS);
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
-  dense<4, true>(net.w[2], net.w[3], kH, kH, h1, 2 * kH, h2, 2 * kH, R);
-  dense<4, true>(net.w[6], net.w[7], kH, kH, h1 + kH, 2 * kH, h2 + kH, 2 * kH, R);
+  dense_s<ROWS, 8, true>(swa2, kLdw, net.w[3], kH, kH, h1, 2 * kH, h2, 2 * kH, ROWS);
+  dense_s<ROWS, 8, true>(swc2, kLdw, net.w[7], kH, kH, h1 + kH, 2 * kH, h2 + kH, 2 * kH, ROWS);
   __syncthreads();
-  dense<1, false>(net.w[4], net.w[5], NO, kH, h2, 2 * kH, z, L.ldz, R);
+  dense_s<ROWS, (ROWS >= 16 ? 2 : 1), false>(swh, kLdw, net.w[5], NO, kH, h2, 2 * kH, z, L.ldz, R);
   {  // value: one warp per row, lanes over the 64 inputs
     const int w = t >> 5, l = t & 31;
     for (int r = w; r < R; r += kThreads / 32) {
@@ -308,27 +399,29 @@ __global__ void __launch_bounds__(kThreads) k_ppo_grad(const Net net, const Batc
     const int r = e / (NO - SA);
     z[r * L.ldz + SA + (e - r * (NO - SA))] = 0.f;
   }
+  for (int e = t; e < (ROWS - R) * L.ldz; e += kThreads) z[R * L.ldz + e] = 0.f;  // rows past R: no gradient
+  if (t >= R && t < ROWS) dv[t] = 0.f;
   __syncthreads();
 
   // backward: dz2 = [d h2a-pre | d h2c-pre], dz1 = d h1-pre
-  dense_t<4>(net.w[4], NO, kH, z, L.ldz, h2, 2 * kH, dz2, 2 * kH, R);
-  for (int e = t; e < R * kH; e += kThreads) {  // critic: d h2c = dv * wv
+  dense_t<ROWS, 8>(swh, kLdw, NO, kH, z, L.ldz, h2, 2 * kH, dz2, 2 * kH);
+  for (int e = t; e < ROWS * kH; e += kThreads) {  // critic: d h2c = dv * wv
     const int r = e / kH, j = e - r * kH;
     const float hv = h2[r * 2 * kH + kH + j];
     dz2[r * 2 * kH + kH + j] = dv[r] * __ldg(net.w[8] + j) * (1.f - hv * hv);
   }
   __syncthreads();
-  dense_t<4>(net.w[2], kH, kH, dz2, 2 * kH, h1, 2 * kH, dz1, 2 * kH, R);
-  dense_t<4>(net.w[6], kH, kH, dz2 + kH, 2 * kH, h1 + kH, 2 * kH, dz1 + kH, 2 * kH, R);
+  dense_t<ROWS, 8>(swa2, kLdw, kH, kH, dz2, 2 * kH, h1, 2 * kH, dz1, 2 * kH);
+  dense_t<ROWS, 8>(swc2, kLdw, kH, kH, dz2 + kH, 2 * kH, h1 + kH, 2 * kH, dz1 + kH, 2 * kH);
   __syncthreads();
 
   // this CTA's partial gradients, the module's parameter order
   float* pd = wk.part + (int64_t)blockIdx.x * P;
-  wgrad(dz1, 2 * kH, x, L.ldx, 2 * kH, K1, R, pd + net.off[0], pd + net.off[1]);
-  wgrad(dz2, 2 * kH, h1, 2 * kH, kH, kH, R, pd + net.off[2], pd + net.off[3]);
-  wgrad(z, L.ldz, h2, 2 * kH, NO, kH, R, pd + net.off[4], pd + net.off[5]);
-  wgrad(dz2 + kH, 2 * kH, h1 + kH, 2 * kH, kH, kH, R, pd + net.off[6], pd + net.off[7]);
-  wgrad(dv, 1, h2 + kH, 2 * kH, 1, kH, R, pd + net.off[8], pd + net.off[9]);
+  wgrad<ROWS>(dz1, 2 * kH, x, L.ldx, 2 * kH, K1, pd + net.off[0], pd + net.off[1]);
+  wgrad<ROWS>(dz2, 2 * kH, h1, 2 * kH, kH, kH, pd + net.off[2], pd + net.off[3]);
+  wgrad<ROWS>(z, L.ldz, h2, 2 * kH, NO, kH, pd + net.off[4], pd + net.off[5]);
+  wgrad<ROWS>(dz2 + kH, 2 * kH, h1 + kH, 2 * kH, kH, kH, pd + net.off[6], pd + net.off[7]);
+  wgrad<ROWS>(dv, 1, h2 + kH, 2 * kH, 1, kH, pd + net.off[8], pd + net.off[9]);
   // loss sums of this CTA (threads 0..R-1 hold one row each)
   const float a0 = block_sum(l_loss, red), a1 = block_sum(l_pg, red), a2 = block_sum(l_vf, red),
               a3 = block_sum(l_ent, red);
@@ -341,15 +434,29 @@ __global__ void __launch_bounds__(kThreads) k_ppo_grad(const Net net, const Batc
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_ppo_gsum(const Work wk, int64_t P, int nparts, int64_t M) {
+constexpr int kSumThreads = 256;
+constexpr int kSplit = 4;  // threads per parameter in k_ppo_gsum
+
+// four consecutive threads per parameter sum contiguous quarters of the CTA
+// partials; the quarter sums are added in quarter order (deterministic)
+__global__ void __launch_bounds__(kSumThreads) k_ppo_gsum(const Work wk, int64_t P, int nparts, int64_t M) {
   __shared__ float red[40];
-  const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const int64_t p = ((int64_t)blockIdx.x * kSumThreads + threadIdx.x) / kSplit;
+  const int qtr = threadIdx.x % kSplit;
+  const int per = (nparts + kSplit - 1) / kSplit, c0 = qtr * per, c1 = min(nparts, c0 + per);
   float g = 0.f;
   if (p < P)
 #pragma unroll 8
-    for (int c = 0; c < nparts; ++c) g += wk.part[(int64_t)c * P + p];
-  if (p < P) wk.grad[p] = g;
-  const float s = block_sum(g * g, red);
+    for (int c = c0; c < c1; ++c) g += wk.part[(int64_t)c * P + p];
+  // in-order combine of the four quarter sums (lanes 4i .. 4i+3 of one warp)
+  const unsigned FULL = 0xffffffffu;
+  const int base = (threadIdx.x & 31) & ~(kSplit - 1);
+  const float q0 = __shfl_sync(FULL, g, base), q1 = __shfl_sync(FULL, g, base + 1);
+  const float q2 = __shfl_sync(FULL, g, base + 2), q3 = __shfl_sync(FULL, g, base + 3);
+  g = ((q0 + q1) + q2) + q3;
+  const bool lead = qtr == 0 && p < P;
+  if (lead) wk.grad[p] = g;
+  const float s = block_sum(lead ? g * g : 0.f, red);
   if (threadIdx.x == 0) wk.sq[blockIdx.x] = s;
   if (blockIdx.x == 0 && threadIdx.x < 4) {
     float a = 0.f;
@@ -361,6 +468,8 @@ __global__ void __launch_bounds__(kThreads) k_ppo_gsum(const Work wk, int64_t P,
 
 struct AdamArgs {
   float* p[kNP];
+  float* w1t;  // W1 transposed, kept in step with W1
+  int K1;
   int64_t off[kNP + 1];
   float* m;  // exp_avg [P]
   float* v;  // exp_avg_sq [P]
@@ -368,13 +477,13 @@ struct AdamArgs {
   float beta1, beta2, eps, max_norm;
 };
 
-__global__ void __launch_bounds__(kThreads) k_ppo_adam(const Work wk, const AdamArgs ad, int64_t P, int nsq) {
+__global__ void __launch_bounds__(kSumThreads) k_ppo_adam(const Work wk, const AdamArgs ad, int64_t P, int nsq) {
   __shared__ float red[40];
   float s = 0.f;
-  for (int i = threadIdx.x; i < nsq; i += kThreads) s += wk.sq[i];
+  for (int i = threadIdx.x; i < nsq; i += kSumThreads) s += wk.sq[i];
   const float norm = sqrtf(block_sum(s, red));
   const float coef = fminf(ad.max_norm / (norm + 1e-6f), 1.f);  // torch clip_grad_norm_ (clamped to 1)
-  const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const int64_t p = (int64_t)blockIdx.x * kSumThreads + threadIdx.x;
   if (p >= P) return;
   int q = 0;
   while (p >= ad.off[q + 1]) ++q;
@@ -387,79 +496,104 @@ __global__ void __launch_bounds__(kThreads) k_ppo_adam(const Work wk, const Adam
   ad.v[p] = v;
   const float bc1 = 1.f - powf(ad.beta1, stp), bc2 = 1.f - powf(ad.beta2, stp);
   const float denom = sqrtf(v) / sqrtf(bc2) + ad.eps;
-  *prm -= (*ad.lr / bc1) * m / denom;
+  const float np = *prm - (*ad.lr / bc1) * m / denom;
+  *prm = np;
+  if (q == 0) {  // W1 element (row, col) of [2H][K1] -> [col][row] of the copy
+    const int64_t row = p / ad.K1, col = p - row * ad.K1;
+    ad.w1t[col * (2 * kH) + row] = np;
+  }
 }
 
 }  // namespace vyu
 
+namespace {
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      n = 148;
+  }
+  return n;
+}
+struct Geo {
+  int K1, NO, rows;
+  int64_t P, grid, nsq, sizes[vyu::kNP];
+};
+int geo(int32_t obs_dim, int32_t S, int32_t A, int32_t hidden, int64_t M, Geo& g) {
+  if (hidden != vyu::kH || obs_dim < 1 || S < 1 || A < 2 || M < 2) return VY_ERR_UNSUPPORTED;
+  const int H = vyu::kH;
+  g.K1 = (obs_dim + 7) / 8 * 8;
+  g.NO = (S * A + 7) / 8 * 8;
+  const int64_t sizes[vyu::kNP] = {2 * H * g.K1, 2 * H, H * H, H, (int64_t)g.NO * H, g.NO, H * H, H, H, 1};
+  g.P = 0;
+  for (int i = 0; i < vyu::kNP; ++i) g.sizes[i] = sizes[i], g.P += sizes[i];
+  g.rows = vyu::rows_per_cta(M, num_sms());
+  g.grid = (M + g.rows - 1) / g.rows;
+  g.nsq = (g.P * vyu::kSplit + vyu::kSumThreads - 1) / vyu::kSumThreads;  // k_ppo_gsum blocks
+  return vyu::smem_layout(g.rows, g.K1, g.NO, S).bytes > 227 * 1024 ? VY_ERR_UNSUPPORTED : VY_OK;
+}
+}  // namespace
+
 extern "C" {
 
 int vy_ppo_update_workspace(int32_t obs_dim, int32_t S, int32_t A, int32_t hidden, int64_t M, int64_t out[4]) {
-  if (hidden != vyu::kH || obs_dim < 1 || S < 1 || A < 2 || M < 2) return VY_ERR_UNSUPPORTED;
-  const int K1 = (obs_dim + 7) / 8 * 8, NO = (S * A + 7) / 8 * 8;
-  const int64_t P = (int64_t)2 * vyu::kH * K1 + 2 * vyu::kH + vyu::kH * vyu::kH + vyu::kH + (int64_t)NO * vyu::kH + NO +
-                    vyu::kH * vyu::kH + vyu::kH + vyu::kH + 1;
-  const int64_t grid = (M + vyu::kRows - 1) / vyu::kRows;
-  const int64_t nsq = (P + vyu::kThreads - 1) / vyu::kThreads;
-  out[0] = P;                                // parameters
-  out[1] = grid * P + grid * 4 + nsq;       // float workspace: partials, loss partials, block squares
-  out[2] = grid;                             // k_ppo_grad CTAs
-  out[3] = vyu::smem_layout(K1, NO, S).bytes;
-  return out[3] > 227 * 1024 ? VY_ERR_UNSUPPORTED : VY_OK;
+  Geo g;
+  if (int rc = geo(obs_dim, S, A, hidden, M, g)) return rc;
+  out[0] = g.P;                                // parameters
+  out[1] = g.grid * g.P + g.grid * 4 + g.nsq;  // float workspace: partials, loss partials, block squares
+  out[2] = g.grid;                             // k_ppo_grad CTAs
+  out[3] = vyu::smem_layout(g.rows, g.K1, g.NO, S).bytes;
+  return VY_OK;
 }
 
-int vy_ppo_update_grad(const float* const* weights, int32_t obs_dim, int32_t S, int32_t A, int32_t hidden,
-                       const float* obs, int64_t obs_ld, const uint8_t* actions, const float* scal4,
+int vy_ppo_update_grad(const float* const* weights, const float* w1t, int32_t obs_dim, int32_t S, int32_t A,
+                       int32_t hidden, const float* obs, int64_t obs_ld, const uint8_t* actions, const float* scal4,
                        const int64_t* idx, int64_t M, float clip_eps, float vf_clip, float vf_coef, float ent_coef,
                        float* work, float* grad_out, float* stats, float* step, void* stream) {
-  int64_t ws[4];
-  if (int rc = vy_ppo_update_workspace(obs_dim, S, A, hidden, M, ws)) return rc;
-  if (!weights || !obs || !actions || !scal4 || !idx || !work || !grad_out || !stats || !step) return VY_ERR_ARG;
+  Geo g;
+  if (int rc = geo(obs_dim, S, A, hidden, M, g)) return rc;
+  if (!weights || !w1t || !obs || !actions || !scal4 || !idx || !work || !grad_out || !stats || !step)
+    return VY_ERR_ARG;
   if ((reinterpret_cast<uintptr_t>(scal4) & 15u) != 0) return VY_ERR_ARG;
   vyu::Net net{};
-  const int K1 = (obs_dim + 7) / 8 * 8, NO = (S * A + 7) / 8 * 8, H = vyu::kH;
-  const int64_t sizes[vyu::kNP] = {2 * H * K1, 2 * H, H * H, H, (int64_t)NO * H, NO, H * H, H, H, 1};
   net.off[0] = 0;
   for (int i = 0; i < vyu::kNP; ++i) {
     if (!weights[i] || (reinterpret_cast<uintptr_t>(weights[i]) & 15u) != 0) return VY_ERR_ARG;
     net.w[i] = weights[i];
-    net.off[i + 1] = net.off[i] + sizes[i];
+    net.off[i + 1] = net.off[i] + g.sizes[i];
   }
-  net.K1 = K1;
-  net.NO = NO;
-  const int64_t P = ws[0], grid = ws[2];
+  net.wt = w1t;
+  net.K1 = g.K1;
+  net.NO = g.NO;
+  const int64_t P = g.P, grid = g.grid;
   vyu::Batch bt{obs, obs_ld, obs_dim, actions, reinterpret_cast<const float4*>(scal4), idx, M, S, A,
                 clip_eps, vf_clip, vf_coef, ent_coef};
   vyu::Work wk{work, work + grid * P, grad_out, work + grid * P + grid * 4, stats, step};
-  const int smem = (int)ws[3];
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(vyu::k_ppo_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
-      return VY_ERR_CUDA;
-    attr = true;
-  }
+  const int smem = vyu::smem_layout(g.rows, g.K1, g.NO, S).bytes;
+  auto* kern = g.rows == 8 ? vyu::k_ppo_grad<8> : vyu::k_ppo_grad<16>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return VY_ERR_CUDA;
   cudaStream_t st = (cudaStream_t)stream;
-  vyu::k_ppo_grad<<<(unsigned)grid, vyu::kThreads, smem, st>>>(net, bt, wk, P);
-  const unsigned nsq = (unsigned)((P + vyu::kThreads - 1) / vyu::kThreads);
-  vyu::k_ppo_gsum<<<nsq, vyu::kThreads, 0, st>>>(wk, P, (int)grid, M);
+  kern<<<(unsigned)grid, vyu::kThreads, smem, st>>>(net, bt, wk, P);
+  vyu::k_ppo_gsum<<<(unsigned)g.nsq, vyu::kSumThreads, 0, st>>>(wk, P, (int)grid, M);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 
-int vy_ppo_update_adam(float* const* params, int32_t obs_dim, int32_t S, int32_t A, int32_t hidden, int64_t M,
-                       float* work, const float* grad, float* exp_avg, float* exp_avg_sq, const float* lr,
+int vy_ppo_update_adam(float* const* params, float* w1t, int32_t obs_dim, int32_t S, int32_t A, int32_t hidden,
+                       int64_t M, float* work, const float* grad, float* exp_avg, float* exp_avg_sq, const float* lr,
                        const float* step, float beta1, float beta2, float eps, float max_grad_norm, void* stream) {
-  int64_t ws[4];
-  if (int rc = vy_ppo_update_workspace(obs_dim, S, A, hidden, M, ws)) return rc;
-  if (!params || !work || !grad || !exp_avg || !exp_avg_sq || !lr || !step) return VY_ERR_ARG;
-  const int K1 = (obs_dim + 7) / 8 * 8, NO = (S * A + 7) / 8 * 8, H = vyu::kH;
-  const int64_t sizes[vyu::kNP] = {2 * H * K1, 2 * H, H * H, H, (int64_t)NO * H, NO, H * H, H, H, 1};
+  Geo g;
+  if (int rc = geo(obs_dim, S, A, hidden, M, g)) return rc;
+  if (!params || !w1t || !work || !grad || !exp_avg || !exp_avg_sq || !lr || !step) return VY_ERR_ARG;
   vyu::AdamArgs ad{};
   ad.off[0] = 0;
   for (int i = 0; i < vyu::kNP; ++i) {
     if (!params[i]) return VY_ERR_ARG;
     ad.p[i] = params[i];
-    ad.off[i + 1] = ad.off[i] + sizes[i];
+    ad.off[i + 1] = ad.off[i] + g.sizes[i];
   }
+  ad.w1t = w1t;
+  ad.K1 = g.K1;
   ad.m = exp_avg;
   ad.v = exp_avg_sq;
   ad.lr = lr;
@@ -467,11 +601,11 @@ int vy_ppo_update_adam(float* const* params, int32_t obs_dim, int32_t S, int32_t
   ad.beta2 = beta2;
   ad.eps = eps;
   ad.max_norm = max_grad_norm;
-  const int64_t P = ws[0], grid = ws[2];
+  const int64_t P = g.P, grid = g.grid;
   vyu::Work wk{work, work + grid * P, const_cast<float*>(grad), work + grid * P + grid * 4, nullptr,
                const_cast<float*>(step)};
-  const unsigned nsq = (unsigned)((P + vyu::kThreads - 1) / vyu::kThreads);
-  vyu::k_ppo_adam<<<nsq, vyu::kThreads, 0, (cudaStream_t)stream>>>(wk, ad, P, (int)nsq);
+  const unsigned nadam = (unsigned)((P + vyu::kSumThreads - 1) / vyu::kSumThreads);
+  vyu::k_ppo_adam<<<nadam, vyu::kSumThreads, 0, (cudaStream_t)stream>>>(wk, ad, P, (int)g.nsq);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 

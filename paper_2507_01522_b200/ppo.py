@@ -539,6 +539,9 @@ class PPOTrainer:
                 prm = list(self.net.parameters())
                 assert sum(p.numel() for p in prm) == P
                 self._uparams = (C.c_void_p * len(prm))(*[p.data_ptr() for p in prm])
+                # W1 transposed for the first layer's coalesced reads (refreshed at
+                # the start of every update, kept in step by the Adam kernel)
+                self._uw1t = torch.empty(self.net.inp.weight.shape[1], self.net.inp.weight.shape[0], device=dev)
         env.reset(as_numpy=False)
         self.obs[0].copy_(env.outs.obs)
 
@@ -746,11 +749,13 @@ class PPOTrainer:
         act = self.actions.reshape(n, -1)
         scal = scal.contiguous()
         S, A, H, od = self.net.n_slots, self.net.n_actions, cfg.hidden, self.net.obs_dim
+        with torch.no_grad():
+            self._uw1t.copy_(self.net.inp.weight.t())
         for _ in range(cfg.update_epochs):
             perm = torch.argsort(torch.rand(n, device=obs.device))  # a uniform permutation, capture-safe
             for k in range(cfg.n_minibatches):
                 idx = perm[k * mb:(k + 1) * mb]
-                nat.check(lib.vy_ppo_update_grad(self._uparams, od, S, A, H, obs.data_ptr(), obs.stride(0),
+                nat.check(lib.vy_ppo_update_grad(self._uparams, self._uw1t.data_ptr(), od, S, A, H, obs.data_ptr(), obs.stride(0),
                                                  act.data_ptr(), scal.data_ptr(), idx.data_ptr(), mb, cfg.clip_eps,
                                                  cfg.vf_clip, cfg.vf_coef, cfg.ent_coef, self._uwork.data_ptr(),
                                                  self._ugrad.data_ptr(), self._ustats_buf.data_ptr(),
@@ -758,7 +763,7 @@ class PPOTrainer:
                 if self._allreduce:  # the flat gradient, SUM then / world (gloo has no AVG)
                     dist.all_reduce(self._ugrad, op=dist.ReduceOp.SUM)
                     self._ugrad.div_(self.world)
-                nat.check(lib.vy_ppo_update_adam(self._uparams, od, S, A, H, mb, self._uwork.data_ptr(),
+                nat.check(lib.vy_ppo_update_adam(self._uparams, self._uw1t.data_ptr(), od, S, A, H, mb, self._uwork.data_ptr(),
                                                  self._ugrad.data_ptr(), self._adam_m.data_ptr(),
                                                  self._adam_v.data_ptr(), self._lr.data_ptr(),
                                                  self._adam_step.data_ptr(), 0.9, 0.999, 1e-5, cfg.max_grad_norm, st),
@@ -770,7 +775,7 @@ class PPOTrainer:
     def describe_update(self) -> str:
         if self._fused_update:
             return ("per minibatch: vy_ppo_update_grad (fp32 forward, clipped loss, backward, per-CTA partial "
-                    "gradients; 16 samples per CTA) + k_ppo_gsum (ordered sum, squares) + vy_ppo_update_adam "
+                    "gradients; 8 or 16 samples per CTA, second layers and head staged in shared memory) + k_ppo_gsum (ordered sum, squares) + vy_ppo_update_adam "
                     "(clip_grad_norm_ + Adam in place); epochs x minibatches in one CUDA graph")
         return ("one CUDA graph per update: vy_gae, vy_gather_rows minibatch gather, bf16 GEMMs with column-sum "
                 "bias gradients (vy_colsum), vy_ppo_loss, fused Adam")

@@ -51,12 +51,13 @@ def _fused_grad(net, obs, act, scal, idx, cfg, step):
     stats = torch.zeros(4, device="cuda")
     prm = list(net.parameters())
     ptrs = (C.c_void_p * len(prm))(*[p.data_ptr() for p in prm])
-    nat.check(nat.lib().vy_ppo_update_grad(ptrs, od, S, A, 64, obs.data_ptr(), obs.stride(0), act.data_ptr(),
+    w1t = net.inp.weight.detach().t().contiguous()
+    nat.check(nat.lib().vy_ppo_update_grad(ptrs, w1t.data_ptr(), od, S, A, 64, obs.data_ptr(), obs.stride(0), act.data_ptr(),
                                            scal.data_ptr(), idx.data_ptr(), M, cfg.clip_eps, cfg.vf_clip,
                                            cfg.vf_coef, cfg.ent_coef, work.data_ptr(), grad.data_ptr(),
                                            stats.data_ptr(), step.data_ptr(), torch.cuda.current_stream().cuda_stream),
               "vy_ppo_update_grad")
-    return grad, stats, work, ptrs
+    return grad, stats, work, w1t
 
 
 @pytest.mark.parametrize("M,scale", [(1200, 1.0), (75, 1.0), (900, 30.0), (37, 1.0)])
@@ -107,7 +108,7 @@ def test_fused_adam_matches_torch_adam():
     obs, act, scal = _data(4 * M, od, S, A, seed=11)
     for it in range(3):
         idx = torch.randperm(4 * M, device="cuda")[:M].contiguous()
-        grad, _, work, ptrs = _fused_grad(net, obs, act, scal, idx, cfg, step)
+        grad, _, work, w1t = _fused_grad(net, obs, act, scal, idx, cfg, step)
         # the reference optimiser gets exactly the fused gradient
         off = 0
         for p in ref.parameters():
@@ -117,12 +118,13 @@ def test_fused_adam_matches_torch_adam():
         opt.step()
         prm = list(net.parameters())
         pp = (C.c_void_p * len(prm))(*[p.data_ptr() for p in prm])
-        nat.check(nat.lib().vy_ppo_update_adam(pp, od, S, A, 64, M, work.data_ptr(), grad.data_ptr(), m.data_ptr(),
+        nat.check(nat.lib().vy_ppo_update_adam(pp, w1t.data_ptr(), od, S, A, 64, M, work.data_ptr(), grad.data_ptr(), m.data_ptr(),
                                                v.data_ptr(), lr.data_ptr(), step.data_ptr(), 0.9, 0.999, 1e-5,
                                                cfg.max_grad_norm, torch.cuda.current_stream().cuda_stream),
                   "vy_ppo_update_adam")
         for (name, a), b in zip(net.named_parameters(), ref.parameters()):
             torch.testing.assert_close(a, b, rtol=1e-5, atol=2e-7, msg=f"{name} after step {it + 1}")
+        assert torch.equal(w1t, net.inp.weight.detach().t())  # the transposed copy follows the update exactly
     assert step.item() == 3.0
 
 
