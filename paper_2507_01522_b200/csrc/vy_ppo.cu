@@ -34,6 +34,9 @@ __global__ void k_gae(const float* __restrict__ values, const float* __restrict_
   if (b >= B) return;
   float next_v = last_value[b];
   float gae = 0.f;
+  // unrolled so each batch of steps' loads is in flight before the
+  // recurrence reaches it (at 16 envs the scan is one dependent chain per env)
+#pragma unroll 8
   for (int t = T - 1; t >= 0; --t) {
     const int64_t i = (int64_t)t * B + b;
     const float v = values[i];
@@ -799,5 +802,64 @@ extern "C" int vy_scale_bf16(void* x, int64_t n, const float* g, void* stream) {
   if (n == 0) return VY_OK;
   const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
   k_scale_bf16_unless_one<<<grid, 256, 0, (cudaStream_t)stream>>>(static_cast<__nv_bfloat16*>(x), n, g);
+  return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
+}
+
+namespace {
+__device__ __forceinline__ uint64_t perm_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+// count uniform random permutations of 0..n-1, one CTA each: element i gets
+// the key (hash(seed, call, c, i) >> 32) << 32 | i (ties broken by index),
+// and a bitonic sort of the n keys (padded to a power of two) in shared
+// memory orders them; the last CTA out advances the call counter
+__global__ void __launch_bounds__(1024) k_random_perms(int64_t n, int p2, uint64_t seed,
+                                                        unsigned long long* counter, int64_t* __restrict__ out) {
+  extern __shared__ unsigned long long pk[];
+  const int c = blockIdx.x;
+  const uint64_t key = perm_mix(seed ^ perm_mix(counter[0] * 0x9E3779B97F4A7C15ULL + (uint64_t)c + 1));
+  for (int i = threadIdx.x; i < p2; i += blockDim.x)
+    pk[i] = i < n ? ((perm_mix(key + (uint64_t)i * 0x9E3779B97F4A7C15ULL) >> 32) << 32) | (uint64_t)i : ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= p2; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long a = pk[i], b = pk[ixj];
+          if ((a > b) == ((i & k) == 0)) {
+            pk[i] = b;
+            pk[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) out[(int64_t)c * n + i] = (int64_t)(pk[i] & 0xffffffffull);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(counter + 1, 1ull) == gridDim.x - 1) {
+      counter[1] = 0;
+      counter[0] += 1;
+      __threadfence();
+    }
+  }
+}
+}  // namespace
+
+extern "C" int vy_random_perms(int64_t n, int32_t count, uint64_t seed, int64_t* counter, int64_t* out,
+                               void* stream) {
+  if (!counter || !out || n < 1 || count < 1) return VY_ERR_ARG;
+  int p2 = 1;
+  while (p2 < n) p2 <<= 1;
+  if (p2 > 16384) return VY_ERR_UNSUPPORTED;
+  const int smem = p2 * 8;
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(k_random_perms, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return VY_ERR_CUDA;
+  k_random_perms<<<count, 1024, smem, (cudaStream_t)stream>>>(n, p2, seed,
+                                                               reinterpret_cast<unsigned long long*>(counter), out);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }

@@ -542,6 +542,11 @@ class PPOTrainer:
                 # W1 transposed for the first layer's coalesced reads (refreshed at
                 # the start of every update, kept in step by the Adam kernel)
                 self._uw1t = torch.empty(self.net.inp.weight.shape[1], self.net.inp.weight.shape[0], device=dev)
+                # the epochs' minibatch shuffles in one launch (vy_random_perms, n <= 16384)
+                self._perms = torch.empty(cfg.update_epochs, T * B, dtype=torch.int64, device=dev) \
+                    if T * B <= 16384 else None
+                self._perm_ctr = torch.zeros(2, dtype=torch.int64, device=dev)
+                self._perm_seed = (cfg.seed * 0x2545F4914F6CDD1D + env.global_offset + 7) & ((1 << 64) - 1)
         env.reset(as_numpy=False)
         self.obs[0].copy_(env.outs.obs)
 
@@ -751,8 +756,14 @@ class PPOTrainer:
         S, A, H, od = self.net.n_slots, self.net.n_actions, cfg.hidden, self.net.obs_dim
         with torch.no_grad():
             self._uw1t.copy_(self.net.inp.weight.t())
-        for _ in range(cfg.update_epochs):
-            perm = torch.argsort(torch.rand(n, device=obs.device))  # a uniform permutation, capture-safe
+        if self._perms is not None:
+            nat.check(lib.vy_random_perms(n, cfg.update_epochs, self._perm_seed, self._perm_ctr.data_ptr(),
+                                          self._perms.data_ptr(), st), "vy_random_perms")
+        for ep in range(cfg.update_epochs):
+            if self._perms is not None:
+                perm = self._perms[ep]
+            else:
+                perm = torch.argsort(torch.rand(n, device=obs.device))  # a uniform permutation, capture-safe
             for k in range(cfg.n_minibatches):
                 idx = perm[k * mb:(k + 1) * mb]
                 nat.check(lib.vy_ppo_update_grad(self._uparams, self._uw1t.data_ptr(), od, S, A, H, obs.data_ptr(), obs.stride(0),
@@ -776,7 +787,8 @@ class PPOTrainer:
         if self._fused_update:
             return ("per minibatch: vy_ppo_update_grad (fp32 forward, clipped loss, backward, per-CTA partial "
                     "gradients; 8 or 16 samples per CTA, second layers and head staged in shared memory) + k_ppo_gsum (ordered sum, squares) + vy_ppo_update_adam "
-                    "(clip_grad_norm_ + Adam in place); epochs x minibatches in one CUDA graph")
+                    "(clip_grad_norm_ + Adam in place); the epochs' shuffles in one vy_random_perms launch; epochs x "
+                    "minibatches in one CUDA graph")
         return ("one CUDA graph per update: vy_gae, vy_gather_rows minibatch gather, bf16 GEMMs with column-sum "
                 "bias gradients (vy_colsum), vy_ppo_loss, fused Adam")
 

@@ -173,3 +173,27 @@ def test_trainer_fused_update_equals_eager_replay():
         assert torch.equal(a, b)
     for tr in trs:
         tr.env.close()
+
+
+@pytest.mark.parametrize("n", [1, 300, 4800, 16384])
+def test_random_perms_are_permutations(n):
+    from paper_2507_01522_b200 import _native as nat
+
+    ctr = torch.zeros(2, dtype=torch.int64, device="cuda")
+    out = torch.empty(4, n, dtype=torch.int64, device="cuda")
+    seen = []
+    for _ in range(2):
+        nat.check(nat.lib().vy_random_perms(n, 4, 123, ctr.data_ptr(), out.data_ptr(),
+                                            torch.cuda.current_stream().cuda_stream), "vy_random_perms")
+        for row in out:
+            assert torch.equal(torch.sort(row).values, torch.arange(n, device="cuda"))
+        seen.append(out.clone())
+    assert ctr.tolist() == [2, 0]
+    if n >= 300:
+        rows = torch.cat(seen)
+        assert len({tuple(r[:16].tolist()) for r in rows}) == 8  # every draw differs
+        # roughly uniform: the mean position of each element over the draws is near (n - 1) / 2
+        pos = torch.argsort(rows, dim=1).float().mean(0)
+        assert abs(pos.mean().item() - (n - 1) / 2) < 0.02 * n
+    big = torch.empty(1, 16385, dtype=torch.int64, device="cuda")
+    assert nat.lib().vy_random_perms(16385, 1, 1, ctr.data_ptr(), big.data_ptr(), None) == nat.VY_ERR_UNSUPPORTED
