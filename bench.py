@@ -549,20 +549,23 @@ def main() -> None:
         penv.close()
         if world == 1:
             # the paper's own PPO workload: Table 4 -- 12 vectorised envs, rollout 300
-            # (batch 3600), 4 minibatches of 900, 4 epochs -- and the PPO(16) row's 16 envs
+            # (batch 3600), 4 minibatches of 900, 4 epochs -- and the PPO(16) / PPO(1) rows' 16 and 1 envs
+            #
             legs = {}
-            for n_envs in (12, 16):
+            for n_envs in (1, 12, 16):
                 qenv = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=n_envs, master_seed=1)
                 qtr = PPOTrainer(qenv, PPOConfig(rollout_steps=300))
                 qres = seconds_per_100k(qtr, 6, warmup=1)
                 legs[f"envs_{n_envs}"] = {"value": qres["s_per_100k_steps"], "env_steps_per_s": qres["env_steps_per_s"],
-                                          "minibatch": n_envs * 300 // 4, "timed_iterations": 6}
+                                          "minibatch": n_envs * 300 // 4, "timed_iterations": 6,
+                                          "rollout": qtr.describe_rollout(), "update": qtr.describe_update()}
                 qenv.close()
             result["ppo_paper"] = {"metric": "s per 100k PPO steps", "unit": "s", "higher_is_better": False,
                                    "legs": legs, "paper": {"PPO(16)": 0.65, "PPO(1)": 9.79, "hardware":
                                                            "RTX 4000 Ada (PAPER.md:239)"},
-                                   "note": "same trainer and kernels as the ppo leg; at 12-16 envs a step is "
-                                           "launch/latency bound (CUDA graphs: one replay per rollout, one per update)"}
+                                   "note": "same trainer as the ppo leg; at 1-16 envs the rollout is one vy_ppo_rollout "
+                                           "launch and each minibatch three fused update kernels (CUDA graphs: one "
+                                           "replay per rollout, one per update)"}
 
     if not args.no_extras:
         # config C5: 36 heterogeneous (region, scenario, traffic, station layout) groups sharing the GPU,

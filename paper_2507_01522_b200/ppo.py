@@ -10,7 +10,7 @@ loop B200-first:
   bias epilogues and the categorical sampling of the 17 x 21 multi-discrete
   head fused) and the fused env step kernel, for T steps, captured once as a
   CUDA graph and replayed every iteration (fused_policy=False keeps the
-  earlier cuBLAS + sampler-kernel path for comparison); at up to 2368 envs
+  earlier cuBLAS + sampler-kernel path for comparison); at up to 4736 envs
   on lean stations the whole rollout is ONE kernel instead
   (csrc/vy_ppo_rollout.cuh: 16 envs per CTA, the same policy arithmetic and
   env step, weights and TMEM set up once for all T steps);
@@ -64,9 +64,10 @@ class PPOConfig:
     fused_head: bool = True  # vy_ppo_sample / vy_ppo_head_* kernels instead of the torch op chain
     graph_update: bool = True  # the whole update (GAE + epochs x minibatches + Adam) as one CUDA graph (1 GPU)
     fused_policy: bool = True  # rollout forward + sampling in the tcgen05 kernel (vy_policy_step)
-    # the whole rollout (policy passes + env steps) as one kernel at <= 2368 envs
-    # (vy_ppo_rollout: 16 envs per CTA, one wave on 148 SMs); lean stations
-    # without a battery, else the per-step pair
+    # the whole rollout (policy passes + env steps) as one kernel at <= 4736 envs
+    # (vy_ppo_rollout: up to 16 envs per CTA, at most two waves on 148 SMs:
+    # 4096 envs 17.0 vs 25.0 us per step); lean stations without a battery,
+    # else the per-step pair
     fused_rollout: bool = True
     # minibatches of <= 8192 samples: forward + loss + backward + clip + Adam as
     # three kernels per minibatch, fp32 (vy_ppo_update_*), instead of autograd
@@ -515,7 +516,7 @@ class PPOTrainer:
         self.n_iters = max(1, cfg.total_timesteps // (T * B * self.world))
         self._graph = None
         self._fused_policy = cfg.fused_policy
-        self._fused_rollout = cfg.fused_rollout and self._fused_policy and B <= 148 * 16
+        self._fused_rollout = cfg.fused_rollout and self._fused_policy and B <= 2 * 148 * 16
         if self._fused_policy:
             self._geo = policy_geometry(self.net)
             self._scratch_a = torch.zeros(B, A, dtype=torch.uint8, device=dev)
