@@ -18,7 +18,12 @@ loop B200-first:
 * update: clipped PPO objective with value clipping, entropy bonus, Adam,
   global-norm gradient clipping; under torch.distributed the flattened
   gradient is all-reduced (NCCL over NVLink) once per minibatch — the only
-  data-path collective of the whole system.
+  data-path collective of the whole system.  Minibatches of <= 8192 samples
+  (the paper's 1-16 env workloads) run as three kernels each
+  (csrc/vy_ppo_update.cu: fp32 forward + loss + backward with per-CTA
+  partial gradients, their ordered sum, clip + Adam in place) with the
+  epochs' shuffles from one vy_random_perms launch; larger ones through
+  autograd (bf16 GEMMs, the fused loss head, fused Adam).
 
 Network: PureJaxRL's default actor-critic (two 64-unit tanh layers each for
 actor and critic, orthogonal init); the paper does not pin the width, so it
