@@ -76,4 +76,14 @@ for _ in range(12):
 torch.cuda.synchronize()
 print("multi", hb.multi_info())
 hb.close()
+# PPO at small batches: the one-kernel rollout (ragged CTAs) and the fused update
+from paper_2507_01522_b200.ppo import PPOConfig, PPOTrainer  # noqa: E402
+
+for B in (16, 37):
+    env = BatchEnv(rc.env, rc.station, rc.dataset, batch_size=B, master_seed=7)
+    tr = PPOTrainer(env, PPOConfig(rollout_steps=6, use_graph=False, n_minibatches=2, update_epochs=1))
+    tr.iterate()
+    torch.cuda.synchronize()
+    print("ppo", B, tr._fused_rollout, tr._fused_update, env.last_step_mode())
+    env.close()
 print("ok")
