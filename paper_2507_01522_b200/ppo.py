@@ -800,7 +800,7 @@ class PPOTrainer:
 
     def describe_rollout(self) -> str:
         if self._fused_rollout:
-            return ("one kernel per rollout: vy_ppo_rollout (per CTA 16 envs x T steps: tcgen05 3-layer MLP, TMEM "
+            return ("one kernel per rollout: vy_ppo_rollout (per CTA 2-16 envs x T steps: tcgen05 3-layer MLP, TMEM "
                     "accumulators, fused epilogues + inverse-CDF sampling, then the one-warp-per-env step; weights, "
                     "TMEM and station tables set up once) + pack_policy")
         if self._fused_policy:
