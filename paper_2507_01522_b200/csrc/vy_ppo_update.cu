@@ -60,7 +60,8 @@ struct Batch {
 };
 
 struct Work {
-  float* part;   // [grid][P] per-CTA gradient partials
+  int64_t pld;   // row stride of the partials (P rounded up to 4: 16-byte aligned rows)
+  float* part;   // [grid][pld] per-CTA gradient partials
   float* lstat;  // [grid][4] per-CTA loss sums {loss, pg, vf, ent}
   float* grad;   // [P] flat gradient
   float* sq;     // [gsum blocks] sums of squares
@@ -187,12 +188,55 @@ __device__ __forceinline__ void dense_t(const float* W, int ldw, int N, int J, c
   }
 }
 
-// partial gradients of y = W x + b over this CTA's rows: gW[n][k] = sum_r
+// partial gradients of y = W x + b over this CTA's rows, register-tiled:
+// gW[n][k] = sum_r d[r][n] in[r][k] -> dst[n*K + k], gb[n] = sum_r d[r][n].
+// A warp owns a 32 (n) x 16 (k) block, a lane a 4 x 4 tile (lanes 4i..4i+3:
+// n-quad i, k-quads 0..3), so per row a warp reads 8 d-quads and 4 in-quads
+// (one wavefront each) for 16 FMAs per lane.  N, K, ldd, ldi multiples of 4,
+// dst rows 16-byte aligned; d is zero past the CTA's rows.
+template <int ROWS>
+__device__ __forceinline__ void wgrad(const float* d, int ldd, const float* in, int ldi, int N, int K,
+                                      float* __restrict__ dst, float* __restrict__ dstb) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NB = (N + 31) / 32, KB = (K + 15) / 16;
+  for (int wb = warp; wb < NB * KB; wb += kThreads / 32) {
+    const int bn = wb / KB, bk = wb - bn * KB;
+    const int n = bn * 32 + (lane >> 2) * 4, k = bk * 16 + (lane & 3) * 4;
+    if (n < N && k < K) {
+      float4 acc[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) {
+        const float4 dq = *reinterpret_cast<const float4*>(d + r * ldd + n);
+        const float4 xq = *reinterpret_cast<const float4*>(in + r * ldi + k);
+        const float dd[4] = {dq.x, dq.y, dq.z, dq.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[i].x = fmaf(dd[i], xq.x, acc[i].x);
+          acc[i].y = fmaf(dd[i], xq.y, acc[i].y);
+          acc[i].z = fmaf(dd[i], xq.z, acc[i].z);
+          acc[i].w = fmaf(dd[i], xq.w, acc[i].w);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) *reinterpret_cast<float4*>(dst + (int64_t)(n + i) * K + k) = acc[i];
+    }
+  }
+  for (int n = threadIdx.x; n < N; n += kThreads) {
+    float acc = 0.f;
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) acc += d[r * ldd + n];
+    dstb[n] = acc;
+  }
+}
+
+// the same with one thread per 4 k (any N, ldd; the value head): gW[n][k] = sum_r
 // d[r][n] in[r][k] -> dst[n*K + k], gb[n] = sum_r d[r][n] -> dstb[n].  All
 // ROWS rows (d is zero past the CTA's rows), four k per thread: 16-byte
 // loads, the whole row loop unrolled so its loads are in flight together.
 template <int ROWS>
-__device__ __forceinline__ void wgrad(const float* d, int ldd, const float* in, int ldi, int N, int K,
+__device__ __forceinline__ void wgrad_rows(const float* d, int ldd, const float* in, int ldi, int N, int K,
                                       float* __restrict__ dst, float* __restrict__ dstb) {
   const int K4 = K / 4;
   for (int e = threadIdx.x; e < N * K4; e += kThreads) {
@@ -416,12 +460,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_ppo_grad(const Net net, const B
   __syncthreads();
 
   // this CTA's partial gradients, the module's parameter order
-  float* pd = wk.part + (int64_t)blockIdx.x * P;
+  float* pd = wk.part + (int64_t)blockIdx.x * wk.pld;
   wgrad<ROWS>(dz1, 2 * kH, x, L.ldx, 2 * kH, K1, pd + net.off[0], pd + net.off[1]);
   wgrad<ROWS>(dz2, 2 * kH, h1, 2 * kH, kH, kH, pd + net.off[2], pd + net.off[3]);
   wgrad<ROWS>(z, L.ldz, h2, 2 * kH, NO, kH, pd + net.off[4], pd + net.off[5]);
   wgrad<ROWS>(dz2 + kH, 2 * kH, h1 + kH, 2 * kH, kH, kH, pd + net.off[6], pd + net.off[7]);
-  wgrad<ROWS>(dv, 1, h2 + kH, 2 * kH, 1, kH, pd + net.off[8], pd + net.off[9]);
+  wgrad_rows<ROWS>(dv, 1, h2 + kH, 2 * kH, 1, kH, pd + net.off[8], pd + net.off[9]);
   // loss sums of this CTA (threads 0..R-1 hold one row each)
   const float a0 = block_sum(l_loss, red), a1 = block_sum(l_pg, red), a2 = block_sum(l_vf, red),
               a3 = block_sum(l_ent, red);
@@ -447,7 +491,7 @@ __global__ void __launch_bounds__(kSumThreads) k_ppo_gsum(const Work wk, int64_t
   float g = 0.f;
   if (p < P)
 #pragma unroll 8
-    for (int c = c0; c < c1; ++c) g += wk.part[(int64_t)c * P + p];
+    for (int c = c0; c < c1; ++c) g += wk.part[(int64_t)c * wk.pld + p];
   // in-order combine of the four quarter sums (lanes 4i .. 4i+3 of one warp)
   const unsigned FULL = 0xffffffffu;
   const int base = (threadIdx.x & 31) & ~(kSplit - 1);
@@ -518,7 +562,7 @@ int num_sms() {
 }
 struct Geo {
   int K1, NO, rows;
-  int64_t P, grid, nsq, sizes[vyu::kNP];
+  int64_t P, pld, grid, nsq, sizes[vyu::kNP];
 };
 int geo(int32_t obs_dim, int32_t S, int32_t A, int32_t hidden, int64_t M, Geo& g) {
   if (hidden != vyu::kH || obs_dim < 1 || S < 1 || A < 2 || M < 2) return VY_ERR_UNSUPPORTED;
@@ -528,6 +572,7 @@ int geo(int32_t obs_dim, int32_t S, int32_t A, int32_t hidden, int64_t M, Geo& g
   const int64_t sizes[vyu::kNP] = {2 * H * g.K1, 2 * H, H * H, H, (int64_t)g.NO * H, g.NO, H * H, H, H, 1};
   g.P = 0;
   for (int i = 0; i < vyu::kNP; ++i) g.sizes[i] = sizes[i], g.P += sizes[i];
+  g.pld = (g.P + 3) / 4 * 4;
   g.rows = vyu::rows_per_cta(M, num_sms());
   g.grid = (M + g.rows - 1) / g.rows;
   g.nsq = (g.P * vyu::kSplit + vyu::kSumThreads - 1) / vyu::kSumThreads;  // k_ppo_gsum blocks
@@ -541,7 +586,7 @@ int vy_ppo_update_workspace(int32_t obs_dim, int32_t S, int32_t A, int32_t hidde
   Geo g;
   if (int rc = geo(obs_dim, S, A, hidden, M, g)) return rc;
   out[0] = g.P;                                // parameters
-  out[1] = g.grid * g.P + g.grid * 4 + g.nsq;  // float workspace: partials, loss partials, block squares
+  out[1] = g.grid * g.pld + g.grid * 4 + g.nsq;  // float workspace: partials, loss partials, block squares
   out[2] = g.grid;                             // k_ppo_grad CTAs
   out[3] = vyu::smem_layout(g.rows, g.K1, g.NO, S).bytes;
   return VY_OK;
@@ -569,7 +614,9 @@ int vy_ppo_update_grad(const float* const* weights, const float* w1t, int32_t ob
   const int64_t P = g.P, grid = g.grid;
   vyu::Batch bt{obs, obs_ld, obs_dim, actions, reinterpret_cast<const float4*>(scal4), idx, M, S, A,
                 clip_eps, vf_clip, vf_coef, ent_coef};
-  vyu::Work wk{work, work + grid * P, grad_out, work + grid * P + grid * 4, stats, step};
+  const int64_t pld = g.pld;
+  if ((reinterpret_cast<uintptr_t>(work) & 15u) != 0) return VY_ERR_ARG;
+  vyu::Work wk{pld, work, work + grid * pld, grad_out, work + grid * pld + grid * 4, stats, step};
   const int smem = vyu::smem_layout(g.rows, g.K1, g.NO, S).bytes;
   auto* kern = g.rows == 8 ? vyu::k_ppo_grad<8> : vyu::k_ppo_grad<16>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return VY_ERR_CUDA;
@@ -602,7 +649,7 @@ int vy_ppo_update_adam(float* const* params, float* w1t, int32_t obs_dim, int32_
   ad.eps = eps;
   ad.max_norm = max_grad_norm;
   const int64_t P = g.P, grid = g.grid;
-  vyu::Work wk{work, work + grid * P, const_cast<float*>(grad), work + grid * P + grid * 4, nullptr,
+  vyu::Work wk{g.pld, work, work + grid * g.pld, const_cast<float*>(grad), work + grid * g.pld + grid * 4, nullptr,
                const_cast<float*>(step)};
   const unsigned nadam = (unsigned)((P + vyu::kSumThreads - 1) / vyu::kSumThreads);
   vyu::k_ppo_adam<<<nadam, vyu::kSumThreads, 0, (cudaStream_t)stream>>>(wk, ad, P, (int)g.nsq);
