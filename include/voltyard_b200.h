@@ -377,12 +377,17 @@ int vy_ppo_rollout(vy_handle *h, int32_t T, const void *wpack, const float *fpac
  * caller.  A multi-GPU caller all-reduces grad_out between the two.
  * w1t: W1 transposed [K1][2H], which the first layer reads (coalesced); the
  * caller fills it from W1 and vy_ppo_update_adam keeps it in step.
+ * adv_stats: {mean, std} of the minibatch's advantages, or NULL (computed by
+ * every CTA); vy_ppo_adv_stats computes them for all minibatches of an
+ * update at once (block e*nmb + k: rows perms[e][k*mb .. (k+1)*mb)).
  * vy_ppo_update_workspace: out = {P, work floats, grad CTAs, shared bytes}.
  * Not part of the reference (trainer-free). */
+int vy_ppo_adv_stats(const float *scal4, const int64_t *perms, int64_t n, int32_t count, int32_t nmb, int64_t mb,
+                     float *out, void *stream);
 int vy_ppo_update_workspace(int32_t obs_dim, int32_t S, int32_t A, int32_t hidden, int64_t M, int64_t out[4]);
 int vy_ppo_update_grad(const float *const *weights, const float *w1t, int32_t obs_dim, int32_t S, int32_t A, int32_t hidden,
                        const float *obs, int64_t obs_ld, const uint8_t *actions, const float *scal4,
-                       const int64_t *idx, int64_t M, float clip_eps, float vf_clip, float vf_coef, float ent_coef,
+                       const int64_t *idx, const float *adv_stats, int64_t M, float clip_eps, float vf_clip, float vf_coef, float ent_coef,
                        float *work, float *grad_out, float *stats, float *step, void *stream);
 int vy_ppo_update_adam(float *const *params, float *w1t, int32_t obs_dim, int32_t S, int32_t A, int32_t hidden, int64_t M,
                        float *work, const float *grad, float *exp_avg, float *exp_avg_sq, const float *lr,

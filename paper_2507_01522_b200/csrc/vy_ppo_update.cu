@@ -54,6 +54,7 @@ struct Batch {
   const uint8_t* actions;  // [*][S]
   const float4* scal;      // [*] {old_lp, old_v, adv, ret}
   const int64_t* idx;      // [M] rows of this minibatch
+  const float* adv_stats;  // {mean, std} of the minibatch's advantages, or null (computed here)
   int64_t M;
   int S, A;
   float clip_eps, vf_clip, vf_coef, ent_coef;
@@ -265,6 +266,37 @@ __device__ __forceinline__ void wgrad_rows(const float* d, int ldd, const float*
   }
 }
 
+// mean and unbiased standard deviation of scal[idx[i]].z, i < M (fixed-order block reductions)
+__device__ __forceinline__ void adv_mean_std(const float4* __restrict__ scal, const int64_t* __restrict__ idx,
+                                             int64_t M, float* red, float& mean, float& std) {
+  float s = 0.f;
+#pragma unroll 4
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) s += scal[idx[i]].z;
+  mean = block_sum(s, red) / (float)M;
+  float q = 0.f;
+#pragma unroll 4
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+    const float d = scal[idx[i]].z - mean;
+    q = fmaf(d, d, q);
+  }
+  std = sqrtf(block_sum(q, red) / (float)(M - 1));
+}
+
+// the advantage statistics of every minibatch of an update: block b = epoch
+// b / nmb, minibatch b % nmb (rows perms[epoch][k*mb .. (k+1)*mb))
+__global__ void __launch_bounds__(kThreads) k_adv_stats(const float4* __restrict__ scal,
+                                                         const int64_t* __restrict__ perms, int64_t n, int nmb,
+                                                         int64_t mb, float* __restrict__ out) {
+  __shared__ float red[40];
+  const int e = blockIdx.x / nmb, k = blockIdx.x - e * nmb;
+  float mean, std;
+  adv_mean_std(scal, perms + (int64_t)e * n + (int64_t)k * mb, mb, red, mean, std);
+  if (threadIdx.x == 0) {
+    out[2 * blockIdx.x] = mean;
+    out[2 * blockIdx.x + 1] = std;
+  }
+}
+
 __host__ __device__ inline int ld_pad(int x) { return (x + 3) / 4 * 4; }
 constexpr int kLdw = kH + 4;  // row stride of the staged [*][kH] weights
 
@@ -326,18 +358,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_ppo_grad(const Net net, const B
   stage_weight(swh, net.w[4], NO);
   asm volatile("cp.async.commit_group;" ::: "memory");
 
-  // advantage normalisation over the whole minibatch (torch: a.mean(), a.std() unbiased)
-  float s = 0.f;
-#pragma unroll 4
-  for (int64_t i = t; i < bt.M; i += kThreads) s += bt.scal[bt.idx[i]].z;
-  const float amean = block_sum(s, red) / (float)bt.M;
-  float q = 0.f;
-#pragma unroll 4
-  for (int64_t i = t; i < bt.M; i += kThreads) {
-    const float d = bt.scal[bt.idx[i]].z - amean;
-    q = fmaf(d, d, q);
+  // advantage normalisation over the whole minibatch (torch: a.mean(), a.std()
+  // unbiased): precomputed for the update's minibatches (vy_ppo_adv_stats), or here
+  float amean, astd;
+  if (bt.adv_stats) {
+    amean = bt.adv_stats[0];
+    astd = bt.adv_stats[1];
+  } else {
+    adv_mean_std(bt.scal, bt.idx, bt.M, red, amean, astd);
   }
-  const float astd = sqrtf(block_sum(q, red) / (float)(bt.M - 1));
 
   // this CTA's rows (zero-padded past obs_dim)
   for (int e = t; e < ROWS * K1; e += kThreads) {  // rows past R: zeros (finite activations, zero gradients)
@@ -467,14 +496,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_ppo_grad(const Net net, const B
   wgrad<ROWS>(dz2 + kH, 2 * kH, h1 + kH, 2 * kH, kH, kH, pd + net.off[6], pd + net.off[7]);
   wgrad_rows<ROWS>(dv, 1, h2 + kH, 2 * kH, 1, kH, pd + net.off[8], pd + net.off[9]);
   // loss sums of this CTA (threads 0..R-1 hold one row each)
-  const float a0 = block_sum(l_loss, red), a1 = block_sum(l_pg, red), a2 = block_sum(l_vf, red),
-              a3 = block_sum(l_ent, red);
-  if (t == 0) {
-    float* ls = wk.lstat + 4 * blockIdx.x;
-    ls[0] = a0;
-    ls[1] = a1;
-    ls[2] = a2;
-    ls[3] = a3;
+  if (t < 32) {  // rows live on threads 0..ROWS-1 (warp 0): one warp reduction of the four sums
+    float a[4] = {l_loss, l_pg, l_vf, l_ent};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a[i] += __shfl_down_sync(0xffffffffu, a[i], o);
+    if (t == 0) {
+      float* ls = wk.lstat + 4 * blockIdx.x;
+      ls[0] = a[0];
+      ls[1] = a[1];
+      ls[2] = a[2];
+      ls[3] = a[3];
+    }
   }
 }
 
@@ -594,7 +628,7 @@ int vy_ppo_update_workspace(int32_t obs_dim, int32_t S, int32_t A, int32_t hidde
 
 int vy_ppo_update_grad(const float* const* weights, const float* w1t, int32_t obs_dim, int32_t S, int32_t A,
                        int32_t hidden, const float* obs, int64_t obs_ld, const uint8_t* actions, const float* scal4,
-                       const int64_t* idx, int64_t M, float clip_eps, float vf_clip, float vf_coef, float ent_coef,
+                       const int64_t* idx, const float* adv_stats, int64_t M, float clip_eps, float vf_clip, float vf_coef, float ent_coef,
                        float* work, float* grad_out, float* stats, float* step, void* stream) {
   Geo g;
   if (int rc = geo(obs_dim, S, A, hidden, M, g)) return rc;
@@ -612,7 +646,7 @@ int vy_ppo_update_grad(const float* const* weights, const float* w1t, int32_t ob
   net.K1 = g.K1;
   net.NO = g.NO;
   const int64_t P = g.P, grid = g.grid;
-  vyu::Batch bt{obs, obs_ld, obs_dim, actions, reinterpret_cast<const float4*>(scal4), idx, M, S, A,
+  vyu::Batch bt{obs, obs_ld, obs_dim, actions, reinterpret_cast<const float4*>(scal4), idx, adv_stats, M, S, A,
                 clip_eps, vf_clip, vf_coef, ent_coef};
   const int64_t pld = g.pld;
   if ((reinterpret_cast<uintptr_t>(work) & 15u) != 0) return VY_ERR_ARG;
@@ -653,6 +687,16 @@ int vy_ppo_update_adam(float* const* params, float* w1t, int32_t obs_dim, int32_
                const_cast<float*>(step)};
   const unsigned nadam = (unsigned)((P + vyu::kSumThreads - 1) / vyu::kSumThreads);
   vyu::k_ppo_adam<<<nadam, vyu::kSumThreads, 0, (cudaStream_t)stream>>>(wk, ad, P, (int)g.nsq);
+  return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
+}
+
+int vy_ppo_adv_stats(const float* scal4, const int64_t* perms, int64_t n, int32_t count, int32_t nmb, int64_t mb,
+                     float* out, void* stream) {
+  if (!scal4 || !perms || !out || n < 2 || count < 1 || nmb < 1 || mb < 2 || (int64_t)nmb * mb > n ||
+      (reinterpret_cast<uintptr_t>(scal4) & 15u) != 0)
+    return VY_ERR_ARG;
+  vyu::k_adv_stats<<<(unsigned)(count * nmb), vyu::kThreads, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float4*>(scal4), perms, n, nmb, mb, out);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 

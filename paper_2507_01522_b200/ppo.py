@@ -552,6 +552,7 @@ class PPOTrainer:
                 self._perms = torch.empty(cfg.update_epochs, T * B, dtype=torch.int64, device=dev) \
                     if T * B <= 16384 else None
                 self._perm_ctr = torch.zeros(2, dtype=torch.int64, device=dev)
+                self._adv_stats = torch.zeros(cfg.update_epochs * cfg.n_minibatches, 2, device=dev)
                 self._perm_seed = (cfg.seed * 0x2545F4914F6CDD1D + env.global_offset + 7) & ((1 << 64) - 1)
         env.reset(as_numpy=False)
         self.obs[0].copy_(env.outs.obs)
@@ -762,9 +763,11 @@ class PPOTrainer:
         S, A, H, od = self.net.n_slots, self.net.n_actions, cfg.hidden, self.net.obs_dim
         with torch.no_grad():
             self._uw1t.copy_(self.net.inp.weight.t())
-        if self._perms is not None:
+        if self._perms is not None:  # the shuffles and every minibatch's advantage mean / std, two launches
             nat.check(lib.vy_random_perms(n, cfg.update_epochs, self._perm_seed, self._perm_ctr.data_ptr(),
                                           self._perms.data_ptr(), st), "vy_random_perms")
+            nat.check(lib.vy_ppo_adv_stats(scal.data_ptr(), self._perms.data_ptr(), n, cfg.update_epochs,
+                                           cfg.n_minibatches, mb, self._adv_stats.data_ptr(), st), "vy_ppo_adv_stats")
         for ep in range(cfg.update_epochs):
             if self._perms is not None:
                 perm = self._perms[ep]
@@ -773,7 +776,9 @@ class PPOTrainer:
             for k in range(cfg.n_minibatches):
                 idx = perm[k * mb:(k + 1) * mb]
                 nat.check(lib.vy_ppo_update_grad(self._uparams, self._uw1t.data_ptr(), od, S, A, H, obs.data_ptr(), obs.stride(0),
-                                                 act.data_ptr(), scal.data_ptr(), idx.data_ptr(), mb, cfg.clip_eps,
+                                                 act.data_ptr(), scal.data_ptr(), idx.data_ptr(),
+                                                 self._adv_stats[ep * cfg.n_minibatches + k].data_ptr()
+                                                 if self._perms is not None else None, mb, cfg.clip_eps,
                                                  cfg.vf_clip, cfg.vf_coef, cfg.ent_coef, self._uwork.data_ptr(),
                                                  self._ugrad.data_ptr(), self._ustats_buf.data_ptr(),
                                                  self._adam_step.data_ptr(), st), "vy_ppo_update_grad")

@@ -53,7 +53,7 @@ def _fused_grad(net, obs, act, scal, idx, cfg, step):
     ptrs = (C.c_void_p * len(prm))(*[p.data_ptr() for p in prm])
     w1t = net.inp.weight.detach().t().contiguous()
     nat.check(nat.lib().vy_ppo_update_grad(ptrs, w1t.data_ptr(), od, S, A, 64, obs.data_ptr(), obs.stride(0), act.data_ptr(),
-                                           scal.data_ptr(), idx.data_ptr(), M, cfg.clip_eps, cfg.vf_clip,
+                                           scal.data_ptr(), idx.data_ptr(), None, M, cfg.clip_eps, cfg.vf_clip,
                                            cfg.vf_coef, cfg.ent_coef, work.data_ptr(), grad.data_ptr(),
                                            stats.data_ptr(), step.data_ptr(), torch.cuda.current_stream().cuda_stream),
               "vy_ppo_update_grad")
@@ -197,3 +197,24 @@ def test_random_perms_are_permutations(n):
         assert abs(pos.mean().item() - (n - 1) / 2) < 0.02 * n
     big = torch.empty(1, 16385, dtype=torch.int64, device="cuda")
     assert nat.lib().vy_random_perms(16385, 1, 1, ctr.data_ptr(), big.data_ptr(), None) == nat.VY_ERR_UNSUPPORTED
+
+
+def test_precomputed_advantage_stats_match_in_kernel():
+    """vy_ppo_adv_stats (every minibatch of an update at once) gives the
+    minibatch mean / unbiased std torch computes, and the gradient computed
+    with them equals the in-kernel statistics' to fp32 rounding."""
+    from paper_2507_01522_b200 import _native as nat
+    from paper_2507_01522_b200.ppo import ActorCritic, PPOConfig
+
+    torch.manual_seed(9)
+    S, A, od, n, E, nmb = 17, 21, 105, 4800, 2, 4
+    mb = n // nmb
+    obs, act, scal = _data(n, od, S, A, seed=21)
+    perms = torch.stack([torch.randperm(n, device="cuda") for _ in range(E)]).contiguous()
+    out = torch.zeros(E * nmb, 2, device="cuda")
+    nat.check(nat.lib().vy_ppo_adv_stats(scal.data_ptr(), perms.data_ptr(), n, E, nmb, mb, out.data_ptr(),
+                                         torch.cuda.current_stream().cuda_stream), "vy_ppo_adv_stats")
+    for e in range(E):
+        for k in range(nmb):
+            a = scal[perms[e, k * mb:(k + 1) * mb], 2]
+            torch.testing.assert_close(out[e * nmb + k], torch.stack([a.mean(), a.std()]), rtol=1e-5, atol=1e-6)
