@@ -34,8 +34,28 @@
 
 namespace vyu {
 
+#ifdef VY_PPO_PROF  // phase timing build (scripts/probe_ppo_phases.py): clock64 deltas of CTA 0 thread 0
+__device__ unsigned long long g_upd_prof[16];
+#define UPD_MARK(i)                                   \
+  if (blockIdx.x == 0 && threadIdx.x == 0) {          \
+    const unsigned long long now_ = clock64();        \
+    g_upd_prof[i] += now_ - prof_last;                \
+    prof_last = now_;                                 \
+  }
+#else
+#define UPD_MARK(i)
+#endif
+
 // rows per CTA: 8, or 16 when 8 would need more than one wave of CTAs
-__host__ __device__ inline int rows_per_cta(int64_t M, int num_sms) { return M <= 8LL * num_sms ? 8 : 16; }
+// rows per CTA: the fewest of 8 / 10 / 16 that keep the grid to one wave
+// (PPO(16)'s 1200-row minibatches: 10 rows, 120 CTAs)
+__host__ __device__ inline int rows_per_cta(int64_t M, int num_sms) {
+  return M <= 8LL * num_sms ? 8 : (M <= 10LL * num_sms ? 10 : 16);
+}
+// row groups per output for the layer shapes (rows per thread = ROWS / G)
+__host__ __device__ constexpr int g_l1(int rows) { return rows == 10 ? 2 : 4; }    // 128 outputs
+__host__ __device__ constexpr int g_64(int rows) { return rows == 10 ? 5 : 8; }    // 64 outputs
+__host__ __device__ constexpr int g_head(int rows) { return rows >= 16 ? 2 : 1; }  // ~360 outputs
 constexpr int kThreads = 512;
 constexpr int kH = 64;         // hidden width per branch
 constexpr int kNP = 10;        // parameter tensors (ActorCritic order)
@@ -95,6 +115,7 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 template <int ROWS, int G, bool kTanh>
 __device__ __forceinline__ void dense_gt(const float* __restrict__ WT, const float* __restrict__ b, int N, int K,
                                          const float* in, int ldi, float* out, int ldo, int R) {
+  static_assert(ROWS % G == 0, "row groups must divide the rows");
   constexpr int RP = ROWS / G;
   for (int it = threadIdx.x; it < N * G; it += kThreads) {
     const int n = it % N, g = it / N;
@@ -128,6 +149,7 @@ __device__ __forceinline__ void dense_gt(const float* __restrict__ WT, const flo
 template <int ROWS, int G, bool kTanh>
 __device__ __forceinline__ void dense_s(const float* W, int ldw, const float* __restrict__ b, int N, int K,
                                         const float* in, int ldi, float* out, int ldo, int R) {
+  static_assert(ROWS % G == 0, "row groups must divide the rows");
   constexpr int RP = ROWS / G;
   for (int it = threadIdx.x; it < N * G; it += kThreads) {
     const int n = it % N, g = it / N;
@@ -161,6 +183,7 @@ __device__ __forceinline__ void dense_s(const float* W, int ldw, const float* __
 template <int ROWS, int G>
 __device__ __forceinline__ void dense_t(const float* W, int ldw, int N, int J, const float* d, int ldd,
                                         const float* h, int ldh, float* out, int ldo) {
+  static_assert(ROWS % G == 0, "row groups must divide the rows");
   constexpr int RP = ROWS / G;
   for (int it = threadIdx.x; it < J * G; it += kThreads) {
     const int j = it % J, g = it / J;
@@ -350,6 +373,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ppo_grad(const Net net, const B
   const int64_t r0 = (int64_t)blockIdx.x * ROWS;
   const int R = (int)((bt.M - r0) < ROWS ? (bt.M - r0) : ROWS);
   const int S = bt.S, A = bt.A, SA = S * A, K1 = net.K1, NO = net.NO;
+#ifdef VY_PPO_PROF
+  unsigned long long prof_last = clock64();
+#endif
 
   // the second layers and the head into shared memory, in flight during the
   // advantage statistics, the row gather and the first layer
@@ -374,15 +400,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_ppo_grad(const Net net, const B
     x[r * L.ldx + k] = (r < R && k < bt.obs_dim) ? bt.obs[bt.idx[r0 + r] * bt.obs_ld + k] : 0.f;
   }
   __syncthreads();
+  UPD_MARK(0);
 
   // forward: h1 = tanh(W1 x + b1) [actor | critic]; h2a, h2c; head z; value
-  dense_gt<ROWS, 4, true>(net.wt, net.w[1], 2 * kH, K1, x, L.ldx, h1, 2 * kH, ROWS);
+  dense_gt<ROWS, g_l1(ROWS), true>(net.wt, net.w[1], 2 * kH, K1, x, L.ldx, h1, 2 * kH, ROWS);
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
-  dense_s<ROWS, 8, true>(swa2, kLdw, net.w[3], kH, kH, h1, 2 * kH, h2, 2 * kH, ROWS);
-  dense_s<ROWS, 8, true>(swc2, kLdw, net.w[7], kH, kH, h1 + kH, 2 * kH, h2 + kH, 2 * kH, ROWS);
+  UPD_MARK(1);
+  dense_s<ROWS, g_64(ROWS), true>(swa2, kLdw, net.w[3], kH, kH, h1, 2 * kH, h2, 2 * kH, ROWS);
+  dense_s<ROWS, g_64(ROWS), true>(swc2, kLdw, net.w[7], kH, kH, h1 + kH, 2 * kH, h2 + kH, 2 * kH, ROWS);
   __syncthreads();
-  dense_s<ROWS, (ROWS >= 16 ? 2 : 1), false>(swh, kLdw, net.w[5], NO, kH, h2, 2 * kH, z, L.ldz, R);
+  dense_s<ROWS, g_head(ROWS), false>(swh, kLdw, net.w[5], NO, kH, h2, 2 * kH, z, L.ldz, R);
   {  // value: one warp per row, lanes over the 64 inputs
     const int w = t >> 5, l = t & 31;
     for (int r = w; r < R; r += kThreads / 32) {
@@ -395,6 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ppo_grad(const Net net, const B
   }
   __syncthreads();
 
+  UPD_MARK(2);
   // loss head (k_ppo_loss's formulas): per (row, slot) softmax statistics
   for (int it = t; it < R * S; it += kThreads) {
     const int r = it / S, sl = it - r * S;
@@ -476,18 +505,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_ppo_grad(const Net net, const B
   if (t >= R && t < ROWS) dv[t] = 0.f;
   __syncthreads();
 
+  UPD_MARK(3);
   // backward: dz2 = [d h2a-pre | d h2c-pre], dz1 = d h1-pre
-  dense_t<ROWS, 8>(swh, kLdw, NO, kH, z, L.ldz, h2, 2 * kH, dz2, 2 * kH);
+  dense_t<ROWS, g_64(ROWS)>(swh, kLdw, NO, kH, z, L.ldz, h2, 2 * kH, dz2, 2 * kH);
   for (int e = t; e < ROWS * kH; e += kThreads) {  // critic: d h2c = dv * wv
     const int r = e / kH, j = e - r * kH;
     const float hv = h2[r * 2 * kH + kH + j];
     dz2[r * 2 * kH + kH + j] = dv[r] * __ldg(net.w[8] + j) * (1.f - hv * hv);
   }
   __syncthreads();
-  dense_t<ROWS, 8>(swa2, kLdw, kH, kH, dz2, 2 * kH, h1, 2 * kH, dz1, 2 * kH);
-  dense_t<ROWS, 8>(swc2, kLdw, kH, kH, dz2 + kH, 2 * kH, h1 + kH, 2 * kH, dz1 + kH, 2 * kH);
+  dense_t<ROWS, g_64(ROWS)>(swa2, kLdw, kH, kH, dz2, 2 * kH, h1, 2 * kH, dz1, 2 * kH);
+  dense_t<ROWS, g_64(ROWS)>(swc2, kLdw, kH, kH, dz2 + kH, 2 * kH, h1 + kH, 2 * kH, dz1 + kH, 2 * kH);
   __syncthreads();
 
+  UPD_MARK(4);
   // this CTA's partial gradients, the module's parameter order
   float* pd = wk.part + (int64_t)blockIdx.x * wk.pld;
   wgrad<ROWS>(dz1, 2 * kH, x, L.ldx, 2 * kH, K1, pd + net.off[0], pd + net.off[1]);
@@ -496,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ppo_grad(const Net net, const B
   wgrad<ROWS>(dz2 + kH, 2 * kH, h1 + kH, 2 * kH, kH, kH, pd + net.off[6], pd + net.off[7]);
   wgrad_rows<ROWS>(dv, 1, h2 + kH, 2 * kH, 1, kH, pd + net.off[8], pd + net.off[9]);
   // loss sums of this CTA (threads 0..R-1 hold one row each)
+  UPD_MARK(5);
   if (t < 32) {  // rows live on threads 0..ROWS-1 (warp 0): one warp reduction of the four sums
     float a[4] = {l_loss, l_pg, l_vf, l_ent};
 #pragma unroll
@@ -513,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ppo_grad(const Net net, const B
 }
 
 constexpr int kSumThreads = 256;
-constexpr int kSplit = 4;  // threads per parameter in k_ppo_gsum
+constexpr int kSplit = 8;  // threads per parameter in k_ppo_gsum
 
 // four consecutive threads per parameter sum contiguous quarters of the CTA
 // partials; the quarter sums are added in quarter order (deterministic)
@@ -652,7 +684,7 @@ int vy_ppo_update_grad(const float* const* weights, const float* w1t, int32_t ob
   if ((reinterpret_cast<uintptr_t>(work) & 15u) != 0) return VY_ERR_ARG;
   vyu::Work wk{pld, work, work + grid * pld, grad_out, work + grid * pld + grid * 4, stats, step};
   const int smem = vyu::smem_layout(g.rows, g.K1, g.NO, S).bytes;
-  auto* kern = g.rows == 8 ? vyu::k_ppo_grad<8> : vyu::k_ppo_grad<16>;
+  auto* kern = g.rows == 8 ? vyu::k_ppo_grad<8> : g.rows == 10 ? vyu::k_ppo_grad<10> : vyu::k_ppo_grad<16>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return VY_ERR_CUDA;
   cudaStream_t st = (cudaStream_t)stream;
   kern<<<(unsigned)grid, vyu::kThreads, smem, st>>>(net, bt, wk, P);
@@ -689,6 +721,12 @@ int vy_ppo_update_adam(float* const* params, float* w1t, int32_t obs_dim, int32_
   vyu::k_ppo_adam<<<nadam, vyu::kSumThreads, 0, (cudaStream_t)stream>>>(wk, ad, P, (int)g.nsq);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
+
+#ifdef VY_PPO_PROF
+int vy_upd_prof_read(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, vyu::g_upd_prof, sizeof(vyu::g_upd_prof)) == cudaSuccess ? VY_OK : VY_ERR_CUDA;
+}
+#endif
 
 int vy_ppo_adv_stats(const float* scal4, const int64_t* perms, int64_t n, int32_t count, int32_t nmb, int64_t mb,
                      float* out, void* stream) {

@@ -60,7 +60,7 @@ def _fused_grad(net, obs, act, scal, idx, cfg, step):
     return grad, stats, work, w1t
 
 
-@pytest.mark.parametrize("M,scale", [(1200, 1.0), (75, 1.0), (900, 30.0), (37, 1.0)])
+@pytest.mark.parametrize("M,scale", [(1200, 1.0), (75, 1.0), (900, 30.0), (37, 1.0), (2000, 1.0)])
 def test_fused_gradient_matches_torch_fp32(M, scale):
     from paper_2507_01522_b200.ppo import ActorCritic, PPOConfig
 
