@@ -177,6 +177,13 @@ __device__ __forceinline__ float exp2_sfu(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// two values rounded to bf16 (RNE) and back to float with one packed
+// conversion (cvt.rn.bf16x2.f32) and two unpacks
+__device__ __forceinline__ void bf16r2(float a, float b, float& ra, float& rb) {
+  const __nv_bfloat162 p = __floats2bfloat162_rn(a, b);
+  ra = __low2float(p);
+  rb = __high2float(p);
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   const __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&p);
@@ -194,9 +201,9 @@ __device__ __forceinline__ void act_to_a(const uint32_t* v, const float* bias, u
   uint32_t w[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const float x0 = tanh_sfu(bf16r(__uint_as_float(v[2 * j]) + bias[2 * j]));
-    const float x1 = tanh_sfu(bf16r(__uint_as_float(v[2 * j + 1]) + bias[2 * j + 1]));
-    w[j] = pack_bf16(x0, x1);
+    float y0, y1;
+    bf16r2(__uint_as_float(v[2 * j]) + bias[2 * j], __uint_as_float(v[2 * j + 1]) + bias[2 * j + 1], y0, y1);
+    w[j] = pack_bf16(tanh_sfu(y0), tanh_sfu(y1));
   }
   const uint4 val = make_uint4(w[0], w[1], w[2], w[3]);
 #pragma unroll
@@ -227,12 +234,14 @@ __device__ __forceinline__ void sample_slot(const uint32_t* v, const float* bias
     bq[4 * q + 3] = f.w;
   }
   constexpr int KN = AC ? AC : kMaxA;
-  float z[KN], e[KN];
+  float z[KN + 1], e[KN];
+#pragma unroll
+  for (int k = 0; k < KN; k += 2)  // bf16 logits, two per packed conversion (v / bq have 24 entries)
+    bf16r2(__uint_as_float(v[k]) + bq[k], __uint_as_float(v[k + 1]) + bq[k + 1], z[k], z[k + 1]);
   float m = -INFINITY;
 #pragma unroll
   for (int k = 0; k < KN; ++k) {
-    const float zk = bf16r(__uint_as_float(v[k]) + bq[k]);  // bf16 logits
-    z[k] = (AC || k < A) ? zk : -INFINITY;
+    if (!(AC || k < A)) z[k] = -INFINITY;
     m = fmaxf(m, z[k]);
   }
   const float mb = m * kLog2e;
