@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ppo_grad(const Net net, const B
 }
 
 constexpr int kSumThreads = 256;
-constexpr int kSplit = 8;  // threads per parameter in k_ppo_gsum
+constexpr int kSplit = 4;  // threads per parameter in k_ppo_gsum
 
 // four consecutive threads per parameter sum contiguous quarters of the CTA
 // partials; the quarter sums are added in quarter order (deterministic)

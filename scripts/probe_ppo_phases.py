@@ -69,3 +69,16 @@ full = np.frombuffer(st, dtype=np.uint64).reshape(256, 16).astype(np.int64)[1:]
 pre, fit = full[:, 9] - full[:, 1], full[:, 2] - full[:, 9]
 print(f"  node sums before the rescale: mean {pre.mean():.0f}; rescale: mean {fit.mean():.0f}, "
       f"steps with a rescale {(fit > 200).mean() * 100:.0f}%")
+
+# the fused update's gradient kernel: one update (16 minibatch launches), CTA 0 thread 0
+tr.update()
+torch.cuda.synchronize()
+h.vy_upd_prof_read.argtypes = [C.c_void_p]
+ub = (C.c_ulonglong * 16)()
+h.vy_upd_prof_read(ub)
+launches = tr.cfg.update_epochs * tr.cfg.n_minibatches
+unames = ["stage issue + adv stats + row gather", "layer 1 + weights landed", "layers 2, head, value",
+          "loss head + d logits", "backward to dz1", "weight gradients"]
+utot = sum(ub[i] for i in range(6))
+for i, nm in enumerate(unames):
+    print(f"  grad {nm:38s} {ub[i] / launches:8.0f} cyc/launch  {100 * ub[i] / max(utot, 1):5.1f}%")
