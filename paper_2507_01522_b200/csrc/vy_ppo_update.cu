@@ -558,12 +558,14 @@ __global__ void __launch_bounds__(kSumThreads) k_ppo_gsum(const Work wk, int64_t
   if (p < P)
 #pragma unroll 8
     for (int c = c0; c < c1; ++c) g += wk.part[(int64_t)c * wk.pld + p];
-  // in-order combine of the four quarter sums (lanes 4i .. 4i+3 of one warp)
+  // in-order combine of the kSplit range sums (lanes base .. base + kSplit - 1 of one warp)
+  static_assert(kSplit >= 1 && kSplit <= 32 && (kSplit & (kSplit - 1)) == 0, "kSplit: a power of two <= 32");
   const unsigned FULL = 0xffffffffu;
   const int base = (threadIdx.x & 31) & ~(kSplit - 1);
-  const float q0 = __shfl_sync(FULL, g, base), q1 = __shfl_sync(FULL, g, base + 1);
-  const float q2 = __shfl_sync(FULL, g, base + 2), q3 = __shfl_sync(FULL, g, base + 3);
-  g = ((q0 + q1) + q2) + q3;
+  float tot = __shfl_sync(FULL, g, base);
+#pragma unroll
+  for (int i = 1; i < kSplit; ++i) tot += __shfl_sync(FULL, g, base + i);
+  g = tot;
   const bool lead = qtr == 0 && p < P;
   if (lead) wk.grad[p] = g;
   const float s = block_sum(lead ? g * g : 0.f, red);
