@@ -393,13 +393,20 @@ int vy_ppo_update_adam(float *const *params, float *w1t, int32_t obs_dim, int32_
                        float *work, const float *grad, float *exp_avg, float *exp_avg_sq, const float *lr,
                        const float *step, float beta1, float beta2, float eps, float max_grad_norm, void *stream);
 
-/* count independent uniform random permutations of 0..n-1 (n <= 16384) into
- * out [count][n] int64 — the PPO update's minibatch shuffles, one launch per
- * update: one CTA per permutation sorts 32-bit counter-based random keys
- * (ties by index) with a shared-memory bitonic sort.  counter = {call,
- * scratch} on the device, advanced by one per launch (graph replays draw
- * fresh permutations). */
+/* count pseudo-random permutations of 0..n-1 (n <= 2^30) into out
+ * [count][n] int64 — the PPO update's minibatch shuffles, one launch per
+ * update: element i maps through a keyed 4-round Feistel bijection on
+ * [0, 4^h) >= n with cycle-walking (no sort), one key per permutation from
+ * (seed, call, c).  counter = {call, scratch} on the device, advanced by one
+ * per launch (graph replays draw fresh permutations). */
 int vy_random_perms(int64_t n, int32_t count, uint64_t seed, int64_t *counter, int64_t *out, void *stream);
+
+/* GAE (vy_gae's recurrence and roundings) written straight into the update's
+ * per-sample rows: scal4 [T*B] float4 = {logp, value, advantage, return};
+ * values / rewards / logp [T][B] float32, dones [T][B] uint8, last_value [B].
+ * Small rollouts run as one block staging the inputs in shared memory. */
+int vy_gae_scal(const float *values, const float *rewards, const uint8_t *dones, const float *last_value,
+                const float *logp, int32_t T, int64_t B, float gamma, float lam, float *scal4, void *stream);
 
 int vy_gather_rows(const void *src, int64_t row_bytes, const int64_t *idx, int64_t n, void *dst, void *stream);
 /* Column sums (a linear layer's bias gradient): out[c] = sum over m < M of

@@ -86,6 +86,7 @@ _SIGS = {
     "vy_ppo_update_adam": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, _P, _P, _P, _P, _P,
                                      _P, C.c_float, C.c_float, C.c_float, C.c_float, _P]),
     "vy_ppo_adv_stats": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, C.c_int64, _P, _P]),
+    "vy_gae_scal": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, C.c_int64, C.c_float, C.c_float, _P, _P]),
     "vy_random_perms": (C.c_int, [C.c_int64, C.c_int32, C.c_uint64, _P, _P, _P]),
     "vy_selftest_div": (C.c_int, [C.POINTER(C.c_double), C.c_int32, C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),
     "vy_ppo_loss": (C.c_int, [_P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P, C.c_float, C.c_float,

@@ -49,6 +49,69 @@ __global__ void k_gae(const float* __restrict__ values, const float* __restrict_
   }
 }
 
+// GAE straight into the update's per-sample rows {old log-prob, value,
+// advantage, return} (float4), the same recurrence and roundings as k_gae.
+// Small rollouts (the paper's 1-16 envs): one block stages values, rewards
+// and dones in shared memory with coalesced loads, threads b < B scan their
+// env from shared memory, then the block writes the rows coalesced.
+__global__ void __launch_bounds__(1024) k_gae_scal_small(const float* __restrict__ values,
+                                                          const float* __restrict__ rewards,
+                                                          const uint8_t* __restrict__ dones,
+                                                          const float* __restrict__ last_value,
+                                                          const float* __restrict__ logp, int T, int B, float gamma,
+                                                          float lam, float4* __restrict__ scal) {
+  extern __shared__ float gs[];
+  const int n = T * B;
+  float* sv = gs;
+  float* sr = gs + n;  // rewards, then advantages in place
+  uint8_t* sd = reinterpret_cast<uint8_t*>(gs + 2 * n);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    sv[i] = values[i];
+    sr[i] = rewards[i];
+    sd[i] = dones[i];
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < B) {
+    const int b = threadIdx.x;
+    float next_v = last_value[b];
+    float gae = 0.f;
+    for (int t = T - 1; t >= 0; --t) {
+      const int i = t * B + b;
+      const float v = sv[i];
+      const float nonterm = sd[i] ? 0.f : 1.f;
+      const float delta = sr[i] + gamma * next_v * nonterm - v;
+      gae = delta + gamma * lam * nonterm * gae;
+      sr[i] = gae;
+      next_v = v;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float v = sv[i], a = sr[i];
+    scal[i] = make_float4(logp[i], v, a, a + v);
+  }
+}
+
+__global__ void k_gae_scal(const float* __restrict__ values, const float* __restrict__ rewards,
+                           const uint8_t* __restrict__ dones, const float* __restrict__ last_value,
+                           const float* __restrict__ logp, int T, int64_t B, float gamma, float lam,
+                           float4* __restrict__ scal) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  float next_v = last_value[b];
+  float gae = 0.f;
+#pragma unroll 8
+  for (int t = T - 1; t >= 0; --t) {
+    const int64_t i = (int64_t)t * B + b;
+    const float v = values[i];
+    const float nonterm = dones[i] ? 0.f : 1.f;
+    const float delta = rewards[i] + gamma * next_v * nonterm - v;
+    gae = delta + gamma * lam * nonterm * gae;
+    scal[i] = make_float4(logp[i], v, gae, gae + v);
+    next_v = v;
+  }
+}
+
 __device__ __forceinline__ float to_f(float v) { return v; }
 __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
 template <class T> __device__ __forceinline__ T from_f(float v);
@@ -761,6 +824,27 @@ extern "C" int vy_gae(const float* values, const float* rewards, const uint8_t* 
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }
 
+extern "C" int vy_gae_scal(const float* values, const float* rewards, const uint8_t* dones, const float* last_value,
+                           const float* logp, int32_t T, int64_t B, float gamma, float lam, float* scal4,
+                           void* stream) {
+  if (!values || !rewards || !dones || !last_value || !logp || !scal4 || T < 1 || B < 1 ||
+      (reinterpret_cast<uintptr_t>(scal4) & 15u))
+    return VY_ERR_ARG;
+  const int64_t n = (int64_t)T * B;
+  const size_t smem = (size_t)n * 9 + 16;
+  if (B <= 1024 && smem <= 160 * 1024) {
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(k_gae_scal_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024) != cudaSuccess)
+      return VY_ERR_CUDA;
+    k_gae_scal_small<<<1, 1024, smem, (cudaStream_t)stream>>>(values, rewards, dones, last_value, logp, T, (int)B,
+                                                               gamma, lam, reinterpret_cast<float4*>(scal4));
+  } else {
+    k_gae_scal<<<(unsigned)((B + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        values, rewards, dones, last_value, logp, T, B, gamma, lam, reinterpret_cast<float4*>(scal4));
+  }
+  return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
+}
+
 extern "C" int vy_ppo_loss(const void* logits, int64_t ld, const uint8_t* actions, int64_t N, int32_t S, int32_t A,
                            const float* scal4, const float* adv_stats, float clip_eps, float vf_clip, float vf_coef,
                            float ent_coef, int32_t value_col, void* grad, float* stats, void* stream) {
@@ -811,36 +895,35 @@ __device__ __forceinline__ uint64_t perm_mix(uint64_t z) {
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
   return z ^ (z >> 31);
 }
-// count uniform random permutations of 0..n-1, one CTA each: element i gets
-// the key (hash(seed, call, c, i) >> 32) << 32 | i (ties broken by index),
-// and a bitonic sort of the n keys (padded to a power of two) in shared
-// memory orders them; the last CTA out advances the call counter
-__global__ void __launch_bounds__(1024) k_random_perms(int64_t n, int p2, uint64_t seed,
-                                                        unsigned long long* counter, int64_t* __restrict__ out) {
-  extern __shared__ unsigned long long pk[];
-  const int c = blockIdx.x;
+// count pseudo-random permutations of 0..n-1 (the PPO update's minibatch
+// shuffles): element i maps through a keyed 4-round Feistel bijection on
+// [0, 4^h) (4^h >= n), cycle-walking until the image is < n — a bijection of
+// [0, n) evaluated independently per element, no sort; each permutation has
+// its own key from (seed, call, c).  The last CTA out advances the call counter.
+__global__ void __launch_bounds__(256) k_random_perms(int64_t n, int h, uint64_t seed, unsigned long long* counter,
+                                                       int64_t* __restrict__ out) {
+  const int c = blockIdx.y;
   const uint64_t key = perm_mix(seed ^ perm_mix(counter[0] * 0x9E3779B97F4A7C15ULL + (uint64_t)c + 1));
-  for (int i = threadIdx.x; i < p2; i += blockDim.x)
-    pk[i] = i < n ? ((perm_mix(key + (uint64_t)i * 0x9E3779B97F4A7C15ULL) >> 32) << 32) | (uint64_t)i : ~0ull;
-  __syncthreads();
-  for (int k = 2; k <= p2; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < p2; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const unsigned long long a = pk[i], b = pk[ixj];
-          if ((a > b) == ((i & k) == 0)) {
-            pk[i] = b;
-            pk[ixj] = a;
-          }
-        }
+  const uint32_t mask = (1u << h) - 1u;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t x = (uint32_t)i;
+    do {
+      uint32_t L = x >> h, R = x & mask;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t f = (uint32_t)perm_mix(key + ((uint64_t)r << 40) + R) & mask;
+        const uint32_t t = L ^ f;
+        L = R;
+        R = t;
       }
-      __syncthreads();
-    }
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) out[(int64_t)c * n + i] = (int64_t)(pk[i] & 0xffffffffull);
+      x = (L << h) | R;
+    } while ((int64_t)x >= n);
+    out[(int64_t)c * n + i] = (int64_t)x;
+  }
+  __syncthreads();  // every thread of the CTA has read the call counter
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(counter + 1, 1ull) == gridDim.x - 1) {
+    if (atomicAdd(counter + 1, 1ull) == gridDim.x * gridDim.y - 1) {
       counter[1] = 0;
       counter[0] += 1;
       __threadfence();
@@ -852,14 +935,11 @@ __global__ void __launch_bounds__(1024) k_random_perms(int64_t n, int p2, uint64
 extern "C" int vy_random_perms(int64_t n, int32_t count, uint64_t seed, int64_t* counter, int64_t* out,
                                void* stream) {
   if (!counter || !out || n < 1 || count < 1) return VY_ERR_ARG;
-  int p2 = 1;
-  while (p2 < n) p2 <<= 1;
-  if (p2 > 16384) return VY_ERR_UNSUPPORTED;
-  const int smem = p2 * 8;
-  if (smem > 48 * 1024 &&
-      cudaFuncSetAttribute(k_random_perms, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return VY_ERR_CUDA;
-  k_random_perms<<<count, 1024, smem, (cudaStream_t)stream>>>(n, p2, seed,
-                                                               reinterpret_cast<unsigned long long*>(counter), out);
+  if (n > (int64_t)1 << 30) return VY_ERR_UNSUPPORTED;
+  int h = 1;
+  while (((int64_t)1 << (2 * h)) < n) ++h;  // 4^h >= n: at most 4x the elements, ~2 walk steps on average
+  const unsigned gx = (unsigned)std::min<int64_t>((n + 255) / 256, 1024);
+  k_random_perms<<<dim3(gx, (unsigned)count), 256, 0, (cudaStream_t)stream>>>(
+      n, h, seed, reinterpret_cast<unsigned long long*>(counter), out);
   return cudaGetLastError() == cudaSuccess ? VY_OK : VY_ERR_CUDA;
 }

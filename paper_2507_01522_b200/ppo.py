@@ -553,6 +553,7 @@ class PPOTrainer:
                     if T * B <= 16384 else None
                 self._perm_ctr = torch.zeros(2, dtype=torch.int64, device=dev)
                 self._adv_stats = torch.zeros(cfg.update_epochs * cfg.n_minibatches, 2, device=dev)
+                self._scal = torch.zeros(T * B, 4, device=dev)  # {old log-prob, value, advantage, return}
                 self._perm_seed = (cfg.seed * 0x2545F4914F6CDD1D + env.global_offset + 7) & ((1 << 64) - 1)
         env.reset(as_numpy=False)
         self.obs[0].copy_(env.outs.obs)
@@ -692,6 +693,8 @@ class PPOTrainer:
     def _update_body(self) -> dict:
         cfg = self.cfg
         T, B = cfg.rollout_steps, self.env.batch_size
+        if self._fused_update:
+            return self._fused_update_body(T * B, T * B // cfg.n_minibatches)
         adv, ret = gae(self.values[:T], self.rewards, self.dones, self.values[T], cfg.gamma, cfg.gae_lambda)
         # aligned bf16 rows once per update (the value autocast would cast each
         # minibatch to anyway); minibatches gather half the bytes
@@ -702,8 +705,6 @@ class PPOTrainer:
         n = T * B
         mb = n // cfg.n_minibatches
         stats = {}
-        if self._fused_update:
-            return self._fused_update_body(adv, ret, scal, n, mb)
         for _ in range(cfg.update_epochs):
             perm = torch.argsort(torch.rand(n, device=obs.device))  # a uniform permutation, capture-safe
             for k in range(cfg.n_minibatches):
@@ -751,15 +752,20 @@ class PPOTrainer:
         self.obs[0].copy_(self.obs[T])
         return stats
 
-    def _fused_update_body(self, adv, ret, scal, n: int, mb: int) -> dict:
-        """Epochs x minibatches of vy_ppo_update_grad (+ the gradient all-reduce
-        across ranks) + vy_ppo_update_adam; the rollout rows are read in place
-        through each minibatch's index slice."""
+    def _fused_update_body(self, n: int, mb: int) -> dict:
+        """GAE into the per-sample rows (vy_gae_scal), then epochs x
+        minibatches of vy_ppo_update_grad (+ the gradient all-reduce across
+        ranks) + vy_ppo_update_adam; the rollout rows are read in place through
+        each minibatch's index slice."""
         cfg, T = self.cfg, self.cfg.rollout_steps
         lib, st = nat.lib(), torch.cuda.current_stream().cuda_stream
         obs = self.obs[:T].reshape(n, -1)
         act = self.actions.reshape(n, -1)
-        scal = scal.contiguous()
+        scal = self._scal
+        nat.check(lib.vy_gae_scal(self.values.data_ptr(), self.rewards.data_ptr(), self.dones.data_ptr(),
+                                  self.values[T].data_ptr(), self.logp.data_ptr(), T, self.env.batch_size,
+                                  C.c_float(cfg.gamma), C.c_float(cfg.gae_lambda), scal.data_ptr(), st),
+                  "vy_gae_scal")
         S, A, H, od = self.net.n_slots, self.net.n_actions, cfg.hidden, self.net.obs_dim
         with torch.no_grad():
             self._uw1t.copy_(self.net.inp.weight.t())
