@@ -54,6 +54,11 @@ METRIC = "env-steps/sec (whole box)"
 UNIT = "env-steps/s"
 
 
+# HBM throughput of plain read/write streams at the step kernel's mid-day
+# mix (scripts/micro/rw_mix.cu, R:W = 3:5, profiles/r2_rw_mix.txt)
+MIX_PEAK_GBS = 5821.0
+
+
 def survey_bytes(t, T: int = 1) -> dict:
     """SURVEY.md §8(d) algorithmic bytes per env-step (the canonical roofline
     figure): minimal lossless SoA state S = 15 B/port + 44 B/env, read and
@@ -366,7 +371,13 @@ def main() -> None:
                      "contract_f64": {"bytes_per_env_step": cb["per_env_step"],
                                       "frac": cb["per_env_step"] * B / (step_kernel_ms / 1e3) / 1e9 / hbm,
                                       "note": "the kernel's own float64-state contract (24 B of floats per port)"},
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not peaks.get("_fallback") else "fallback"},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not peaks.get("_fallback") else "fallback",
+                     "mix_peak": {"gbs": MIX_PEAK_GBS,
+                                  "traffic_frac": traffic / (step_kernel_ms / 1e3) / 1e9 / MIX_PEAK_GBS
+                                  if traffic else None,
+                                  "note": "plain 16-byte streams at the step's 0.37 R : 0.63 W DRAM mix "
+                                          "(R:W = 3:5), profiles/r2_rw_mix.txt: the practical ceiling of "
+                                          "the bytes the kernel moves; context only, frac uses peak"}},
         "clocks": clocks.summary(),
     }
 

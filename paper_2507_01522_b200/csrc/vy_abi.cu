@@ -215,6 +215,18 @@ TileLayout tile_layout(const vy_tables& t, bool rollout, bool acts, bool stream 
 
 double rcp(double d) { return 1.0 / d; }
 
+// L2 prefetch distance of the streamed step (Params::pf_dist), in tiles: a
+// fraction (percent; VY_PF overrides) of the resident warps, i.e. of the tiles
+// in flight at once
+int g_pf_percent = -1;
+int64_t pf_dist(unsigned grid, int warps) {
+  if (g_pf_percent < 0) {
+    const char* v = std::getenv("VY_PF");
+    g_pf_percent = v ? std::atoi(v) : 12;  // 5-25 measured equal, 50+ slower (profiles/r2_c4_prefetch_ab.txt)
+  }
+  return (int64_t)grid * warps * g_pf_percent / 100;
+}
+
 void fill(vy_handle* h, Params& P, bool rollout, bool acts, bool stream = false) {
   const vy_tables& t = h->t;
   std::memset(&P, 0, sizeof(P));
@@ -658,6 +670,7 @@ int vy_step(vy_handle* h, const void* actions, int32_t dtype, int64_t row_stride
     const unsigned k = (unsigned)h->tiles_per_warp, want = (g.grid + k - 1) / k;
     grid = want < grid ? want : grid;
   }
+  if (mode == 4) P.pf_dist = pf_dist(grid, g.warps);
   kern<<<grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P);
   VY_CUDA(cudaGetLastError());
   ++h->launches;
@@ -692,6 +705,7 @@ int vy_step_random(vy_handle* h, uint64_t seed, int64_t index0, int64_t call, in
     const unsigned k = (unsigned)h->tiles_per_warp, want = (g.grid + k - 1) / k;
     grid = want < grid ? want : grid;
   }
+  if (mode == 4) P.pf_dist = pf_dist(grid, g.warps);
   kern<<<grid, g.warps * 32, g.smem, (cudaStream_t)stream>>>(P);
   VY_CUDA(cudaGetLastError());
   ++h->launches;

@@ -148,6 +148,7 @@ struct Params {
   uint8_t* pol_out;           // optional uint8 [B][n+1] copy of the generated actions
   uint32_t* err;
   unsigned long long* tile_ctr;  // [2] work-stealing tile counter, finished-warp counter (k_step)
+  int64_t pf_dist;               // streamed k_step: L2 prefetch of tile t + pf_dist while tile t runs (0: off)
   TileLayout L;
 };
 

@@ -105,6 +105,10 @@ __device__ __forceinline__ void step_tile(const Params& P, Prof prof, const doub
   const Frame F = load_frame<M>(P, E.step, E.day);
   const ObsGlobals G = load_obs_globals(P, E.step + 1, E.day);
   const uint64_t occ_ports = tile_issue_ports(P, tile, b0, lane, wb, C::stream);
+  if (C::stream && P.pf_dist) {
+    const int64_t bp0 = b0 + 32 * P.pf_dist;
+    if (bp0 + 32 <= P.B) tile_prefetch_l2(P, bp0, lane, occ_ports, C::battery(P));
+  }
   if (P.policy) policy_row(P, tile, b0, lane, pol_call);  // ALU work under the copies' latency
   tile_wait(wb);
   // state goes back to HBM port by port; obs staged in the consumed port slots,

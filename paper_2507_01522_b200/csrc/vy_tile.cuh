@@ -427,6 +427,45 @@ __device__ __forceinline__ uint64_t tile_issue_ports(const Params& P, uint32_t t
   return mask;
 }
 
+// L2 prefetch (TMA engine: no shared memory, no registers held) of the state
+// a later tile will read: its meta and per-env scalars, and the float64 slots
+// and dwell times of the ports in `mask` (this tile's occupied ports; tiles at
+// the same step have similar occupancy).  The persistent grid claims tiles in
+// increasing order, so tile t + pf_dist is claimed a fraction of a tile
+// lifetime later and its state loads then hit L2.  Used by the streamed tile
+// (Spec<4>, config C4), whose in-loop state loads wait on memory latency with
+// the DRAM system mostly idle; the resident-tile step is bound by DRAM
+// throughput and measured slower with it (profiles/r2_l2_prefetch_ab.txt).
+__device__ __forceinline__ void l2_prefetch(const void* g, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(g), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tile_prefetch_l2(const Params& P, int64_t bp0, int lane, uint64_t mask, bool battery) {
+  const int n = P.n_ports;
+  const int64_t ld = P.ld;
+  const vy_state& s = P.st;
+  for (int i = lane; i < n; i += 32) {
+    const int64_t e = (int64_t)i * ld + bp0;
+    l2_prefetch(s.port_meta + e, 32);
+    if ((mask >> i) & 1ull) {
+      l2_prefetch(s.port_i + e, 256);
+      l2_prefetch(s.port_soc + e, 256);
+      l2_prefetch(s.port_de + e, 256);
+      l2_prefetch(s.port_dtrem + e, 64);
+    }
+  }
+  const int j = 31 - lane;  // the per-env scalars from the top lanes
+  if (j < 10 || (battery && j < 12)) {
+    const void* a = j == 0 ? (const void*)(s.step + bp0) : j == 1 ? (const void*)(s.day + bp0)
+                  : j == 2 ? (const void*)(s.akey + bp0) : j == 3 ? (const void*)(s.ep_profit + bp0)
+                  : j == 4 ? (const void*)(s.ep_reward + bp0) : j == 5 ? (const void*)(s.ep_missing + bp0)
+                  : j == 6 ? (const void*)(s.ep_energy + bp0) : j == 7 ? (const void*)(s.ep_overtime + bp0)
+                  : j == 8 ? (const void*)(s.ep_declined + bp0) : j == 9 ? (const void*)(s.ep_departures + bp0)
+                  : j == 10 ? (const void*)(s.b_i + bp0) : (const void*)(s.b_soc + bp0);
+    const bool wide = (j >= 2 && j <= 6) || j >= 10;
+    l2_prefetch(a, wide ? 256u : 128u);
+  }
+}
+
 __device__ __forceinline__ void tile_wait(WarpBar& wb) {
   bar_wait(wb);
 #if !VY_BULK_SLOTS || !VY_BULK_META
