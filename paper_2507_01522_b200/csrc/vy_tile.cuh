@@ -92,6 +92,14 @@ struct Prof {
 // Per-port constants staged in shared memory (one 96-byte record per port):
 // every lane reads the same address (broadcast), two doubles per 16-byte
 // load, instead of one indexed constant-bank load per value.
+#ifndef VY_U1
+#define VY_U1 1
+#endif
+#ifndef VY_U2
+#define VY_U2 1
+#endif
+#define VY_PRAGMA(x) _Pragma(#x)
+#define VY_UNROLL(n) VY_PRAGMA(unroll n)
 struct PortC {
   uint32_t a;  // shared address of port 0's record
   __device__ __forceinline__ void pair(int i, int w, double& x, double& y) const {
@@ -884,7 +892,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
     soc_q0 = soc_at(0);
     soc_q1 = soc_at(1);
   }
-#pragma unroll 1  // rolled: smaller hot loop measured faster than unroll 2 or 4
+VY_UNROLL(VY_U1)  // rolled: smaller hot loop measured faster than unroll 2 or 4
   for (int i = 0; i < n; ++i) {
     const double d = delta_of(act(i));
     const uint32_t mt = T.meta(i);
@@ -994,7 +1002,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
     q0 = q_at(0);
     q1 = q_at(1);
   }
-#pragma unroll 1  // rolled: smaller hot loop measured faster than unroll 2 or 4
+VY_UNROLL(VY_U2)  // rolled: smaller hot loop measured faster than unroll 2 or 4
   for (int i = 0; i < n; ++i) {
     uint32_t mt = T.meta(i);
     double cur = T.idr(i), soc, de;
