@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
     const uint64_t j0 = (uint64_t)(call0 + t) * (uint64_t)ns;
     auto act = [&](int slot) -> int { return policy_action(pkey, j0 + slot + 1, hi); };
     const Frame F = load_frame<M>(P, E.step, E.day);
-    const StepResult r = tile_step<M>(P, prof, dtab, pc, tc, T, E, b, F, S, active, act, nullptr);
+    const StepResult r = tile_step<M, decltype(act), 2>(P, prof, dtab, pc, tc, T, E, b, F, S, active, act, nullptr);
     if (r.done) {
       ++episode;
       reset_scalars(P, E, seed, episode, 0, false);

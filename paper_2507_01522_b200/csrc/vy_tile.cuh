@@ -92,14 +92,6 @@ struct Prof {
 // Per-port constants staged in shared memory (one 96-byte record per port):
 // every lane reads the same address (broadcast), two doubles per 16-byte
 // load, instead of one indexed constant-bank load per value.
-#ifndef VY_U1
-#define VY_U1 1
-#endif
-#ifndef VY_U2
-#define VY_U2 1
-#endif
-#define VY_PRAGMA(x) _Pragma(#x)
-#define VY_UNROLL(n) VY_PRAGMA(unroll n)
 struct PortC {
   uint32_t a;  // shared address of port 0's record
   __device__ __forceinline__ void pair(int i, int w, double& x, double& y) const {
@@ -845,7 +837,12 @@ __device__ __forceinline__ void store_port(const Params& P, int64_t b, int i, ui
 
 // One transition of one env (_kernel.pyx:283-571).  `act(slot)` returns the
 // action index of a slot; `b` is the global env index (infos / injected draws).
-template <int M, class Act>
+// U2: unroll factor of the charge/departure port loop.  1 for the single step
+// (rolled: its hot loop is smaller; 2 measured 6% slower, the step being bound
+// by DRAM); 2 for the rollout, which is latency-bound with its state resident
+// and gains from the two ports' independent float64 chains (-1.8% per step,
+// profiles/r2_unroll_ab.txt).
+template <int M, class Act, int U2 = 1>
 __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
                                                 const double* __restrict__ dtab, PortC pc, TreeC tc, const Lane& T,
                                                 EnvRegs& E, int64_t b, const Frame& F, const ObsSink& S, bool active,
@@ -892,7 +889,7 @@ __device__ __forceinline__ StepResult tile_step(const Params& P, Prof prof,
     soc_q0 = soc_at(0);
     soc_q1 = soc_at(1);
   }
-VY_UNROLL(VY_U1)  // rolled: smaller hot loop measured faster than unroll 2 or 4
+#pragma unroll 1  // rolled: smaller hot loop measured faster than unroll 2 or 4
   for (int i = 0; i < n; ++i) {
     const double d = delta_of(act(i));
     const uint32_t mt = T.meta(i);
@@ -1002,7 +999,7 @@ VY_UNROLL(VY_U1)  // rolled: smaller hot loop measured faster than unroll 2 or 4
     q0 = q_at(0);
     q1 = q_at(1);
   }
-VY_UNROLL(VY_U2)  // rolled: smaller hot loop measured faster than unroll 2 or 4
+#pragma unroll U2
   for (int i = 0; i < n; ++i) {
     uint32_t mt = T.meta(i);
     double cur = T.idr(i), soc, de;
