@@ -316,6 +316,9 @@ __global__ void __launch_bounds__(kMultiThreads) k_step_multi(const __grid_const
   }
 }
 
+#ifndef VY_ROLL_U2
+#define VY_ROLL_U2 2  // the rollout's charge/departure loop unroll (tile_step U2)
+#endif
 template <int M>
 __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params P, int T_steps, uint64_t policy_seed,
                                                  int64_t index0, int64_t call0, int64_t obs_stride,
@@ -354,7 +357,7 @@ __global__ void __launch_bounds__(256) k_rollout(const __grid_constant__ Params 
     const uint64_t j0 = (uint64_t)(call0 + t) * (uint64_t)ns;
     auto act = [&](int slot) -> int { return policy_action(pkey, j0 + slot + 1, hi); };
     const Frame F = load_frame<M>(P, E.step, E.day);
-    const StepResult r = tile_step<M, decltype(act), 2>(P, prof, dtab, pc, tc, T, E, b, F, S, active, act, nullptr);
+    const StepResult r = tile_step<M, decltype(act), VY_ROLL_U2>(P, prof, dtab, pc, tc, T, E, b, F, S, active, act, nullptr);
     if (r.done) {
       ++episode;
       reset_scalars(P, E, seed, episode, 0, false);
