@@ -65,6 +65,17 @@ for _ in range(15):
 print("mode", env.last_step_mode())
 torch.cuda.synchronize()
 env.close()
+# streamed C4 tile with its L2 prefetch of later tiles active (40 tiles; run with VY_PF=10 so the
+# prefetch distance is a few tiles at this size)
+env = BatchEnv(cfg, c4.station, c4.dataset, batch_size=1280, master_seed=6)
+pol = DeviceRandomPolicy(seed=3, n_ports=env.n_ports, k=cfg.discretization_k)
+pol.bind(range(1280))
+env.reset(as_numpy=False)
+for _ in range(6):
+    env.step_random(pol)
+print("mode", env.last_step_mode())
+torch.cuda.synchronize()
+env.close()
 # one-launch heterogeneous batch (ragged last group)
 groups = sweep_groups(36 * 32 + 7, days=20)[:6]
 for g in groups:
