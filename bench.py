@@ -614,6 +614,13 @@ def main() -> None:
                                                   "note": "one fused step kernel per group on 12 streams, "
                                                           "one CUDA graph per step"},
                             "workload": "C5: regions x scenarios x traffic, single/multi/nested stations"}
+        # roofline on SURVEY §8(d) bytes, per group (its station's port count / battery), env-weighted
+        hbytes = sum(g.batch_size * survey_bytes(e.tables)["per_env_step"] for g, e in zip(hb.groups, hb.envs))
+        avg_b = hbytes / hb.total
+        result["hetero"]["roofline"] = {"bound": "hbm", "bytes_per_env_step": avg_b,
+                                        "achieved": value / world * avg_b / 1e9, "peak": hbm, "unit": "GB/s",
+                                        "frac": value / world * avg_b / 1e9 / hbm,
+                                        "note": "SURVEY §8(d) bytes of each group's station, weighted by its envs"}
         hb.close()
 
     if rank == 0 and world == 1 and not args.no_cpu:
